@@ -1,0 +1,17 @@
+"""B200-native bundle-adjustment inner loop (MegBA, arXiv 2112.01349).
+
+Drop-in for the reference's ``dba`` LM / DSE / DPCG path: the public names of
+``dba.py`` mirror the reference's C++ API; every operator runs in the in-tree
+``libdbag.so`` (hand-written sm_100a kernels + C++ host runtime, C ABI in
+``include/dbag.h``). There is no CPU fallback.
+"""
+from . import _native
+from .dba import *  # noqa: F401,F403
+from .dba import (BAProblem, CameraState, PointState, Observation, SolverConfig, SolverState, IterationRecord,
+                  SyntheticOptions, RankContext, lm_solve, lm_solve_rank, partition_edges, generate_synthetic,
+                  group_operator, group_allreduce, shared_points, nccl_unique_id, total_cost, device_count)
+
+__all__ = ["BAProblem", "CameraState", "PointState", "Observation", "SolverConfig", "SolverState",
+           "IterationRecord", "SyntheticOptions", "RankContext", "lm_solve", "lm_solve_rank", "partition_edges",
+           "generate_synthetic", "group_operator", "group_allreduce", "shared_points", "nccl_unique_id",
+           "total_cost", "device_count"]

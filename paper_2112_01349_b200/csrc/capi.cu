@@ -1,0 +1,569 @@
+// capi.cu — the extern "C" boundary (include/dbag.h).
+//
+// Status codes carry the reference's exception types across the ABI
+// (dba/errors.hpp); every entry point catches, records the message and the
+// payload (edge id / block index + size) in thread-local storage, and
+// returns the code.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <cstring>
+#include <exception>
+#include <memory>
+#include <mutex>
+#include <thread>
+#include <vector>
+
+#include "comm.hpp"
+#include "common.hpp"
+#include "partition.hpp"
+#include "rank.cuh"
+#include "solver.cuh"
+
+namespace dbag {
+std::int64_t synthetic_count(const dbag_synthetic_options& o);
+void generate_synthetic(const dbag_synthetic_options& o, double* cams, double* pts, std::int32_t* cam_id,
+                        std::int32_t* pt_id, double* pix_x, double* pix_y);
+}  // namespace dbag
+
+using namespace dbag;
+
+struct dbag_ctx {
+  int precision = 8;
+  std::unique_ptr<Comm> comm;
+  std::unique_ptr<Rank<float>> r32;
+  std::unique_ptr<Rank<double>> r64;
+  std::int64_t num_obs = 0;
+  bool cost_valid = false;
+  double cost = 0;
+};
+
+namespace {
+
+thread_local std::string g_err;
+thread_local std::int64_t g_err_index = -1;
+thread_local int g_err_bs = 0;
+
+template <class Fn>
+int guarded(Fn&& fn) {
+  try {
+    fn();
+    return DBAG_OK;
+  } catch (const Error& e) {
+    g_err = e.what();
+    g_err_index = e.index;
+    g_err_bs = e.block_size;
+    return e.code;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    g_err_index = -1;
+    g_err_bs = 0;
+    return DBAG_INTERNAL;
+  }
+}
+
+void check_precision(int p) {
+  if (p != 4 && p != 8) throw Error(DBAG_INVALID_ARGUMENT, "precision must be 4 or 8");
+}
+
+void check_ctx(dbag_ctx* c) {
+  if (!c || (!c->r32 && !c->r64)) throw Error(DBAG_INVALID_ARGUMENT, "null or empty context");
+}
+
+// Calls fn(Rank<S>&) on the context's typed rank.
+template <class Fn>
+void with_rank(dbag_ctx* c, Fn&& fn) {
+  check_ctx(c);
+  if (c->r64) fn(*c->r64);
+  else fn(*c->r32);
+}
+
+void fill_result(const Outcome& o, int K, dbag_result* out) {
+  out->iterations = o.iteration;
+  out->termination = o.termination;
+  out->cost = o.cost;
+  out->lambda = o.lambda;
+  out->nu = o.nu;
+  out->workers = K;
+  const int n = std::min<int>(out->capacity, static_cast<int>(o.history.size()));
+  for (int i = 0; i < n; ++i) {
+    const Record& r = o.history[static_cast<std::size_t>(i)];
+    if (out->rec_iteration) out->rec_iteration[i] = r.iteration;
+    if (out->rec_cost) out->rec_cost[i] = r.cost;
+    if (out->rec_mse) out->rec_mse[i] = r.mse;
+    if (out->rec_lambda) out->rec_lambda[i] = r.lambda;
+    if (out->rec_pcg) out->rec_pcg[i] = r.pcg_iterations;
+    if (out->rec_accepted) out->rec_accepted[i] = r.accepted ? 1 : 0;
+    if (out->rec_wall) out->rec_wall[i] = r.wall_seconds;
+    for (int k = 0; k < K; ++k) {
+      const std::size_t at = static_cast<std::size_t>(i) * K + k;
+      if (out->rec_worker_edges) out->rec_worker_edges[at] = r.worker_edges[static_cast<std::size_t>(k)];
+      if (out->rec_worker_block_ops) out->rec_worker_block_ops[at] = r.worker_block_ops[static_cast<std::size_t>(k)];
+    }
+  }
+}
+
+// Writes this rank's owned points (and, on rank 0, the cameras) of the
+// current state into full-size host vectors.
+template <class S>
+void export_state(Rank<S>& rk, S* xc, S* xp) {
+  const ShardPlan& pl = rk.plan();
+  std::vector<S> cams(static_cast<std::size_t>(pl.m) * 9), pts(static_cast<std::size_t>(pl.n) * 3);
+  rk.get_state(cams.data(), pts.data());
+  if (xc && pl.rank == 0) std::copy(cams.begin(), cams.end(), xc);
+  if (xp)
+    for (std::int32_t lp = 0; lp < pl.pts.size(); ++lp) {
+      if (!pl.owned_lpt[static_cast<std::size_t>(lp)]) continue;
+      const std::size_t g = static_cast<std::size_t>(pl.pts.to_global[static_cast<std::size_t>(lp)]);
+      for (int k = 0; k < 3; ++k) xp[g * 3 + k] = pts[g * 3 + k];
+    }
+}
+
+// Runs body(rank) on one host thread per rank (run_on_workers,
+// dba/comms.hpp:214-234): the first failure aborts the group and is
+// rethrown after every thread joined.
+template <class Fn>
+void run_ranks(Group& g, Fn&& body) {
+  std::vector<std::thread> th;
+  std::exception_ptr first;
+  std::mutex mu;
+  for (int r = 0; r < g.size(); ++r) {
+    th.emplace_back([&, r] {
+      try {
+        DBAG_CUDA(cudaSetDevice(g.device_of(r)));
+        body(r);
+      } catch (const std::exception& e) {
+        {
+          std::lock_guard<std::mutex> lk(mu);
+          if (!first) first = std::current_exception();
+        }
+        g.abort(std::string("rank ") + std::to_string(r) + " failed: " + e.what());
+      }
+    });
+  }
+  for (auto& t : th) t.join();
+  if (first) std::rethrow_exception(first);
+}
+
+template <class S>
+void lm_group(const dbag_problem* p, const dbag_config* c, const int* devices, int n_devices, dbag_result* out) {
+  const int K = c->workers;
+  std::vector<int> devs(devices, devices + std::max(n_devices, 0));
+  if (devs.empty()) devs.push_back(0);
+  split_edges(p->num_observations, K);  // validates K like partition_edges
+  Group g(K, devs);
+  if (out->x_p) std::memcpy(out->x_p, p->points, sizeof(S) * 3 * static_cast<std::size_t>(p->num_points));
+  run_ranks(g, [&](int r) {
+    GroupComm comm(&g, r);
+    Rank<S> rk(g.device_of(r), &comm);
+    rk.upload(*p, c->jacobian);
+    const Outcome o = lm_solve_rank(rk, *c, p->num_observations);
+    export_state(rk, static_cast<S*>(out->x_c), static_cast<S*>(out->x_p));
+    if (r == 0) fill_result(o, K, out);
+  });
+}
+
+template <class S>
+void lm_nccl(const dbag_problem* p, const dbag_config* c, int rank, int nranks, const unsigned char* id, int device,
+             dbag_result* out) {
+  DBAG_CUDA(cudaSetDevice(device));
+  if (c->workers != nranks) throw Error(DBAG_INVALID_ARGUMENT, "config.workers must equal nranks");
+  NcclComm comm(rank, nranks, id);
+  Rank<S> rk(device, &comm);
+  rk.upload(*p, c->jacobian);
+  const Outcome o = lm_solve_rank(rk, *c, p->num_observations);
+  if (out->x_p) std::memcpy(out->x_p, p->points, sizeof(S) * 3 * static_cast<std::size_t>(p->num_points));
+  export_state(rk, static_cast<S*>(out->x_c), static_cast<S*>(out->x_p));
+  fill_result(o, nranks, out);
+}
+
+template <class S>
+void group_operator(const dbag_problem* p, int k, int device, double lambda, int policy, const void* B,
+                    const void* C, const void* E, int mode, const void* x, double tol, int max_iters, void* out,
+                    int* iterations, int* rank_identical) {
+  split_edges(p->num_observations, k);
+  Group g(k, {device});
+  const std::size_t len = static_cast<std::size_t>(p->num_cameras) * 9;
+  std::vector<std::vector<S>> outs(static_cast<std::size_t>(k), std::vector<S>(len));
+  std::vector<int> its(static_cast<std::size_t>(k), 0);
+  run_ranks(g, [&](int r) {
+    GroupComm comm(&g, r);
+    Rank<S> rk(device, &comm);
+    rk.upload(*p, 0);
+    if (B) {
+      rk.set_system(static_cast<const S*>(B), static_cast<const S*>(C), static_cast<const S*>(E), nullptr, nullptr);
+      rk.factor_as_is();
+    } else {
+      rk.linearize();
+      rk.damp_factor(lambda, policy);
+    }
+    if (mode == 0) {
+      rk.dse_host(static_cast<const S*>(x), outs[static_cast<std::size_t>(r)].data());
+    } else {
+      its[static_cast<std::size_t>(r)] =
+          rk.dpcg_host(static_cast<const S*>(x), tol, max_iters, outs[static_cast<std::size_t>(r)].data()).iterations;
+    }
+  });
+  *rank_identical = 1;
+  for (int r = 1; r < k; ++r)
+    if (std::memcmp(outs[static_cast<std::size_t>(r)].data(), outs[0].data(), len * sizeof(S)) != 0) *rank_identical = 0;
+  std::memcpy(out, outs[0].data(), len * sizeof(S));
+  if (iterations) *iterations = its[0];
+}
+
+}  // namespace
+
+extern "C" {
+
+int dbag_version(void) { return 1; }
+const char* dbag_last_error(void) { return g_err.c_str(); }
+int64_t dbag_last_error_index(void) { return g_err_index; }
+int dbag_last_error_block_size(void) { return g_err_bs; }
+
+void dbag_default_config(dbag_config* c) {  // dba/solver.hpp:39-55
+  std::memset(c, 0, sizeof(*c));
+  c->workers = 1;
+  c->max_iterations = 50;
+  c->pcg_tol = 1e-6;
+  c->pcg_max_iters = 500;
+  c->lambda0 = 1e-4;
+  c->lambda_max = 1e32;
+  c->rel_tol = 1e-6;
+  c->step_tol = 1e-8;
+  c->damping = 1;
+  c->mse_half = 1;
+  c->jacobian = 0;
+  c->check_rank_identity = 0;
+}
+
+int dbag_device_count(int* out) {
+  return guarded([&] {
+    int n = 0;
+    const cudaError_t e = cudaGetDeviceCount(&n);
+    *out = e == cudaSuccess ? n : 0;
+    (void)cudaGetLastError();
+  });
+}
+
+int dbag_partition(const dbag_problem* p, int k, int rank, int64_t* start, int64_t* count, int32_t* n_cams,
+                   int32_t* cam_g, int32_t* n_pts, int32_t* pt_g, int64_t* cam_ptr, int64_t* cam_blk, int64_t* pt_ptr,
+                   int64_t* pt_blk) {
+  return guarded([&] {
+    const ShardPlan s = plan_shard(p->camera_id, p->point_id, p->num_observations, p->num_cameras, p->num_points, k,
+                                   rank);
+    *start = s.range.start;
+    *count = s.range.count;
+    *n_cams = s.cams.size();
+    *n_pts = s.pts.size();
+    std::copy(s.cams.to_global.begin(), s.cams.to_global.end(), cam_g);
+    std::copy(s.pts.to_global.begin(), s.pts.to_global.end(), pt_g);
+    std::copy(s.cam_ptr.begin(), s.cam_ptr.end(), cam_ptr);
+    std::copy(s.cam_blk.begin(), s.cam_blk.end(), cam_blk);
+    std::copy(s.pt_ptr.begin(), s.pt_ptr.end(), pt_ptr);
+    std::copy(s.pt_blk.begin(), s.pt_blk.end(), pt_blk);
+  });
+}
+
+int dbag_shared_points(const dbag_problem* p, int k, int64_t* n_shared, int32_t* ids) {
+  return guarded([&] {
+    const auto ranges = split_edges(p->num_observations, k);
+    const Coverage cov = point_coverage(p->point_id, p->num_points, ranges);
+    *n_shared = cov.n_shared;
+    if (ids)
+      for (std::int32_t q = 0; q < p->num_points; ++q)
+        if (cov.shared_index[static_cast<std::size_t>(q)] >= 0) ids[cov.shared_index[static_cast<std::size_t>(q)]] = q;
+  });
+}
+
+int dbag_synthetic_count(const dbag_synthetic_options* o, int64_t* n_obs) {
+  return guarded([&] { *n_obs = synthetic_count(*o); });
+}
+
+int dbag_generate_synthetic(const dbag_synthetic_options* o, double* cameras, double* points, int32_t* camera_id,
+                            int32_t* point_id, double* pixel_x, double* pixel_y) {
+  return guarded([&] { generate_synthetic(*o, cameras, points, camera_id, point_id, pixel_x, pixel_y); });
+}
+
+int dbag_lm_solve(int precision, const dbag_problem* p, const dbag_config* c, const int* devices, int n_devices,
+                  dbag_result* out) {
+  return guarded([&] {
+    check_precision(precision);
+    if (precision == 8) lm_group<double>(p, c, devices, n_devices, out);
+    else lm_group<float>(p, c, devices, n_devices, out);
+  });
+}
+
+int dbag_nccl_unique_id(unsigned char* out128) {
+  return guarded([&] {
+    ncclUniqueId id;
+    const ncclResult_t r = ncclGetUniqueId(&id);
+    if (r != ncclSuccess) throw Error(DBAG_NCCL_ERROR, std::string("ncclGetUniqueId: ") + ncclGetErrorString(r));
+    std::memcpy(out128, id.internal, 128);
+  });
+}
+
+int dbag_lm_solve_rank(int precision, const dbag_problem* p, const dbag_config* c, int rank, int nranks,
+                       const unsigned char* id, int device, dbag_result* out) {
+  return guarded([&] {
+    check_precision(precision);
+    if (precision == 8) lm_nccl<double>(p, c, rank, nranks, id, device, out);
+    else lm_nccl<float>(p, c, rank, nranks, id, device, out);
+  });
+}
+
+int dbag_create(int device, int precision, dbag_ctx** out) {
+  return guarded([&] {
+    check_precision(precision);
+    auto ctx = std::make_unique<dbag_ctx>();
+    ctx->precision = precision;
+    ctx->comm = std::make_unique<SelfComm>();
+    if (precision == 8) ctx->r64 = std::make_unique<Rank<double>>(device, ctx->comm.get());
+    else ctx->r32 = std::make_unique<Rank<float>>(device, ctx->comm.get());
+    *out = ctx.release();
+  });
+}
+
+int dbag_create_nccl(int device, int rank, int nranks, const unsigned char* id, int precision, dbag_ctx** out) {
+  return guarded([&] {
+    check_precision(precision);
+    DBAG_CUDA(cudaSetDevice(device));
+    auto ctx = std::make_unique<dbag_ctx>();
+    ctx->precision = precision;
+    ctx->comm = std::make_unique<NcclComm>(rank, nranks, id);
+    if (precision == 8) ctx->r64 = std::make_unique<Rank<double>>(device, ctx->comm.get());
+    else ctx->r32 = std::make_unique<Rank<float>>(device, ctx->comm.get());
+    *out = ctx.release();
+  });
+}
+
+int dbag_destroy(dbag_ctx* ctx) {
+  return guarded([&] { delete ctx; });
+}
+
+int dbag_upload_problem(dbag_ctx* ctx, const dbag_problem* p, int jacobian_mode) {
+  return guarded([&] {
+    with_rank(ctx, [&](auto& rk) { rk.upload(*p, jacobian_mode); });
+    ctx->num_obs = p->num_observations;
+    ctx->cost_valid = false;
+  });
+}
+
+int dbag_set_state(dbag_ctx* ctx, const void* x_c, const void* x_p) {
+  return guarded([&] {
+    with_rank(ctx, [&](auto& rk) {
+      using S = std::remove_reference_t<decltype(rk)>;
+      using T = std::conditional_t<std::is_same_v<S, Rank<double>>, double, float>;
+      rk.set_state(static_cast<const T*>(x_c), static_cast<const T*>(x_p));
+    });
+    ctx->cost_valid = false;
+  });
+}
+
+int dbag_get_state(dbag_ctx* ctx, void* x_c, void* x_p) {
+  return guarded([&] {
+    with_rank(ctx, [&](auto& rk) {
+      using S = std::remove_reference_t<decltype(rk)>;
+      using T = std::conditional_t<std::is_same_v<S, Rank<double>>, double, float>;
+      rk.get_state(static_cast<T*>(x_c), static_cast<T*>(x_p));
+    });
+  });
+}
+
+int dbag_cost(dbag_ctx* ctx, int use_trial, double* cost, int64_t* bad_edge) {
+  return guarded([&] {
+    std::int64_t bad = -1;
+    with_rank(ctx, [&](auto& rk) { *cost = rk.cost(use_trial != 0, &bad); });
+    if (bad_edge) *bad_edge = bad;
+  });
+}
+
+int dbag_linearize(dbag_ctx* ctx, int64_t* bad_edge) {
+  if (bad_edge) *bad_edge = -1;
+  const int rc = guarded([&] { with_rank(ctx, [&](auto& rk) { rk.linearize(); }); });
+  if (rc == DBAG_DEGENERATE_DEPTH && bad_edge) *bad_edge = g_err_index;
+  return rc;
+}
+
+int dbag_damp_factor(dbag_ctx* ctx, double lambda, int policy, int64_t* bad_block, int* bad_bs) {
+  if (bad_block) *bad_block = -1;
+  if (bad_bs) *bad_bs = 0;
+  const int rc = guarded([&] { with_rank(ctx, [&](auto& rk) { rk.damp_factor(lambda, policy); }); });
+  if (rc == DBAG_SINGULAR_BLOCK) {
+    if (bad_block) *bad_block = g_err_index;
+    if (bad_bs) *bad_bs = g_err_bs;
+  }
+  return rc;
+}
+
+int dbag_rhs(dbag_ctx* ctx) {
+  return guarded([&] { with_rank(ctx, [&](auto& rk) { rk.rhs(); }); });
+}
+
+int dbag_pcg(dbag_ctx* ctx, double tol, int max_iters, int* iterations, int* converged) {
+  return guarded([&] {
+    with_rank(ctx, [&](auto& rk) {
+      const PcgOut o = rk.pcg(tol, max_iters);
+      if (iterations) *iterations = o.iterations;
+      if (converged) *converged = o.converged ? 1 : 0;
+    });
+  });
+}
+
+int dbag_backsub_trial(dbag_ctx* ctx) {
+  return guarded([&] { with_rank(ctx, [&](auto& rk) { rk.backsub_trial(); }); });
+}
+
+int dbag_model_terms(dbag_ctx* ctx, double lambda, int policy, double* step_inf, double* damping_term, double* gv) {
+  (void)lambda;
+  (void)policy;  // fixed by the preceding damp_factor, as in the reference trial
+  return guarded([&] { with_rank(ctx, [&](auto& rk) { rk.model_terms(step_inf, damping_term, gv); }); });
+}
+
+int dbag_accept(dbag_ctx* ctx) {
+  return guarded([&] {
+    with_rank(ctx, [&](auto& rk) { rk.accept(); });
+    ctx->cost_valid = false;
+  });
+}
+
+int dbag_lm_probe_step(dbag_ctx* ctx, double lambda, const dbag_config* c, double* cost_new, int* pcg_iterations,
+                       int* accepted) {
+  return guarded([&] {
+    with_rank(ctx, [&](auto& rk) {
+      if (!ctx->cost_valid) {
+        std::int64_t bad = -1;
+        ctx->cost = rk.cost(false, &bad);
+        if (!std::isfinite(ctx->cost)) throw degenerate_depth(bad);
+        ctx->cost_valid = true;
+      }
+      rk.linearize();
+      const Trial t = run_trial(rk, *c, lambda, ctx->cost);
+      if (cost_new) *cost_new = t.cost_new;
+      if (pcg_iterations) *pcg_iterations = t.factorization_ok ? t.pcg_iterations : 0;
+      if (accepted) *accepted = t.accepted ? 1 : 0;
+    });
+  });
+}
+
+int dbag_profile(dbag_ctx* ctx, int enable, double* dse_ms, int64_t* dse_launches, double* dse_point_ms,
+                 double* dse_cam_ms) {
+  return guarded([&] {
+    with_rank(ctx, [&](auto& rk) {
+      if (enable >= 0) {
+        rk.set_profiling(enable != 0);
+      } else {
+        double t = 0, a = 0, b = 0;
+        std::int64_t n = 0;
+        rk.profile(&t, &n, &a, &b);
+        if (dse_ms) *dse_ms = t;
+        if (dse_launches) *dse_launches = n;
+        if (dse_point_ms) *dse_point_ms = a;
+        if (dse_cam_ms) *dse_cam_ms = b;
+      }
+    });
+  });
+}
+
+int dbag_event_mark(dbag_ctx* ctx, int which) {
+  return guarded([&] { with_rank(ctx, [&](auto& rk) { rk.mark(which); }); });
+}
+
+int dbag_event_elapsed(dbag_ctx* ctx, double* ms) {
+  return guarded([&] { with_rank(ctx, [&](auto& rk) { *ms = rk.elapsed_ms(); }); });
+}
+
+int dbag_synchronize(dbag_ctx* ctx) {
+  return guarded([&] { with_rank(ctx, [&](auto& rk) { rk.sync(); }); });
+}
+
+int dbag_get_jacobians(dbag_ctx* ctx, void* res, void* jac) {
+  return guarded([&] {
+    with_rank(ctx, [&](auto& rk) {
+      using S = std::remove_reference_t<decltype(rk)>;
+      using T = std::conditional_t<std::is_same_v<S, Rank<double>>, double, float>;
+      rk.get_jacobians(static_cast<T*>(res), static_cast<T*>(jac));
+    });
+  });
+}
+
+int dbag_get_system(dbag_ctx* ctx, void* B, void* C, void* E, void* v, void* w) {
+  return guarded([&] {
+    with_rank(ctx, [&](auto& rk) {
+      using S = std::remove_reference_t<decltype(rk)>;
+      using T = std::conditional_t<std::is_same_v<S, Rank<double>>, double, float>;
+      rk.get_system(static_cast<T*>(B), static_cast<T*>(C), static_cast<T*>(E), static_cast<T*>(v),
+                    static_cast<T*>(w));
+    });
+  });
+}
+
+int dbag_set_system(dbag_ctx* ctx, const void* B, const void* C, const void* E_table, const void* v, const void* w) {
+  return guarded([&] {
+    with_rank(ctx, [&](auto& rk) {
+      using S = std::remove_reference_t<decltype(rk)>;
+      using T = std::conditional_t<std::is_same_v<S, Rank<double>>, double, float>;
+      rk.set_system(static_cast<const T*>(B), static_cast<const T*>(C), static_cast<const T*>(E_table),
+                    static_cast<const T*>(v), static_cast<const T*>(w));
+    });
+  });
+}
+
+int dbag_dse(dbag_ctx* ctx, const void* x, void* out) {
+  return guarded([&] {
+    with_rank(ctx, [&](auto& rk) {
+      using S = std::remove_reference_t<decltype(rk)>;
+      using T = std::conditional_t<std::is_same_v<S, Rank<double>>, double, float>;
+      rk.dse_host(static_cast<const T*>(x), static_cast<T*>(out));
+    });
+  });
+}
+
+int dbag_dpcg(dbag_ctx* ctx, const void* rhs, double tol, int max_iters, void* x_out, int* iterations,
+              int* converged) {
+  return guarded([&] {
+    with_rank(ctx, [&](auto& rk) {
+      using S = std::remove_reference_t<decltype(rk)>;
+      using T = std::conditional_t<std::is_same_v<S, Rank<double>>, double, float>;
+      const PcgOut o = rk.dpcg_host(static_cast<const T*>(rhs), tol, max_iters, static_cast<T*>(x_out));
+      if (iterations) *iterations = o.iterations;
+      if (converged) *converged = o.converged ? 1 : 0;
+    });
+  });
+}
+
+int dbag_group_operator(int precision, const dbag_problem* p, int k, int device, double lambda, int policy,
+                        const void* B, const void* C, const void* E_table, int mode, const void* x, double tol,
+                        int max_iters, void* out, int* iterations, int* rank_identical) {
+  return guarded([&] {
+    check_precision(precision);
+    if (precision == 8)
+      group_operator<double>(p, k, device, lambda, policy, B, C, E_table, mode, x, tol, max_iters, out, iterations,
+                             rank_identical);
+    else
+      group_operator<float>(p, k, device, lambda, policy, B, C, E_table, mode, x, tol, max_iters, out, iterations,
+                            rank_identical);
+  });
+}
+
+int dbag_group_allreduce(int k, int device, int64_t len, double* data) {
+  return guarded([&] {
+    Group g(k, {device});
+    run_ranks(g, [&](int r) {
+      GroupComm comm(&g, r);
+      double* d = nullptr;
+      DBAG_CUDA(cudaMalloc(&d, sizeof(double) * std::max<int64_t>(len, 1)));
+      cudaStream_t s;
+      DBAG_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+      DBAG_CUDA(cudaMemcpyAsync(d, data + static_cast<std::size_t>(r) * len, sizeof(double) * len,
+                                cudaMemcpyHostToDevice, s));
+      comm.allreduce_sum(d, len, DType::f64, s);
+      DBAG_CUDA(cudaMemcpyAsync(data + static_cast<std::size_t>(r) * len, d, sizeof(double) * len,
+                                cudaMemcpyDeviceToHost, s));
+      DBAG_CUDA(cudaStreamSynchronize(s));
+      cudaStreamDestroy(s);
+      cudaFree(d);
+    });
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,222 @@
+// comm.cu — Group (in-process ranks) and NCCL backends of comm.hpp.
+#include <algorithm>
+
+#include "comm.hpp"
+
+namespace dbag {
+namespace {
+
+constexpr int kMaxGroup = 16;
+struct SlotPtrs {
+  const void* p[kMaxGroup];
+};
+
+// Ascending-rank fold of the K deposited buffers (dba/comms.hpp:76-81):
+// acc = s0; acc += s1; ... (sum) or acc = max(acc, s_r) (max).
+template <class T, bool MAX>
+__global__ void k_fold_slots(std::int64_t len, int k, SlotPtrs sp, T* __restrict__ out) {
+  for (std::int64_t i = blockIdx.x * std::int64_t(blockDim.x) + threadIdx.x; i < len;
+       i += std::int64_t(gridDim.x) * blockDim.x) {
+    T acc = static_cast<const T*>(sp.p[0])[i];
+    for (int r = 1; r < k; ++r) {
+      const T v = static_cast<const T*>(sp.p[r])[i];
+      acc = MAX ? (v > acc ? v : acc) : acc + v;
+    }
+    out[i] = acc;
+  }
+}
+
+ncclDataType_t nccl_type(DType t) { return t == DType::f64 ? ncclDouble : ncclFloat; }
+
+#define DBAG_NCCL(expr)                                                                           \
+  do {                                                                                            \
+    ncclResult_t _r = (expr);                                                                     \
+    if (_r != ncclSuccess)                                                                        \
+      throw ::dbag::Error(DBAG_NCCL_ERROR, std::string(#expr " failed: ") + ncclGetErrorString(_r)); \
+  } while (0)
+
+}  // namespace
+
+Group::Group(int k, std::vector<int> devices, std::chrono::milliseconds timeout)
+    : k_(k), devices_(std::move(devices)), timeout_(timeout) {
+  if (k < 1) throw Error(DBAG_INVALID_ARGUMENT, "worker group needs at least one rank");
+  if (k > kMaxGroup) throw Error(DBAG_INVALID_ARGUMENT, "in-process group supports at most 16 ranks");
+  if (devices_.empty()) devices_.push_back(0);
+  std::vector<int> dev(static_cast<std::size_t>(k));
+  for (int r = 0; r < k; ++r) dev[static_cast<std::size_t>(r)] = devices_[static_cast<std::size_t>(r) % devices_.size()];
+  devices_ = dev;
+  here_.assign(static_cast<std::size_t>(k), false);
+  slots_.resize(static_cast<std::size_t>(k));
+  seq_.assign(static_cast<std::size_t>(k), 0);
+  ready_.resize(static_cast<std::size_t>(k));
+  done_.resize(static_cast<std::size_t>(k));
+  scratch_.assign(static_cast<std::size_t>(k), nullptr);
+  scratch_bytes_.assign(static_cast<std::size_t>(k), 0);
+  int prev = 0;
+  DBAG_CUDA(cudaGetDevice(&prev));
+  for (int r = 0; r < k; ++r) {
+    DBAG_CUDA(cudaSetDevice(device_of(r)));
+    DBAG_CUDA(cudaEventCreateWithFlags(&ready_[static_cast<std::size_t>(r)], cudaEventDisableTiming));
+    DBAG_CUDA(cudaEventCreateWithFlags(&done_[static_cast<std::size_t>(r)], cudaEventDisableTiming));
+  }
+  // Peer access between the distinct devices of the group (NVLink / NVSwitch).
+  std::vector<int> uniq = devices_;
+  std::sort(uniq.begin(), uniq.end());
+  uniq.erase(std::unique(uniq.begin(), uniq.end()), uniq.end());
+  for (int a : uniq) {
+    DBAG_CUDA(cudaSetDevice(a));
+    for (int b : uniq) {
+      if (a == b) continue;
+      int ok = 0;
+      DBAG_CUDA(cudaDeviceCanAccessPeer(&ok, a, b));
+      if (!ok) throw Error(DBAG_CUDA_ERROR, "devices " + std::to_string(a) + " and " + std::to_string(b) + " lack peer access");
+      const cudaError_t e = cudaDeviceEnablePeerAccess(b, 0);
+      if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) DBAG_CUDA(e);
+      (void)cudaGetLastError();
+    }
+  }
+  DBAG_CUDA(cudaSetDevice(prev));
+}
+
+Group::~Group() {
+  for (int r = 0; r < k_; ++r) {
+    cudaSetDevice(device_of(r));
+    cudaEventDestroy(ready_[static_cast<std::size_t>(r)]);
+    cudaEventDestroy(done_[static_cast<std::size_t>(r)]);
+    if (scratch_[static_cast<std::size_t>(r)]) cudaFree(scratch_[static_cast<std::size_t>(r)]);
+  }
+}
+
+void Group::abort(const std::string& why) {
+  std::lock_guard<std::mutex> lk(mu_);
+  if (!aborted_) {
+    aborted_ = true;
+    why_ = why;
+  }
+  cv_.notify_all();
+}
+
+bool Group::aborted() const {
+  std::lock_guard<std::mutex> lk(mu_);
+  return aborted_;
+}
+
+// Generation barrier with a timeout that names the absent ranks
+// (dba/comms.hpp:136-165).
+void Group::rendezvous(int rank) {
+  std::unique_lock<std::mutex> lk(mu_);
+  if (aborted_) throw Error(DBAG_COLLECTIVE, "collective aborted: " + why_);
+  here_[static_cast<std::size_t>(rank)] = true;
+  if (++arrived_ == k_) {
+    arrived_ = 0;
+    std::fill(here_.begin(), here_.end(), false);
+    ++gen_;
+    cv_.notify_all();
+    return;
+  }
+  const std::uint64_t g = gen_;
+  while (gen_ == g && !aborted_) {
+    if (cv_.wait_for(lk, timeout_) == std::cv_status::timeout && gen_ == g && !aborted_) {
+      std::string missing;
+      for (int r = 0; r < k_; ++r)
+        if (!here_[static_cast<std::size_t>(r)]) missing += (missing.empty() ? "" : ", ") + std::to_string(r);
+      aborted_ = true;
+      why_ = "collective timeout at sequence " + std::to_string(seq_[static_cast<std::size_t>(rank)]) +
+             "; still waiting on ranks: " + missing;
+      cv_.notify_all();
+      throw Error(DBAG_COLLECTIVE, why_);
+    }
+  }
+  if (aborted_) throw Error(DBAG_COLLECTIVE, "collective aborted: " + why_);
+}
+
+// Call-sequence / kind / length agreement (dba/comms.hpp:167-193).
+void Group::validate(int rank, std::int64_t count, int kind) {
+  std::lock_guard<std::mutex> lk(mu_);
+  const std::uint64_t seq = seq_[static_cast<std::size_t>(rank)];
+  for (int r = 0; r < k_; ++r) {
+    const Slot& s = slots_[static_cast<std::size_t>(r)];
+    std::string problem;
+    if (s.seq != seq) problem = "is at call sequence " + std::to_string(s.seq) + ", this rank at " + std::to_string(seq);
+    else if (s.kind != kind) problem = "entered a different collective kind or element type";
+    else if (s.count != count)
+      problem = "passed length " + std::to_string(s.count) + ", this rank passed " + std::to_string(count);
+    if (!problem.empty()) {
+      aborted_ = true;
+      why_ = "collective mismatch: rank " + std::to_string(r) + " " + problem;
+      cv_.notify_all();
+      throw Error(DBAG_COLLECTIVE, why_);
+    }
+  }
+}
+
+void* Group::scratch(int rank, std::size_t bytes) {
+  auto& p = scratch_[static_cast<std::size_t>(rank)];
+  auto& n = scratch_bytes_[static_cast<std::size_t>(rank)];
+  if (n < bytes) {
+    if (p) DBAG_CUDA(cudaFree(p));
+    DBAG_CUDA(cudaMalloc(&p, bytes));
+    n = bytes;
+  }
+  return p;
+}
+
+void Group::allreduce(int rank, void* data, std::int64_t count, DType t, bool is_max, cudaStream_t s) {
+  if (k_ == 1) return;
+  const int kind = (t == DType::f64 ? 2 : 0) + (is_max ? 1 : 0);
+  const std::size_t bytes = static_cast<std::size_t>(count) * dsize(t);
+  void* out = count > 0 ? scratch(rank, bytes) : nullptr;  // before publishing: no allocation inside the window
+  {
+    std::lock_guard<std::mutex> lk(mu_);
+    if (aborted_) throw Error(DBAG_COLLECTIVE, "collective aborted: " + why_);
+    slots_[static_cast<std::size_t>(rank)] = Slot{data, count, kind, ++seq_[static_cast<std::size_t>(rank)]};
+  }
+  DBAG_CUDA(cudaEventRecord(ready_[static_cast<std::size_t>(rank)], s));
+  rendezvous(rank);
+  validate(rank, count, kind);
+  SlotPtrs sp{};
+  for (int r = 0; r < k_; ++r) {
+    sp.p[r] = slots_[static_cast<std::size_t>(r)].ptr;
+    if (r != rank) DBAG_CUDA(cudaStreamWaitEvent(s, ready_[static_cast<std::size_t>(r)], 0));
+  }
+  if (count > 0) {
+    const int threads = 256;
+    const int blocks = static_cast<int>(std::min<std::int64_t>((count + threads - 1) / threads, 1184));
+    if (t == DType::f64) {
+      if (is_max) k_fold_slots<double, true><<<blocks, threads, 0, s>>>(count, k_, sp, static_cast<double*>(out));
+      else k_fold_slots<double, false><<<blocks, threads, 0, s>>>(count, k_, sp, static_cast<double*>(out));
+    } else {
+      if (is_max) k_fold_slots<float, true><<<blocks, threads, 0, s>>>(count, k_, sp, static_cast<float*>(out));
+      else k_fold_slots<float, false><<<blocks, threads, 0, s>>>(count, k_, sp, static_cast<float*>(out));
+    }
+    DBAG_LAUNCH_CHECK();
+  }
+  DBAG_CUDA(cudaEventRecord(done_[static_cast<std::size_t>(rank)], s));
+  rendezvous(rank);  // every rank has enqueued its reads of the deposited sources
+  for (int r = 0; r < k_; ++r)
+    if (r != rank) DBAG_CUDA(cudaStreamWaitEvent(s, done_[static_cast<std::size_t>(r)], 0));
+  if (count > 0) DBAG_CUDA(cudaMemcpyAsync(data, out, bytes, cudaMemcpyDeviceToDevice, s));
+}
+
+NcclComm::NcclComm(int rank, int nranks, const unsigned char* id128) : rank_(rank), size_(nranks) {
+  ncclUniqueId id;
+  static_assert(sizeof(id.internal) == 128, "ncclUniqueId is 128 bytes");
+  std::copy(id128, id128 + 128, reinterpret_cast<unsigned char*>(id.internal));
+  DBAG_NCCL(ncclCommInitRank(&comm_, nranks, id, rank));
+}
+
+NcclComm::~NcclComm() {
+  if (comm_) ncclCommDestroy(comm_);
+}
+
+void NcclComm::allreduce_sum(void* d, std::int64_t n, DType t, cudaStream_t s) {
+  if (size_ == 1 || n == 0) return;
+  DBAG_NCCL(ncclAllReduce(d, d, static_cast<size_t>(n), nccl_type(t), ncclSum, comm_, s));
+}
+
+void NcclComm::allreduce_max(void* d, std::int64_t n, DType t, cudaStream_t s) {
+  if (size_ == 1 || n == 0) return;
+  DBAG_NCCL(ncclAllReduce(d, d, static_cast<size_t>(n), nccl_type(t), ncclMax, comm_, s));
+}
+
+}  // namespace dbag

@@ -1,0 +1,124 @@
+// comm.hpp — collectives between rank contexts (dba/comms.hpp:35-234 role).
+//
+// Three backends behind one interface, all in-place on device buffers and
+// stream-ordered on the calling rank's stream:
+//   SelfComm   K = 1: every collective is the identity.
+//   GroupComm  K ranks inside one process (one host thread per rank, the
+//              reference's run_on_workers model, dba/comms.hpp:214-234),
+//              ranks on one or several GPUs. A host rendezvous publishes each
+//              rank's device buffer, then every rank sums the K deposited
+//              buffers in ascending rank order on its own stream
+//              (k_sum_slots) — bit-identical to WorkerGroup::allreduce_sum
+//              (dba/comms.hpp:76-81) and rank-identical by construction.
+//              Cross-rank ordering uses CUDA events, so no host<->device sync
+//              is needed. Also carries the reference's call-sequence / kind /
+//              length validation and rendezvous timeout (dba/comms.hpp:136-193).
+//   NcclComm   one process per GPU (torchrun), ncclAllReduce over NVLink /
+//              NVSwitch on the rank's stream.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <chrono>
+#include <condition_variable>
+#include <cstdint>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "common.hpp"
+
+namespace dbag {
+
+enum class DType { f32, f64 };
+inline std::size_t dsize(DType t) { return t == DType::f64 ? 8 : 4; }
+
+class Comm {
+ public:
+  virtual ~Comm() = default;
+  virtual int rank() const = 0;
+  virtual int size() const = 0;
+  // data := sum over ranks (in place, device pointer, stream-ordered)
+  virtual void allreduce_sum(void* data, std::int64_t count, DType t, cudaStream_t s) = 0;
+  // data := max over ranks
+  virtual void allreduce_max(void* data, std::int64_t count, DType t, cudaStream_t s) = 0;
+};
+
+class SelfComm final : public Comm {
+ public:
+  int rank() const override { return 0; }
+  int size() const override { return 1; }
+  void allreduce_sum(void*, std::int64_t, DType, cudaStream_t) override {}
+  void allreduce_max(void*, std::int64_t, DType, cudaStream_t) override {}
+};
+
+// Shared state of an in-process group of K ranks.
+class Group {
+ public:
+  Group(int k, std::vector<int> devices, std::chrono::milliseconds timeout = std::chrono::milliseconds(600000));
+  ~Group();
+  int size() const { return k_; }
+  int device_of(int rank) const { return devices_[static_cast<std::size_t>(rank)]; }
+
+  void allreduce(int rank, void* data, std::int64_t count, DType t, bool is_max, cudaStream_t s);
+  void abort(const std::string& why);
+  bool aborted() const;
+
+ private:
+  struct Slot {
+    void* ptr = nullptr;
+    std::int64_t count = 0;
+    int kind = 0;  // dtype * 2 + is_max
+    std::uint64_t seq = 0;
+  };
+  void rendezvous(int rank);
+  void validate(int rank, std::int64_t count, int kind);
+  void* scratch(int rank, std::size_t bytes);
+
+  int k_;
+  std::vector<int> devices_;
+  std::chrono::milliseconds timeout_;
+  mutable std::mutex mu_;
+  std::condition_variable cv_;
+  int arrived_ = 0;
+  std::uint64_t gen_ = 0;
+  std::vector<bool> here_;
+  bool aborted_ = false;
+  std::string why_;
+  std::vector<Slot> slots_;
+  std::vector<std::uint64_t> seq_;
+  std::vector<cudaEvent_t> ready_, done_;
+  std::vector<void*> scratch_;
+  std::vector<std::size_t> scratch_bytes_;
+  std::vector<void**> dev_slots_;  // per rank: device array of K pointers
+};
+
+class GroupComm final : public Comm {
+ public:
+  GroupComm(Group* g, int rank) : g_(g), rank_(rank) {}
+  int rank() const override { return rank_; }
+  int size() const override { return g_->size(); }
+  void allreduce_sum(void* d, std::int64_t n, DType t, cudaStream_t s) override { g_->allreduce(rank_, d, n, t, false, s); }
+  void allreduce_max(void* d, std::int64_t n, DType t, cudaStream_t s) override { g_->allreduce(rank_, d, n, t, true, s); }
+
+ private:
+  Group* g_;
+  int rank_;
+};
+
+class NcclComm final : public Comm {
+ public:
+  NcclComm(int rank, int nranks, const unsigned char* id128);
+  ~NcclComm() override;
+  int rank() const override { return rank_; }
+  int size() const override { return size_; }
+  void allreduce_sum(void* d, std::int64_t n, DType t, cudaStream_t s) override;
+  void allreduce_max(void* d, std::int64_t n, DType t, cudaStream_t s) override;
+
+ private:
+  ncclComm_t comm_ = nullptr;
+  int rank_, size_;
+};
+
+}  // namespace dbag

@@ -1,0 +1,747 @@
+// kernels.cuh — the sm_100a kernels of the LM inner loop.
+//
+// Layout (per rank):
+//   slot s        : point-major position of shard edge pt_blk[s]
+//                   (dba/block_matrix.hpp:309-320 grouping); slot_* arrays are
+//                   SoA and streamed coalesced.
+//   cslot c       : camera-major position (cam_blk order); cslot_pslot maps it
+//                   to the point-major slot.
+//   E_pm / E_cm   : the 9x3 coupling blocks (dba/block_matrix.hpp:174-329),
+//                   SoA by element (27 lanes x N), in slot / cslot order.
+//   Jb            : per-slot residual + 2x12 Jacobian + weight, AoS of 28.
+//   cameras       : global ids, 9m vectors, 81m blocks (replicated).
+//   points        : local ids (first appearance), 3 n_loc vectors.
+// Reductions that feed LM / PCG decisions are deterministic: fixed grid,
+// fixed per-thread order, fixed shuffle tree, and a last-block finalize that
+// sums per-block partials in block order.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "jets.cuh"
+
+namespace dbag {
+namespace dev {
+
+constexpr int kTile = 128;        // point-pass tile (slots) == block size
+constexpr int kRedThreads = 256;  // reduction kernels' block size
+constexpr int kRedBlocksMax = 592;  // 4 x 148 SMs
+
+struct SumOp {
+  __device__ static double id() { return 0.0; }
+  __device__ static double op(double a, double b) { return a + b; }
+};
+struct MaxOp {
+  __device__ static double id() { return 0.0; }  // used on |x| >= 0
+  __device__ static double op(double a, double b) { return fmax(a, b); }
+};
+
+template <class Op>
+__device__ __forceinline__ double warp_reduce(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = Op::op(v, __shfl_down_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// Block reduction, result valid in thread 0. smem: >= blockDim/32 doubles.
+template <class Op>
+__device__ __forceinline__ double block_reduce(double v, double* smem) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+  v = warp_reduce<Op>(v);
+  __syncthreads();
+  if (lane == 0) smem[warp] = v;
+  __syncthreads();
+  if (warp == 0) {
+    v = lane < nw ? smem[lane] : Op::id();
+    v = warp_reduce<Op>(v);
+  }
+  return v;
+}
+
+// Grid-wide deterministic reduction of NV values: every block calls this
+// once; the last block to arrive reduces the per-block partials in block
+// order and writes out[0..NV). Returns true in the finalizing block (all
+// threads), after out[] is written and visible to that block.
+template <class Op, int NV>
+__device__ __forceinline__ bool grid_reduce(const double (&v)[NV], double* partials, unsigned* counter,
+                                            double* out) {
+  __shared__ double red[32];
+  __shared__ bool last;
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    const double b = block_reduce<Op>(v[k], red);
+    if (threadIdx.x == 0) partials[k * gridDim.x + blockIdx.x] = b;
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = (atomicAdd(counter, 1u) == gridDim.x - 1);
+  __syncthreads();
+  if (!last) return false;
+  __threadfence();
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    double acc = Op::id();
+    for (unsigned i = threadIdx.x; i < gridDim.x; i += blockDim.x) acc = Op::op(acc, __ldcg(partials + k * gridDim.x + i));
+    acc = block_reduce<Op>(acc, red);
+    if (threadIdx.x == 0) out[k] = acc;
+  }
+  if (threadIdx.x == 0) *counter = 0u;
+  __threadfence();
+  __syncthreads();
+  return true;
+}
+
+struct RedWs {  // per-launch scratch of the grid reductions
+  double* partials;   // >= 8 * kRedBlocksMax
+  unsigned* counter;  // zero-initialized
+};
+
+// ---------------------------------------------------------------- cost ----
+// EdgeEvaluator::cost (dba/edge_eval.hpp:289-309): sum w |r|^2 with the
+// squared norm in Scalar and the accumulation in double. Degenerate depth ->
+// +inf and atomicMin of the global edge id.
+template <class S>
+__global__ void __launch_bounds__(kRedThreads) k_cost(std::int64_t N, const std::int32_t* __restrict__ slot_cam,
+                                                      const std::int32_t* __restrict__ slot_pt,
+                                                      const std::int32_t* __restrict__ slot_edge,
+                                                      std::int64_t edge_base, const S* __restrict__ px,
+                                                      const S* __restrict__ py, const S* __restrict__ w,
+                                                      const S* __restrict__ xc, const S* __restrict__ xp,
+                                                      RedWs ws, double* out_cost, unsigned long long* bad_edge) {
+  double acc = 0.0;
+  bool bad = false;
+  for (std::int64_t s = blockIdx.x * std::int64_t(blockDim.x) + threadIdx.x; s < N;
+       s += std::int64_t(gridDim.x) * blockDim.x) {
+    const S* cam = xc + std::size_t(slot_cam[s]) * 9;
+    const S* x = xp + std::size_t(slot_pt[s]) * 3;
+    S c[9], X[3], r[2];
+#pragma unroll
+    for (int k = 0; k < 9; ++k) c[k] = cam[k];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) X[k] = x[k];
+    if (edge_residual(c, X, px[s], py[s], r)) {
+      acc += double(w[s]) * double(r[0] * r[0] + r[1] * r[1]);
+    } else {
+      bad = true;
+      atomicMin(bad_edge, (unsigned long long)(edge_base + slot_edge[s]));
+    }
+  }
+  const double v[2] = {acc, bad ? 1.0 : 0.0};
+  __shared__ double fin[2];
+  if (grid_reduce<SumOp, 2>(v, ws.partials, ws.counter, fin)) {
+    if (threadIdx.x == 0) *out_cost = fin[1] > 0 ? __longlong_as_double(0x7ff0000000000000LL) : fin[0];
+  }
+}
+
+// ---------------------------------------------------------- linearize ----
+// Fused K1+K2(+K3)+K5-E: gather, jets (or closed form), residual, Jacobian,
+// E = w Jc^T Jp. Jb row: [r0 r1 | J0[12] | J1[12] | w pad].
+template <class S, int MODE>
+__global__ void __launch_bounds__(128) k_linearize(std::int64_t N, const std::int32_t* __restrict__ slot_cam,
+                                                   const std::int32_t* __restrict__ slot_pt,
+                                                   const std::int32_t* __restrict__ slot_edge,
+                                                   std::int64_t edge_base, const S* __restrict__ px,
+                                                   const S* __restrict__ py, const S* __restrict__ w,
+                                                   const S* __restrict__ xc, const S* __restrict__ xp,
+                                                   S* __restrict__ Jb, S* __restrict__ E,
+                                                   unsigned long long* bad_edge) {
+  const std::int64_t s = blockIdx.x * std::int64_t(blockDim.x) + threadIdx.x;
+  if (s >= N) return;
+  const S* cam = xc + std::size_t(slot_cam[s]) * 9;
+  const S* x = xp + std::size_t(slot_pt[s]) * 3;
+  S c[9], X[3], r[2], J[2][12];
+#pragma unroll
+  for (int k = 0; k < 9; ++k) c[k] = cam[k];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) X[k] = x[k];
+  const bool ok = MODE == 0 ? edge_autodiff(c, X, px[s], py[s], r, J) : edge_analytic(c, X, px[s], py[s], r, J);
+  if (!ok) {
+    atomicMin(bad_edge, (unsigned long long)(edge_base + slot_edge[s]));
+    return;
+  }
+  const S wt = w[s];
+  S* row = Jb + std::size_t(s) * 28;
+  row[0] = r[0];
+  row[1] = r[1];
+#pragma unroll
+  for (int j = 0; j < 12; ++j) {
+    row[2 + j] = J[0][j];
+    row[14 + j] = J[1][j];
+  }
+  row[26] = wt;
+  row[27] = S(0);
+#pragma unroll
+  for (int i = 0; i < 9; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) E[std::size_t(i * 3 + j) * N + s] = wt * (J[0][i] * J[0][9 + j] + J[1][i] * J[1][9 + j]);
+}
+
+// C[p] += w Jp^T Jp, w[p] -= w Jp^T r over the point's slots in edge order
+// (dba/block_matrix.hpp:382-386). Thread per local point.
+template <class S>
+__global__ void k_assemble_points(std::int32_t n_loc, const std::int32_t* __restrict__ pt_ptr,
+                                  const S* __restrict__ Jb, S* __restrict__ C, S* __restrict__ wv) {
+  const std::int32_t p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n_loc) return;
+  S c[3][3] = {}, g[3] = {};
+  for (std::int32_t s = pt_ptr[p]; s < pt_ptr[p + 1]; ++s) {
+    const S* row = Jb + std::size_t(s) * 28;
+    const S r0 = row[0], r1 = row[1], wt = row[26];
+    S jp0[3], jp1[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      jp0[k] = row[2 + 9 + k];
+      jp1[k] = row[14 + 9 + k];
+    }
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+#pragma unroll
+      for (int j = 0; j < 3; ++j) c[i][j] += wt * (jp0[i] * jp0[j] + jp1[i] * jp1[j]);
+      g[i] -= wt * (jp0[i] * r0 + jp1[i] * r1);
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+#pragma unroll
+    for (int j = 0; j < 3; ++j) C[std::size_t(p) * 9 + i * 3 + j] = c[i][j];
+    wv[std::size_t(p) * 3 + i] = g[i];
+  }
+}
+
+// B[c] += w Jc^T Jc, v[c] -= w Jc^T r (dba/block_matrix.hpp:378-385), one CTA
+// per local camera over its camera-major slots; also builds E_cm by copying
+// E_pm (bitwise-identical coupling blocks in both orders).
+template <class S, int NT>
+__global__ void __launch_bounds__(NT) k_assemble_cameras(const std::int32_t* __restrict__ cam_ptr,
+                                                         const std::int32_t* __restrict__ cam_glob,
+                                                         const std::int32_t* __restrict__ cslot_pslot,
+                                                         const S* __restrict__ Jb, std::int64_t N,
+                                                         const S* __restrict__ E_pm, S* __restrict__ E_cm,
+                                                         S* __restrict__ B, S* __restrict__ v) {
+  const std::int32_t lc = blockIdx.x;
+  double acc[54];  // 45 upper-triangular B entries + 9 v entries
+#pragma unroll
+  for (int k = 0; k < 54; ++k) acc[k] = 0.0;
+  for (std::int32_t cs = cam_ptr[lc] + threadIdx.x; cs < cam_ptr[lc + 1]; cs += NT) {
+    const std::int32_t ps = cslot_pslot[cs];
+    const S* row = Jb + std::size_t(ps) * 28;
+    S jc0[9], jc1[9];
+#pragma unroll
+    for (int k = 0; k < 9; ++k) {
+      jc0[k] = row[2 + k];
+      jc1[k] = row[14 + k];
+    }
+    const S r0 = row[0], r1 = row[1], wt = row[26];
+    int q = 0;
+#pragma unroll
+    for (int i = 0; i < 9; ++i)
+#pragma unroll
+      for (int j = i; j < 9; ++j) acc[q++] += double(wt * (jc0[i] * jc0[j] + jc1[i] * jc1[j]));
+#pragma unroll
+    for (int i = 0; i < 9; ++i) acc[45 + i] -= double(wt * (jc0[i] * r0 + jc1[i] * r1));
+#pragma unroll
+    for (int k = 0; k < 27; ++k) E_cm[std::size_t(k) * N + cs] = E_pm[std::size_t(k) * N + ps];
+  }
+  __shared__ double red[32];
+  const std::int32_t cg = cam_glob[lc];
+  int q = 0;
+  double out[54];
+#pragma unroll
+  for (int k = 0; k < 54; ++k) out[k] = block_reduce<SumOp>(acc[k], red);
+  if (threadIdx.x == 0) {
+    S* b = B + std::size_t(cg) * 81;
+#pragma unroll
+    for (int i = 0; i < 9; ++i)
+#pragma unroll
+      for (int j = i; j < 9; ++j) {
+        b[i * 9 + j] = S(out[q]);
+        b[j * 9 + i] = S(out[q]);
+        ++q;
+      }
+#pragma unroll
+    for (int i = 0; i < 9; ++i) v[std::size_t(cg) * 9 + i] = S(out[45 + i]);
+  }
+}
+
+// ------------------------------------------------------ damp + factor ----
+// damp_into (dba/block_matrix.hpp:86-99) + per-block LLT that fails on a
+// pivot <= 0 (Eigen llt_inplace::unblocked semantics, :123-134) + explicit
+// inverse L^-T L^-1 for the GEMV-style block solves. Thread per block.
+template <class S, int BS>
+__global__ void k_damp_factor(std::int64_t nb, const S* __restrict__ A, S lambda, int policy, S* __restrict__ Ad,
+                              S* __restrict__ Ainv, const std::int32_t* __restrict__ index_map,
+                              unsigned long long* bad) {
+  const std::int64_t i = blockIdx.x * std::int64_t(blockDim.x) + threadIdx.x;
+  if (i >= nb) return;
+  S m[BS][BS];
+  const S* a = A + std::size_t(i) * BS * BS;
+#pragma unroll
+  for (int r = 0; r < BS; ++r)
+#pragma unroll
+    for (int c = 0; c < BS; ++c) m[r][c] = a[r * BS + c];
+#pragma unroll
+  for (int j = 0; j < BS; ++j) {
+    if (policy == 0) {
+      m[j][j] += lambda;
+    } else {
+      const S d = m[j][j];
+      const S cl = fmin(S(1e32), fmax(S(1e-6), d));
+      m[j][j] += lambda * cl;
+    }
+  }
+  S* ad = Ad + std::size_t(i) * BS * BS;
+#pragma unroll
+  for (int r = 0; r < BS; ++r)
+#pragma unroll
+    for (int c = 0; c < BS; ++c) ad[r * BS + c] = m[r][c];
+  // Cholesky, lower factor in m's lower triangle
+  bool ok = true;
+#pragma unroll
+  for (int k = 0; k < BS; ++k) {
+    S x = m[k][k];
+    if (k > 0) {
+      S sq = S(0);
+#pragma unroll
+      for (int j = 0; j < k; ++j) sq += m[k][j] * m[k][j];
+      x -= sq;
+    }
+    if (!(x > S(0)) && !(x != x)) {  // x <= 0 fails; NaN passes (Eigen)
+      ok = false;
+      break;
+    }
+    x = sqrt(x);
+    m[k][k] = x;
+#pragma unroll
+    for (int r = k + 1; r < BS; ++r) {
+      S acc = m[r][k];
+#pragma unroll
+      for (int j = 0; j < k; ++j) acc -= m[r][j] * m[k][j];
+      m[r][k] = acc / x;
+    }
+  }
+  if (!ok) {
+    atomicMin(bad, (unsigned long long)(index_map ? index_map[i] : i));
+    return;
+  }
+  // L^-1 (lower) by forward substitution, stored in the upper triangle's
+  // mirror: li[r][c] for c <= r.
+  S li[BS][BS];
+#pragma unroll
+  for (int c = 0; c < BS; ++c) {
+#pragma unroll
+    for (int r = 0; r < BS; ++r) {
+      if (r < c) {
+        li[r][c] = S(0);
+      } else {
+        S acc = (r == c) ? S(1) : S(0);
+#pragma unroll
+        for (int k = c; k < r; ++k) acc -= m[r][k] * li[k][c];
+        li[r][c] = acc / m[r][r];
+      }
+    }
+  }
+  S* ai = Ainv + std::size_t(i) * BS * BS;
+#pragma unroll
+  for (int r = 0; r < BS; ++r)
+#pragma unroll
+    for (int c = r; c < BS; ++c) {
+      S acc = S(0);
+#pragma unroll
+      for (int k = c; k < BS; ++k) acc += li[k][r] * li[k][c];
+      ai[r * BS + c] = acc;
+      ai[c * BS + r] = acc;
+    }
+}
+
+// --------------------------------------------------------- point pass ----
+// Tile = whole points (<= kTile slots, or one long point). Thread per slot
+// computes a_s = E_s^T x[cam_s]; the tile's points sum their slots' partials
+// in slot (edge) order from shared memory, then finish per MODE:
+//   MODE 0 (DSE):     b_p = C_p^-1 a_p                (dba/solver.hpp:159-162)
+//   MODE 1 (backsub): dx_p = C_p^-1 (w_p - a_p)       (dba/solver.hpp:371-376)
+// Shared (halo) points store a_p into the halo buffer instead; the finish is
+// applied after the halo all-reduce by k_halo_finish.
+template <class S, int MODE>
+__global__ void __launch_bounds__(kTile) k_point_pass(std::int64_t N, const std::int32_t* __restrict__ tile_pt,
+                                                      const std::int32_t* __restrict__ pt_ptr,
+                                                      const std::int32_t* __restrict__ slot_cam,
+                                                      const S* __restrict__ E, const S* __restrict__ xcam,
+                                                      const S* __restrict__ Cinv, const S* __restrict__ wv,
+                                                      const std::int32_t* __restrict__ halo_of,
+                                                      S* __restrict__ halo_buf, S* __restrict__ out) {
+  __shared__ S part[kTile][3];
+  const std::int32_t p0 = tile_pt[blockIdx.x], p1 = tile_pt[blockIdx.x + 1];
+  const std::int32_t s0 = pt_ptr[p0], s1 = pt_ptr[p1];
+  S a[3] = {S(0), S(0), S(0)};
+  for (std::int32_t s = s0 + threadIdx.x; s < s1; s += kTile) {
+    const S* xc = xcam + std::size_t(slot_cam[s]) * 9;
+    S x[9];
+#pragma unroll
+    for (int i = 0; i < 9; ++i) x[i] = xc[i];
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      S acc = S(0);
+#pragma unroll
+      for (int i = 0; i < 9; ++i) acc += E[std::size_t(i * 3 + j) * N + s] * x[i];
+      a[j] += acc;
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < 3; ++j) part[threadIdx.x][j] = a[j];
+  __syncthreads();
+  const std::int32_t np = p1 - p0;
+  if (int(threadIdx.x) >= np) return;
+  const std::int32_t p = p0 + threadIdx.x;
+  S t[3] = {S(0), S(0), S(0)};
+  if (s1 - s0 > kTile) {  // one long point: partials of all threads, thread order
+    for (int k = 0; k < kTile; ++k)
+#pragma unroll
+      for (int j = 0; j < 3; ++j) t[j] += part[k][j];
+  } else {
+    for (std::int32_t s = pt_ptr[p]; s < pt_ptr[p + 1]; ++s)
+#pragma unroll
+      for (int j = 0; j < 3; ++j) t[j] += part[s - s0][j];
+  }
+  const std::int32_t h = halo_of ? halo_of[p] : -1;
+  if (h >= 0) {
+#pragma unroll
+    for (int j = 0; j < 3; ++j) halo_buf[std::size_t(h) * 3 + j] = t[j];
+    return;
+  }
+  if (MODE == 1) {
+#pragma unroll
+    for (int j = 0; j < 3; ++j) t[j] = wv[std::size_t(p) * 3 + j] - t[j];
+  }
+  const S* ci = Cinv + std::size_t(p) * 9;
+#pragma unroll
+  for (int r = 0; r < 3; ++r) out[std::size_t(p) * 3 + r] = (ci[r * 3 + 0] * t[0] + ci[r * 3 + 1] * t[1]) + ci[r * 3 + 2] * t[2];
+}
+
+// Finish of k_point_pass for halo points after the all-reduce.
+template <class S, int MODE>
+__global__ void k_halo_finish(std::int32_t n, const std::int32_t* __restrict__ lpts,
+                              const std::int32_t* __restrict__ hidx, const S* __restrict__ halo_buf,
+                              const S* __restrict__ Cinv, const S* __restrict__ wv, S* __restrict__ out) {
+  const std::int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const std::int32_t p = lpts[i];
+  S t[3];
+#pragma unroll
+  for (int j = 0; j < 3; ++j) t[j] = halo_buf[std::size_t(hidx[i]) * 3 + j];
+  if (MODE == 1)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) t[j] = wv[std::size_t(p) * 3 + j] - t[j];
+  const S* ci = Cinv + std::size_t(p) * 9;
+#pragma unroll
+  for (int r = 0; r < 3; ++r) out[std::size_t(p) * 3 + r] = (ci[r * 3 + 0] * t[0] + ci[r * 3 + 1] * t[1]) + ci[r * 3 + 2] * t[2];
+}
+
+// b_p = C_p^-1 w_p for the right-hand side (dba/solver.hpp:358).
+template <class S>
+__global__ void k_point_solve(std::int32_t n, const S* __restrict__ Cinv, const S* __restrict__ wv,
+                              S* __restrict__ out) {
+  const std::int32_t p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  const S* ci = Cinv + std::size_t(p) * 9;
+  const S t0 = wv[std::size_t(p) * 3], t1 = wv[std::size_t(p) * 3 + 1], t2 = wv[std::size_t(p) * 3 + 2];
+#pragma unroll
+  for (int r = 0; r < 3; ++r) out[std::size_t(p) * 3 + r] = (ci[r * 3 + 0] * t0 + ci[r * 3 + 1] * t1) + ci[r * 3 + 2] * t2;
+}
+
+// Halo scatter / gather of W-wide point records.
+template <class S, int W>
+__global__ void k_halo_scatter(std::int32_t n, const std::int32_t* __restrict__ lpts,
+                               const std::int32_t* __restrict__ hidx, const S* __restrict__ src,
+                               S* __restrict__ halo) {
+  const std::int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+#pragma unroll
+  for (int k = 0; k < W; ++k) halo[std::size_t(hidx[i]) * W + k] = src[std::size_t(lpts[i]) * W + k];
+}
+template <class S, int W>
+__global__ void k_halo_gather(std::int32_t n, const std::int32_t* __restrict__ lpts,
+                              const std::int32_t* __restrict__ hidx, const S* __restrict__ halo,
+                              S* __restrict__ dst) {
+  const std::int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+#pragma unroll
+  for (int k = 0; k < W; ++k) dst[std::size_t(lpts[i]) * W + k] = halo[std::size_t(hidx[i]) * W + k];
+}
+
+// -------------------------------------------------------- camera pass ----
+// c_c = sum over the camera's cslots of E_s b[pt_s] (dba/block_matrix.hpp:
+// 265-289), one CTA per local camera, written to the full 9m vector.
+template <class S, int NT>
+__global__ void __launch_bounds__(NT) k_cam_pass(const std::int32_t* __restrict__ cam_ptr,
+                                                 const std::int32_t* __restrict__ cam_glob,
+                                                 const std::int32_t* __restrict__ cslot_pt, std::int64_t N,
+                                                 const S* __restrict__ E, const S* __restrict__ bpt,
+                                                 S* __restrict__ out) {
+  const std::int32_t lc = blockIdx.x;
+  S acc[9];
+#pragma unroll
+  for (int i = 0; i < 9; ++i) acc[i] = S(0);
+  for (std::int32_t cs = cam_ptr[lc] + threadIdx.x; cs < cam_ptr[lc + 1]; cs += NT) {
+    const S* b = bpt + std::size_t(cslot_pt[cs]) * 3;
+    const S b0 = b[0], b1 = b[1], b2 = b[2];
+#pragma unroll
+    for (int i = 0; i < 9; ++i)
+      acc[i] += (E[std::size_t(i * 3) * N + cs] * b0 + E[std::size_t(i * 3 + 1) * N + cs] * b1) +
+                E[std::size_t(i * 3 + 2) * N + cs] * b2;
+  }
+  __shared__ double red[32];
+  const std::int32_t cg = cam_glob[lc];
+#pragma unroll
+  for (int i = 0; i < 9; ++i) {
+    const double t = block_reduce<SumOp>(double(acc[i]), red);
+    if (threadIdx.x == 0) out[std::size_t(cg) * 9 + i] = S(t);
+  }
+}
+
+// -------------------------------------------------------- camera space ----
+// PCG scalars kept on the device so the recurrences never round-trip.
+template <class S>
+struct PcgScal {
+  double rho, rho_prev, pq, rnorm2, rhs_norm2;
+  double dot_a, dot_b, dot_c;  // generic reduction outputs
+  S alpha, beta;
+  int status;  // bit 1: rho breakdown, bit 2: pq breakdown
+  int n;
+};
+
+// q = Bd x - c, and p.q in double when PQ (dba/solver.hpp:166-167, 238).
+template <class S, bool PQ>
+__global__ void __launch_bounds__(kRedThreads) k_cam_epilogue(std::int32_t m, const S* __restrict__ Bd,
+                                                              const S* __restrict__ x, const S* __restrict__ c,
+                                                              S* __restrict__ q, RedWs ws, PcgScal<S>* sc) {
+  double acc = 0.0;
+  for (std::int32_t cam = blockIdx.x * blockDim.x + threadIdx.x; cam < m; cam += gridDim.x * blockDim.x) {
+    const S* b = Bd + std::size_t(cam) * 81;
+    S xv[9];
+#pragma unroll
+    for (int k = 0; k < 9; ++k) xv[k] = x[std::size_t(cam) * 9 + k];
+#pragma unroll
+    for (int r = 0; r < 9; ++r) {
+      S s = S(0);
+#pragma unroll
+      for (int k = 0; k < 9; ++k) s += b[r * 9 + k] * xv[k];
+      const S qv = s - c[std::size_t(cam) * 9 + r];
+      q[std::size_t(cam) * 9 + r] = qv;
+      if (PQ) acc += double(xv[r]) * double(qv);
+    }
+  }
+  if (PQ) {
+    const double v[1] = {acc};
+    __shared__ double fin[1];
+    if (grid_reduce<SumOp, 1>(v, ws.partials, ws.counter, fin)) {
+      if (threadIdx.x == 0) {
+        const double pq = fin[0];
+        sc->pq = pq;
+        if (!(pq > 0.0) || isinf(pq)) sc->status |= 2;
+        sc->alpha = S(sc->rho / pq);
+      }
+    }
+  }
+}
+
+// z = B^-1 r, rho = r.z; beta = (S)(rho / rho_prev) (dba/solver.hpp:224-236).
+template <class S>
+__global__ void __launch_bounds__(kRedThreads) k_pcg_precond(std::int32_t m, const S* __restrict__ Binv,
+                                                             const S* __restrict__ r, S* __restrict__ z, RedWs ws,
+                                                             PcgScal<S>* sc) {
+  double acc = 0.0;
+  for (std::int32_t cam = blockIdx.x * blockDim.x + threadIdx.x; cam < m; cam += gridDim.x * blockDim.x) {
+    const S* b = Binv + std::size_t(cam) * 81;
+    S rv[9];
+#pragma unroll
+    for (int k = 0; k < 9; ++k) rv[k] = r[std::size_t(cam) * 9 + k];
+#pragma unroll
+    for (int i = 0; i < 9; ++i) {
+      S s = S(0);
+#pragma unroll
+      for (int k = 0; k < 9; ++k) s += b[i * 9 + k] * rv[k];
+      z[std::size_t(cam) * 9 + i] = s;
+      acc += double(rv[i]) * double(s);
+    }
+  }
+  const double v[1] = {acc};
+  __shared__ double fin[1];
+  if (grid_reduce<SumOp, 1>(v, ws.partials, ws.counter, fin)) {
+    if (threadIdx.x == 0) {
+      const double rho = fin[0];
+      sc->rho = rho;
+      if (!(rho > 0.0) || isinf(rho)) sc->status |= 1;
+      sc->beta = sc->n == 0 ? S(0) : S(rho / sc->rho_prev);
+    }
+  }
+}
+
+// p = z (n == 0) or z + beta p.
+template <class S>
+__global__ void k_pcg_p(std::int64_t len, const S* __restrict__ z, S* __restrict__ p, const PcgScal<S>* sc) {
+  const std::int64_t i = blockIdx.x * std::int64_t(blockDim.x) + threadIdx.x;
+  if (i >= len) return;
+  if (sc->n == 0) p[i] = z[i];
+  else p[i] = z[i] + sc->beta * p[i];
+}
+
+// x += alpha p; if UPD_R: r -= alpha q and |r|^2 (dba/solver.hpp:243-254).
+template <class S, bool UPD_R>
+__global__ void __launch_bounds__(kRedThreads) k_pcg_xr(std::int64_t len, const S* __restrict__ p,
+                                                        const S* __restrict__ q, S* __restrict__ x,
+                                                        S* __restrict__ r, RedWs ws, PcgScal<S>* sc) {
+  const S alpha = sc->alpha;
+  double acc = 0.0;
+  for (std::int64_t i = blockIdx.x * std::int64_t(blockDim.x) + threadIdx.x; i < len;
+       i += std::int64_t(gridDim.x) * blockDim.x) {
+    x[i] += alpha * p[i];
+    if (UPD_R) {
+      const S rv = r[i] - alpha * q[i];
+      r[i] = rv;
+      acc += double(rv) * double(rv);
+    }
+  }
+  if (UPD_R) {
+    const double v[1] = {acc};
+    __shared__ double fin[1];
+    if (grid_reduce<SumOp, 1>(v, ws.partials, ws.counter, fin)) {
+      if (threadIdx.x == 0) {
+        sc->rnorm2 = fin[0];
+        sc->rho_prev = sc->rho;
+        sc->n += 1;
+      }
+    }
+  } else if (blockIdx.x == 0 && threadIdx.x == 0) {
+    // counter bookkeeping done by the refresh kernel
+  }
+}
+
+// r = g - q and |r|^2 (the every-50 refresh, and the start r = g - S x0).
+template <class S>
+__global__ void __launch_bounds__(kRedThreads) k_pcg_refresh(std::int64_t len, const S* __restrict__ g,
+                                                             const S* __restrict__ q, S* __restrict__ r, RedWs ws,
+                                                             PcgScal<S>* sc, int bump) {
+  double acc = 0.0;
+  for (std::int64_t i = blockIdx.x * std::int64_t(blockDim.x) + threadIdx.x; i < len;
+       i += std::int64_t(gridDim.x) * blockDim.x) {
+    const S rv = g[i] - q[i];
+    r[i] = rv;
+    acc += double(rv) * double(rv);
+  }
+  const double v[1] = {acc};
+  __shared__ double fin[1];
+  if (grid_reduce<SumOp, 1>(v, ws.partials, ws.counter, fin)) {
+    if (threadIdx.x == 0) {
+      sc->rnorm2 = fin[0];
+      if (bump) {
+        sc->rho_prev = sc->rho;
+        sc->n += 1;
+      }
+    }
+  }
+}
+
+// Generic double dot of two S vectors into sc->dot_a.
+template <class S>
+__global__ void __launch_bounds__(kRedThreads) k_dot(std::int64_t len, const S* __restrict__ a,
+                                                     const S* __restrict__ b, RedWs ws, double* out) {
+  double acc = 0.0;
+  for (std::int64_t i = blockIdx.x * std::int64_t(blockDim.x) + threadIdx.x; i < len;
+       i += std::int64_t(gridDim.x) * blockDim.x)
+    acc += double(a[i]) * double(b[i]);
+  const double v[1] = {acc};
+  __shared__ double fin[1];
+  if (grid_reduce<SumOp, 1>(v, ws.partials, ws.counter, fin))
+    if (threadIdx.x == 0) *out = fin[0];
+}
+
+// out = a - b.
+template <class S>
+__global__ void k_sub(std::int64_t len, const S* __restrict__ a, const S* __restrict__ b, S* __restrict__ out) {
+  const std::int64_t i = blockIdx.x * std::int64_t(blockDim.x) + threadIdx.x;
+  if (i < len) out[i] = a[i] - b[i];
+}
+
+// ---------------------------------------------------------- trial / model ----
+// trial = x + dx, and the model terms of dba/solver.hpp:383-410 over one
+// parameter block family: out[0] = max |dx|, out[1] = damping sum
+// (identity: sum dx^2, scaled by lambda on the host; diag_scaled:
+// sum lambda clamp(D_jj) dx^2), out[2] = dx . grad. BS = 9 (cameras, all
+// entries) or 3 (local points, owned ones only for the sums).
+template <class S, int BS>
+__global__ void __launch_bounds__(kRedThreads) k_trial(std::int32_t nb, const S* __restrict__ x,
+                                                       const S* __restrict__ dx, S* __restrict__ xt,
+                                                       const S* __restrict__ D, const S* __restrict__ grad,
+                                                       const std::uint8_t* __restrict__ owned, double lambda,
+                                                       int policy, RedWs ws, double* out) {
+  double smax = 0.0, damp = 0.0, gv = 0.0;
+  for (std::int32_t b = blockIdx.x * blockDim.x + threadIdx.x; b < nb; b += gridDim.x * blockDim.x) {
+    const bool own = owned ? owned[b] != 0 : true;
+#pragma unroll
+    for (int k = 0; k < BS; ++k) {
+      const std::size_t i = std::size_t(b) * BS + k;
+      const S d = dx[i];
+      xt[i] = x[i] + d;
+      if (own) {
+        const double dd = double(d);
+        smax = fmax(smax, fabs(dd));
+        if (policy == 0) {
+          damp += dd * dd;
+        } else {
+          const S djj = D[std::size_t(b) * BS * BS + k * BS + k];
+          const S cl = fmin(S(1e32), fmax(S(1e-6), djj));
+          damp += lambda * double(cl) * dd * dd;
+        }
+        gv += dd * double(grad[i]);
+      }
+    }
+  }
+  __shared__ double red[32];
+  __shared__ bool last;
+  const double bm = block_reduce<MaxOp>(smax, red);
+  const double bd = block_reduce<SumOp>(damp, red);
+  const double bg = block_reduce<SumOp>(gv, red);
+  if (threadIdx.x == 0) {
+    ws.partials[blockIdx.x] = bm;
+    ws.partials[gridDim.x + blockIdx.x] = bd;
+    ws.partials[2 * gridDim.x + blockIdx.x] = bg;
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = (atomicAdd(ws.counter, 1u) == gridDim.x - 1);
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  double m0 = 0.0, s1 = 0.0, s2 = 0.0;
+  for (unsigned i = threadIdx.x; i < gridDim.x; i += blockDim.x) {
+    m0 = fmax(m0, __ldcg(ws.partials + i));
+    s1 += __ldcg(ws.partials + gridDim.x + i);
+    s2 += __ldcg(ws.partials + 2 * gridDim.x + i);
+  }
+  m0 = block_reduce<MaxOp>(m0, red);
+  s1 = block_reduce<SumOp>(s1, red);
+  s2 = block_reduce<SumOp>(s2, red);
+  if (threadIdx.x == 0) {
+    out[0] = m0;
+    out[1] = s1;
+    out[2] = s2;
+    *ws.counter = 0u;
+  }
+}
+
+// Ascending-rank sum of K deposited buffers (WorkerGroup::allreduce_sum,
+// dba/comms.hpp:76-81): out = ((s0 + s1) + s2) + ...
+template <class T>
+__global__ void k_sum_slots(std::int64_t len, int k, const T* const* __restrict__ slots, T* __restrict__ out) {
+  for (std::int64_t i = blockIdx.x * std::int64_t(blockDim.x) + threadIdx.x; i < len;
+       i += std::int64_t(gridDim.x) * blockDim.x) {
+    T acc = slots[0][i];
+    for (int r = 1; r < k; ++r) acc += slots[r][i];
+    out[i] = acc;
+  }
+}
+
+}  // namespace dev
+}  // namespace dbag

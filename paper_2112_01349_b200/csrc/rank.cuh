@@ -1,0 +1,774 @@
+// rank.cuh — one rank's device context: the shard, the normal equations and
+// the operators of the LM inner loop, each a short sequence of sm_100a kernel
+// launches on the rank's stream. The host LM loop (solver.cuh) drives it.
+//
+// Operator map (reference symbol -> method):
+//   EdgeEvaluator::cost + detail::distributed_cost   cost()          dba/edge_eval.hpp:289, dba/solver.hpp:264
+//   linearize + assemble_local + 4 all-reduces       linearize()     dba/solver.hpp:330-340
+//   damp_into + FactoredBlockDiagonal::factor        damp_factor()   dba/solver.hpp:350-355
+//   g = v - allreduce(E_k C^-1 w)                    rhs()           dba/solver.hpp:357-363
+//   dse                                              dse()           dba/solver.hpp:149-181
+//   dpcg                                             pcg()           dba/solver.hpp:202-257
+//   back-substitution + trial + model terms          backsub_trial() dba/solver.hpp:371-410
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <limits>
+#include <memory>
+#include <vector>
+
+#include "comm.hpp"
+#include "common.hpp"
+#include "kernels.cuh"
+#include "partition.hpp"
+
+namespace dbag {
+
+template <class T>
+class DevBuf {
+ public:
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf() { release(); }
+  void alloc(std::size_t n) {
+    release();
+    n_ = n;
+    if (n) DBAG_CUDA(cudaMalloc(&p_, n * sizeof(T)));
+  }
+  void upload(const T* h, std::size_t n) {
+    alloc(n);
+    if (n) DBAG_CUDA(cudaMemcpy(p_, h, n * sizeof(T), cudaMemcpyHostToDevice));
+  }
+  void upload(const std::vector<T>& v) { upload(v.data(), v.size()); }
+  T* get() const { return p_; }
+  std::size_t size() const { return n_; }
+  void swap(DevBuf& o) {
+    std::swap(p_, o.p_);
+    std::swap(n_, o.n_);
+  }
+
+ private:
+  void release() {
+    if (p_) cudaFree(p_);
+    p_ = nullptr;
+    n_ = 0;
+  }
+  T* p_ = nullptr;
+  std::size_t n_ = 0;
+};
+
+inline int grid_for(std::int64_t n, int threads, int cap) {
+  const std::int64_t b = (n + threads - 1) / threads;
+  return static_cast<int>(std::max<std::int64_t>(1, std::min<std::int64_t>(b, cap)));
+}
+
+struct PcgOut {
+  int iterations = 0;
+  bool converged = false;
+};
+
+struct Tally {  // dba/counters.hpp:11-24
+  std::uint64_t edges = 0, block_ops = 0;
+};
+
+template <class S>
+class Rank {
+ public:
+  using Scal = dev::PcgScal<S>;
+  static constexpr DType kT = sizeof(S) == 8 ? DType::f64 : DType::f32;
+
+  Rank(int device, Comm* comm) : device_(device), comm_(comm) {
+    DBAG_CUDA(cudaSetDevice(device_));
+    DBAG_CUDA(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking));
+    DBAG_CUDA(cudaMallocHost(&hsc_, sizeof(Scal)));
+    DBAG_CUDA(cudaMallocHost(&hbuf_, 64 * sizeof(double)));
+    DBAG_CUDA(cudaEventCreate(&mark_[0]));
+    DBAG_CUDA(cudaEventCreate(&mark_[1]));
+    sc_.alloc(1);
+    red_part_.alloc(8 * dev::kRedBlocksMax);
+    red_cnt_.alloc(1);
+    DBAG_CUDA(cudaMemset(red_cnt_.get(), 0, sizeof(unsigned)));
+    dsc_.alloc(64);
+    bad_.alloc(4);
+  }
+  ~Rank() {
+    cudaSetDevice(device_);
+    cudaStreamSynchronize(st_);
+    for (auto e : prof_ev_) cudaEventDestroy(e);
+    cudaEventDestroy(mark_[0]);
+    cudaEventDestroy(mark_[1]);
+    cudaFreeHost(hsc_);
+    cudaFreeHost(hbuf_);
+    cudaStreamDestroy(st_);
+  }
+
+  cudaStream_t stream() const { return st_; }
+  int device() const { return device_; }
+  const ShardPlan& plan() const { return plan_; }
+  std::int64_t edges() const { return N_; }
+  Tally& tally() { return tally_; }
+  int last_dse_count() const { return dse_count_; }
+
+  // ------------------------------------------------------------ upload ----
+  void upload(const dbag_problem& p, int jac_mode) {
+    DBAG_CUDA(cudaSetDevice(device_));
+    if (p.num_cameras < 0 || p.num_points < 0 || p.num_observations < 0)
+      throw Error(DBAG_SHAPE, "negative problem dimensions");
+    for (std::int64_t e = 0; e < p.num_observations; ++e) {
+      if (p.camera_id[e] < 0 || p.camera_id[e] >= p.num_cameras)
+        throw Error(DBAG_INVALID_ARGUMENT, "edge references unknown camera " + std::to_string(p.camera_id[e]));
+      if (p.point_id[e] < 0 || p.point_id[e] >= p.num_points)
+        throw Error(DBAG_INVALID_ARGUMENT, "edge references unknown point " + std::to_string(p.point_id[e]));
+    }
+    jac_mode_ = jac_mode;
+    plan_ = plan_shard(p.camera_id, p.point_id, p.num_observations, p.num_cameras, p.num_points, comm_->size(),
+                       comm_->rank(), dev::kTile);
+    m_ = plan_.m;
+    n_glob_ = plan_.n;
+    n_loc_ = plan_.pts.size();
+    m_loc_ = plan_.cams.size();
+    N_ = plan_.range.count;
+    H_ = plan_.n_shared;
+    const std::int64_t base = plan_.range.start;
+    const S* px = static_cast<const S*>(p.pixel_x);
+    const S* py = static_cast<const S*>(p.pixel_y);
+    const S* wt = static_cast<const S*>(p.weight);
+    std::vector<std::int32_t> s_cam(N_), s_pt(N_), s_edge(N_);
+    std::vector<S> s_px(N_), s_py(N_), s_w(N_);
+    for (std::int64_t s = 0; s < N_; ++s) {
+      const std::int64_t e = plan_.pt_blk[static_cast<std::size_t>(s)];
+      s_edge[s] = static_cast<std::int32_t>(e);
+      s_cam[s] = p.camera_id[base + e];
+      s_pt[s] = plan_.pt_of[static_cast<std::size_t>(e)];
+      s_px[s] = px[base + e];
+      s_py[s] = py[base + e];
+      s_w[s] = wt ? wt[base + e] : S(1);
+      if (!(s_w[s] >= S(0))) throw Error(DBAG_INVALID_ARGUMENT, "edge weight must be >= 0");
+    }
+    slot_cam_.upload(s_cam);
+    slot_pt_.upload(s_pt);
+    slot_edge_.upload(s_edge);
+    slot_px_.upload(s_px);
+    slot_py_.upload(s_py);
+    slot_w_.upload(s_w);
+    std::vector<std::int32_t> ptr32(plan_.pt_ptr.begin(), plan_.pt_ptr.end());
+    pt_ptr_.upload(ptr32);
+    tile_pt_.upload(plan_.tile_pt);
+    n_tiles_ = static_cast<int>(plan_.tile_pt.size()) - 1;
+    std::vector<std::int32_t> cptr32(plan_.cam_ptr.begin(), plan_.cam_ptr.end());
+    cam_ptr_.upload(cptr32);
+    cam_glob_.upload(plan_.cams.to_global);
+    pt_glob_.upload(plan_.pts.to_global);
+    cslot_pslot_.upload(plan_.cslot_pslot);
+    std::vector<std::int32_t> cslot_pt(N_);
+    for (std::int64_t c = 0; c < N_; ++c) cslot_pt[c] = s_pt[plan_.cslot_pslot[static_cast<std::size_t>(c)]];
+    cslot_pt_.upload(cslot_pt);
+    owned_.upload(plan_.owned_lpt);
+    // halo
+    std::vector<std::int32_t> hl, hi;
+    for (std::int32_t lp = 0; lp < n_loc_; ++lp)
+      if (plan_.halo_of_lpt[static_cast<std::size_t>(lp)] >= 0) {
+        hl.push_back(lp);
+        hi.push_back(plan_.halo_of_lpt[static_cast<std::size_t>(lp)]);
+      }
+    n_halo_loc_ = static_cast<std::int32_t>(hl.size());
+    halo_of_.upload(plan_.halo_of_lpt);
+    halo_lpt_.upload(hl);
+    halo_idx_.upload(hi);
+    halo_buf_.alloc(static_cast<std::size_t>(std::max<std::int64_t>(H_, 1)) * 12);
+    // state + system
+    const std::size_t cm = static_cast<std::size_t>(m_) * 9, pl = static_cast<std::size_t>(n_loc_) * 3;
+    for (DevBuf<S>* b : {&xc_, &xct_, &dxc_, &v_, &g_, &r_, &z_, &p_, &q_, &ctmp_}) b->alloc(std::max<std::size_t>(cm, 1));
+    for (DevBuf<S>* b : {&xp_, &xpt_, &dxp_, &w_, &bpt_}) b->alloc(std::max<std::size_t>(pl, 1));
+    for (DevBuf<S>* b : {&B_, &Bd_, &Binv_}) b->alloc(std::max<std::size_t>(cm * 9, 1));
+    for (DevBuf<S>* b : {&C_, &Cd_, &Cinv_}) b->alloc(std::max<std::size_t>(pl * 3, 1));
+    Jb_.alloc(std::max<std::size_t>(static_cast<std::size_t>(N_) * 28, 1));
+    E_pm_.alloc(std::max<std::size_t>(static_cast<std::size_t>(N_) * 27, 1));
+    E_cm_.alloc(std::max<std::size_t>(static_cast<std::size_t>(N_) * 27, 1));
+    set_state(static_cast<const S*>(p.cameras), static_cast<const S*>(p.points));
+    have_system_ = false;
+  }
+
+  // Full-size host x_c (9m) and x_p (3n); this rank keeps its local points.
+  void set_state(const S* xc, const S* xp) {
+    DBAG_CUDA(cudaSetDevice(device_));
+    DBAG_CUDA(cudaMemcpyAsync(xc_.get(), xc, sizeof(S) * 9 * static_cast<std::size_t>(m_), cudaMemcpyHostToDevice, st_));
+    std::vector<S> loc(static_cast<std::size_t>(n_loc_) * 3);
+    for (std::int32_t lp = 0; lp < n_loc_; ++lp) {
+      const std::size_t g = static_cast<std::size_t>(plan_.pts.to_global[static_cast<std::size_t>(lp)]);
+      for (int k = 0; k < 3; ++k) loc[static_cast<std::size_t>(lp) * 3 + k] = xp[g * 3 + k];
+    }
+    DBAG_CUDA(cudaMemcpyAsync(xp_.get(), loc.data(), sizeof(S) * loc.size(), cudaMemcpyHostToDevice, st_));
+    DBAG_CUDA(cudaStreamSynchronize(st_));
+    have_system_ = false;
+  }
+
+  void get_state(S* xc, S* xp) {
+    DBAG_CUDA(cudaSetDevice(device_));
+    if (xc) DBAG_CUDA(cudaMemcpyAsync(xc, xc_.get(), sizeof(S) * 9 * static_cast<std::size_t>(m_), cudaMemcpyDeviceToHost, st_));
+    std::vector<S> loc(static_cast<std::size_t>(n_loc_) * 3);
+    DBAG_CUDA(cudaMemcpyAsync(loc.data(), xp_.get(), sizeof(S) * loc.size(), cudaMemcpyDeviceToHost, st_));
+    DBAG_CUDA(cudaStreamSynchronize(st_));
+    if (xp)
+      for (std::int32_t lp = 0; lp < n_loc_; ++lp) {
+        const std::size_t g = static_cast<std::size_t>(plan_.pts.to_global[static_cast<std::size_t>(lp)]);
+        for (int k = 0; k < 3; ++k) xp[g * 3 + k] = loc[static_cast<std::size_t>(lp) * 3 + k];
+      }
+  }
+
+  // ------------------------------------------------------------- cost ----
+  // Returns the all-reduced cost (+inf if any rank saw P_z == 0); bad_edge
+  // is the lowest offending global edge id over ranks, or -1.
+  double cost(bool trial, std::int64_t* bad_edge) {
+    DBAG_CUDA(cudaSetDevice(device_));
+    DBAG_CUDA(cudaMemsetAsync(bad_.get(), 0xff, sizeof(unsigned long long), st_));
+    dev::k_cost<S><<<grid_for(N_, dev::kRedThreads, dev::kRedBlocksMax), dev::kRedThreads, 0, st_>>>(
+        N_, slot_cam_.get(), slot_pt_.get(), slot_edge_.get(), plan_.range.start, slot_px_.get(), slot_py_.get(),
+        slot_w_.get(), trial ? xct_.get() : xc_.get(), trial ? xpt_.get() : xp_.get(), red(), dsc_.get(),
+        bad_.get());
+    DBAG_LAUNCH_CHECK();
+    if (N_ == 0) DBAG_CUDA(cudaMemsetAsync(dsc_.get(), 0, sizeof(double), st_));
+    tally_.edges += static_cast<std::uint64_t>(N_);
+    comm_->allreduce_sum(dsc_.get(), 1, DType::f64, st_);
+    const std::int64_t bad = agree_min_index(bad_.get());
+    DBAG_CUDA(cudaMemcpyAsync(hbuf_, dsc_.get(), sizeof(double), cudaMemcpyDeviceToHost, st_));
+    DBAG_CUDA(cudaStreamSynchronize(st_));
+    if (bad_edge) *bad_edge = bad;
+    return bad >= 0 ? std::numeric_limits<double>::infinity() : hbuf_[0];
+  }
+
+  // --------------------------------------------------------- linearize ----
+  void linearize() {
+    DBAG_CUDA(cudaSetDevice(device_));
+    DBAG_CUDA(cudaMemsetAsync(bad_.get(), 0xff, sizeof(unsigned long long), st_));
+    if (N_ > 0) {
+      const int blocks = static_cast<int>((N_ + 127) / 128);
+      if (jac_mode_ == 1)
+        dev::k_linearize<S, 1><<<blocks, 128, 0, st_>>>(N_, slot_cam_.get(), slot_pt_.get(), slot_edge_.get(),
+                                                         plan_.range.start, slot_px_.get(), slot_py_.get(),
+                                                         slot_w_.get(), xc_.get(), xp_.get(), Jb_.get(), E_pm_.get(),
+                                                         bad_.get());
+      else
+        dev::k_linearize<S, 0><<<blocks, 128, 0, st_>>>(N_, slot_cam_.get(), slot_pt_.get(), slot_edge_.get(),
+                                                         plan_.range.start, slot_px_.get(), slot_py_.get(),
+                                                         slot_w_.get(), xc_.get(), xp_.get(), Jb_.get(), E_pm_.get(),
+                                                         bad_.get());
+      DBAG_LAUNCH_CHECK();
+    }
+    tally_.edges += static_cast<std::uint64_t>(N_);
+    const std::int64_t bad = agree_min_index(bad_.get());
+    if (bad >= 0) throw degenerate_depth(bad);
+    DBAG_CUDA(cudaMemsetAsync(B_.get(), 0, B_.size() * sizeof(S), st_));
+    DBAG_CUDA(cudaMemsetAsync(v_.get(), 0, v_.size() * sizeof(S), st_));
+    if (n_loc_ > 0) {
+      dev::k_assemble_points<S><<<grid_for(n_loc_, 128, 1 << 30), 128, 0, st_>>>(n_loc_, pt_ptr_.get(), Jb_.get(),
+                                                                                 C_.get(), w_.get());
+      DBAG_LAUNCH_CHECK();
+    }
+    if (m_loc_ > 0) {
+      dev::k_assemble_cameras<S, 256><<<m_loc_, 256, 0, st_>>>(cam_ptr_.get(), cam_glob_.get(), cslot_pslot_.get(),
+                                                               Jb_.get(), N_, E_pm_.get(), E_cm_.get(), B_.get(),
+                                                               v_.get());
+      DBAG_LAUNCH_CHECK();
+    }
+    comm_->allreduce_sum(B_.get(), static_cast<std::int64_t>(m_) * 81, kT, st_);
+    comm_->allreduce_sum(C_halo_exchange_begin(), halo_count(12), kT, st_);
+    C_halo_exchange_end();
+    comm_->allreduce_sum(v_.get(), static_cast<std::int64_t>(m_) * 9, kT, st_);
+    have_system_ = true;
+  }
+
+  // ------------------------------------------------------ damp + factor ----
+  void damp_factor(double lambda, int policy) {
+    DBAG_CUDA(cudaSetDevice(device_));
+    lambda_ = lambda;
+    policy_ = policy;
+    DBAG_CUDA(cudaMemsetAsync(bad_.get(), 0xff, 2 * sizeof(unsigned long long), st_));
+    const S lam = static_cast<S>(lambda);
+    if (n_loc_ > 0) {
+      dev::k_damp_factor<S, 3><<<grid_for(n_loc_, 128, 1 << 30), 128, 0, st_>>>(
+          n_loc_, C_.get(), lam, policy, Cd_.get(), Cinv_.get(), pt_glob_.get(), bad_.get());
+      DBAG_LAUNCH_CHECK();
+    }
+    if (m_ > 0) {
+      dev::k_damp_factor<S, 9><<<grid_for(m_, 64, 1 << 30), 64, 0, st_>>>(m_, B_.get(), lam, policy, Bd_.get(),
+                                                                          Binv_.get(), nullptr, bad_.get() + 1);
+      DBAG_LAUNCH_CHECK();
+    }
+    // C failures are reported by global point id: the reference factors the
+    // full-size C in global order and names the first failing block, C
+    // before B (dba/solver.hpp:354-355, dba/block_matrix.hpp:123-134).
+    DBAG_CUDA(cudaMemcpyAsync(hbuf_, bad_.get(), 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st_));
+    DBAG_CUDA(cudaStreamSynchronize(st_));
+    unsigned long long raw[2];
+    std::memcpy(raw, hbuf_, sizeof(raw));
+    // -index (none = -inf): the max over ranks is the lowest failing index.
+    const double none = -std::numeric_limits<double>::infinity();
+    double agree[2] = {raw[0] == ~0ull ? none : -double(raw[0]), raw[1] == ~0ull ? none : -double(raw[1])};
+    if (comm_->size() > 1) {
+      double* d = dsc_.get();
+      DBAG_CUDA(cudaMemcpyAsync(d + 8, agree, sizeof(agree), cudaMemcpyHostToDevice, st_));
+      comm_->allreduce_max(d + 8, 2, DType::f64, st_);
+      DBAG_CUDA(cudaMemcpyAsync(agree, d + 8, sizeof(agree), cudaMemcpyDeviceToHost, st_));
+      DBAG_CUDA(cudaStreamSynchronize(st_));
+    }
+    if (std::isfinite(agree[0])) throw singular_block(static_cast<std::int64_t>(-agree[0]), 3);
+    if (std::isfinite(agree[1])) throw singular_block(static_cast<std::int64_t>(-agree[1]), 9);
+  }
+
+  // ---------------------------------------------------------------- rhs ----
+  void rhs() {
+    DBAG_CUDA(cudaSetDevice(device_));
+    if (n_loc_ > 0) {
+      dev::k_point_solve<S><<<grid_for(n_loc_, 128, 1 << 30), 128, 0, st_>>>(n_loc_, Cinv_.get(), w_.get(), bpt_.get());
+      DBAG_LAUNCH_CHECK();
+    }
+    cam_apply(bpt_.get(), ctmp_.get());
+    tally_.block_ops += static_cast<std::uint64_t>(N_);
+    const std::int64_t len = static_cast<std::int64_t>(m_) * 9;
+    if (len > 0) {
+      dev::k_sub<S><<<grid_for(len, 256, 1 << 30), 256, 0, st_>>>(len, v_.get(), ctmp_.get(), g_.get());
+      DBAG_LAUNCH_CHECK();
+    }
+  }
+
+  // ---------------------------------------------------------------- DSE ----
+  // q = (B_d - E C^-1 E^T) x; with PQ the epilogue also forms p.q -> alpha.
+  template <bool PQ>
+  void dse(const S* x, S* q) {
+    const bool prof = profiling_;
+    if (prof) DBAG_CUDA(cudaEventRecord(prof_event(), st_));
+    if (H_ > 0) DBAG_CUDA(cudaMemsetAsync(halo_buf_.get(), 0, sizeof(S) * 3 * static_cast<std::size_t>(H_), st_));
+    if (n_tiles_ > 0) {
+      dev::k_point_pass<S, 0><<<n_tiles_, dev::kTile, 0, st_>>>(N_, tile_pt_.get(), pt_ptr_.get(), slot_cam_.get(),
+                                                               E_pm_.get(), x, Cinv_.get(), nullptr,
+                                                               H_ > 0 ? halo_of_.get() : nullptr, halo_buf_.get(),
+                                                               bpt_.get());
+      DBAG_LAUNCH_CHECK();
+    }
+    if (prof) DBAG_CUDA(cudaEventRecord(prof_event(), st_));
+    if (H_ > 0) {
+      comm_->allreduce_sum(halo_buf_.get(), 3 * H_, kT, st_);
+      if (n_halo_loc_ > 0) {
+        dev::k_halo_finish<S, 0><<<grid_for(n_halo_loc_, 128, 1 << 30), 128, 0, st_>>>(
+            n_halo_loc_, halo_lpt_.get(), halo_idx_.get(), halo_buf_.get(), Cinv_.get(), nullptr, bpt_.get());
+        DBAG_LAUNCH_CHECK();
+      }
+    }
+    if (prof) DBAG_CUDA(cudaEventRecord(prof_event(), st_));
+    cam_apply(bpt_.get(), ctmp_.get());
+    if (prof) DBAG_CUDA(cudaEventRecord(prof_event(), st_));
+    if (m_ > 0) {
+      dev::k_cam_epilogue<S, PQ><<<grid_for(m_, dev::kRedThreads, dev::kRedBlocksMax), dev::kRedThreads, 0, st_>>>(
+          m_, Bd_.get(), x, ctmp_.get(), q, red(), sc_.get());
+      DBAG_LAUNCH_CHECK();
+    }
+    tally_.block_ops += 2 * static_cast<std::uint64_t>(N_);
+    ++dse_count_;
+    ++dse_launches_;
+  }
+
+  // --------------------------------------------------------------- DPCG ----
+  PcgOut pcg(double tol, int max_iters, S* x_out_dev = nullptr) {
+    DBAG_CUDA(cudaSetDevice(device_));
+    S* x = x_out_dev ? x_out_dev : dxc_.get();
+    const std::int64_t len = static_cast<std::int64_t>(m_) * 9;
+    dse_count_ = 0;
+    DBAG_CUDA(cudaMemsetAsync(x, 0, sizeof(S) * std::max<std::int64_t>(len, 1), st_));
+    Scal init{};
+    DBAG_CUDA(cudaMemcpyAsync(sc_.get(), &init, sizeof(Scal), cudaMemcpyHostToDevice, st_));
+    launch_dot(g_.get(), g_.get(), len, &sc_.get()->rhs_norm2);
+    read_scal();
+    const double rhs_norm = std::sqrt(hsc_->rhs_norm2);
+    if (rhs_norm == 0.0) return {0, true};
+    // r = g - S x0 with x0 = 0: S 0 = 0 exactly, so r = g; the reference's
+    // DSE on x0 (dba/solver.hpp:217) is still counted in the tallies.
+    tally_.block_ops += 2 * static_cast<std::uint64_t>(N_);
+    ++dse_count_;
+    DBAG_CUDA(cudaMemcpyAsync(r_.get(), g_.get(), sizeof(S) * len, cudaMemcpyDeviceToDevice, st_));
+    double r_norm = rhs_norm;
+    int n = 0;
+    const int rb = grid_for(m_, dev::kRedThreads, dev::kRedBlocksMax);
+    const int vb = grid_for(len, dev::kRedThreads, dev::kRedBlocksMax);
+    while (r_norm > tol * rhs_norm && n < max_iters) {
+      const std::uint64_t ops0 = tally_.block_ops;
+      const int dse0 = dse_count_;
+      dev::k_pcg_precond<S><<<rb, dev::kRedThreads, 0, st_>>>(m_, Binv_.get(), r_.get(), z_.get(), red(), sc_.get());
+      dev::k_pcg_p<S><<<grid_for(len, 256, 1 << 30), 256, 0, st_>>>(len, z_.get(), p_.get(), sc_.get());
+      DBAG_LAUNCH_CHECK();
+      dse<true>(p_.get(), q_.get());
+      const std::uint64_t ops1 = tally_.block_ops;
+      const int dse1 = dse_count_;
+      const bool refresh = (n + 1) % 50 == 0;
+      if (refresh) {
+        dev::k_pcg_xr<S, false><<<vb, dev::kRedThreads, 0, st_>>>(len, p_.get(), q_.get(), x, r_.get(), red(), sc_.get());
+        DBAG_LAUNCH_CHECK();
+        dse<false>(x, q_.get());
+        dev::k_pcg_refresh<S><<<vb, dev::kRedThreads, 0, st_>>>(len, g_.get(), q_.get(), r_.get(), red(), sc_.get(), 1);
+      } else {
+        dev::k_pcg_xr<S, true><<<vb, dev::kRedThreads, 0, st_>>>(len, p_.get(), q_.get(), x, r_.get(), red(), sc_.get());
+      }
+      DBAG_LAUNCH_CHECK();
+      read_scal();
+      if (hsc_->status & 1) {  // rho breakdown: thrown before this iteration's DSE
+        tally_.block_ops = ops0;
+        dse_count_ = dse0;
+        throw Error(DBAG_PCG_BREAKDOWN, "preconditioned residual norm rho = " + std::to_string(hsc_->rho) +
+                                            " at iteration " + std::to_string(n));
+      }
+      if (hsc_->status & 2) {  // p'q breakdown: thrown after the DSE of p
+        tally_.block_ops = ops1;
+        dse_count_ = dse1;
+        throw Error(DBAG_PCG_BREAKDOWN, "operator lost positive definiteness (p'q = " + std::to_string(hsc_->pq) +
+                                            ") at iteration " + std::to_string(n));
+      }
+      ++n;
+      r_norm = std::sqrt(hsc_->rnorm2);
+    }
+    return {n, r_norm <= tol * rhs_norm};
+  }
+
+  // ------------------------------------------- back-substitution + trial ----
+  void backsub_trial() {
+    DBAG_CUDA(cudaSetDevice(device_));
+    if (H_ > 0) DBAG_CUDA(cudaMemsetAsync(halo_buf_.get(), 0, sizeof(S) * 3 * static_cast<std::size_t>(H_), st_));
+    if (n_tiles_ > 0) {
+      dev::k_point_pass<S, 1><<<n_tiles_, dev::kTile, 0, st_>>>(N_, tile_pt_.get(), pt_ptr_.get(), slot_cam_.get(),
+                                                               E_pm_.get(), dxc_.get(), Cinv_.get(), w_.get(),
+                                                               H_ > 0 ? halo_of_.get() : nullptr, halo_buf_.get(),
+                                                               dxp_.get());
+      DBAG_LAUNCH_CHECK();
+    }
+    if (H_ > 0) {
+      comm_->allreduce_sum(halo_buf_.get(), 3 * H_, kT, st_);
+      if (n_halo_loc_ > 0) {
+        dev::k_halo_finish<S, 1><<<grid_for(n_halo_loc_, 128, 1 << 30), 128, 0, st_>>>(
+            n_halo_loc_, halo_lpt_.get(), halo_idx_.get(), halo_buf_.get(), Cinv_.get(), w_.get(), dxp_.get());
+        DBAG_LAUNCH_CHECK();
+      }
+    }
+    tally_.block_ops += static_cast<std::uint64_t>(N_);
+    double* d = dsc_.get();
+    const int cb = grid_for(m_, dev::kRedThreads, dev::kRedBlocksMax);
+    dev::k_trial<S, 9><<<cb, dev::kRedThreads, 0, st_>>>(m_, xc_.get(), dxc_.get(), xct_.get(), B_.get(), v_.get(),
+                                                         nullptr, lambda_, policy_, red(), d + 16);
+    DBAG_LAUNCH_CHECK();
+    const int pb = grid_for(n_loc_, dev::kRedThreads, dev::kRedBlocksMax);
+    DBAG_CUDA(cudaMemsetAsync(d + 20, 0, 4 * sizeof(double), st_));
+    if (n_loc_ > 0) {
+      dev::k_trial<S, 3><<<pb, dev::kRedThreads, 0, st_>>>(n_loc_, xp_.get(), dxp_.get(), xpt_.get(), C_.get(),
+                                                           w_.get(), owned_.get(), lambda_, policy_, red(), d + 20);
+      DBAG_LAUNCH_CHECK();
+    }
+    // point terms: [max, damp, gv] -> max over ranks for d[20], sum for d[21..22]
+    comm_->allreduce_max(d + 20, 1, DType::f64, st_);
+    comm_->allreduce_sum(d + 21, 2, DType::f64, st_);
+    DBAG_CUDA(cudaMemcpyAsync(hbuf_, d + 16, 8 * sizeof(double), cudaMemcpyDeviceToHost, st_));
+    DBAG_CUDA(cudaStreamSynchronize(st_));
+    step_inf_ = std::max(hbuf_[0], hbuf_[4]);
+    damp_term_ = policy_ == 0 ? lambda_ * (hbuf_[1] + hbuf_[5]) : hbuf_[1] + hbuf_[5];
+    gv_ = hbuf_[2] + hbuf_[6];
+  }
+
+  void model_terms(double* step_inf, double* damp, double* gv) const {
+    *step_inf = step_inf_;
+    *damp = damp_term_;
+    *gv = gv_;
+  }
+
+  void accept() {
+    xc_.swap(xct_);
+    xp_.swap(xpt_);
+    have_system_ = false;
+  }
+
+  bool have_system() const { return have_system_; }
+
+  // ---------------------------------------------------- rank identity ----
+  // |x_c|_inf and |x_p|_inf (over owned points, max over ranks).
+  void state_inf(double* ic, double* ip) {
+    DBAG_CUDA(cudaSetDevice(device_));
+    std::vector<S> hc(static_cast<std::size_t>(m_) * 9), hp(static_cast<std::size_t>(n_loc_) * 3);
+    DBAG_CUDA(cudaMemcpyAsync(hc.data(), xc_.get(), sizeof(S) * hc.size(), cudaMemcpyDeviceToHost, st_));
+    DBAG_CUDA(cudaMemcpyAsync(hp.data(), xp_.get(), sizeof(S) * hp.size(), cudaMemcpyDeviceToHost, st_));
+    DBAG_CUDA(cudaStreamSynchronize(st_));
+    double a = 0, b = 0;
+    for (S v : hc) a = std::max(a, double(std::abs(v)));
+    for (std::int32_t lp = 0; lp < n_loc_; ++lp)
+      if (plan_.owned_lpt[static_cast<std::size_t>(lp)])
+        for (int k = 0; k < 3; ++k) b = std::max(b, double(std::abs(hp[static_cast<std::size_t>(lp) * 3 + k])));
+    double* d = dsc_.get();
+    hbuf_[0] = b;
+    DBAG_CUDA(cudaMemcpyAsync(d + 30, hbuf_, sizeof(double), cudaMemcpyHostToDevice, st_));
+    comm_->allreduce_max(d + 30, 1, DType::f64, st_);
+    DBAG_CUDA(cudaMemcpyAsync(hbuf_, d + 30, sizeof(double), cudaMemcpyDeviceToHost, st_));
+    DBAG_CUDA(cudaStreamSynchronize(st_));
+    *ic = a;
+    *ip = hbuf_[0];
+  }
+
+  // Sum-all-reduce of a small host vector through a device bounce buffer.
+  void allreduce_host(double* v, int n) {
+    DBAG_CUDA(cudaSetDevice(device_));
+    if (comm_->size() == 1) return;
+    if (!bounce_.get() || bounce_.size() < static_cast<std::size_t>(n)) bounce_.alloc(static_cast<std::size_t>(n));
+    DBAG_CUDA(cudaMemcpyAsync(bounce_.get(), v, sizeof(double) * n, cudaMemcpyHostToDevice, st_));
+    comm_->allreduce_sum(bounce_.get(), n, DType::f64, st_);
+    DBAG_CUDA(cudaMemcpyAsync(v, bounce_.get(), sizeof(double) * n, cudaMemcpyDeviceToHost, st_));
+    DBAG_CUDA(cudaStreamSynchronize(st_));
+  }
+
+  // ------------------------------------------------------- test hooks ----
+  void get_jacobians(S* res, S* jac) {
+    DBAG_CUDA(cudaSetDevice(device_));
+    std::vector<S> jb(static_cast<std::size_t>(N_) * 28);
+    DBAG_CUDA(cudaMemcpy(jb.data(), Jb_.get(), sizeof(S) * jb.size(), cudaMemcpyDeviceToHost));
+    for (std::int64_t s = 0; s < N_; ++s) {
+      const std::int64_t e = plan_.pt_blk[static_cast<std::size_t>(s)];
+      const S* row = jb.data() + static_cast<std::size_t>(s) * 28;
+      res[e] = row[0];
+      res[N_ + e] = row[1];
+      for (int j = 0; j < 12; ++j) {
+        jac[static_cast<std::size_t>(j) * N_ + e] = row[2 + j];
+        jac[static_cast<std::size_t>(12 + j) * N_ + e] = row[14 + j];
+      }
+    }
+  }
+
+  void get_system(S* B, S* C, S* E, S* v, S* w) {
+    DBAG_CUDA(cudaSetDevice(device_));
+    DBAG_CUDA(cudaStreamSynchronize(st_));
+    if (B) DBAG_CUDA(cudaMemcpy(B, B_.get(), sizeof(S) * 81 * static_cast<std::size_t>(m_), cudaMemcpyDeviceToHost));
+    if (v) DBAG_CUDA(cudaMemcpy(v, v_.get(), sizeof(S) * 9 * static_cast<std::size_t>(m_), cudaMemcpyDeviceToHost));
+    std::vector<S> c(static_cast<std::size_t>(n_loc_) * 9), ww(static_cast<std::size_t>(n_loc_) * 3);
+    DBAG_CUDA(cudaMemcpy(c.data(), C_.get(), sizeof(S) * c.size(), cudaMemcpyDeviceToHost));
+    DBAG_CUDA(cudaMemcpy(ww.data(), w_.get(), sizeof(S) * ww.size(), cudaMemcpyDeviceToHost));
+    if (C) std::fill(C, C + static_cast<std::size_t>(n_glob_) * 9, S(0));
+    if (w) std::fill(w, w + static_cast<std::size_t>(n_glob_) * 3, S(0));
+    for (std::int32_t lp = 0; lp < n_loc_; ++lp) {
+      const std::size_t g = static_cast<std::size_t>(plan_.pts.to_global[static_cast<std::size_t>(lp)]);
+      if (C) std::copy(c.begin() + lp * 9, c.begin() + lp * 9 + 9, C + g * 9);
+      if (w) std::copy(ww.begin() + lp * 3, ww.begin() + lp * 3 + 3, w + g * 3);
+    }
+    if (E) {
+      std::vector<S> e(static_cast<std::size_t>(N_) * 27);
+      DBAG_CUDA(cudaMemcpy(e.data(), E_pm_.get(), sizeof(S) * e.size(), cudaMemcpyDeviceToHost));
+      for (std::int64_t s = 0; s < N_; ++s) {
+        const std::int64_t ed = plan_.pt_blk[static_cast<std::size_t>(s)];
+        for (int k = 0; k < 27; ++k) E[ed * 27 + k] = e[static_cast<std::size_t>(k) * N_ + s];
+      }
+    }
+  }
+
+  // Caller-fabricated system (test hook): full-size B, C, v, w and the
+  // E_table of the whole problem in global edge order.
+  void set_system(const S* B, const S* C, const S* E_table, const S* v, const S* w) {
+    DBAG_CUDA(cudaSetDevice(device_));
+    DBAG_CUDA(cudaStreamSynchronize(st_));
+    if (B) DBAG_CUDA(cudaMemcpy(B_.get(), B, sizeof(S) * 81 * static_cast<std::size_t>(m_), cudaMemcpyHostToDevice));
+    if (v) DBAG_CUDA(cudaMemcpy(v_.get(), v, sizeof(S) * 9 * static_cast<std::size_t>(m_), cudaMemcpyHostToDevice));
+    if (C || w) {
+      std::vector<S> c(static_cast<std::size_t>(n_loc_) * 9), ww(static_cast<std::size_t>(n_loc_) * 3);
+      for (std::int32_t lp = 0; lp < n_loc_; ++lp) {
+        const std::size_t g = static_cast<std::size_t>(plan_.pts.to_global[static_cast<std::size_t>(lp)]);
+        if (C) std::copy(C + g * 9, C + g * 9 + 9, c.begin() + lp * 9);
+        if (w) std::copy(w + g * 3, w + g * 3 + 3, ww.begin() + lp * 3);
+      }
+      if (C) DBAG_CUDA(cudaMemcpy(C_.get(), c.data(), sizeof(S) * c.size(), cudaMemcpyHostToDevice));
+      if (w) DBAG_CUDA(cudaMemcpy(w_.get(), ww.data(), sizeof(S) * ww.size(), cudaMemcpyHostToDevice));
+    }
+    if (E_table) {
+      std::vector<S> pm(static_cast<std::size_t>(N_) * 27), cmv(static_cast<std::size_t>(N_) * 27);
+      for (std::int64_t s = 0; s < N_; ++s) {
+        const std::int64_t ed = plan_.range.start + plan_.pt_blk[static_cast<std::size_t>(s)];
+        for (int k = 0; k < 27; ++k) pm[static_cast<std::size_t>(k) * N_ + s] = E_table[ed * 27 + k];
+      }
+      for (std::int64_t c = 0; c < N_; ++c) {
+        const std::int64_t s = plan_.cslot_pslot[static_cast<std::size_t>(c)];
+        for (int k = 0; k < 27; ++k) cmv[static_cast<std::size_t>(k) * N_ + c] = pm[static_cast<std::size_t>(k) * N_ + s];
+      }
+      DBAG_CUDA(cudaMemcpy(E_pm_.get(), pm.data(), sizeof(S) * pm.size(), cudaMemcpyHostToDevice));
+      DBAG_CUDA(cudaMemcpy(E_cm_.get(), cmv.data(), sizeof(S) * cmv.size(), cudaMemcpyHostToDevice));
+    }
+    have_system_ = true;
+  }
+
+  // Fabricated blocks are already damped: factor them as-is (lambda = 0,
+  // identity policy adds exactly 0 to every diagonal entry).
+  void factor_as_is() { damp_factor(0.0, 0); }
+
+  void dse_host(const S* x, S* out) {
+    DBAG_CUDA(cudaSetDevice(device_));
+    const std::size_t len = static_cast<std::size_t>(m_) * 9;
+    DBAG_CUDA(cudaMemcpyAsync(p_.get(), x, sizeof(S) * len, cudaMemcpyHostToDevice, st_));
+    dse<false>(p_.get(), q_.get());
+    DBAG_CUDA(cudaMemcpyAsync(out, q_.get(), sizeof(S) * len, cudaMemcpyDeviceToHost, st_));
+    DBAG_CUDA(cudaStreamSynchronize(st_));
+  }
+
+  PcgOut dpcg_host(const S* rhs, double tol, int max_iters, S* x_out) {
+    DBAG_CUDA(cudaSetDevice(device_));
+    const std::size_t len = static_cast<std::size_t>(m_) * 9;
+    DBAG_CUDA(cudaMemcpyAsync(g_.get(), rhs, sizeof(S) * len, cudaMemcpyHostToDevice, st_));
+    const PcgOut o = pcg(tol, max_iters);
+    DBAG_CUDA(cudaMemcpyAsync(x_out, dxc_.get(), sizeof(S) * len, cudaMemcpyDeviceToHost, st_));
+    DBAG_CUDA(cudaStreamSynchronize(st_));
+    return o;
+  }
+
+  // ---------------------------------------------------- timing hooks ----
+  void mark(int which) { DBAG_CUDA(cudaEventRecord(mark_[which & 1], st_)); }
+  double elapsed_ms() {
+    DBAG_CUDA(cudaEventSynchronize(mark_[1]));
+    float ms = 0;
+    DBAG_CUDA(cudaEventElapsedTime(&ms, mark_[0], mark_[1]));
+    return ms;
+  }
+  void set_profiling(bool on) {
+    collect_profile();
+    profiling_ = on;
+    prof_point_ms_ = prof_cam_ms_ = 0;
+    dse_launches_ = 0;
+  }
+  void profile(double* total, std::int64_t* launches, double* point_ms, double* cam_ms) {
+    collect_profile();
+    *total = prof_point_ms_ + prof_cam_ms_;
+    *launches = dse_launches_;
+    *point_ms = prof_point_ms_;
+    *cam_ms = prof_cam_ms_;
+  }
+  void sync() { DBAG_CUDA(cudaStreamSynchronize(st_)); }
+
+ private:
+  dev::RedWs red() { return dev::RedWs{red_part_.get(), red_cnt_.get()}; }
+
+  void read_scal() {
+    DBAG_CUDA(cudaMemcpyAsync(hsc_, sc_.get(), sizeof(Scal), cudaMemcpyDeviceToHost, st_));
+    DBAG_CUDA(cudaStreamSynchronize(st_));
+    collect_profile();
+  }
+
+  void launch_dot(const S* a, const S* b, std::int64_t len, double* out) {
+    dev::k_dot<S><<<grid_for(len, dev::kRedThreads, dev::kRedBlocksMax), dev::kRedThreads, 0, st_>>>(len, a, b, red(),
+                                                                                                     out);
+    DBAG_LAUNCH_CHECK();
+  }
+
+  // c = E b over this rank's cameras, all-reduced (9m).
+  void cam_apply(const S* bpt, S* out) {
+    const std::size_t len = static_cast<std::size_t>(m_) * 9;
+    DBAG_CUDA(cudaMemsetAsync(out, 0, sizeof(S) * std::max<std::size_t>(len, 1), st_));
+    if (m_loc_ > 0) {
+      dev::k_cam_pass<S, 256><<<m_loc_, 256, 0, st_>>>(cam_ptr_.get(), cam_glob_.get(), cslot_pt_.get(), N_,
+                                                       E_cm_.get(), bpt, out);
+      DBAG_LAUNCH_CHECK();
+    }
+    comm_->allreduce_sum(out, static_cast<std::int64_t>(len), kT, st_);
+  }
+
+  // Lowest index over ranks from a device u64 (all-ones = none); -1 if none.
+  std::int64_t agree_min_index(unsigned long long* dev_bad) {
+    unsigned long long raw = 0;
+    DBAG_CUDA(cudaMemcpyAsync(hbuf_, dev_bad, sizeof(raw), cudaMemcpyDeviceToHost, st_));
+    DBAG_CUDA(cudaStreamSynchronize(st_));
+    std::memcpy(&raw, hbuf_, sizeof(raw));
+    if (comm_->size() == 1) return raw == ~0ull ? -1 : static_cast<std::int64_t>(raw);
+    double neg = raw == ~0ull ? -std::numeric_limits<double>::infinity() : -double(raw);
+    double* d = dsc_.get();
+    hbuf_[0] = neg;
+    DBAG_CUDA(cudaMemcpyAsync(d + 28, hbuf_, sizeof(double), cudaMemcpyHostToDevice, st_));
+    comm_->allreduce_max(d + 28, 1, DType::f64, st_);
+    DBAG_CUDA(cudaMemcpyAsync(hbuf_, d + 28, sizeof(double), cudaMemcpyDeviceToHost, st_));
+    DBAG_CUDA(cudaStreamSynchronize(st_));
+    return std::isfinite(hbuf_[0]) ? static_cast<std::int64_t>(-hbuf_[0]) : -1;
+  }
+
+  std::int64_t halo_count(int width) const { return H_ > 0 ? H_ * width : 0; }
+  // C (9) and w (3) of shared points into the 12-wide halo buffer.
+  S* C_halo_exchange_begin() {
+    if (H_ == 0) return halo_buf_.get();
+    DBAG_CUDA(cudaMemsetAsync(halo_buf_.get(), 0, sizeof(S) * 12 * static_cast<std::size_t>(H_), st_));
+    if (n_halo_loc_ > 0) {
+      // [C(9) | w(3)] per halo point: scatter C into a 9-wide view, w after it
+      dev::k_halo_scatter<S, 9><<<grid_for(n_halo_loc_, 128, 1 << 30), 128, 0, st_>>>(
+          n_halo_loc_, halo_lpt_.get(), halo_idx_.get(), C_.get(), halo_buf_.get());
+      dev::k_halo_scatter<S, 3><<<grid_for(n_halo_loc_, 128, 1 << 30), 128, 0, st_>>>(
+          n_halo_loc_, halo_lpt_.get(), halo_idx_.get(), w_.get(), halo_buf_.get() + 9 * static_cast<std::size_t>(H_));
+      DBAG_LAUNCH_CHECK();
+    }
+    return halo_buf_.get();
+  }
+  void C_halo_exchange_end() {
+    if (H_ == 0 || n_halo_loc_ == 0) return;
+    dev::k_halo_gather<S, 9><<<grid_for(n_halo_loc_, 128, 1 << 30), 128, 0, st_>>>(
+        n_halo_loc_, halo_lpt_.get(), halo_idx_.get(), halo_buf_.get(), C_.get());
+    dev::k_halo_gather<S, 3><<<grid_for(n_halo_loc_, 128, 1 << 30), 128, 0, st_>>>(
+        n_halo_loc_, halo_lpt_.get(), halo_idx_.get(), halo_buf_.get() + 9 * static_cast<std::size_t>(H_), w_.get());
+    DBAG_LAUNCH_CHECK();
+  }
+
+  cudaEvent_t prof_event() {
+    if (prof_next_ == prof_ev_.size()) {
+      cudaEvent_t e;
+      DBAG_CUDA(cudaEventCreate(&e));
+      prof_ev_.push_back(e);
+    }
+    return prof_ev_[prof_next_++];
+  }
+  // Events come in groups of 4 per DSE: [start, point done, halo done, cam done].
+  void collect_profile() {
+    if (prof_next_ == 0) return;
+    DBAG_CUDA(cudaStreamSynchronize(st_));
+    for (std::size_t i = 0; i + 3 < prof_next_; i += 4) {
+      float a = 0, b = 0;
+      DBAG_CUDA(cudaEventElapsedTime(&a, prof_ev_[i], prof_ev_[i + 1]));
+      DBAG_CUDA(cudaEventElapsedTime(&b, prof_ev_[i + 2], prof_ev_[i + 3]));
+      prof_point_ms_ += a;
+      prof_cam_ms_ += b;
+    }
+    prof_next_ = 0;
+  }
+
+  int device_;
+  Comm* comm_;
+  cudaStream_t st_ = nullptr;
+  ShardPlan plan_;
+  int jac_mode_ = 0;
+  std::int32_t m_ = 0, n_glob_ = 0, n_loc_ = 0, m_loc_ = 0, n_halo_loc_ = 0;
+  std::int64_t N_ = 0, H_ = 0;
+  int n_tiles_ = 0;
+  bool have_system_ = false;
+  double lambda_ = 0;
+  int policy_ = 1;
+  double step_inf_ = 0, damp_term_ = 0, gv_ = 0;
+  int dse_count_ = 0;
+  std::int64_t dse_launches_ = 0;
+  Tally tally_;
+  Scal* hsc_ = nullptr;
+  double* hbuf_ = nullptr;
+  cudaEvent_t mark_[2];
+  bool profiling_ = false;
+  std::vector<cudaEvent_t> prof_ev_;
+  std::size_t prof_next_ = 0;
+  double prof_point_ms_ = 0, prof_cam_ms_ = 0;
+
+  DevBuf<std::int32_t> slot_cam_, slot_pt_, slot_edge_, pt_ptr_, tile_pt_, cam_ptr_, cam_glob_, pt_glob_,
+      cslot_pslot_, cslot_pt_, halo_of_, halo_lpt_, halo_idx_;
+  DevBuf<std::uint8_t> owned_;
+  DevBuf<S> slot_px_, slot_py_, slot_w_;
+  DevBuf<S> xc_, xct_, dxc_, v_, g_, r_, z_, p_, q_, ctmp_;
+  DevBuf<S> xp_, xpt_, dxp_, w_, bpt_;
+  DevBuf<S> B_, Bd_, Binv_, C_, Cd_, Cinv_;
+  DevBuf<S> Jb_, E_pm_, E_cm_, halo_buf_;
+  DevBuf<Scal> sc_;
+  DevBuf<double> red_part_, dsc_, bounce_;
+  DevBuf<unsigned> red_cnt_;
+  DevBuf<unsigned long long> bad_;
+};
+
+}  // namespace dbag

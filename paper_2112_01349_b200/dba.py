@@ -1,0 +1,708 @@
+"""Host-side mirror of the reference's ``dba`` API for the LM inner loop.
+
+Same names, argument meaning and error behaviour as the header-only C++ API
+of the reference:
+
+  BAProblem / CameraState / PointState / Observation   dba/problem.hpp:34-261
+  partition_edges / EdgePartition / LocalIndexMap       dba/partition.hpp:14-103
+  SolverConfig / IterationRecord / SolverState          dba/solver.hpp:39-85
+  lm_solve                                              dba/solver.hpp:523-534
+  generate_synthetic / SyntheticOptions                 dba/synthetic.hpp:19-146
+  errors                                                dba/errors.hpp:17-84
+
+Every numeric operator runs in libdbag.so (hand-written sm_100a kernels); this
+module only marshals arrays and maps status codes back to exceptions.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import dataclasses
+from dataclasses import dataclass, field
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+from . import _native as N
+
+# ------------------------------------------------------------------ errors --
+
+
+class Error(RuntimeError):
+    """dba::Error (dba/errors.hpp:10-13)."""
+
+
+class ParseError(Error):
+    pass
+
+
+class InvalidArgumentError(Error):
+    pass
+
+
+class DegenerateDepthError(Error):
+    def __init__(self, msg: str = "degenerate depth (P_z = 0)", edge_id: int = -1):
+        super().__init__(msg)
+        self.edge_id = edge_id
+
+
+class ShapeError(Error):
+    pass
+
+
+class SingularBlockError(Error):
+    def __init__(self, msg: str, block_index: int, block_size: int):
+        super().__init__(msg)
+        self.block_index = block_index
+        self.block_size = block_size
+
+
+class CollectiveError(Error):
+    pass
+
+
+class PcgBreakdownError(Error):
+    pass
+
+
+class CudaError(Error):
+    pass
+
+
+class NcclError(Error):
+    pass
+
+
+def _check(rc: int) -> None:
+    if rc == 0:
+        return
+    lib = N.lib()
+    msg = (lib.dbag_last_error() or b"").decode(errors="replace")
+    idx = int(lib.dbag_last_error_index())
+    if rc == 1:
+        raise DegenerateDepthError(msg, idx)
+    if rc == 2:
+        raise SingularBlockError(msg, idx, int(lib.dbag_last_error_block_size()))
+    raise {3: PcgBreakdownError, 4: ShapeError, 5: InvalidArgumentError, 6: CollectiveError, 7: CudaError,
+           8: NcclError}.get(rc, Error)(msg)
+
+
+# ----------------------------------------------------------------- problem --
+
+MSE_PER_OBSERVATION, MSE_HALF_PER_OBSERVATION = 0, 1
+
+
+def mse_from_cost(cost: float, num_observations: int, convention: int = MSE_HALF_PER_OBSERVATION) -> float:
+    """dba/problem.hpp:22-29."""
+    if num_observations <= 0:
+        return 0.0
+    return cost / (2.0 * num_observations if convention == MSE_HALF_PER_OBSERVATION else float(num_observations))
+
+
+@dataclass
+class CameraState:
+    """BAL 9-parameter camera (dba/problem.hpp:34-49)."""
+    rotation: Sequence[float] = (0.0, 0.0, 0.0)
+    translation: Sequence[float] = (0.0, 0.0, 0.0)
+    focal: float = 1.0
+    k1: float = 0.0
+    k2: float = 0.0
+
+    def params(self):
+        return [*self.rotation, *self.translation, self.focal, self.k1, self.k2]
+
+
+@dataclass
+class PointState:
+    position: Sequence[float] = (0.0, 0.0, 0.0)
+
+
+@dataclass
+class Observation:
+    camera_id: int = 0
+    point_id: int = 0
+    pixel: Sequence[float] = (0.0, 0.0)
+    weight: float = 1.0
+
+
+class BAProblem:
+    """Camera nodes, point nodes and observation edges (dba/problem.hpp:171-261).
+
+    ``dtype`` is the reference's Scalar template parameter (float32 or float64).
+    Storage is packed: cameras (m, 9) as pack_cameras, points (n, 3) as
+    pack_points, observations as SoA arrays in canonical edge order.
+    """
+
+    def __init__(self, dtype=np.float64):
+        self.dtype = np.dtype(dtype)
+        if self.dtype not in (np.float32, np.float64):
+            raise InvalidArgumentError("BAProblem dtype must be float32 or float64")
+        self._cams: list = []
+        self._pts: list = []
+        self._obs: list = []
+        self._frozen = None
+
+    @classmethod
+    def from_arrays(cls, cameras, points, camera_id, point_id, pixels, weight=None, dtype=None):
+        if dtype is None:
+            src = np.asarray(cameras).dtype
+            dtype = src if src in (np.float32, np.float64) else np.float64
+        dtype = np.dtype(dtype)
+        p = cls(dtype)
+        cams = np.ascontiguousarray(np.asarray(cameras, dtype=dtype).reshape(-1, 9))
+        pts = np.ascontiguousarray(np.asarray(points, dtype=dtype).reshape(-1, 3))
+        cid = np.ascontiguousarray(np.asarray(camera_id, dtype=np.int32))
+        pid = np.ascontiguousarray(np.asarray(point_id, dtype=np.int32))
+        pix = np.asarray(pixels, dtype=dtype).reshape(-1, 2)
+        w = np.ones(len(cid), dtype=dtype) if weight is None else np.ascontiguousarray(np.asarray(weight, dtype=dtype))
+        if not (np.isfinite(cams).all() and np.isfinite(pts).all()):
+            raise InvalidArgumentError("node has non-finite components")
+        if len(cid) and (cid.min() < 0 or cid.max() >= len(cams)):
+            raise InvalidArgumentError("edge references unknown camera")
+        if len(pid) and (pid.min() < 0 or pid.max() >= len(pts)):
+            raise InvalidArgumentError("edge references unknown point")
+        if not (w >= 0).all():
+            raise InvalidArgumentError("edge weight must be >= 0")
+        p._frozen = (cams, pts, cid, pid, np.ascontiguousarray(pix[:, 0]), np.ascontiguousarray(pix[:, 1]), w)
+        return p
+
+    # -- append API (dba/problem.hpp:180-207)
+    def _thaw(self):
+        if self._frozen is not None:
+            cams, pts, cid, pid, px, py, w = self._frozen
+            self._cams = [list(r) for r in cams]
+            self._pts = [list(r) for r in pts]
+            self._obs = [(int(a), int(b), float(x), float(y), float(ww)) for a, b, x, y, ww in zip(cid, pid, px, py, w)]
+            self._frozen = None
+
+    def add_node(self, node) -> int:
+        self._thaw()
+        if isinstance(node, CameraState):
+            v = [float(x) for x in node.params()]
+            if not np.isfinite(v).all():
+                raise InvalidArgumentError("camera node has non-finite components")
+            self._cams.append(v)
+            return len(self._cams) - 1
+        if isinstance(node, PointState):
+            v = [float(x) for x in node.position]
+            if not np.isfinite(v).all():
+                raise InvalidArgumentError("point node has non-finite components")
+            self._pts.append(v)
+            return len(self._pts) - 1
+        raise InvalidArgumentError("add_node expects a CameraState or PointState")
+
+    def add_edge(self, obs: Observation) -> int:
+        self._thaw()
+        if not 0 <= obs.camera_id < len(self._cams):
+            raise InvalidArgumentError(f"edge references unknown camera {obs.camera_id}")
+        if not 0 <= obs.point_id < len(self._pts):
+            raise InvalidArgumentError(f"edge references unknown point {obs.point_id}")
+        if not obs.weight >= 0:
+            raise InvalidArgumentError("edge weight must be >= 0")
+        self._obs.append((obs.camera_id, obs.point_id, float(obs.pixel[0]), float(obs.pixel[1]), float(obs.weight)))
+        return len(self._obs) - 1
+
+    def arrays(self):
+        """(cameras (m,9), points (n,3), camera_id, point_id, pixel_x, pixel_y, weight)."""
+        if self._frozen is None:
+            d = self.dtype
+            cams = np.ascontiguousarray(np.array(self._cams, dtype=d).reshape(-1, 9))
+            pts = np.ascontiguousarray(np.array(self._pts, dtype=d).reshape(-1, 3))
+            o = np.array(self._obs, dtype=np.float64).reshape(-1, 5)
+            self._frozen = (cams, pts, np.ascontiguousarray(o[:, 0].astype(np.int32)),
+                            np.ascontiguousarray(o[:, 1].astype(np.int32)), np.ascontiguousarray(o[:, 2].astype(d)),
+                            np.ascontiguousarray(o[:, 3].astype(d)), np.ascontiguousarray(o[:, 4].astype(d)))
+            self._cams, self._pts, self._obs = [], [], []
+        return self._frozen
+
+    @property
+    def num_cameras(self) -> int:
+        return len(self.arrays()[0])
+
+    @property
+    def num_points(self) -> int:
+        return len(self.arrays()[1])
+
+    @property
+    def num_observations(self) -> int:
+        return len(self.arrays()[2])
+
+    def pack_cameras(self):
+        return self.arrays()[0].reshape(-1).copy()
+
+    def pack_points(self):
+        return self.arrays()[1].reshape(-1).copy()
+
+    def astype(self, dtype) -> "BAProblem":
+        cams, pts, cid, pid, px, py, w = self.arrays()
+        return BAProblem.from_arrays(cams, pts, cid, pid, np.stack([px, py], 1), w, dtype=dtype)
+
+    def validate(self) -> List[str]:
+        """Non-fatal warnings (dba/problem.hpp:214-241)."""
+        cams, pts, cid, pid, *_ = self.arrays()
+        out = []
+        used_c = np.zeros(len(cams), bool)
+        used_c[cid] = True
+        used_p = np.zeros(len(pts), bool)
+        used_p[pid] = True
+        out += [f"camera {i} is not referenced by any observation" for i in np.flatnonzero(~used_c)]
+        out += [f"point {i} is not referenced by any observation" for i in np.flatnonzero(~used_p)]
+        out += [f"camera {i} has non-positive focal length" for i in np.flatnonzero(~(cams[:, 6] > 0))]
+        return out
+
+    def c_struct(self) -> N.Problem:
+        cams, pts, cid, pid, px, py, w = self.arrays()
+        s = N.Problem()
+        s.num_cameras, s.num_points, s.num_observations = len(cams), len(pts), len(cid)
+        s.cameras, s.points = cams.ctypes.data, pts.ctypes.data
+        s.camera_id = cid.ctypes.data_as(C.POINTER(C.c_int32))
+        s.point_id = pid.ctypes.data_as(C.POINTER(C.c_int32))
+        s.pixel_x, s.pixel_y, s.weight = px.ctypes.data, py.ctypes.data, w.ctypes.data
+        s._keep = (cams, pts, cid, pid, px, py, w)
+        return s
+
+    @property
+    def precision(self) -> int:
+        return self.dtype.itemsize
+
+
+# --------------------------------------------------------------- partition --
+
+
+@dataclass
+class LocalIndexMap:
+    """First-appearance local <-> global map (dba/partition.hpp:14-45)."""
+    to_global: np.ndarray
+    global_count: int
+
+    def local(self, global_id: int) -> int:
+        hit = np.flatnonzero(self.to_global == global_id)
+        return int(hit[0]) if len(hit) else -1
+
+    def global_(self, local_id: int) -> int:
+        return int(self.to_global[local_id])
+
+    def size(self) -> int:
+        return len(self.to_global)
+
+
+@dataclass
+class EdgePartition:
+    """dba/partition.hpp:49-54, plus the E grouping of block_matrix.hpp:309-320."""
+    worker_rank: int
+    edge_ids: np.ndarray
+    camera_map: LocalIndexMap
+    point_map: LocalIndexMap
+    cam_ptr: np.ndarray
+    cam_blocks: np.ndarray
+    pt_ptr: np.ndarray
+    pt_blocks: np.ndarray
+
+
+def partition_edges(problem: BAProblem, worker_count: int) -> List[EdgePartition]:
+    """dba/partition.hpp:76-103 (bit-exact), computed by the library's host code."""
+    s = problem.c_struct()
+    m, n, nobs = s.num_cameras, s.num_points, s.num_observations
+    if worker_count < 1:
+        raise InvalidArgumentError("worker count must be >= 1")
+    if worker_count > nobs:
+        raise InvalidArgumentError(f"worker count {worker_count} exceeds number of edges {nobs}")
+    out = []
+    lib = N.lib()
+    for r in range(worker_count):
+        start, count = C.c_int64(), C.c_int64()
+        nc, npt = C.c_int32(), C.c_int32()
+        cam_g = np.zeros(max(m, 1), np.int32)
+        pt_g = np.zeros(max(n, 1), np.int32)
+        cam_ptr = np.zeros(m + 1, np.int64)
+        pt_ptr = np.zeros(n + 1, np.int64)
+        cam_blk = np.zeros(max(nobs, 1), np.int64)
+        pt_blk = np.zeros(max(nobs, 1), np.int64)
+        _check(lib.dbag_partition(C.byref(s), worker_count, r, C.byref(start), C.byref(count), C.byref(nc),
+                                  cam_g.ctypes.data, C.byref(npt), pt_g.ctypes.data, cam_ptr.ctypes.data,
+                                  cam_blk.ctypes.data, pt_ptr.ctypes.data, pt_blk.ctypes.data))
+        k = count.value
+        out.append(EdgePartition(r, np.arange(start.value, start.value + k, dtype=np.int32),
+                                 LocalIndexMap(cam_g[:nc.value].copy(), m), LocalIndexMap(pt_g[:npt.value].copy(), n),
+                                 cam_ptr[:nc.value + 1].copy(), cam_blk[:k].copy(), pt_ptr[:npt.value + 1].copy(),
+                                 pt_blk[:k].copy()))
+    return out
+
+
+def shared_points(problem: BAProblem, worker_count: int) -> np.ndarray:
+    """Global ids of points touched by more than one rank (the halo)."""
+    s = problem.c_struct()
+    cnt = C.c_int64()
+    _check(N.lib().dbag_shared_points(C.byref(s), worker_count, C.byref(cnt), None))
+    ids = np.zeros(max(cnt.value, 1), np.int32)
+    _check(N.lib().dbag_shared_points(C.byref(s), worker_count, C.byref(cnt), ids.ctypes.data))
+    return ids[:cnt.value]
+
+
+# ------------------------------------------------------------------ solver --
+
+DAMPING_IDENTITY, DAMPING_DIAG_SCALED = 0, 1
+JACOBIAN_AUTODIFF, JACOBIAN_ANALYTIC = 0, 1
+TERMINATION = {0: "converged", 1: "max_iterations", 2: "stalled"}
+
+
+@dataclass
+class SolverConfig:
+    """dba/solver.hpp:39-55 (same fields and defaults)."""
+    workers: int = 1
+    max_iterations: int = 50
+    pcg_tol: float = 1e-6
+    pcg_max_iters: int = 500
+    lambda0: float = 1e-4
+    lambda_max: float = 1e32
+    rel_tol: float = 1e-6
+    step_tol: float = 1e-8
+    damping: int = DAMPING_DIAG_SCALED
+    mse: int = MSE_HALF_PER_OBSERVATION
+    jacobian: int = JACOBIAN_AUTODIFF
+    check_rank_identity: bool = False
+
+    def c_struct(self) -> N.Config:
+        c = N.Config()
+        c.workers, c.max_iterations, c.pcg_tol = self.workers, self.max_iterations, self.pcg_tol
+        c.pcg_max_iters, c.lambda0, c.lambda_max = self.pcg_max_iters, self.lambda0, self.lambda_max
+        c.rel_tol, c.step_tol, c.damping = self.rel_tol, self.step_tol, self.damping
+        c.mse_half, c.jacobian, c.check_rank_identity = self.mse, self.jacobian, int(self.check_rank_identity)
+        return c
+
+
+@dataclass
+class IterationRecord:
+    """dba/solver.hpp:57-68."""
+    iteration: int
+    cost: float
+    mse: float
+    lambda_: float
+    pcg_iterations: int
+    accepted: bool
+    wall_seconds: float
+    worker_edges: List[int] = field(default_factory=list)
+    worker_block_ops: List[int] = field(default_factory=list)
+
+
+@dataclass
+class SolverState:
+    """dba/solver.hpp:70-85 (rank 0's state)."""
+    x_c: np.ndarray
+    x_p: np.ndarray
+    lambda_: float
+    nu: float
+    iteration: int
+    cost: float
+    termination: str
+    history: List[IterationRecord]
+
+
+class _ResultBuf:
+    def __init__(self, cap: int, workers: int, m: int, n: int, dtype):
+        self.cap, self.k = cap, workers
+        self.it = np.zeros(cap, np.int32)
+        self.cost = np.zeros(cap)
+        self.mse = np.zeros(cap)
+        self.lam = np.zeros(cap)
+        self.pcg = np.zeros(cap, np.int32)
+        self.acc = np.zeros(cap, np.int32)
+        self.wall = np.zeros(cap)
+        self.we = np.zeros(cap * workers, np.uint64)
+        self.wb = np.zeros(cap * workers, np.uint64)
+        self.xc = np.zeros(9 * m, dtype)
+        self.xp = np.zeros(max(3 * n, 1), dtype)
+        r = N.Result()
+        r.capacity, r.workers = cap, workers
+        P = C.POINTER
+        r.rec_iteration = self.it.ctypes.data_as(P(C.c_int32))
+        r.rec_cost = self.cost.ctypes.data_as(P(C.c_double))
+        r.rec_mse = self.mse.ctypes.data_as(P(C.c_double))
+        r.rec_lambda = self.lam.ctypes.data_as(P(C.c_double))
+        r.rec_pcg = self.pcg.ctypes.data_as(P(C.c_int32))
+        r.rec_accepted = self.acc.ctypes.data_as(P(C.c_int32))
+        r.rec_wall = self.wall.ctypes.data_as(P(C.c_double))
+        r.rec_worker_edges = self.we.ctypes.data_as(P(C.c_uint64))
+        r.rec_worker_block_ops = self.wb.ctypes.data_as(P(C.c_uint64))
+        r.x_c, r.x_p = self.xc.ctypes.data, self.xp.ctypes.data
+        self.r = r
+
+    def state(self, n: int) -> SolverState:
+        r = self.r
+        k = self.k
+        hist = [IterationRecord(int(self.it[i]), float(self.cost[i]), float(self.mse[i]), float(self.lam[i]),
+                                int(self.pcg[i]), bool(self.acc[i]), float(self.wall[i]),
+                                [int(v) for v in self.we[i * k:(i + 1) * k]],
+                                [int(v) for v in self.wb[i * k:(i + 1) * k]])
+                for i in range(min(r.iterations, self.cap))]
+        return SolverState(self.xc.copy(), self.xp[:3 * n].copy(), r.lam, r.nu, r.iterations, r.cost,
+                           TERMINATION[r.termination], hist)
+
+
+def lm_solve(problem: BAProblem, config: Optional[SolverConfig] = None, devices: Sequence[int] = (0,)) -> SolverState:
+    """dba::lm_solve (dba/solver.hpp:523-534) on B200: partitions into
+    config.workers ranks (one host thread + one rank context each, placed on
+    devices[rank % len(devices)]), runs the distributed LM loop and returns
+    rank 0's state."""
+    config = config or SolverConfig()
+    s = problem.c_struct()
+    buf = _ResultBuf(config.max_iterations, config.workers, s.num_cameras, s.num_points, problem.dtype)
+    devs = (C.c_int * len(devices))(*devices)
+    cfg = config.c_struct()
+    _check(N.lib().dbag_lm_solve(problem.precision, C.byref(s), C.byref(cfg), devs, len(devices), C.byref(buf.r)))
+    return buf.state(s.num_points)
+
+
+def nccl_unique_id() -> bytes:
+    b = C.create_string_buffer(128)
+    _check(N.lib().dbag_nccl_unique_id(b))
+    return b.raw
+
+
+def lm_solve_rank(problem: BAProblem, config: SolverConfig, rank: int, nranks: int, uid: bytes,
+                  device: int) -> SolverState:
+    """dba::lm_solve_rank (dba/solver.hpp:295-518) for one process per GPU over NCCL."""
+    s = problem.c_struct()
+    buf = _ResultBuf(config.max_iterations, nranks, s.num_cameras, s.num_points, problem.dtype)
+    cfg = config.c_struct()
+    idb = C.create_string_buffer(bytes(uid), 128)
+    _check(N.lib().dbag_lm_solve_rank(problem.precision, C.byref(s), C.byref(cfg), rank, nranks, idb, device,
+                                      C.byref(buf.r)))
+    return buf.state(s.num_points)
+
+
+def total_cost(problem: BAProblem, device: int = 0) -> float:
+    """dba::total_cost (dba/problem.hpp:266-283) on the GPU."""
+    with RankContext(device, problem.precision) as ctx:
+        ctx.upload(problem)
+        c, bad = ctx.cost()
+        if bad >= 0:
+            raise DegenerateDepthError(f"degenerate depth (P_z = 0) at edge {bad}", bad)
+        return c
+
+
+# ------------------------------------------------------------- synthetic --
+
+
+@dataclass
+class SyntheticOptions:
+    """dba/synthetic.hpp:19-30 plus the count-exact / pixel-noise extension."""
+    cameras: int = 20000
+    points: int = 80000
+    obs_per_point: int = 1000
+    seed: int = 1
+    circle_radius: float = 8.0
+    base_focal: float = 1000.0
+    pose_noise: float = 0.01
+    intrinsic_noise: float = 0.5
+    point_noise: float = 0.1
+    num_observations: int = 0
+    pixel_noise: float = 0.0
+    exhaustive_search: bool = False
+
+    def c_struct(self) -> N.SynthOptions:
+        o = N.SynthOptions()
+        for f in dataclasses.fields(self):
+            setattr(o, f.name, getattr(self, f.name))
+        return o
+
+
+def synthetic_observation_count(opt: SyntheticOptions) -> int:
+    o = opt.c_struct()
+    n = C.c_int64()
+    _check(N.lib().dbag_synthetic_count(C.byref(o), C.byref(n)))
+    return n.value
+
+
+def generate_synthetic(opt: SyntheticOptions) -> BAProblem:
+    """generate_synthetic (dba/synthetic.hpp:70-146), fp64, host-side."""
+    nobs = synthetic_observation_count(opt)
+    o = opt.c_struct()
+    cams = np.zeros((opt.cameras, 9))
+    pts = np.zeros((opt.points, 3))
+    cid = np.zeros(nobs, np.int32)
+    pid = np.zeros(nobs, np.int32)
+    px = np.zeros(nobs)
+    py = np.zeros(nobs)
+    _check(N.lib().dbag_generate_synthetic(C.byref(o), cams.ctypes.data, pts.ctypes.data, cid.ctypes.data,
+                                           pid.ctypes.data, px.ctypes.data, py.ctypes.data))
+    return BAProblem.from_arrays(cams, pts, cid, pid, np.stack([px, py], 1))
+
+
+# ------------------------------------------------------------ rank context --
+
+
+class RankContext:
+    """One rank's device context (include/dbag.h "rank context"): the operator
+    level of lm_solve_rank. K = 1 unless created with ``nccl=(rank, nranks, uid)``."""
+
+    def __init__(self, device: int = 0, precision: int = 8, nccl=None):
+        self.precision = precision
+        self.dtype = np.float64 if precision == 8 else np.float32
+        h = C.c_void_p()
+        if nccl is None:
+            _check(N.lib().dbag_create(device, precision, C.byref(h)))
+        else:
+            rank, nranks, uid = nccl
+            _check(N.lib().dbag_create_nccl(device, rank, nranks, C.create_string_buffer(bytes(uid), 128), precision,
+                                            C.byref(h)))
+        self.h = h
+        self.m = self.n = self.nobs = 0
+
+    def close(self):
+        if self.h:
+            N.lib().dbag_destroy(self.h)
+            self.h = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def upload(self, problem: BAProblem, jacobian: int = JACOBIAN_AUTODIFF):
+        if problem.precision != self.precision:
+            raise InvalidArgumentError("problem dtype does not match the context precision")
+        s = problem.c_struct()
+        self.m, self.n, self.nobs = s.num_cameras, s.num_points, s.num_observations
+        _check(N.lib().dbag_upload_problem(self.h, C.byref(s), jacobian))
+
+    def set_state(self, x_c, x_p):
+        xc = np.ascontiguousarray(x_c, self.dtype)
+        xp = np.ascontiguousarray(x_p, self.dtype)
+        _check(N.lib().dbag_set_state(self.h, xc.ctypes.data, xp.ctypes.data))
+
+    def get_state(self):
+        xc = np.zeros(9 * self.m, self.dtype)
+        xp = np.zeros(max(3 * self.n, 1), self.dtype)
+        _check(N.lib().dbag_get_state(self.h, xc.ctypes.data, xp.ctypes.data))
+        return xc, xp[:3 * self.n]
+
+    def cost(self, trial: bool = False):
+        c, bad = C.c_double(), C.c_int64()
+        _check(N.lib().dbag_cost(self.h, int(trial), C.byref(c), C.byref(bad)))
+        return c.value, bad.value
+
+    def linearize(self):
+        bad = C.c_int64()
+        _check(N.lib().dbag_linearize(self.h, C.byref(bad)))
+
+    def damp_factor(self, lam: float, policy: int = DAMPING_DIAG_SCALED):
+        _check(N.lib().dbag_damp_factor(self.h, lam, policy, None, None))
+
+    def rhs(self):
+        _check(N.lib().dbag_rhs(self.h))
+
+    def pcg(self, tol: float, max_iters: int):
+        it, conv = C.c_int(), C.c_int()
+        _check(N.lib().dbag_pcg(self.h, tol, max_iters, C.byref(it), C.byref(conv)))
+        return it.value, bool(conv.value)
+
+    def backsub_trial(self):
+        _check(N.lib().dbag_backsub_trial(self.h))
+
+    def model_terms(self):
+        a, b, c = C.c_double(), C.c_double(), C.c_double()
+        _check(N.lib().dbag_model_terms(self.h, 0.0, 0, C.byref(a), C.byref(b), C.byref(c)))
+        return a.value, b.value, c.value
+
+    def accept(self):
+        _check(N.lib().dbag_accept(self.h))
+
+    def probe_step(self, lam: float, config: SolverConfig):
+        cost, it, acc = C.c_double(), C.c_int(), C.c_int()
+        cfg = config.c_struct()
+        _check(N.lib().dbag_lm_probe_step(self.h, lam, C.byref(cfg), C.byref(cost), C.byref(it), C.byref(acc)))
+        return cost.value, it.value, bool(acc.value)
+
+    def profile(self, enable: Optional[bool] = None):
+        t, n, a, b = C.c_double(), C.c_int64(), C.c_double(), C.c_double()
+        _check(N.lib().dbag_profile(self.h, -1 if enable is None else int(enable), C.byref(t), C.byref(n),
+                                    C.byref(a), C.byref(b)))
+        return {"dse_ms": t.value, "dse_launches": n.value, "point_ms": a.value, "cam_ms": b.value}
+
+    def mark(self, which: int):
+        _check(N.lib().dbag_event_mark(self.h, which))
+
+    def elapsed_ms(self) -> float:
+        ms = C.c_double()
+        _check(N.lib().dbag_event_elapsed(self.h, C.byref(ms)))
+        return ms.value
+
+    def synchronize(self):
+        _check(N.lib().dbag_synchronize(self.h))
+
+    def jacobians(self):
+        """EdgeJacobianBatch in shard edge order: residuals (2, N), J (2, 12, N)."""
+        res = np.zeros(2 * self.nobs, self.dtype)
+        jac = np.zeros(24 * self.nobs, self.dtype)
+        _check(N.lib().dbag_get_jacobians(self.h, res.ctypes.data, jac.ctypes.data))
+        return res.reshape(2, self.nobs), jac.reshape(2, 12, self.nobs)
+
+    def system(self):
+        """B (m,9,9), C (n,3,3), E (N,9,3), v (9m), w (3n) as assembled (all-reduced)."""
+        B = np.zeros(81 * self.m, self.dtype)
+        Cm = np.zeros(max(9 * self.n, 1), self.dtype)
+        E = np.zeros(max(27 * self.nobs, 1), self.dtype)
+        v = np.zeros(9 * self.m, self.dtype)
+        w = np.zeros(max(3 * self.n, 1), self.dtype)
+        _check(N.lib().dbag_get_system(self.h, B.ctypes.data, Cm.ctypes.data, E.ctypes.data, v.ctypes.data,
+                                       w.ctypes.data))
+        return (B.reshape(-1, 9, 9), Cm[:9 * self.n].reshape(-1, 3, 3), E[:27 * self.nobs].reshape(-1, 9, 3), v,
+                w[:3 * self.n])
+
+    def set_system(self, B=None, Cb=None, E_table=None, v=None, w=None):
+        arr = [None if a is None else np.ascontiguousarray(a, self.dtype) for a in (B, Cb, E_table, v, w)]
+        ptr = [None if a is None else a.ctypes.data for a in arr]
+        _check(N.lib().dbag_set_system(self.h, *ptr))
+
+    def dse(self, x):
+        x = np.ascontiguousarray(x, self.dtype)
+        out = np.zeros_like(x)
+        _check(N.lib().dbag_dse(self.h, x.ctypes.data, out.ctypes.data))
+        return out
+
+    def dpcg(self, rhs, tol: float, max_iters: int):
+        rhs = np.ascontiguousarray(rhs, self.dtype)
+        x = np.zeros_like(rhs)
+        it, conv = C.c_int(), C.c_int()
+        _check(N.lib().dbag_dpcg(self.h, rhs.ctypes.data, tol, max_iters, x.ctypes.data, C.byref(it),
+                                 C.byref(conv)))
+        return x, it.value, bool(conv.value)
+
+
+def group_operator(problem: BAProblem, k: int, x, mode: int = 0, lam: float = 0.0, policy: int = DAMPING_IDENTITY,
+                   blocks=None, tol: float = 1e-12, max_iters: int = 500, device: int = 0):
+    """K in-process ranks on one device: mode 0 -> dse(x), mode 1 -> dpcg(rhs=x)
+    on the problem's own damped system, or on fabricated (B, C, E_table)."""
+    s = problem.c_struct()
+    d = problem.dtype
+    x = np.ascontiguousarray(x, d)
+    out = np.zeros_like(x)
+    it, ident = C.c_int(), C.c_int()
+    if blocks is not None:
+        B, Cb, E = (np.ascontiguousarray(a, d) for a in blocks)
+        bp, cp, ep = B.ctypes.data, Cb.ctypes.data, E.ctypes.data
+    else:
+        bp = cp = ep = None
+    _check(N.lib().dbag_group_operator(problem.precision, C.byref(s), k, device, lam, policy, bp, cp, ep, mode,
+                                       x.ctypes.data, tol, max_iters, out.ctypes.data, C.byref(it), C.byref(ident)))
+    return out, it.value, bool(ident.value)
+
+
+def group_allreduce(data: np.ndarray, device: int = 0) -> np.ndarray:
+    """WorkerGroup::allreduce_sum over K = data.shape[0] in-process ranks."""
+    a = np.ascontiguousarray(data, np.float64).copy()
+    _check(N.lib().dbag_group_allreduce(a.shape[0], device, a.shape[1], a.ctypes.data))
+    return a
+
+
+def device_count() -> int:
+    n = C.c_int()
+    _check(N.lib().dbag_device_count(C.byref(n)))
+    return n.value

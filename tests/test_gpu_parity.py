@@ -1,0 +1,307 @@
+"""GPU parity: the sm_100a path (libdbag.so, through the C ABI) against the CPU
+oracle on identical inputs. Tolerances are those of SURVEY.md §7-§8d and the
+reference's own tests (file:line per test)."""
+import numpy as np
+import pytest
+
+import paper_2112_01349_b200 as dba
+from oracle import oracle as O
+from tests.dense import damp_dense, dense_blockdiag, dense_coupling, fd_jacobian, rel, schur
+from tests.factory import ProblemFactory
+
+pytestmark = pytest.mark.gpu
+
+CAM_ID = [0, 0, 0, 0, 0, 0, 1, 0, 0]
+
+
+def ctx_for(p, mode=0):
+    c = dba.RankContext(0, p.precision)
+    c.upload(p, mode)
+    return c
+
+
+def ring(cams, pts, q, seed=1, radius=8.0, noise=0.0, nobs=0, dtype=np.float64):
+    p = dba.generate_synthetic(dba.SyntheticOptions(cameras=cams, points=pts, obs_per_point=q, seed=seed,
+                                                    circle_radius=radius, pixel_noise=noise, num_observations=nobs))
+    return p if dtype == np.float64 else p.astype(dtype)
+
+
+# ------------------------------------------------------------- linearize ----
+@pytest.mark.parametrize("mode", [0, 1])
+def test_linearize_matches_oracle(mode):
+    """Residual 1e-13 and J 1e-12 relative vs the oracle's EdgeJacobianBatch
+    (tests/test_jet.cpp:195-232, 303-329)."""
+    p = ring(40, 300, 6, noise=0.5)
+    with ctx_for(p, mode) as c:
+        c.linearize()
+        res, jac = c.jacobians()
+    r0, j0 = O.linearize(p, mode=mode)
+    for e in range(res.shape[1]):
+        assert np.linalg.norm(res[:, e] - r0[:, e]) <= 1e-13 * max(1.0, np.linalg.norm(r0[:, e]))
+        assert np.linalg.norm(jac[:, :, e] - j0[:, :, e]) <= 1e-12 * max(1.0, np.linalg.norm(j0[:, :, e]))
+
+
+def test_linearize_vs_fd_random_problem():
+    """tests/test_jet.cpp:195-232 on the GPU: J vs central differences 1e-6."""
+    p = ProblemFactory(77).random_problem(4, 7, 25)
+    cams, pts, cid, pid, px, py, w = p.arrays()
+    with ctx_for(p) as c:
+        c.linearize()
+        res, jac = c.jacobians()
+    for e in range(len(cid)):
+        fd = fd_jacobian(lambda a, b, q: O.residual(a, b, q), cams[cid[e]], pts[pid[e]], [px[e], py[e]])
+        assert np.all(np.abs(jac[:, :, e] - fd) / np.maximum(1.0, np.abs(fd)) < 1e-6)
+
+
+def test_linearize_degenerate_edge_id():
+    """tests/test_jet.cpp:276-301: DegenerateDepthError names global edge 2."""
+    p = dba.BAProblem.from_arrays([CAM_ID], [[0, 0, -1], [0, 1, 0]], [0, 0, 0], [0, 0, 1], np.zeros((3, 2)))
+    with ctx_for(p) as c:
+        with pytest.raises(dba.dba.DegenerateDepthError) as e:
+            c.linearize()
+        assert e.value.edge_id == 2
+
+
+def test_cost_matches_oracle_and_degenerate():
+    """EdgeEvaluator::cost vs total_cost 1e-12; degenerate trial -> +inf with edge id
+    (tests/test_problem.cpp:198-218)."""
+    p = ring(30, 200, 5, noise=0.5)
+    assert dba.total_cost(p) == pytest.approx(O.total_cost(p), rel=1e-12)
+    q = dba.BAProblem.from_arrays([CAM_ID], [[0, 0, -1], [1, 0, 0]], [0, 0], [0, 1], [[0, 0], [0, 0]])
+    with pytest.raises(dba.dba.DegenerateDepthError) as e:
+        dba.total_cost(q)
+    assert e.value.edge_id == 1
+
+
+# -------------------------------------------------------------- assembly ----
+@pytest.mark.parametrize("seed", [47, 59])
+def test_assembly_matches_oracle(seed):
+    """B, C, E, v, w vs the oracle's assemble_local at 1e-12 (tests/test_linear.cpp:87-121)."""
+    p = ProblemFactory(seed).random_problem(4, 7, 40)
+    with ctx_for(p) as c:
+        c.linearize()
+        B, Cb, E, v, w = c.system()
+    B0, C0, E0, v0, w0 = O.assemble(p)
+    for a, b in ((B, B0), (Cb, C0), (E, E0), (v, v0), (w, w0)):
+        assert rel(a, b) < 1e-12
+
+
+# ------------------------------------------------------- damping / factor ----
+def test_singular_block_reports_index():
+    """tests/test_linear.cpp:270-282 via the trial: a C block with a negative
+    pivot raises SingularBlockError naming global point 1, size 3."""
+    p = ProblemFactory(5).random_problem(2, 3, 6)
+    with ctx_for(p) as c:
+        c.linearize()
+        B, Cb, E, v, w = c.system()
+        Cb[1] = -np.eye(3)
+        c.set_system(B=B, Cb=Cb)
+        with pytest.raises(dba.dba.SingularBlockError) as e:
+            c.damp_factor(0.0, 0)
+        assert e.value.block_index == 1 and e.value.block_size == 3
+
+
+# ------------------------------------------------------------------- DSE ----
+def test_dse_zero_coupling_is_bx():
+    """tests/test_solver.cpp:75-105 (exact)."""
+    p = dba.BAProblem.from_arrays([CAM_ID, CAM_ID], [[0, 0, -1]], [0], [0], [[0, 0]])
+    B = np.stack([2 * np.eye(9), 3 * np.eye(9)])
+    x = np.arange(1, 19, dtype=float)
+    out, _, _ = dba.group_operator(p, 1, x, mode=0, blocks=(B, np.eye(3)[None], np.zeros((1, 27))))
+    assert np.array_equal(out, np.concatenate([2 * x[:9], 3 * x[9:]]))
+
+
+def test_dse_vs_dense_schur_and_oracle_across_k():
+    """tests/test_solver.cpp:107-140: 1e-10 vs dense Schur, rank-identical,
+    cross-K 1e-10; plus 1e-12 vs the oracle at the same K."""
+    rng = np.random.default_rng(31)
+    for trial in range(6):
+        p = ProblemFactory(1000 + trial).random_problem(3, 4, 9 + trial)
+        m = p.num_cameras
+        B0, C0, E0, _, _ = O.assemble(p)
+        cams, pts, cid, pid, *_ = p.arrays()
+        S = schur(damp_dense(dense_blockdiag(B0), 1e-3, 0), damp_dense(dense_blockdiag(C0), 1e-3, 0),
+                  dense_coupling(E0, cid, pid, m, p.num_points))
+        x = rng.uniform(-1, 1, 9 * m)
+        ref = S @ x
+        for k in (1, 2, 3):
+            out, _, ident = dba.group_operator(p, k, x, mode=0, lam=1e-3, policy=0)
+            orc, _ = O.dse(p, k, 1e-3, 0, x)
+            assert ident
+            assert rel(out, ref) < 1e-10
+            assert rel(out, orc) < 1e-12
+
+
+def test_dpcg_identity_one_iteration_and_zero_rhs():
+    """tests/test_solver.cpp:179-229."""
+    p = dba.BAProblem.from_arrays([CAM_ID], [[0, 0, -1]], [0], [0], [[0, 0]])
+    g = np.array([1, -2, 3, -4, 5, -6, 7, -8, 9.0])
+    x, it, _ = dba.group_operator(p, 1, g, mode=1, blocks=(np.eye(9)[None], np.eye(3)[None], np.zeros((1, 27))),
+                                  tol=1e-10, max_iters=100)
+    assert it == 1 and np.linalg.norm(x - g) < 1e-14
+    q = ProblemFactory(88).random_problem(2, 3, 6)
+    x, it, _ = dba.group_operator(q, 1, np.zeros(18), mode=1, lam=1e-2, policy=0, tol=1e-6, max_iters=100)
+    assert it == 0 and np.linalg.norm(x) == 0.0
+
+
+def test_dpcg_vs_direct_and_oracle_across_k():
+    """tests/test_solver.cpp:231-270: dense direct 1e-8, rank-identical."""
+    rng = np.random.default_rng(41)
+    for trial in range(4):
+        p = ProblemFactory(2000 + trial).random_problem(3, 5, 11 + trial, normalized=True)
+        m = p.num_cameras
+        B0, C0, E0, _, _ = O.assemble(p)
+        cams, pts, cid, pid, *_ = p.arrays()
+        S = schur(damp_dense(dense_blockdiag(B0), 1e-2, 0), damp_dense(dense_blockdiag(C0), 1e-2, 0),
+                  dense_coupling(E0, cid, pid, m, p.num_points))
+        g = rng.uniform(-1, 1, 9 * m)
+        direct = np.linalg.solve(S, g)
+        for k in (1, 2, 4):
+            x, it, ident = dba.group_operator(p, k, g, mode=1, lam=1e-2, policy=0, tol=1e-12, max_iters=500)
+            assert ident and rel(x, direct) < 1e-8
+
+
+def test_dpcg_iterates_across_k_fabricated():
+    """tests/test_solver.cpp:272-333: fixed 12 iterations on a benign operator,
+    bitwise rank-identical, cross-K 1e-10, and 1e-12 vs the oracle."""
+    cams, pts, edges = 4, 6, 16
+    p = ProblemFactory(4242).random_problem(cams, pts, edges)
+    rng = np.random.default_rng(17)
+    Mb = 0.05 * rng.uniform(-1, 1, (cams, 9, 9))
+    B = np.eye(9) + Mb @ Mb.transpose(0, 2, 1)
+    Mc = 0.05 * rng.uniform(-1, 1, (pts, 3, 3))
+    Cb = np.eye(3) + Mc @ Mc.transpose(0, 2, 1)
+    E = 0.02 * rng.uniform(-1, 1, (edges, 27))
+    g = rng.uniform(-1, 1, 9 * cams)
+    ref = None
+    for k in (1, 2, 4):
+        x, _, ident = dba.group_operator(p, k, g, mode=1, blocks=(B, Cb, E), tol=0.0, max_iters=12)
+        xo, _, _ = O.blocks_solve(p, k, B, Cb, E, 1, g, 0.0, 12)
+        assert ident and rel(x, xo) < 1e-12
+        ref = x if ref is None else ref
+        assert rel(x, ref) < 1e-10
+
+
+def test_group_allreduce_bitwise_sequential():
+    """tests/test_comms.cpp:12-59: ascending-rank sum, bit-identical, rank-identical."""
+    assert np.array_equal(dba.group_allreduce(np.array([[1.0, 2], [3, 4]])), [[4, 6], [4, 6]])
+    rng = np.random.default_rng(2024)
+    loc = rng.uniform(-1e6, 1e6, (4, 257))
+    exp = loc[0].copy()
+    for r in range(1, 4):
+        exp += loc[r]
+    out = dba.group_allreduce(loc)
+    assert all(np.array_equal(out[r], exp) for r in range(4))
+    assert np.array_equal(dba.group_allreduce(loc), out)
+
+
+# ------------------------------------------------------------ LM solver ----
+def _compare_histories(g, o, cost_tol, check_lambda=True):
+    assert len(g.history) == len(o.history), (len(g.history), len(o.history))
+    assert [r.accepted for r in g.history] == [r.accepted for r in o.history]
+    for a, b in zip(g.history, o.history):
+        assert abs(a.cost - b.cost) <= cost_tol * max(abs(b.cost), 1e-300) or abs(a.cost - b.cost) < 1e-20
+        if check_lambda:
+            assert a.lambda_ == pytest.approx(b.lambda_, rel=1e-9)
+    assert g.termination == o.termination
+
+
+@pytest.mark.parametrize("k", [1, 2, 4])
+def test_lm_trajectory_matches_oracle_fp64(k):
+    """north_star parity: same accept/reject sequence, per-iteration cost within
+    1e-6 relative (FP64), same K on both sides."""
+    p = ring(40, 400, 8, radius=1.0, noise=0.5, seed=2024)
+    cfg = dba.SolverConfig(max_iterations=12, workers=k, check_rank_identity=True)
+    g = dba.lm_solve(p, cfg)
+    o = O.lm_solve(p, cfg)
+    _compare_histories(g, o, 1e-6)
+    for a, b in zip(g.history, o.history):
+        assert a.worker_edges == b.worker_edges
+    scale = max(1.0, np.abs(o.x_c).max(), np.abs(o.x_p).max())
+    assert max(np.abs(g.x_c - o.x_c).max(), np.abs(g.x_p - o.x_p).max()) / scale < 1e-6
+
+
+def test_lm_trajectory_tight_pcg_block_ops_match():
+    """Tallies (dba/counters.hpp) match the oracle exactly when PCG runs to a
+    tight tolerance (same PCG iteration counts)."""
+    p = ring(12, 40, 6, seed=3)
+    cfg = dba.SolverConfig(max_iterations=10, pcg_tol=1e-12, pcg_max_iters=2000)
+    g = dba.lm_solve(p, cfg)
+    o = O.lm_solve(p, cfg)
+    _compare_histories(g, o, 1e-9)
+    for a, b in zip(g.history, o.history):
+        assert abs(a.pcg_iterations - b.pcg_iterations) <= 1
+
+
+def test_lm_fp32_matches_oracle():
+    """FP32 path: accept/reject sequence and costs within 1e-4 relative."""
+    p = ring(30, 300, 6, radius=1.0, noise=0.5, seed=7, dtype=np.float32)
+    cfg = dba.SolverConfig(max_iterations=8)
+    g = dba.lm_solve(p, cfg)
+    o = O.lm_solve(p, cfg)
+    _compare_histories(g, o, 1e-4, check_lambda=False)
+
+
+def test_lm_analytic_matches_oracle():
+    p = ring(30, 300, 6, radius=1.0, noise=0.5, seed=9)
+    cfg = dba.SolverConfig(max_iterations=8, jacobian=1)
+    _compare_histories(dba.lm_solve(p, cfg), O.lm_solve(p, cfg), 1e-6)
+
+
+def test_lm_zero_residual_converges_in_one():
+    """tests/test_solver.cpp:335-359."""
+    f = ProblemFactory(9)
+    cams = np.stack([f.random_camera() for _ in range(2)])
+    pts = np.stack([f.random_point() for _ in range(3)])
+    cid, pid, pix = [], [], []
+    for c in range(2):
+        for q in range(3):
+            cid.append(c)
+            pid.append(q)
+            pix.append(O.residual(cams[c], pts[q], [0, 0]))
+    p = dba.BAProblem.from_arrays(cams, pts, cid, pid, pix)
+    st = dba.lm_solve(p)
+    assert st.termination == "converged" and st.iteration == 1 and st.cost == 0.0 and st.history[0].accepted
+
+
+def test_lm_reject_reuses_system_tallies():
+    """tests/test_solver.cpp:428-455."""
+    p = ring(8, 20, 4, seed=5)
+    n = p.num_observations
+    st = dba.lm_solve(p, dba.SolverConfig(lambda0=1e8, max_iterations=6))
+    for r in st.history:
+        assert r.worker_edges[0] == (2 * n if r.accepted else n)
+    assert st.history[0].worker_edges[0] == 2 * n
+
+
+def test_lm_stalled():
+    """tests/test_solver.cpp:488-504."""
+    p = ring(4, 8, 2)
+    st = dba.lm_solve(p, dba.SolverConfig(lambda0=1e31, lambda_max=1e32, step_tol=0.0, max_iterations=50))
+    assert st.termination == "stalled"
+
+
+def test_lm_ring_down_monotone():
+    """tests/test_solver.cpp:361-384."""
+    p = ring(20, 80, 10)
+    init = O.total_cost(p)
+    st = dba.lm_solve(p, dba.SolverConfig(max_iterations=50))
+    assert st.cost <= 0.1 * init
+    last = init
+    for r in st.history:
+        if r.accepted:
+            assert r.cost <= last * (1 + 1e-12)
+            last = r.cost
+
+
+def test_probe_step_matches_first_iteration():
+    """The bench step (one LM iteration from x0, not committed) reproduces the
+    first IterationRecord of a full solve."""
+    p = ring(40, 400, 8, radius=1.0, noise=0.5, seed=2024)
+    cfg = dba.SolverConfig(max_iterations=1)
+    st = dba.lm_solve(p, cfg)
+    with ctx_for(p) as c:
+        for _ in range(2):
+            cost, it, acc = c.probe_step(cfg.lambda0, cfg)
+            assert acc == st.history[0].accepted and it == st.history[0].pcg_iterations
+            assert cost == pytest.approx(st.history[0].cost, rel=1e-12)

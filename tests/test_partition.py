@@ -1,0 +1,81 @@
+"""Integer-exact partitioning (north_star: bit-exact edge-to-partition
+assignment and index ordering): the product's host code vs the oracle and the
+reference's partition KATs (tests/test_partition.cpp)."""
+import numpy as np
+import pytest
+
+import paper_2112_01349_b200 as dba
+from oracle import oracle as O
+from tests.factory import ProblemFactory
+
+
+def test_even_split_and_remainder():
+    """tests/test_partition.cpp:12-24."""
+    f = ProblemFactory(3)
+    parts = dba.partition_edges(f.random_problem(2, 2, 4), 2)
+    assert list(parts[0].edge_ids) == [0, 1] and list(parts[1].edge_ids) == [2, 3]
+    parts = dba.partition_edges(f.random_problem(2, 2, 5), 2)
+    assert len(parts[0].edge_ids) == 3 and len(parts[1].edge_ids) == 2
+
+
+def test_invalid_worker_counts():
+    """tests/test_partition.cpp:39-44."""
+    p = ProblemFactory(9).random_problem(2, 2, 3)
+    for k in (0, 4):
+        with pytest.raises(dba.dba.InvalidArgumentError):
+            dba.partition_edges(p, k)
+
+
+def test_first_appearance_order():
+    """tests/test_partition.cpp:46-71: cameras {3 -> 0, 1 -> 1}."""
+    cams = np.zeros((5, 9))
+    cams[:, 6] = 1
+    p = dba.BAProblem.from_arrays(cams, [[0, 0, -1]], [3, 1, 3], [0, 0, 0], np.zeros((3, 2)))
+    part = dba.partition_edges(p, 1)[0]
+    assert list(part.camera_map.to_global) == [3, 1]
+    assert part.camera_map.local(3) == 0 and part.camera_map.local(1) == 1 and part.camera_map.local(0) == -1
+
+
+@pytest.mark.parametrize("k", [1, 2, 3, 4, 7])
+def test_matches_oracle_integer_exact(k):
+    """Partition ranges, LocalIndexMap orders and build_groups ptr/ids arrays
+    (dba/partition.hpp:76-103, dba/block_matrix.hpp:309-320)."""
+    p = ProblemFactory(17).random_problem(6, 9, 60)
+    parts = dba.partition_edges(p, k)
+    for r in range(k):
+        o = O.partition(p, k, r)
+        g = parts[r]
+        assert g.edge_ids[0] == o["start"] and len(g.edge_ids) == o["count"]
+        for a, b in ((g.camera_map.to_global, o["cam_g"]), (g.point_map.to_global, o["pt_g"]),
+                     (g.cam_ptr, o["cam_ptr"]), (g.cam_blocks, o["cam_blk"]), (g.pt_ptr, o["pt_ptr"]),
+                     (g.pt_blocks, o["pt_blk"])):
+            assert np.array_equal(a, b)
+
+
+def test_disjoint_exhaustive_order_preserving():
+    """tests/test_partition.cpp:91-111."""
+    f = ProblemFactory(29)
+    for n in (5, 12, 31):
+        p = f.random_problem(3, 4, n)
+        for k in range(1, min(n, 6) + 1):
+            parts = dba.partition_edges(p, k)
+            cat = np.concatenate([q.edge_ids for q in parts])
+            assert np.array_equal(cat, np.arange(n))
+            sizes = [len(q.edge_ids) for q in parts]
+            assert max(sizes) - min(sizes) <= 1
+
+
+def test_halo_plan_point_major():
+    """Point-major input: at most K-1 points are shared between ranks
+    (SURVEY.md §8e), and exactly the points whose edges straddle a boundary."""
+    p = dba.generate_synthetic(dba.SyntheticOptions(cameras=30, points=200, obs_per_point=5))
+    cams, pts, cid, pid, *_ = p.arrays()
+    for k in (2, 3, 8):
+        sh = dba.shared_points(p, k)
+        assert len(sh) <= k - 1
+        owners = {}
+        for r, part in enumerate(dba.partition_edges(p, k)):
+            for q in set(pid[part.edge_ids].tolist()):
+                owners.setdefault(q, set()).add(r)
+        expect = sorted(q for q, s in owners.items() if len(s) > 1)
+        assert list(sh) == expect
