@@ -1,0 +1,324 @@
+#!/usr/bin/env python
+"""Bench: seconds per LM iteration and edges/sec (BASELINE.json `metric`).
+
+A step is one LM iteration of the reference's inner loop
+(dba/solver.hpp:330-425) on a synthetic BAL-shaped problem: linearize +
+assemble (+ all-reduce), damp + factor, rhs, DPCG to pcg_tol / pcg_max_iters,
+back-substitution, trial cost and model terms. Every step starts from the
+same state x0 at lambda0 and the accept is not committed, so each step does
+identical work (SURVEY.md §8d timing note).
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--workload NAME]
+
+N > 1 runs under torchrun, one process per GPU, NCCL between ranks.
+`--impl reference` times the CPU restatement of the reference (oracle/, the
+reference itself cannot be compiled here: Eigen/doctest/CLI11 are absent) on
+the host cores, on the same workload.
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WORKLOADS = {  # (cameras, points, observations) — BASELINE.json configs
+    "ladybug-49": (49, 7776, 31843),
+    "trafalgar-257": (257, 65132, 225911),
+    "venice-1778": (1778, 993923, 5001946),
+    "final-13682": (13682, 4456117, 28987644),
+    "city-50k": (50000, 20000000, 150000000),
+}
+DEFAULT_WORKLOAD = "trafalgar-257"  # configs[1]: the 1-B200 configuration
+SECONDARY_WORKLOAD = "venice-1778"  # configs[2]: larger than L2, HBM-bound
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def make_problem(name, dtype=np.float64):
+    import paper_2112_01349_b200 as dba
+    m, n, N = WORKLOADS[name]
+    p = dba.generate_synthetic(dba.SyntheticOptions(cameras=m, points=n, num_observations=N, seed=1,
+                                                    pixel_noise=0.5))
+    return p if dtype == np.float64 else p.astype(dtype)
+
+
+def dse_bytes(N, n, m, s):
+    """Algorithmic bytes of one DSE (SURVEY.md §8d B_DSE): one pass over E plus
+    one camera index per edge, C^-1 per point, B, x, out per camera."""
+    return N * (27 * s + 4) + 9 * n * s + 108 * m * s
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index, self.rows, self.proc = index, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) == 6:
+                self.rows.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def cpu_threads():
+    # The reference's threading model: K worker threads, one rank each
+    # (dba/comms.hpp:214-234). Its all-reduce reads K x len per rank
+    # (dba/comms.hpp:76-81), so more than 16 ranks slows it down.
+    return max(1, min(os.cpu_count() or 1, 16))
+
+
+def run_reference(args):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    from oracle import oracle as O
+    import paper_2112_01349_b200 as dba
+    m, n, N = WORKLOADS[args.workload]
+    p = make_problem(args.workload)
+    k = cpu_threads()
+    cfg = dba.SolverConfig(workers=k)
+    secs, its = O.lm_probe_steps(p, cfg, args.warmup + args.steps)
+    timed = secs[args.warmup:]
+    t = float(np.mean(timed))
+    value = N / t
+    sample = f"{args.workload} full LM iteration from x0 (oracle restatement, {k} rank threads)"
+    print(json.dumps({
+        "impl": "reference", "metric": "edges_per_sec_per_lm_iteration", "value": value, "unit": "edges/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": args.workload, "cameras": m, "points": n, "observations": N,
+                   "pcg_iterations_per_step": int(its[-1]), "solver": "SolverConfig defaults"},
+        "cpu_baseline": {"value": value, "unit": "edges/s", "cores": k, "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": "edges/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+def flush_l2(buf):
+    import torch
+    buf.zero_()
+    torch.cuda.synchronize()
+
+
+def time_steps(ctx, cfg, steps, flush):
+    """Per-step device time (CUDA events on the context's stream), L2 flushed
+    between steps outside the timed window."""
+    ms = []
+    pcg = 0
+    for _ in range(steps):
+        if flush is not None:
+            flush_l2(flush)
+        ctx.synchronize()
+        ctx.mark(0)
+        _, pcg, _ = ctx.probe_step(cfg.lambda0, cfg)
+        ctx.mark(1)
+        ms.append(ctx.elapsed_ms())
+    return ms, pcg
+
+
+def run_ours(args):
+    import torch
+    import paper_2112_01349_b200 as dba
+    world, rank, local = dist_env()
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("gloo")
+        uid = [dba.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        ctx = dba.RankContext(local, 8, nccl=(rank, world, uid[0]))
+    else:
+        ctx = dba.RankContext(0, 8)
+    torch.cuda.set_device(local)
+    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=f"cuda:{local}")
+    m, n, N = WORKLOADS[args.workload]
+    p = make_problem(args.workload)
+    ctx.upload(p)
+    cfg = dba.SolverConfig(workers=world)
+    for _ in range(args.warmup):
+        ctx.probe_step(cfg.lambda0, cfg)
+    if dist:
+        dist.barrier()
+    ctx.synchronize()
+    l0 = ctx.launch_count()
+    ctx.profile(True)
+    with ClockSampler(local) as clk:
+        ms, pcg = time_steps(ctx, cfg, args.steps, flush)
+    prof = ctx.profile()
+    ctx.profile(False)
+    launches = ctx.launch_count() - l0
+    total_ms = float(sum(ms))
+    if dist:
+        t = torch.tensor([total_ms], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t[0])
+    ms_step = total_ms / args.steps
+    value = N / (ms_step / 1e3)
+
+    # e2e through the public API with host buffers: per step the state goes
+    # host -> device, one LM iteration runs, the trial state comes back.
+    x_c, x_p = p.pack_cameras(), p.pack_points()
+    hc = torch.from_numpy(x_c).pin_memory().numpy()
+    hp = torch.from_numpy(x_p).pin_memory().numpy()
+    if dist:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        ctx.set_state(hc, hp)
+        ctx.probe_step(cfg.lambda0, cfg)
+        ctx.get_state()
+    e2e_s = (time.perf_counter() - t0) / args.steps
+    if dist:
+        t = torch.tensor([e2e_s], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t[0])
+    state_bytes = 8 * (9 * m + 3 * n)
+
+    peak, peak_kind = load_peaks()
+    per_dse_ms = prof["dse_ms"] / max(prof["dse_launches"], 1)
+    b_dse = dse_bytes(N // world, n, m, 8)
+    achieved = b_dse / (per_dse_ms / 1e3) / 1e9
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            traffic = json.load(f).get(args.workload)
+    except Exception:
+        pass
+    line = {
+        "metric": "edges_per_sec_per_lm_iteration", "value": value, "unit": "edges/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": args.workload, "cameras": m, "points": n, "observations": N,
+                   "pcg_iterations_per_step": pcg, "parallelism": f"edge-partitioned x{world}",
+                   "solver": "SolverConfig defaults (diag_scaled, lambda0 1e-4, pcg_tol 1e-6, pcg_max_iters 500)",
+                   "l2": "flushed (512 MiB write) between timed steps",
+                   "step": "one LM iteration from x0 (linearize+assemble, factor, rhs, DPCG, backsub, trial cost)"},
+        "roofline": {"bound": "hbm", "kernel": "DSE (k_point_pass + k_cam_pass)", "achieved": achieved,
+                     "peak": peak, "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": traffic, "bytes_per_launch": b_dse, "avg_launch_ms": per_dse_ms,
+                     "launches": prof["dse_launches"], "dse_share_of_step": prof["dse_ms"] / max(total_ms, 1e-9),
+                     "point_ms": prof["point_ms"], "cam_ms": prof["cam_ms"]},
+        "e2e": {"value": N / e2e_s, "unit": "edges/s", "h2d_bytes_per_step": state_bytes,
+                "d2h_bytes_per_step": state_bytes},
+        "clocks": clk.summary(),
+        "gpu_launches": int(launches),
+    }
+    if world == 1 and rank == 0 and not args.no_secondary:
+        line["secondary"] = secondary(args, flush)
+    if world == 1 and rank == 0 and not args.no_cpu:
+        line["cpu_baseline"] = cpu_baseline(args, p)
+    ctx.close()
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def secondary(args, flush):
+    """The same step on the Venice-shaped problem (inputs larger than L2)."""
+    import paper_2112_01349_b200 as dba
+    name = SECONDARY_WORKLOAD
+    m, n, N = WORKLOADS[name]
+    p = make_problem(name)
+    with dba.RankContext(0, 8) as ctx:
+        ctx.upload(p)
+        cfg = dba.SolverConfig()
+        for _ in range(2):
+            ctx.probe_step(cfg.lambda0, cfg)
+        ctx.profile(True)
+        ms, pcg = time_steps(ctx, cfg, 3, flush)
+        prof = ctx.profile()
+    t = sum(ms) / len(ms)
+    peak, _ = load_peaks()
+    per = prof["dse_ms"] / max(prof["dse_launches"], 1)
+    b = dse_bytes(N, n, m, 8)
+    return {"workload": name, "ms_per_step": t, "value": N / (t / 1e3), "unit": "edges/s",
+            "pcg_iterations_per_step": pcg,
+            "roofline": {"achieved": b / (per / 1e3) / 1e9, "peak": peak, "frac": b / (per / 1e3) / 1e9 / peak,
+                         "avg_launch_ms": per, "dse_share_of_step": prof["dse_ms"] / max(sum(ms), 1e-9)}}
+
+
+def cpu_baseline(args, p):
+    """The CPU restatement on this host: one LM-iteration step (bounded sample)."""
+    from oracle import oracle as O
+    import paper_2112_01349_b200 as dba
+    k = cpu_threads()
+    secs, its = O.lm_probe_steps(p, dba.SolverConfig(workers=k), 1)
+    N = WORKLOADS[args.workload][2]
+    return {"value": N / float(secs[0]), "unit": "edges/s", "cores": k, "kind": "port",
+            "sample": f"1 LM-iteration step of {args.workload} ({int(its[0])} PCG iterations), {k} rank threads",
+            "seconds": float(secs[0])}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default=DEFAULT_WORKLOAD, choices=sorted(WORKLOADS))
+    ap.add_argument("--no-secondary", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -195,8 +195,13 @@ int dbag_profile(dbag_ctx* ctx, int enable, double* dse_ms, int64_t* dse_launche
 int dbag_event_mark(dbag_ctx* ctx, int which);
 int dbag_event_elapsed(dbag_ctx* ctx, double* ms);
 int dbag_synchronize(dbag_ctx* ctx);
+/* Number of kernels this context has launched (bench: gpu_launches). */
+int dbag_launch_count(dbag_ctx* ctx, int64_t* out);
 
 /* ---- test hooks (operator-level parity) ------------------- */
+/* Scalar-model residuals (dba/problem.hpp:151-165) of the current (0) or
+ * trial (1) state, res[2][count] in shard edge order; NaN on P_z == 0. */
+int dbag_residuals(dbag_ctx* ctx, int use_trial, void* out);
 /* EdgeJacobianBatch in shard edge order: res[2][count], jac[2][12][count]. */
 int dbag_get_jacobians(dbag_ctx* ctx, void* res, void* jac);
 /* Assembled (all-reduced) system: B[81m], C[9n] and w[3n] full size (zeros

@@ -57,6 +57,7 @@ def lib():
                                            P(C.c_int), P(C.c_int)]),
             "orc_allreduce": (C.c_int, [C.c_int, C.c_int64, vp]),
             "orc_lm_solve": (C.c_int, [C.c_int, P(Problem), P(Config), P(Result)]),
+            "orc_lm_probe_steps": (C.c_int, [C.c_int, P(Problem), P(Config), C.c_int, vp, vp]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(h, name)
@@ -237,3 +238,15 @@ def lm_solve(problem, config):
     cfg = config.c_struct()
     check(lib().orc_lm_solve(problem.precision, C.byref(s), C.byref(cfg), C.byref(buf.r)))
     return buf.state(s.num_points)
+
+
+def lm_probe_steps(problem, config, steps):
+    """Seconds per bench step (one LM iteration from x0, K = config.workers
+    threads) and the PCG count of each step."""
+    s = problem.c_struct()
+    cfg = config.c_struct()
+    secs = np.zeros(steps)
+    its = np.zeros(steps, np.int32)
+    check(lib().orc_lm_probe_steps(problem.precision, C.byref(s), C.byref(cfg), steps, secs.ctypes.data,
+                                   its.ctypes.data))
+    return secs, its

@@ -490,4 +490,90 @@ int orc_lm_solve(int prec, const orc_problem* p, const orc_config* c, orc_result
   return prec == 8 ? lm<double>(p, c, out) : lm<float>(p, c, out);
 }
 
+// The bench step on the CPU (the reference arm / cpu_baseline): `steps`
+// times, one LM iteration of lm_solve_rank (dba/solver.hpp:330-425) from x0
+// at lambda0 — linearize + assemble + all-reduce B, C, v, w, damp, factor,
+// rhs, dpcg, back-substitution, trial cost, model terms — with
+// K = config->workers threads. seconds[i] is the wall time of step i (max
+// over ranks); pcg_iters the PCG count of the step.
+int orc_lm_probe_steps(int prec, const orc_problem* p, const orc_config* c, int steps, double* seconds,
+                       int* pcg_iters) {
+  auto run = [&](auto tag) {
+    using S = decltype(tag);
+    return guarded([&] {
+      const auto pb = load<S>(p);
+      const auto cfg = to_cfg(c);
+      const auto parts = orc::partition_edges(pb, cfg.workers);
+      orc::Group g(cfg.workers);
+      std::vector<double> secs(std::size_t(steps) * cfg.workers, 0.0);
+      std::vector<int> its(std::size_t(steps), 0);
+      orc::run_on_workers(g, [&](int r) {
+        const auto& part = parts[std::size_t(r)];
+        orc::Evaluator<S> ev(pb, part, cfg.jacobian);
+        orc::Hessian<S> h(pb, part);
+        orc::BlockDiag<S, 9> Bd;
+        orc::BlockDiag<S, 3> Cd;
+        orc::Factored<S, 9> Bf;
+        orc::Factored<S, 3> Cf;
+        const std::size_t cdim = std::size_t(pb.m) * 9, pdim = std::size_t(pb.n) * 3;
+        std::vector<S> gvec(cdim), dxc, dxp(pdim), txc(cdim), txp(pdim), ptmp, ctmp(cdim);
+        const double lambda = cfg.lambda0;
+        for (int s = 0; s < steps; ++s) {
+          const auto t0 = std::chrono::steady_clock::now();
+          const auto& bt = ev.linearize(pb.cams.data(), pb.pts.data(), nullptr);
+          orc::assemble(bt, ev, h);
+          g.allreduce_sum(r, h.B.a.data(), h.B.a.size());
+          g.allreduce_sum(r, h.C.a.data(), h.C.a.size());
+          g.allreduce_sum(r, h.v.data(), h.v.size());
+          g.allreduce_sum(r, h.w.data(), h.w.size());
+          int pcg = 0;
+          try {
+            h.B.damp_into(static_cast<S>(lambda), cfg.damping, Bd);
+            h.C.damp_into(static_cast<S>(lambda), cfg.damping, Cd);
+            Cf.factor(Cd);
+            Bf.factor(Bd);
+            ptmp = h.w;
+            Cf.solve_in_place(ptmp.data());
+            h.E.apply(ptmp.data(), ctmp.data(), nullptr);
+            g.allreduce_sum(r, ctmp.data(), ctmp.size());
+            for (std::size_t i = 0; i < cdim; ++i) gvec[i] = h.v[i] - ctmp[i];
+            dxc.assign(cdim, S(0));
+            pcg = orc::dpcg(dxc, Bd, Bf, h.E, Cf, gvec, g, r, cfg.pcg_tol, cfg.pcg_max_iters, nullptr).iterations;
+            ptmp.assign(pdim, S(0));
+            h.E.apply_t(dxc.data(), ptmp.data(), nullptr);
+            g.allreduce_sum(r, ptmp.data(), ptmp.size());
+            for (std::size_t i = 0; i < pdim; ++i) dxp[i] = h.w[i] - ptmp[i];
+            Cf.solve_in_place(dxp.data());
+            for (std::size_t i = 0; i < cdim; ++i) txc[i] = pb.cams[i] + dxc[i];
+            for (std::size_t i = 0; i < pdim; ++i) txp[i] = pb.pts[i] + dxp[i];
+            orc::distributed_cost(ev, txc.data(), txp.data(), g, r, nullptr);
+            double step_inf = 0, damp = 0;
+            for (std::size_t i = 0; i < cdim; ++i) step_inf = std::max(step_inf, std::abs(double(dxc[i])));
+            for (std::size_t i = 0; i < pdim; ++i) step_inf = std::max(step_inf, std::abs(double(dxp[i])));
+            for (std::size_t i = 0; i < cdim; ++i)
+              damp += lambda * double(orc::clamp_curv(h.B.diag(std::int64_t(i)))) * double(dxc[i]) * double(dxc[i]);
+            for (std::size_t i = 0; i < pdim; ++i)
+              damp += lambda * double(orc::clamp_curv(h.C.diag(std::int64_t(i)))) * double(dxp[i]) * double(dxp[i]);
+            volatile double model = damp + orc::dot_d(dxc.data(), h.v.data(), cdim) +
+                                    orc::dot_d(dxp.data(), h.w.data(), pdim) + step_inf;
+            (void)model;
+          } catch (const orc::SingularBlock&) {
+          } catch (const orc::PcgBreakdown&) {
+          }
+          secs[std::size_t(s) * cfg.workers + r] =
+              std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+          if (r == 0) its[std::size_t(s)] = pcg;
+        }
+      });
+      for (int s = 0; s < steps; ++s) {
+        double mx = 0;
+        for (int r = 0; r < cfg.workers; ++r) mx = std::max(mx, secs[std::size_t(s) * cfg.workers + r]);
+        seconds[s] = mx;
+        if (pcg_iters) pcg_iters[s] = its[std::size_t(s)];
+      }
+    });
+  };
+  return prec == 8 ? run(double{}) : run(float{});
+}
+
 }  // extern "C"

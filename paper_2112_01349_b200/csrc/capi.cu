@@ -476,6 +476,20 @@ int dbag_synchronize(dbag_ctx* ctx) {
   return guarded([&] { with_rank(ctx, [&](auto& rk) { rk.sync(); }); });
 }
 
+int dbag_launch_count(dbag_ctx* ctx, int64_t* out) {
+  return guarded([&] { with_rank(ctx, [&](auto& rk) { *out = rk.launches(); }); });
+}
+
+int dbag_residuals(dbag_ctx* ctx, int use_trial, void* out) {
+  return guarded([&] {
+    with_rank(ctx, [&](auto& rk) {
+      using S = std::remove_reference_t<decltype(rk)>;
+      using T = std::conditional_t<std::is_same_v<S, Rank<double>>, double, float>;
+      rk.residuals(use_trial != 0, static_cast<T*>(out));
+    });
+  });
+}
+
 int dbag_get_jacobians(dbag_ctx* ctx, void* res, void* jac) {
   return guarded([&] {
     with_rank(ctx, [&](auto& rk) {

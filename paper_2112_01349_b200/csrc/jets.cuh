@@ -24,33 +24,46 @@ __host__ __device__ constexpr S taylor_threshold() {
   return sizeof(S) == 8 ? S(1e-12) : S(1e-4);
 }
 
+// Round-to-nearest arithmetic that the compiler may not contract into FMAs:
+// the jet and residual code below then performs exactly the IEEE operation
+// sequence of the reference (compiled for x86-64 without FMA), so values
+// agree with the CPU restatement bit-for-bit wherever sin/cos agree.
+__device__ __forceinline__ double fm(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double fa(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double fs(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double fd(double a, double b) { return __ddiv_rn(a, b); }
+__device__ __forceinline__ float fm(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ float fa(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ float fs(float a, float b) { return __fsub_rn(a, b); }
+__device__ __forceinline__ float fd(float a, float b) { return __fdiv_rn(a, b); }
+
 // dba/problem.hpp:89-118
 template <class S>
 __device__ __forceinline__ void rot_coeffs(S t, S& c, S& s1, S& c2) {
   if (t < taylor_threshold<S>()) {
-    c = S(1) - t / S(2) + t * t / S(24);
-    s1 = S(1) - t / S(6) + t * t / S(120);
-    c2 = S(0.5) - t / S(24) + t * t / S(720);
+    c = fa(fs(S(1), fd(t, S(2))), fd(fm(t, t), S(24)));
+    s1 = fa(fs(S(1), fd(t, S(6))), fd(fm(t, t), S(120)));
+    c2 = fa(fs(S(0.5), fd(t, S(24))), fd(fm(t, t), S(720)));
   } else {
     const S th = sqrt(t);
     S sn, cs;
     if constexpr (sizeof(S) == 8) sincos(th, &sn, &cs);
     else sincosf(th, &sn, &cs);
     c = cs;
-    s1 = sn / th;
-    c2 = (S(1) - c) / t;
+    s1 = fd(sn, th);
+    c2 = fd(fs(S(1), c), t);
   }
 }
 template <class S>
 __device__ __forceinline__ void rot_dcoeffs(S t, S c, S s1, S c2, S& dc, S& ds1, S& dc2) {
   if (t < taylor_threshold<S>()) {
-    dc = S(-0.5) + t / S(12);
-    ds1 = S(-1) / S(6) + t / S(60);
-    dc2 = S(-1) / S(24) + t / S(360);
+    dc = fa(S(-0.5), fd(t, S(12)));
+    ds1 = fa(fd(S(-1), S(6)), fd(t, S(60)));
+    dc2 = fa(fd(S(-1), S(24)), fd(t, S(360)));
   } else {
-    dc = -s1 / S(2);
-    ds1 = (c - s1) / (S(2) * t);
-    dc2 = (s1 / S(2) - c2) / t;
+    dc = fd(-s1, S(2));
+    ds1 = fd(fs(c, s1), fm(S(2), t));
+    dc2 = fd(fs(fd(s1, S(2)), c2), t);
   }
 }
 
@@ -75,9 +88,9 @@ __device__ __forceinline__ Jet<S, A | B> operator+(const Jet<S, A>& a, const Jet
   Jet<S, A | B> o;
   DBAG_LANES {
     const bool ia = (A >> j) & 1u, ib = (B >> j) & 1u;
-    o.g[j] = (ia && ib) ? a.g[j] + b.g[j] : ia ? a.g[j] : ib ? b.g[j] : S(0);
+    o.g[j] = (ia && ib) ? fa(a.g[j], b.g[j]) : ia ? a.g[j] : ib ? b.g[j] : S(0);
   }
-  o.v = a.v + b.v;
+  o.v = fa(a.v, b.v);
   return o;
 }
 
@@ -86,9 +99,9 @@ __device__ __forceinline__ Jet<S, A | B> operator-(const Jet<S, A>& a, const Jet
   Jet<S, A | B> o;
   DBAG_LANES {
     const bool ia = (A >> j) & 1u, ib = (B >> j) & 1u;
-    o.g[j] = (ia && ib) ? a.g[j] - b.g[j] : ia ? a.g[j] : ib ? -b.g[j] : S(0);
+    o.g[j] = (ia && ib) ? fs(a.g[j], b.g[j]) : ia ? a.g[j] : ib ? -b.g[j] : S(0);
   }
-  o.v = a.v - b.v;
+  o.v = fs(a.v, b.v);
   return o;
 }
 
@@ -97,21 +110,21 @@ __device__ __forceinline__ Jet<S, A | B> operator*(const Jet<S, A>& a, const Jet
   Jet<S, A | B> o;
   DBAG_LANES {
     const bool ia = (A >> j) & 1u, ib = (B >> j) & 1u;
-    o.g[j] = (ia && ib) ? a.g[j] * b.v + a.v * b.g[j] : ia ? a.g[j] * b.v : ib ? a.v * b.g[j] : S(0);
+    o.g[j] = (ia && ib) ? fa(fm(a.g[j], b.v), fm(a.v, b.g[j])) : ia ? fm(a.g[j], b.v) : ib ? fm(a.v, b.g[j]) : S(0);
   }
-  o.v = a.v * b.v;
+  o.v = fm(a.v, b.v);
   return o;
 }
 
 template <class S, unsigned A, unsigned B>
 __device__ __forceinline__ Jet<S, A | B> operator/(const Jet<S, A>& a, const Jet<S, B>& b) {
   Jet<S, A | B> o;
-  o.v = a.v / b.v;
+  o.v = fd(a.v, b.v);
   DBAG_LANES {
     const bool ia = (A >> j) & 1u, ib = (B >> j) & 1u;
-    o.g[j] = (ia && ib) ? (a.g[j] - o.v * b.g[j]) / b.v
-             : ia       ? a.g[j] / b.v
-             : ib       ? (S(0) - o.v * b.g[j]) / b.v
+    o.g[j] = (ia && ib) ? fd(fs(a.g[j], fm(o.v, b.g[j])), b.v)
+             : ia       ? fd(a.g[j], b.v)
+             : ib       ? fd(fs(S(0), fm(o.v, b.g[j])), b.v)
                         : S(0);
   }
   return o;
@@ -120,8 +133,8 @@ __device__ __forceinline__ Jet<S, A | B> operator/(const Jet<S, A>& a, const Jet
 template <class S, unsigned A>
 __device__ __forceinline__ Jet<S, A> scale(const Jet<S, A>& a, S s) {  // mul_scalar
   Jet<S, A> o;
-  DBAG_LANES o.g[j] = ((A >> j) & 1u) ? a.g[j] * s : S(0);
-  o.v = a.v * s;
+  DBAG_LANES o.g[j] = ((A >> j) & 1u) ? fm(a.g[j], s) : S(0);
+  o.v = fm(a.v, s);
   return o;
 }
 
@@ -129,7 +142,7 @@ template <class S, unsigned A>
 __device__ __forceinline__ Jet<S, A> shift(const Jet<S, A>& a, S s) {  // add_scalar
   Jet<S, A> o;
   DBAG_LANES o.g[j] = ((A >> j) & 1u) ? a.g[j] : S(0);
-  o.v = a.v + s;
+  o.v = fa(a.v, s);
   return o;
 }
 
@@ -142,9 +155,9 @@ __device__ __forceinline__ void rotation_coefficients(const Jet<S, A>& t, Jet<S,
   rot_dcoeffs(t.v, c.v, s1.v, c2.v, dc, ds1, dc2);
   DBAG_LANES {
     const bool on = (A >> j) & 1u;
-    c.g[j] = on ? dc * t.g[j] : S(0);
-    s1.g[j] = on ? ds1 * t.g[j] : S(0);
-    c2.g[j] = on ? dc2 * t.g[j] : S(0);
+    c.g[j] = on ? fm(dc, t.g[j]) : S(0);
+    s1.g[j] = on ? fm(ds1, t.g[j]) : S(0);
+    c2.g[j] = on ? fm(dc2, t.g[j]) : S(0);
   }
 }
 
@@ -186,8 +199,8 @@ __device__ __forceinline__ bool edge_autodiff(const S* cam, const S* X, S pixx, 
   const auto dist = shift(n2 * k1 + (n2 * n2) * k2, S(1)) * f;
   const auto rx = ux * dist;
   const auto ry = uy * dist;
-  r[0] = rx.v - pixx;
-  r[1] = ry.v - pixy;
+  r[0] = fs(rx.v, pixx);
+  r[1] = fs(ry.v, pixy);
   DBAG_LANES {
     J[0][j] = rx.g[j];
     J[1][j] = ry.g[j];
@@ -264,27 +277,28 @@ __device__ __forceinline__ bool edge_analytic(const S* cm, const S* x, S pixx, S
   return true;
 }
 
-// Scalar Snavely residual (dba/problem.hpp:125-165), same op order.
+// Scalar Snavely residual (dba/problem.hpp:125-165), same op order as the
+// jet composition, so its value equals the jets' value lanes bit-for-bit.
 template <class S>
 __device__ __forceinline__ bool edge_residual(const S* cam, const S* x, S pixx, S pixy, S* r) {
-  const S t = (cam[0] * cam[0] + cam[1] * cam[1]) + cam[2] * cam[2];
+  const S t = fa(fa(fm(cam[0], cam[0]), fm(cam[1], cam[1])), fm(cam[2], cam[2]));
   S c, s1, c2;
   rot_coeffs(t, c, s1, c2);
-  const S dc2 = ((cam[0] * x[0] + cam[1] * x[1]) + cam[2] * x[2]) * c2;
-  const S cr0 = cam[1] * x[2] - cam[2] * x[1];
-  const S cr1 = cam[2] * x[0] - cam[0] * x[2];
-  const S cr2 = cam[0] * x[1] - cam[1] * x[0];
-  const S P0 = ((x[0] * c + cr0 * s1) + cam[0] * dc2) + cam[3];
-  const S P1 = ((x[1] * c + cr1 * s1) + cam[1] * dc2) + cam[4];
-  const S P2 = ((x[2] * c + cr2 * s1) + cam[2] * dc2) + cam[5];
+  const S dc2 = fm(fa(fa(fm(cam[0], x[0]), fm(cam[1], x[1])), fm(cam[2], x[2])), c2);
+  const S cr0 = fs(fm(cam[1], x[2]), fm(cam[2], x[1]));
+  const S cr1 = fs(fm(cam[2], x[0]), fm(cam[0], x[2]));
+  const S cr2 = fs(fm(cam[0], x[1]), fm(cam[1], x[0]));
+  const S P0 = fa(fa(fa(fm(x[0], c), fm(cr0, s1)), fm(cam[0], dc2)), cam[3]);
+  const S P1 = fa(fa(fa(fm(x[1], c), fm(cr1, s1)), fm(cam[1], dc2)), cam[4]);
+  const S P2 = fa(fa(fa(fm(x[2], c), fm(cr2, s1)), fm(cam[2], dc2)), cam[5]);
   if (P2 == S(0)) return false;
-  const S ux = -(P0 / P2);
-  const S uy = -(P1 / P2);
-  const S n2 = ux * ux + uy * uy;
-  const S dist = (n2 * cam[7] + (n2 * n2) * cam[8]) + S(1);
-  const S sc = dist * cam[6];
-  r[0] = ux * sc - pixx;
-  r[1] = uy * sc - pixy;
+  const S ux = -fd(P0, P2);
+  const S uy = -fd(P1, P2);
+  const S n2 = fa(fm(ux, ux), fm(uy, uy));
+  const S dist = fa(fa(fm(n2, cam[7]), fm(fm(n2, n2), cam[8])), S(1));
+  const S sc = fm(dist, cam[6]);
+  r[0] = fs(fm(ux, sc), pixx);
+  r[1] = fs(fm(uy, sc), pixy);
   return true;
 }
 

@@ -122,7 +122,7 @@ __global__ void __launch_bounds__(kRedThreads) k_cost(std::int64_t N, const std:
 #pragma unroll
     for (int k = 0; k < 3; ++k) X[k] = x[k];
     if (edge_residual(c, X, px[s], py[s], r)) {
-      acc += double(w[s]) * double(r[0] * r[0] + r[1] * r[1]);
+      acc += double(w[s]) * double(fa(fm(r[0], r[0]), fm(r[1], r[1])));
     } else {
       bad = true;
       atomicMin(bad_edge, (unsigned long long)(edge_base + slot_edge[s]));
@@ -133,6 +133,25 @@ __global__ void __launch_bounds__(kRedThreads) k_cost(std::int64_t N, const std:
   if (grid_reduce<SumOp, 2>(v, ws.partials, ws.counter, fin)) {
     if (threadIdx.x == 0) *out_cost = fin[1] > 0 ? __longlong_as_double(0x7ff0000000000000LL) : fin[0];
   }
+}
+
+// Per-edge cost-path residuals in shard edge order (test hook).
+template <class S>
+__global__ void k_residuals(std::int64_t N, const std::int32_t* __restrict__ slot_cam,
+                            const std::int32_t* __restrict__ slot_pt, const std::int32_t* __restrict__ slot_edge,
+                            const S* __restrict__ px, const S* __restrict__ py, const S* __restrict__ xc,
+                            const S* __restrict__ xp, S* __restrict__ out) {
+  const std::int64_t s = blockIdx.x * std::int64_t(blockDim.x) + threadIdx.x;
+  if (s >= N) return;
+  S c[9], X[3], r[2] = {S(0), S(0)};
+#pragma unroll
+  for (int k = 0; k < 9; ++k) c[k] = xc[std::size_t(slot_cam[s]) * 9 + k];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) X[k] = xp[std::size_t(slot_pt[s]) * 3 + k];
+  if (!edge_residual(c, X, px[s], py[s], r)) r[0] = r[1] = S(NAN);
+  const std::int64_t e = slot_edge[s];
+  out[e] = r[0];
+  out[N + e] = r[1];
 }
 
 // ---------------------------------------------------------- linearize ----
@@ -175,7 +194,7 @@ __global__ void __launch_bounds__(128) k_linearize(std::int64_t N, const std::in
 #pragma unroll
   for (int i = 0; i < 9; ++i)
 #pragma unroll
-    for (int j = 0; j < 3; ++j) E[std::size_t(i * 3 + j) * N + s] = wt * (J[0][i] * J[0][9 + j] + J[1][i] * J[1][9 + j]);
+    for (int j = 0; j < 3; ++j) E[std::size_t(i * 3 + j) * N + s] = fm(wt, fa(fm(J[0][i], J[0][9 + j]), fm(J[1][i], J[1][9 + j])));
 }
 
 // C[p] += w Jp^T Jp, w[p] -= w Jp^T r over the point's slots in edge order
@@ -198,8 +217,8 @@ __global__ void k_assemble_points(std::int32_t n_loc, const std::int32_t* __rest
 #pragma unroll
     for (int i = 0; i < 3; ++i) {
 #pragma unroll
-      for (int j = 0; j < 3; ++j) c[i][j] += wt * (jp0[i] * jp0[j] + jp1[i] * jp1[j]);
-      g[i] -= wt * (jp0[i] * r0 + jp1[i] * r1);
+      for (int j = 0; j < 3; ++j) c[i][j] = fa(c[i][j], fm(wt, fa(fm(jp0[i], jp0[j]), fm(jp1[i], jp1[j]))));
+      g[i] = fs(g[i], fm(wt, fa(fm(jp0[i], r0), fm(jp1[i], r1))));
     }
   }
 #pragma unroll
@@ -238,9 +257,9 @@ __global__ void __launch_bounds__(NT) k_assemble_cameras(const std::int32_t* __r
 #pragma unroll
     for (int i = 0; i < 9; ++i)
 #pragma unroll
-      for (int j = i; j < 9; ++j) acc[q++] += double(wt * (jc0[i] * jc0[j] + jc1[i] * jc1[j]));
+      for (int j = i; j < 9; ++j) acc[q++] += double(fm(wt, fa(fm(jc0[i], jc0[j]), fm(jc1[i], jc1[j]))));
 #pragma unroll
-    for (int i = 0; i < 9; ++i) acc[45 + i] -= double(wt * (jc0[i] * r0 + jc1[i] * r1));
+    for (int i = 0; i < 9; ++i) acc[45 + i] -= double(fm(wt, fa(fm(jc0[i], r0), fm(jc1[i], r1))));
 #pragma unroll
     for (int k = 0; k < 27; ++k) E_cm[std::size_t(k) * N + cs] = E_pm[std::size_t(k) * N + ps];
   }
@@ -325,34 +344,32 @@ __global__ void k_damp_factor(std::int64_t nb, const S* __restrict__ A, S lambda
     atomicMin(bad, (unsigned long long)(index_map ? index_map[i] : i));
     return;
   }
-  // L^-1 (lower) by forward substitution, stored in the upper triangle's
-  // mirror: li[r][c] for c <= r.
-  S li[BS][BS];
-#pragma unroll
-  for (int c = 0; c < BS; ++c) {
-#pragma unroll
-    for (int r = 0; r < BS; ++r) {
-      if (r < c) {
-        li[r][c] = S(0);
-      } else {
-        S acc = (r == c) ? S(1) : S(0);
-#pragma unroll
-        for (int k = c; k < r; ++k) acc -= m[r][k] * li[k][c];
-        li[r][c] = acc / m[r][r];
-      }
-    }
-  }
+  // The factor L (row-major lower triangle, zeros above) — solves are the
+  // reference's forward + back substitution (dba/block_matrix.hpp:140-150).
   S* ai = Ainv + std::size_t(i) * BS * BS;
 #pragma unroll
   for (int r = 0; r < BS; ++r)
 #pragma unroll
-    for (int c = r; c < BS; ++c) {
-      S acc = S(0);
+    for (int c = 0; c < BS; ++c) ai[r * BS + c] = c <= r ? m[r][c] : S(0);
+}
+
+// x := (L L^T)^-1 x with L row-major lower (dba/block_matrix.hpp:140-150).
+template <class S, int BS>
+__device__ __forceinline__ void llt_solve(const S* __restrict__ L, S* x) {
 #pragma unroll
-      for (int k = c; k < BS; ++k) acc += li[k][r] * li[k][c];
-      ai[r * BS + c] = acc;
-      ai[c * BS + r] = acc;
-    }
+  for (int r = 0; r < BS; ++r) {
+    S acc = x[r];
+#pragma unroll
+    for (int c = 0; c < r; ++c) acc -= L[r * BS + c] * x[c];
+    x[r] = acc / L[r * BS + r];
+  }
+#pragma unroll
+  for (int r = BS - 1; r >= 0; --r) {
+    S acc = x[r];
+#pragma unroll
+    for (int c = r + 1; c < BS; ++c) acc -= L[c * BS + r] * x[c];
+    x[r] = acc / L[r * BS + r];
+  }
 }
 
 // --------------------------------------------------------- point pass ----
@@ -414,9 +431,9 @@ __global__ void __launch_bounds__(kTile) k_point_pass(std::int64_t N, const std:
 #pragma unroll
     for (int j = 0; j < 3; ++j) t[j] = wv[std::size_t(p) * 3 + j] - t[j];
   }
-  const S* ci = Cinv + std::size_t(p) * 9;
+  llt_solve<S, 3>(Cinv + std::size_t(p) * 9, t);
 #pragma unroll
-  for (int r = 0; r < 3; ++r) out[std::size_t(p) * 3 + r] = (ci[r * 3 + 0] * t[0] + ci[r * 3 + 1] * t[1]) + ci[r * 3 + 2] * t[2];
+  for (int r = 0; r < 3; ++r) out[std::size_t(p) * 3 + r] = t[r];
 }
 
 // Finish of k_point_pass for halo points after the all-reduce.
@@ -433,9 +450,9 @@ __global__ void k_halo_finish(std::int32_t n, const std::int32_t* __restrict__ l
   if (MODE == 1)
 #pragma unroll
     for (int j = 0; j < 3; ++j) t[j] = wv[std::size_t(p) * 3 + j] - t[j];
-  const S* ci = Cinv + std::size_t(p) * 9;
+  llt_solve<S, 3>(Cinv + std::size_t(p) * 9, t);
 #pragma unroll
-  for (int r = 0; r < 3; ++r) out[std::size_t(p) * 3 + r] = (ci[r * 3 + 0] * t[0] + ci[r * 3 + 1] * t[1]) + ci[r * 3 + 2] * t[2];
+  for (int r = 0; r < 3; ++r) out[std::size_t(p) * 3 + r] = t[r];
 }
 
 // b_p = C_p^-1 w_p for the right-hand side (dba/solver.hpp:358).
@@ -444,10 +461,10 @@ __global__ void k_point_solve(std::int32_t n, const S* __restrict__ Cinv, const 
                               S* __restrict__ out) {
   const std::int32_t p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= n) return;
-  const S* ci = Cinv + std::size_t(p) * 9;
-  const S t0 = wv[std::size_t(p) * 3], t1 = wv[std::size_t(p) * 3 + 1], t2 = wv[std::size_t(p) * 3 + 2];
+  S t[3] = {wv[std::size_t(p) * 3], wv[std::size_t(p) * 3 + 1], wv[std::size_t(p) * 3 + 2]};
+  llt_solve<S, 3>(Cinv + std::size_t(p) * 9, t);
 #pragma unroll
-  for (int r = 0; r < 3; ++r) out[std::size_t(p) * 3 + r] = (ci[r * 3 + 0] * t0 + ci[r * 3 + 1] * t1) + ci[r * 3 + 2] * t2;
+  for (int r = 0; r < 3; ++r) out[std::size_t(p) * 3 + r] = t[r];
 }
 
 // Halo scatter / gather of W-wide point records.
@@ -553,17 +570,14 @@ __global__ void __launch_bounds__(kRedThreads) k_pcg_precond(std::int32_t m, con
                                                              PcgScal<S>* sc) {
   double acc = 0.0;
   for (std::int32_t cam = blockIdx.x * blockDim.x + threadIdx.x; cam < m; cam += gridDim.x * blockDim.x) {
-    const S* b = Binv + std::size_t(cam) * 81;
-    S rv[9];
+    S rv[9], zv[9];
 #pragma unroll
-    for (int k = 0; k < 9; ++k) rv[k] = r[std::size_t(cam) * 9 + k];
+    for (int k = 0; k < 9; ++k) zv[k] = rv[k] = r[std::size_t(cam) * 9 + k];
+    llt_solve<S, 9>(Binv + std::size_t(cam) * 81, zv);
 #pragma unroll
     for (int i = 0; i < 9; ++i) {
-      S s = S(0);
-#pragma unroll
-      for (int k = 0; k < 9; ++k) s += b[i * 9 + k] * rv[k];
-      z[std::size_t(cam) * 9 + i] = s;
-      acc += double(rv[i]) * double(s);
+      z[std::size_t(cam) * 9 + i] = zv[i];
+      acc += double(rv[i]) * double(zv[i]);
     }
   }
   const double v[1] = {acc};

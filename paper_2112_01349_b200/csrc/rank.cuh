@@ -227,12 +227,11 @@ class Rank {
   double cost(bool trial, std::int64_t* bad_edge) {
     DBAG_CUDA(cudaSetDevice(device_));
     DBAG_CUDA(cudaMemsetAsync(bad_.get(), 0xff, sizeof(unsigned long long), st_));
-    dev::k_cost<S><<<grid_for(N_, dev::kRedThreads, dev::kRedBlocksMax), dev::kRedThreads, 0, st_>>>(
+    launch(dev::k_cost<S>, grid_for(N_, dev::kRedThreads, dev::kRedBlocksMax), dev::kRedThreads, 
         N_, slot_cam_.get(), slot_pt_.get(), slot_edge_.get(), plan_.range.start, slot_px_.get(), slot_py_.get(),
         slot_w_.get(), trial ? xct_.get() : xc_.get(), trial ? xpt_.get() : xp_.get(), red(), dsc_.get(),
         bad_.get());
-    DBAG_LAUNCH_CHECK();
-    if (N_ == 0) DBAG_CUDA(cudaMemsetAsync(dsc_.get(), 0, sizeof(double), st_));
+        if (N_ == 0) DBAG_CUDA(cudaMemsetAsync(dsc_.get(), 0, sizeof(double), st_));
     tally_.edges += static_cast<std::uint64_t>(N_);
     comm_->allreduce_sum(dsc_.get(), 1, DType::f64, st_);
     const std::int64_t bad = agree_min_index(bad_.get());
@@ -249,33 +248,30 @@ class Rank {
     if (N_ > 0) {
       const int blocks = static_cast<int>((N_ + 127) / 128);
       if (jac_mode_ == 1)
-        dev::k_linearize<S, 1><<<blocks, 128, 0, st_>>>(N_, slot_cam_.get(), slot_pt_.get(), slot_edge_.get(),
+        launch(dev::k_linearize<S, 1>, blocks, 128, N_, slot_cam_.get(), slot_pt_.get(), slot_edge_.get(),
                                                          plan_.range.start, slot_px_.get(), slot_py_.get(),
                                                          slot_w_.get(), xc_.get(), xp_.get(), Jb_.get(), E_pm_.get(),
                                                          bad_.get());
       else
-        dev::k_linearize<S, 0><<<blocks, 128, 0, st_>>>(N_, slot_cam_.get(), slot_pt_.get(), slot_edge_.get(),
+        launch(dev::k_linearize<S, 0>, blocks, 128, N_, slot_cam_.get(), slot_pt_.get(), slot_edge_.get(),
                                                          plan_.range.start, slot_px_.get(), slot_py_.get(),
                                                          slot_w_.get(), xc_.get(), xp_.get(), Jb_.get(), E_pm_.get(),
                                                          bad_.get());
-      DBAG_LAUNCH_CHECK();
-    }
+          }
     tally_.edges += static_cast<std::uint64_t>(N_);
     const std::int64_t bad = agree_min_index(bad_.get());
     if (bad >= 0) throw degenerate_depth(bad);
     DBAG_CUDA(cudaMemsetAsync(B_.get(), 0, B_.size() * sizeof(S), st_));
     DBAG_CUDA(cudaMemsetAsync(v_.get(), 0, v_.size() * sizeof(S), st_));
     if (n_loc_ > 0) {
-      dev::k_assemble_points<S><<<grid_for(n_loc_, 128, 1 << 30), 128, 0, st_>>>(n_loc_, pt_ptr_.get(), Jb_.get(),
+      launch(dev::k_assemble_points<S>, grid_for(n_loc_, 128, 1 << 30), 128, n_loc_, pt_ptr_.get(), Jb_.get(),
                                                                                  C_.get(), w_.get());
-      DBAG_LAUNCH_CHECK();
-    }
+          }
     if (m_loc_ > 0) {
-      dev::k_assemble_cameras<S, 256><<<m_loc_, 256, 0, st_>>>(cam_ptr_.get(), cam_glob_.get(), cslot_pslot_.get(),
+      launch(dev::k_assemble_cameras<S, 256>, m_loc_, 256, cam_ptr_.get(), cam_glob_.get(), cslot_pslot_.get(),
                                                                Jb_.get(), N_, E_pm_.get(), E_cm_.get(), B_.get(),
                                                                v_.get());
-      DBAG_LAUNCH_CHECK();
-    }
+          }
     comm_->allreduce_sum(B_.get(), static_cast<std::int64_t>(m_) * 81, kT, st_);
     comm_->allreduce_sum(C_halo_exchange_begin(), halo_count(12), kT, st_);
     C_halo_exchange_end();
@@ -291,15 +287,13 @@ class Rank {
     DBAG_CUDA(cudaMemsetAsync(bad_.get(), 0xff, 2 * sizeof(unsigned long long), st_));
     const S lam = static_cast<S>(lambda);
     if (n_loc_ > 0) {
-      dev::k_damp_factor<S, 3><<<grid_for(n_loc_, 128, 1 << 30), 128, 0, st_>>>(
+      launch(dev::k_damp_factor<S, 3>, grid_for(n_loc_, 128, 1 << 30), 128, 
           n_loc_, C_.get(), lam, policy, Cd_.get(), Cinv_.get(), pt_glob_.get(), bad_.get());
-      DBAG_LAUNCH_CHECK();
-    }
+          }
     if (m_ > 0) {
-      dev::k_damp_factor<S, 9><<<grid_for(m_, 64, 1 << 30), 64, 0, st_>>>(m_, B_.get(), lam, policy, Bd_.get(),
+      launch(dev::k_damp_factor<S, 9>, grid_for(m_, 64, 1 << 30), 64, m_, B_.get(), lam, policy, Bd_.get(),
                                                                           Binv_.get(), nullptr, bad_.get() + 1);
-      DBAG_LAUNCH_CHECK();
-    }
+          }
     // C failures are reported by global point id: the reference factors the
     // full-size C in global order and names the first failing block, C
     // before B (dba/solver.hpp:354-355, dba/block_matrix.hpp:123-134).
@@ -325,16 +319,14 @@ class Rank {
   void rhs() {
     DBAG_CUDA(cudaSetDevice(device_));
     if (n_loc_ > 0) {
-      dev::k_point_solve<S><<<grid_for(n_loc_, 128, 1 << 30), 128, 0, st_>>>(n_loc_, Cinv_.get(), w_.get(), bpt_.get());
-      DBAG_LAUNCH_CHECK();
-    }
+      launch(dev::k_point_solve<S>, grid_for(n_loc_, 128, 1 << 30), 128, n_loc_, Cinv_.get(), w_.get(), bpt_.get());
+          }
     cam_apply(bpt_.get(), ctmp_.get());
     tally_.block_ops += static_cast<std::uint64_t>(N_);
     const std::int64_t len = static_cast<std::int64_t>(m_) * 9;
     if (len > 0) {
-      dev::k_sub<S><<<grid_for(len, 256, 1 << 30), 256, 0, st_>>>(len, v_.get(), ctmp_.get(), g_.get());
-      DBAG_LAUNCH_CHECK();
-    }
+      launch(dev::k_sub<S>, grid_for(len, 256, 1 << 30), 256, len, v_.get(), ctmp_.get(), g_.get());
+          }
   }
 
   // ---------------------------------------------------------------- DSE ----
@@ -345,29 +337,26 @@ class Rank {
     if (prof) DBAG_CUDA(cudaEventRecord(prof_event(), st_));
     if (H_ > 0) DBAG_CUDA(cudaMemsetAsync(halo_buf_.get(), 0, sizeof(S) * 3 * static_cast<std::size_t>(H_), st_));
     if (n_tiles_ > 0) {
-      dev::k_point_pass<S, 0><<<n_tiles_, dev::kTile, 0, st_>>>(N_, tile_pt_.get(), pt_ptr_.get(), slot_cam_.get(),
+      launch(dev::k_point_pass<S, 0>, n_tiles_, dev::kTile, N_, tile_pt_.get(), pt_ptr_.get(), slot_cam_.get(),
                                                                E_pm_.get(), x, Cinv_.get(), nullptr,
                                                                H_ > 0 ? halo_of_.get() : nullptr, halo_buf_.get(),
                                                                bpt_.get());
-      DBAG_LAUNCH_CHECK();
-    }
+          }
     if (prof) DBAG_CUDA(cudaEventRecord(prof_event(), st_));
     if (H_ > 0) {
       comm_->allreduce_sum(halo_buf_.get(), 3 * H_, kT, st_);
       if (n_halo_loc_ > 0) {
-        dev::k_halo_finish<S, 0><<<grid_for(n_halo_loc_, 128, 1 << 30), 128, 0, st_>>>(
+        launch(dev::k_halo_finish<S, 0>, grid_for(n_halo_loc_, 128, 1 << 30), 128, 
             n_halo_loc_, halo_lpt_.get(), halo_idx_.get(), halo_buf_.get(), Cinv_.get(), nullptr, bpt_.get());
-        DBAG_LAUNCH_CHECK();
-      }
+              }
     }
     if (prof) DBAG_CUDA(cudaEventRecord(prof_event(), st_));
     cam_apply(bpt_.get(), ctmp_.get());
     if (prof) DBAG_CUDA(cudaEventRecord(prof_event(), st_));
     if (m_ > 0) {
-      dev::k_cam_epilogue<S, PQ><<<grid_for(m_, dev::kRedThreads, dev::kRedBlocksMax), dev::kRedThreads, 0, st_>>>(
+      launch(dev::k_cam_epilogue<S, PQ>, grid_for(m_, dev::kRedThreads, dev::kRedBlocksMax), dev::kRedThreads, 
           m_, Bd_.get(), x, ctmp_.get(), q, red(), sc_.get());
-      DBAG_LAUNCH_CHECK();
-    }
+          }
     tally_.block_ops += 2 * static_cast<std::uint64_t>(N_);
     ++dse_count_;
     ++dse_launches_;
@@ -398,23 +387,20 @@ class Rank {
     while (r_norm > tol * rhs_norm && n < max_iters) {
       const std::uint64_t ops0 = tally_.block_ops;
       const int dse0 = dse_count_;
-      dev::k_pcg_precond<S><<<rb, dev::kRedThreads, 0, st_>>>(m_, Binv_.get(), r_.get(), z_.get(), red(), sc_.get());
-      dev::k_pcg_p<S><<<grid_for(len, 256, 1 << 30), 256, 0, st_>>>(len, z_.get(), p_.get(), sc_.get());
-      DBAG_LAUNCH_CHECK();
-      dse<true>(p_.get(), q_.get());
+      launch(dev::k_pcg_precond<S>, rb, dev::kRedThreads, m_, Binv_.get(), r_.get(), z_.get(), red(), sc_.get());
+      launch(dev::k_pcg_p<S>, grid_for(len, 256, 1 << 30), 256, len, z_.get(), p_.get(), sc_.get());
+            dse<true>(p_.get(), q_.get());
       const std::uint64_t ops1 = tally_.block_ops;
       const int dse1 = dse_count_;
       const bool refresh = (n + 1) % 50 == 0;
       if (refresh) {
-        dev::k_pcg_xr<S, false><<<vb, dev::kRedThreads, 0, st_>>>(len, p_.get(), q_.get(), x, r_.get(), red(), sc_.get());
-        DBAG_LAUNCH_CHECK();
-        dse<false>(x, q_.get());
-        dev::k_pcg_refresh<S><<<vb, dev::kRedThreads, 0, st_>>>(len, g_.get(), q_.get(), r_.get(), red(), sc_.get(), 1);
+        launch(dev::k_pcg_xr<S, false>, vb, dev::kRedThreads, len, p_.get(), q_.get(), x, r_.get(), red(), sc_.get());
+                dse<false>(x, q_.get());
+        launch(dev::k_pcg_refresh<S>, vb, dev::kRedThreads, len, g_.get(), q_.get(), r_.get(), red(), sc_.get(), 1);
       } else {
-        dev::k_pcg_xr<S, true><<<vb, dev::kRedThreads, 0, st_>>>(len, p_.get(), q_.get(), x, r_.get(), red(), sc_.get());
+        launch(dev::k_pcg_xr<S, true>, vb, dev::kRedThreads, len, p_.get(), q_.get(), x, r_.get(), red(), sc_.get());
       }
-      DBAG_LAUNCH_CHECK();
-      read_scal();
+            read_scal();
       if (hsc_->status & 1) {  // rho breakdown: thrown before this iteration's DSE
         tally_.block_ops = ops0;
         dse_count_ = dse0;
@@ -438,33 +424,29 @@ class Rank {
     DBAG_CUDA(cudaSetDevice(device_));
     if (H_ > 0) DBAG_CUDA(cudaMemsetAsync(halo_buf_.get(), 0, sizeof(S) * 3 * static_cast<std::size_t>(H_), st_));
     if (n_tiles_ > 0) {
-      dev::k_point_pass<S, 1><<<n_tiles_, dev::kTile, 0, st_>>>(N_, tile_pt_.get(), pt_ptr_.get(), slot_cam_.get(),
+      launch(dev::k_point_pass<S, 1>, n_tiles_, dev::kTile, N_, tile_pt_.get(), pt_ptr_.get(), slot_cam_.get(),
                                                                E_pm_.get(), dxc_.get(), Cinv_.get(), w_.get(),
                                                                H_ > 0 ? halo_of_.get() : nullptr, halo_buf_.get(),
                                                                dxp_.get());
-      DBAG_LAUNCH_CHECK();
-    }
+          }
     if (H_ > 0) {
       comm_->allreduce_sum(halo_buf_.get(), 3 * H_, kT, st_);
       if (n_halo_loc_ > 0) {
-        dev::k_halo_finish<S, 1><<<grid_for(n_halo_loc_, 128, 1 << 30), 128, 0, st_>>>(
+        launch(dev::k_halo_finish<S, 1>, grid_for(n_halo_loc_, 128, 1 << 30), 128, 
             n_halo_loc_, halo_lpt_.get(), halo_idx_.get(), halo_buf_.get(), Cinv_.get(), w_.get(), dxp_.get());
-        DBAG_LAUNCH_CHECK();
-      }
+              }
     }
     tally_.block_ops += static_cast<std::uint64_t>(N_);
     double* d = dsc_.get();
     const int cb = grid_for(m_, dev::kRedThreads, dev::kRedBlocksMax);
-    dev::k_trial<S, 9><<<cb, dev::kRedThreads, 0, st_>>>(m_, xc_.get(), dxc_.get(), xct_.get(), B_.get(), v_.get(),
+    launch(dev::k_trial<S, 9>, cb, dev::kRedThreads, m_, xc_.get(), dxc_.get(), xct_.get(), B_.get(), v_.get(),
                                                          nullptr, lambda_, policy_, red(), d + 16);
-    DBAG_LAUNCH_CHECK();
-    const int pb = grid_for(n_loc_, dev::kRedThreads, dev::kRedBlocksMax);
+        const int pb = grid_for(n_loc_, dev::kRedThreads, dev::kRedBlocksMax);
     DBAG_CUDA(cudaMemsetAsync(d + 20, 0, 4 * sizeof(double), st_));
     if (n_loc_ > 0) {
-      dev::k_trial<S, 3><<<pb, dev::kRedThreads, 0, st_>>>(n_loc_, xp_.get(), dxp_.get(), xpt_.get(), C_.get(),
+      launch(dev::k_trial<S, 3>, pb, dev::kRedThreads, n_loc_, xp_.get(), dxp_.get(), xpt_.get(), C_.get(),
                                                            w_.get(), owned_.get(), lambda_, policy_, red(), d + 20);
-      DBAG_LAUNCH_CHECK();
-    }
+          }
     // point terms: [max, damp, gv] -> max over ranks for d[20], sum for d[21..22]
     comm_->allreduce_max(d + 20, 1, DType::f64, st_);
     comm_->allreduce_sum(d + 21, 2, DType::f64, st_);
@@ -524,6 +506,19 @@ class Rank {
   }
 
   // ------------------------------------------------------- test hooks ----
+  // Cost-path residuals of the current (or trial) state, shard edge order.
+  void residuals(bool trial, S* out) {
+    DBAG_CUDA(cudaSetDevice(device_));
+    DevBuf<S> r;
+    r.alloc(std::max<std::size_t>(static_cast<std::size_t>(N_) * 2, 1));
+    if (N_ > 0)
+      launch(dev::k_residuals<S>, grid_for(N_, 128, 1 << 30), 128, N_, slot_cam_.get(), slot_pt_.get(),
+             slot_edge_.get(), slot_px_.get(), slot_py_.get(), trial ? xct_.get() : xc_.get(),
+             trial ? xpt_.get() : xp_.get(), r.get());
+    DBAG_CUDA(cudaMemcpyAsync(out, r.get(), sizeof(S) * 2 * static_cast<std::size_t>(N_), cudaMemcpyDeviceToHost, st_));
+    DBAG_CUDA(cudaStreamSynchronize(st_));
+  }
+
   void get_jacobians(S* res, S* jac) {
     DBAG_CUDA(cudaSetDevice(device_));
     std::vector<S> jb(static_cast<std::size_t>(N_) * 28);
@@ -644,7 +639,16 @@ class Rank {
   }
   void sync() { DBAG_CUDA(cudaStreamSynchronize(st_)); }
 
+ public:
+  std::int64_t launches() const { return launches_; }
+
  private:
+  template <class... KA, class... A>
+  void launch(void (*k)(KA...), dim3 grid, dim3 block, A&&... args) {
+    k<<<grid, block, 0, st_>>>(std::forward<A>(args)...);
+    DBAG_LAUNCH_CHECK();
+    ++launches_;
+  }
   dev::RedWs red() { return dev::RedWs{red_part_.get(), red_cnt_.get()}; }
 
   void read_scal() {
@@ -654,20 +658,18 @@ class Rank {
   }
 
   void launch_dot(const S* a, const S* b, std::int64_t len, double* out) {
-    dev::k_dot<S><<<grid_for(len, dev::kRedThreads, dev::kRedBlocksMax), dev::kRedThreads, 0, st_>>>(len, a, b, red(),
+    launch(dev::k_dot<S>, grid_for(len, dev::kRedThreads, dev::kRedBlocksMax), dev::kRedThreads, len, a, b, red(),
                                                                                                      out);
-    DBAG_LAUNCH_CHECK();
-  }
+      }
 
   // c = E b over this rank's cameras, all-reduced (9m).
   void cam_apply(const S* bpt, S* out) {
     const std::size_t len = static_cast<std::size_t>(m_) * 9;
     DBAG_CUDA(cudaMemsetAsync(out, 0, sizeof(S) * std::max<std::size_t>(len, 1), st_));
     if (m_loc_ > 0) {
-      dev::k_cam_pass<S, 256><<<m_loc_, 256, 0, st_>>>(cam_ptr_.get(), cam_glob_.get(), cslot_pt_.get(), N_,
+      launch(dev::k_cam_pass<S, 256>, m_loc_, 256, cam_ptr_.get(), cam_glob_.get(), cslot_pt_.get(), N_,
                                                        E_cm_.get(), bpt, out);
-      DBAG_LAUNCH_CHECK();
-    }
+          }
     comm_->allreduce_sum(out, static_cast<std::int64_t>(len), kT, st_);
   }
 
@@ -695,22 +697,20 @@ class Rank {
     DBAG_CUDA(cudaMemsetAsync(halo_buf_.get(), 0, sizeof(S) * 12 * static_cast<std::size_t>(H_), st_));
     if (n_halo_loc_ > 0) {
       // [C(9) | w(3)] per halo point: scatter C into a 9-wide view, w after it
-      dev::k_halo_scatter<S, 9><<<grid_for(n_halo_loc_, 128, 1 << 30), 128, 0, st_>>>(
+      launch(dev::k_halo_scatter<S, 9>, grid_for(n_halo_loc_, 128, 1 << 30), 128, 
           n_halo_loc_, halo_lpt_.get(), halo_idx_.get(), C_.get(), halo_buf_.get());
-      dev::k_halo_scatter<S, 3><<<grid_for(n_halo_loc_, 128, 1 << 30), 128, 0, st_>>>(
+      launch(dev::k_halo_scatter<S, 3>, grid_for(n_halo_loc_, 128, 1 << 30), 128, 
           n_halo_loc_, halo_lpt_.get(), halo_idx_.get(), w_.get(), halo_buf_.get() + 9 * static_cast<std::size_t>(H_));
-      DBAG_LAUNCH_CHECK();
-    }
+          }
     return halo_buf_.get();
   }
   void C_halo_exchange_end() {
     if (H_ == 0 || n_halo_loc_ == 0) return;
-    dev::k_halo_gather<S, 9><<<grid_for(n_halo_loc_, 128, 1 << 30), 128, 0, st_>>>(
+    launch(dev::k_halo_gather<S, 9>, grid_for(n_halo_loc_, 128, 1 << 30), 128, 
         n_halo_loc_, halo_lpt_.get(), halo_idx_.get(), halo_buf_.get(), C_.get());
-    dev::k_halo_gather<S, 3><<<grid_for(n_halo_loc_, 128, 1 << 30), 128, 0, st_>>>(
+    launch(dev::k_halo_gather<S, 3>, grid_for(n_halo_loc_, 128, 1 << 30), 128, 
         n_halo_loc_, halo_lpt_.get(), halo_idx_.get(), halo_buf_.get() + 9 * static_cast<std::size_t>(H_), w_.get());
-    DBAG_LAUNCH_CHECK();
-  }
+      }
 
   cudaEvent_t prof_event() {
     if (prof_next_ == prof_ev_.size()) {
@@ -747,6 +747,7 @@ class Rank {
   int policy_ = 1;
   double step_inf_ = 0, damp_term_ = 0, gv_ = 0;
   int dse_count_ = 0;
+  std::int64_t launches_ = 0;
   std::int64_t dse_launches_ = 0;
   Tally tally_;
   Scal* hsc_ = nullptr;
@@ -770,5 +771,4 @@ class Rank {
   DevBuf<unsigned> red_cnt_;
   DevBuf<unsigned long long> bad_;
 };
-
 }  // namespace dbag

@@ -637,6 +637,17 @@ class RankContext:
     def synchronize(self):
         _check(N.lib().dbag_synchronize(self.h))
 
+    def launch_count(self) -> int:
+        n = C.c_int64()
+        _check(N.lib().dbag_launch_count(self.h, C.byref(n)))
+        return n.value
+
+    def residuals(self, trial: bool = False):
+        """Scalar-model residuals (2, N) in shard edge order (NaN on zero depth)."""
+        out = np.zeros(max(2 * self.nobs, 1), self.dtype)
+        _check(N.lib().dbag_residuals(self.h, int(trial), out.ctypes.data))
+        return out[:2 * self.nobs].reshape(2, self.nobs)
+
     def jacobians(self):
         """EdgeJacobianBatch in shard edge order: residuals (2, N), J (2, 12, N)."""
         res = np.zeros(2 * self.nobs, self.dtype)
