@@ -108,15 +108,9 @@ void fill_result(const Outcome& o, int K, dbag_result* out) {
 template <class S>
 void export_state(Rank<S>& rk, S* xc, S* xp) {
   const ShardPlan& pl = rk.plan();
-  std::vector<S> cams(static_cast<std::size_t>(pl.m) * 9), pts(static_cast<std::size_t>(pl.n) * 3);
-  rk.get_state(cams.data(), pts.data());
+  std::vector<S> cams(static_cast<std::size_t>(pl.m) * 9);
+  rk.get_state(cams.data(), xp, /*owned_only=*/true);
   if (xc && pl.rank == 0) std::copy(cams.begin(), cams.end(), xc);
-  if (xp)
-    for (std::int32_t lp = 0; lp < pl.pts.size(); ++lp) {
-      if (!pl.owned_lpt[static_cast<std::size_t>(lp)]) continue;
-      const std::size_t g = static_cast<std::size_t>(pl.pts.to_global[static_cast<std::size_t>(lp)]);
-      for (int k = 0; k < 3; ++k) xp[g * 3 + k] = pts[g * 3 + k];
-    }
 }
 
 // Runs body(rank) on one host thread per rank (run_on_workers,

@@ -1,0 +1,233 @@
+// dse.cuh — the streaming pass over the coupling blocks E.
+//
+// One pass over E per DSE (dba/solver.hpp:149-181):
+//   a_p = sum_s E_s^T x[cam_s]   b_p = C_p^-1 a_p   y_s = E_s b_p
+// E is stored as 128-slot chunk records: 27 lanes x 128 slots (lane-major:
+// thread i reads lane k at k*128 + i, fully coalesced) followed by the
+// chunk's static metadata (RecMeta: cameras, slot -> point, slots grouped by
+// camera, camera-major partial positions). One CTA per chunk, one thread per
+// slot; every index the tile needs arrives with the record, so the only
+// dependent loads are the camera-vector gathers (L1/L2-resident) and the
+// points' C factors. The E block stays in registers between the two
+// products, so each coupling block is read exactly once per DSE. y is folded
+// per (chunk, camera) by one warp (fixed lane order + shuffle tree) and
+// written to its camera-major partial slot; k_cam_reduce folds each camera's
+// contiguous partials. No atomics anywhere: deterministic.
+//
+// MODE 0  DSE          a from x, b = C^-1 a, y -> partials
+// MODE 1  back-subst.  a from x (= dx_c), out_pt = C^-1 (w - a)   (dba/solver.hpp:371-376)
+// MODE 2  rhs          b = C^-1 w, y -> partials                  (dba/solver.hpp:358-360)
+// Halo points (shared with other ranks; MODE 0/1) deposit a_p in halo_buf and
+// are finished after the halo all-reduce (k_halo_fix / k_halo_finish).
+// Points with more than 128 slots span several chunks ("long" tiles); their
+// chunks are skipped by k_dse_chunk and handled by k_dse_long.
+#pragma once
+
+#include <cstdint>
+
+#include "kernels.cuh"
+
+namespace dbag {
+namespace dev {
+
+template <class S>
+struct DseArgs {
+  std::int32_t n_chunks;
+  const S* rec;
+  const S* x;
+  const S* Cinv;
+  const S* w;
+  const std::int32_t* halo_of;
+  S* halo_buf;
+  S* part;
+  S* out_pt;
+  const std::int32_t* long_chunk;  // first chunk of each long tile
+  std::int32_t n_long;
+};
+
+template <class S>
+struct DseWork {
+  S a[kTile][3];
+  S b[kTile][3];
+  S y[kTile][9];
+  std::int32_t upart[kTile];
+  std::uint8_t uslot[kTile];
+  std::uint8_t ubeg[kTile + 8];
+};
+
+template <class S>
+__device__ __forceinline__ const RecMeta& rec_meta(const S* R) {
+  return *reinterpret_cast<const RecMeta*>(R + Rec<S>::kE);
+}
+
+// Point finish: halo deposit or b = C^-1 a (MODE 0), dx_p = C^-1 (w - a)
+// (MODE 1), b = C^-1 w (MODE 2). Returns b (zero for halo points).
+template <class S, int MODE>
+__device__ __forceinline__ void finish_point(const DseArgs<S>& A, std::int32_t p, S* tt, S* b) {
+  const std::int32_t h = (MODE != 2 && A.halo_of) ? A.halo_of[p] : -1;
+  if (h >= 0) {
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      A.halo_buf[std::size_t(h) * 3 + j] = tt[j];
+      b[j] = S(0);
+    }
+    return;
+  }
+  if (MODE == 1)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) tt[j] = A.w[std::size_t(p) * 3 + j] - tt[j];
+  if (MODE == 2)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) tt[j] = A.w[std::size_t(p) * 3 + j];
+  llt_solve<S, 3>(A.Cinv + std::size_t(p) * 9, tt);
+#pragma unroll
+  for (int j = 0; j < 3; ++j) b[j] = tt[j];
+  if (MODE == 1)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) A.out_pt[std::size_t(p) * 3 + j] = b[j];
+}
+
+// Folds sm.y per distinct camera of the chunk (warp per camera) into the
+// camera-major partials.
+template <class S>
+__device__ __forceinline__ void fold_cameras(const DseArgs<S>& A, DseWork<S>& sm, int nu) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int u = warp; u < nu; u += kTile / 32) {
+    S acc[9];
+#pragma unroll
+    for (int i = 0; i < 9; ++i) acc[i] = S(0);
+    for (int k = sm.ubeg[u] + lane; k < sm.ubeg[u + 1]; k += 32) {
+      const int o = sm.uslot[k];
+#pragma unroll
+      for (int i = 0; i < 9; ++i) acc[i] += sm.y[o][i];
+    }
+#pragma unroll
+    for (int i = 0; i < 9; ++i) {
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) acc[i] += __shfl_down_sync(0xffffffffu, acc[i], off);
+    }
+    if (lane == 0) {
+      S* out = A.part + std::size_t(sm.upart[u]) * 9;
+#pragma unroll
+      for (int i = 0; i < 9; ++i) out[i] = acc[i];
+    }
+  }
+}
+
+template <class S>
+__device__ __forceinline__ void stage_meta(const RecMeta& M, DseWork<S>& sm) {
+  const int tid = threadIdx.x;
+  sm.upart[tid] = M.upart[tid];
+  sm.uslot[tid] = M.uslot[tid];
+  sm.ubeg[tid] = M.ubeg[tid];
+  if (tid < 8) sm.ubeg[kTile + tid] = M.ubeg[kTile + tid];
+}
+
+template <class S, int MODE>
+__global__ void __launch_bounds__(kTile, 4) k_dse_chunk(DseArgs<S> A) {
+  __shared__ DseWork<S> sm;
+  const int tid = threadIdx.x;
+  const S* R = A.rec + std::size_t(blockIdx.x) * Rec<S>::kLen;
+  const RecMeta& M = rec_meta(R);
+  const std::int32_t p0 = M.p0, np = M.np, nslots = M.nslots, nchunk = M.nchunk, nu = M.nu;
+  if (nchunk > 1) return;  // long tile: k_dse_long
+  const bool mine = tid < nslots;
+  S e[27];
+#pragma unroll
+  for (int k = 0; k < 27; ++k) e[k] = R[k * kTile + tid];  // padding slots hold zeros
+  const int pti = M.pt[tid];
+  const int pb0 = M.pbeg[tid], pb1 = M.pbeg[tid + 1];
+  if (MODE != 1) stage_meta(M, sm);
+  if (MODE != 2) {
+    S a[3] = {S(0), S(0), S(0)};
+    if (mine) {
+      const S* xc = A.x + std::size_t(M.cam[tid]) * 9;
+#pragma unroll
+      for (int i = 0; i < 9; ++i) {
+        const S xv = __ldg(xc + i);
+        a[0] += e[i * 3 + 0] * xv;
+        a[1] += e[i * 3 + 1] * xv;
+        a[2] += e[i * 3 + 2] * xv;
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 3; ++j) sm.a[tid][j] = a[j];
+  }
+  __syncthreads();
+  if (tid < np) {
+    S tt[3] = {S(0), S(0), S(0)}, b[3];
+    if (MODE != 2)
+      for (int q = pb0; q < pb1; ++q)
+#pragma unroll
+        for (int j = 0; j < 3; ++j) tt[j] += sm.a[q][j];
+    finish_point<S, MODE>(A, p0 + tid, tt, b);
+#pragma unroll
+    for (int j = 0; j < 3; ++j) sm.b[tid][j] = b[j];
+  }
+  if constexpr (MODE != 1) {
+    __syncthreads();
+    const S b0 = sm.b[pti][0], b1 = sm.b[pti][1], b2 = sm.b[pti][2];
+#pragma unroll
+    for (int i = 0; i < 9; ++i) sm.y[tid][i] = (e[i * 3] * b0 + e[i * 3 + 1] * b1) + e[i * 3 + 2] * b2;
+    __syncthreads();
+    fold_cameras(A, sm, nu);
+  }
+}
+
+// One CTA per long tile (a single point observed more than 128 times).
+template <class S, int MODE>
+__global__ void __launch_bounds__(kTile) k_dse_long(DseArgs<S> A) {
+  __shared__ DseWork<S> sm;
+  const int tid = threadIdx.x;
+  const std::int32_t c0 = A.long_chunk[blockIdx.x];
+  const RecMeta& M0 = rec_meta(A.rec + std::size_t(c0) * Rec<S>::kLen);
+  const std::int32_t p = M0.p0, nchunk = M0.nchunk;
+  S a[3] = {S(0), S(0), S(0)};
+  if (MODE != 2) {
+    for (std::int32_t c = c0; c < c0 + nchunk; ++c) {
+      const S* R = A.rec + std::size_t(c) * Rec<S>::kLen;
+      const RecMeta& M = rec_meta(R);
+      if (tid < M.nslots) {
+        const S* xc = A.x + std::size_t(M.cam[tid]) * 9;
+#pragma unroll
+        for (int i = 0; i < 9; ++i) {
+          const S xv = __ldg(xc + i);
+          a[0] += R[(i * 3 + 0) * kTile + tid] * xv;
+          a[1] += R[(i * 3 + 1) * kTile + tid] * xv;
+          a[2] += R[(i * 3 + 2) * kTile + tid] * xv;
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < 3; ++j) sm.a[tid][j] = a[j];
+  __syncthreads();
+  if (tid == 0) {
+    S tt[3] = {S(0), S(0), S(0)}, b[3];
+    if (MODE != 2)
+      for (int k = 0; k < kTile; ++k)
+#pragma unroll
+        for (int j = 0; j < 3; ++j) tt[j] += sm.a[k][j];
+    finish_point<S, MODE>(A, p, tt, b);
+#pragma unroll
+    for (int j = 0; j < 3; ++j) sm.b[0][j] = b[j];
+  }
+  if constexpr (MODE != 1) {
+    for (std::int32_t c = c0; c < c0 + nchunk; ++c) {
+      const S* R = A.rec + std::size_t(c) * Rec<S>::kLen;
+      const RecMeta& M = rec_meta(R);
+      __syncthreads();
+      stage_meta(M, sm);
+      const S b0 = sm.b[0][0], b1 = sm.b[0][1], b2 = sm.b[0][2];
+#pragma unroll
+      for (int i = 0; i < 9; ++i)
+        sm.y[tid][i] = (R[(i * 3) * kTile + tid] * b0 + R[(i * 3 + 1) * kTile + tid] * b1) +
+                       R[(i * 3 + 2) * kTile + tid] * b2;
+      __syncthreads();
+      fold_cameras(A, sm, M.nu);
+    }
+  }
+}
+
+}  // namespace dev
+}  // namespace dbag

@@ -29,6 +29,42 @@ constexpr int kTile = 128;        // point-pass tile (slots) == block size
 constexpr int kRedThreads = 256;  // reduction kernels' block size
 constexpr int kRedBlocksMax = 592;  // 4 x 148 SMs
 
+// Static per-chunk metadata stored after the E lanes of its record, so one
+// coalesced read of a record brings every index a tile needs (no pointer
+// chasing through global index arrays on the streaming path).
+struct RecMeta {
+  std::int32_t p0, np, nslots, nchunk;  // first device point, points, slots; nchunk > 1: long tile
+  std::int32_t nu, ci, pad0, pad1;      // distinct cameras; chunk index inside its tile
+  std::int32_t cam[kTile];              // camera of each slot (padding: 0)
+  std::int32_t upart[kTile];            // camera-major partial position of each distinct camera
+  std::uint8_t pt[kTile];               // slot -> point index in the tile
+  std::uint8_t uslot[kTile];            // slots grouped by camera
+  std::uint8_t ubeg[kTile + 8];         // camera u's slots: uslot[ubeg[u] .. ubeg[u+1])
+  std::uint8_t pbeg[kTile + 8];         // point i's slots: [pbeg[i], pbeg[i+1])
+};
+static_assert(sizeof(RecMeta) % 16 == 0, "record metadata must keep 16-byte alignment");
+
+// E chunk record: 27 lanes x kTile slots (lane-major) then RecMeta; one
+// record per 128-slot chunk of the device slot order.
+template <class S>
+struct Rec {
+  static constexpr int kE = 27 * kTile;
+  static constexpr int kMeta = int(sizeof(RecMeta) / sizeof(S));
+  static constexpr int kLen = kE + kMeta;
+  static constexpr int kBytes = kLen * int(sizeof(S));
+};
+
+// Offset of E(k, slot s) inside the record array.
+template <class S>
+__device__ __forceinline__ std::size_t rec_at(const std::int32_t* slot_chunk, const std::int32_t* chunk_slot,
+                                              std::int64_t s) {
+  const std::int32_t c = slot_chunk[s];
+  return std::size_t(c) * Rec<S>::kLen + std::size_t(s - chunk_slot[c]);
+}
+
+template <int BS>
+__host__ __device__ constexpr int rcp_at(int k);
+
 struct SumOp {
   __device__ static double id() { return 0.0; }
   __device__ static double op(double a, double b) { return a + b; }
@@ -165,6 +201,8 @@ __global__ void __launch_bounds__(128) k_linearize(std::int64_t N, const std::in
                                                    const S* __restrict__ py, const S* __restrict__ w,
                                                    const S* __restrict__ xc, const S* __restrict__ xp,
                                                    S* __restrict__ Jb, S* __restrict__ E,
+                                                   const std::int32_t* __restrict__ slot_chunk,
+                                                   const std::int32_t* __restrict__ chunk_slot,
                                                    unsigned long long* bad_edge) {
   const std::int64_t s = blockIdx.x * std::int64_t(blockDim.x) + threadIdx.x;
   if (s >= N) return;
@@ -191,10 +229,12 @@ __global__ void __launch_bounds__(128) k_linearize(std::int64_t N, const std::in
   }
   row[26] = wt;
   row[27] = S(0);
+  const std::size_t base = rec_at<S>(slot_chunk, chunk_slot, s);
 #pragma unroll
   for (int i = 0; i < 9; ++i)
 #pragma unroll
-    for (int j = 0; j < 3; ++j) E[std::size_t(i * 3 + j) * N + s] = fm(wt, fa(fm(J[0][i], J[0][9 + j]), fm(J[1][i], J[1][9 + j])));
+    for (int j = 0; j < 3; ++j)
+      E[base + std::size_t(i * 3 + j) * kTile] = fm(wt, fa(fm(J[0][i], J[0][9 + j]), fm(J[1][i], J[1][9 + j])));
 }
 
 // C[p] += w Jp^T Jp, w[p] -= w Jp^T r over the point's slots in edge order
@@ -230,15 +270,13 @@ __global__ void k_assemble_points(std::int32_t n_loc, const std::int32_t* __rest
 }
 
 // B[c] += w Jc^T Jc, v[c] -= w Jc^T r (dba/block_matrix.hpp:378-385), one CTA
-// per local camera over its camera-major slots; also builds E_cm by copying
-// E_pm (bitwise-identical coupling blocks in both orders).
+// per local camera over its camera-major slots.
 template <class S, int NT>
 __global__ void __launch_bounds__(NT) k_assemble_cameras(const std::int32_t* __restrict__ cam_ptr,
                                                          const std::int32_t* __restrict__ cam_glob,
                                                          const std::int32_t* __restrict__ cslot_pslot,
-                                                         const S* __restrict__ Jb, std::int64_t N,
-                                                         const S* __restrict__ E_pm, S* __restrict__ E_cm,
-                                                         S* __restrict__ B, S* __restrict__ v) {
+                                                         const S* __restrict__ Jb, S* __restrict__ B,
+                                                         S* __restrict__ v) {
   const std::int32_t lc = blockIdx.x;
   double acc[54];  // 45 upper-triangular B entries + 9 v entries
 #pragma unroll
@@ -260,8 +298,6 @@ __global__ void __launch_bounds__(NT) k_assemble_cameras(const std::int32_t* __r
       for (int j = i; j < 9; ++j) acc[q++] += double(fm(wt, fa(fm(jc0[i], jc0[j]), fm(jc1[i], jc1[j]))));
 #pragma unroll
     for (int i = 0; i < 9; ++i) acc[45 + i] -= double(fm(wt, fa(fm(jc0[i], r0), fm(jc1[i], r1))));
-#pragma unroll
-    for (int k = 0; k < 27; ++k) E_cm[std::size_t(k) * N + cs] = E_pm[std::size_t(k) * N + ps];
   }
   __shared__ double red[32];
   const std::int32_t cg = cam_glob[lc];
@@ -286,8 +322,8 @@ __global__ void __launch_bounds__(NT) k_assemble_cameras(const std::int32_t* __r
 
 // ------------------------------------------------------ damp + factor ----
 // damp_into (dba/block_matrix.hpp:86-99) + per-block LLT that fails on a
-// pivot <= 0 (Eigen llt_inplace::unblocked semantics, :123-134) + explicit
-// inverse L^-T L^-1 for the GEMV-style block solves. Thread per block.
+// pivot <= 0 (Eigen llt_inplace::unblocked semantics, :123-134); stores the
+// lower factor for the solves. Thread per block.
 template <class S, int BS>
 __global__ void k_damp_factor(std::int64_t nb, const S* __restrict__ A, S lambda, int policy, S* __restrict__ Ad,
                               S* __restrict__ Ainv, const std::int32_t* __restrict__ index_map,
@@ -351,9 +387,20 @@ __global__ void k_damp_factor(std::int64_t nb, const S* __restrict__ A, S lambda
   for (int r = 0; r < BS; ++r)
 #pragma unroll
     for (int c = 0; c < BS; ++c) ai[r * BS + c] = c <= r ? m[r][c] : S(0);
+#pragma unroll
+  for (int k = 0; k < BS; ++k) ai[rcp_at<BS>(k)] = S(1) / m[k][k];
 }
 
-// x := (L L^T)^-1 x with L row-major lower (dba/block_matrix.hpp:140-150).
+// Position of 1/L_kk in the (otherwise unused) upper triangle of a stored
+// factor: row 0 for k < BS-1, (1, 2) for the last one.
+template <int BS>
+__host__ __device__ constexpr int rcp_at(int k) {
+  return k < BS - 1 ? k + 1 : BS + 2;
+}
+
+// x := (L L^T)^-1 x — the reference's forward + back substitution
+// (dba/block_matrix.hpp:140-150) with the divisions by L_kk replaced by
+// multiplications with the stored reciprocals.
 template <class S, int BS>
 __device__ __forceinline__ void llt_solve(const S* __restrict__ L, S* x) {
 #pragma unroll
@@ -361,82 +408,19 @@ __device__ __forceinline__ void llt_solve(const S* __restrict__ L, S* x) {
     S acc = x[r];
 #pragma unroll
     for (int c = 0; c < r; ++c) acc -= L[r * BS + c] * x[c];
-    x[r] = acc / L[r * BS + r];
+    x[r] = acc * L[rcp_at<BS>(r)];
   }
 #pragma unroll
   for (int r = BS - 1; r >= 0; --r) {
     S acc = x[r];
 #pragma unroll
     for (int c = r + 1; c < BS; ++c) acc -= L[c * BS + r] * x[c];
-    x[r] = acc / L[r * BS + r];
+    x[r] = acc * L[rcp_at<BS>(r)];
   }
 }
 
-// --------------------------------------------------------- point pass ----
-// Tile = whole points (<= kTile slots, or one long point). Thread per slot
-// computes a_s = E_s^T x[cam_s]; the tile's points sum their slots' partials
-// in slot (edge) order from shared memory, then finish per MODE:
-//   MODE 0 (DSE):     b_p = C_p^-1 a_p                (dba/solver.hpp:159-162)
-//   MODE 1 (backsub): dx_p = C_p^-1 (w_p - a_p)       (dba/solver.hpp:371-376)
-// Shared (halo) points store a_p into the halo buffer instead; the finish is
-// applied after the halo all-reduce by k_halo_finish.
-template <class S, int MODE>
-__global__ void __launch_bounds__(kTile) k_point_pass(std::int64_t N, const std::int32_t* __restrict__ tile_pt,
-                                                      const std::int32_t* __restrict__ pt_ptr,
-                                                      const std::int32_t* __restrict__ slot_cam,
-                                                      const S* __restrict__ E, const S* __restrict__ xcam,
-                                                      const S* __restrict__ Cinv, const S* __restrict__ wv,
-                                                      const std::int32_t* __restrict__ halo_of,
-                                                      S* __restrict__ halo_buf, S* __restrict__ out) {
-  __shared__ S part[kTile][3];
-  const std::int32_t p0 = tile_pt[blockIdx.x], p1 = tile_pt[blockIdx.x + 1];
-  const std::int32_t s0 = pt_ptr[p0], s1 = pt_ptr[p1];
-  S a[3] = {S(0), S(0), S(0)};
-  for (std::int32_t s = s0 + threadIdx.x; s < s1; s += kTile) {
-    const S* xc = xcam + std::size_t(slot_cam[s]) * 9;
-    S x[9];
-#pragma unroll
-    for (int i = 0; i < 9; ++i) x[i] = xc[i];
-#pragma unroll
-    for (int j = 0; j < 3; ++j) {
-      S acc = S(0);
-#pragma unroll
-      for (int i = 0; i < 9; ++i) acc += E[std::size_t(i * 3 + j) * N + s] * x[i];
-      a[j] += acc;
-    }
-  }
-#pragma unroll
-  for (int j = 0; j < 3; ++j) part[threadIdx.x][j] = a[j];
-  __syncthreads();
-  const std::int32_t np = p1 - p0;
-  if (int(threadIdx.x) >= np) return;
-  const std::int32_t p = p0 + threadIdx.x;
-  S t[3] = {S(0), S(0), S(0)};
-  if (s1 - s0 > kTile) {  // one long point: partials of all threads, thread order
-    for (int k = 0; k < kTile; ++k)
-#pragma unroll
-      for (int j = 0; j < 3; ++j) t[j] += part[k][j];
-  } else {
-    for (std::int32_t s = pt_ptr[p]; s < pt_ptr[p + 1]; ++s)
-#pragma unroll
-      for (int j = 0; j < 3; ++j) t[j] += part[s - s0][j];
-  }
-  const std::int32_t h = halo_of ? halo_of[p] : -1;
-  if (h >= 0) {
-#pragma unroll
-    for (int j = 0; j < 3; ++j) halo_buf[std::size_t(h) * 3 + j] = t[j];
-    return;
-  }
-  if (MODE == 1) {
-#pragma unroll
-    for (int j = 0; j < 3; ++j) t[j] = wv[std::size_t(p) * 3 + j] - t[j];
-  }
-  llt_solve<S, 3>(Cinv + std::size_t(p) * 9, t);
-#pragma unroll
-  for (int r = 0; r < 3; ++r) out[std::size_t(p) * 3 + r] = t[r];
-}
-
-// Finish of k_point_pass for halo points after the all-reduce.
+// -------------------------------------------------------------- halo ----
+// Finish of the MODE 1 pass (dse.cuh) for halo points after the all-reduce.
 template <class S, int MODE>
 __global__ void k_halo_finish(std::int32_t n, const std::int32_t* __restrict__ lpts,
                               const std::int32_t* __restrict__ hidx, const S* __restrict__ halo_buf,
@@ -450,18 +434,6 @@ __global__ void k_halo_finish(std::int32_t n, const std::int32_t* __restrict__ l
   if (MODE == 1)
 #pragma unroll
     for (int j = 0; j < 3; ++j) t[j] = wv[std::size_t(p) * 3 + j] - t[j];
-  llt_solve<S, 3>(Cinv + std::size_t(p) * 9, t);
-#pragma unroll
-  for (int r = 0; r < 3; ++r) out[std::size_t(p) * 3 + r] = t[r];
-}
-
-// b_p = C_p^-1 w_p for the right-hand side (dba/solver.hpp:358).
-template <class S>
-__global__ void k_point_solve(std::int32_t n, const S* __restrict__ Cinv, const S* __restrict__ wv,
-                              S* __restrict__ out) {
-  const std::int32_t p = blockIdx.x * blockDim.x + threadIdx.x;
-  if (p >= n) return;
-  S t[3] = {wv[std::size_t(p) * 3], wv[std::size_t(p) * 3 + 1], wv[std::size_t(p) * 3 + 2]};
   llt_solve<S, 3>(Cinv + std::size_t(p) * 9, t);
 #pragma unroll
   for (int r = 0; r < 3; ++r) out[std::size_t(p) * 3 + r] = t[r];
@@ -487,36 +459,6 @@ __global__ void k_halo_gather(std::int32_t n, const std::int32_t* __restrict__ l
   for (int k = 0; k < W; ++k) dst[std::size_t(lpts[i]) * W + k] = halo[std::size_t(hidx[i]) * W + k];
 }
 
-// -------------------------------------------------------- camera pass ----
-// c_c = sum over the camera's cslots of E_s b[pt_s] (dba/block_matrix.hpp:
-// 265-289), one CTA per local camera, written to the full 9m vector.
-template <class S, int NT>
-__global__ void __launch_bounds__(NT) k_cam_pass(const std::int32_t* __restrict__ cam_ptr,
-                                                 const std::int32_t* __restrict__ cam_glob,
-                                                 const std::int32_t* __restrict__ cslot_pt, std::int64_t N,
-                                                 const S* __restrict__ E, const S* __restrict__ bpt,
-                                                 S* __restrict__ out) {
-  const std::int32_t lc = blockIdx.x;
-  S acc[9];
-#pragma unroll
-  for (int i = 0; i < 9; ++i) acc[i] = S(0);
-  for (std::int32_t cs = cam_ptr[lc] + threadIdx.x; cs < cam_ptr[lc + 1]; cs += NT) {
-    const S* b = bpt + std::size_t(cslot_pt[cs]) * 3;
-    const S b0 = b[0], b1 = b[1], b2 = b[2];
-#pragma unroll
-    for (int i = 0; i < 9; ++i)
-      acc[i] += (E[std::size_t(i * 3) * N + cs] * b0 + E[std::size_t(i * 3 + 1) * N + cs] * b1) +
-                E[std::size_t(i * 3 + 2) * N + cs] * b2;
-  }
-  __shared__ double red[32];
-  const std::int32_t cg = cam_glob[lc];
-#pragma unroll
-  for (int i = 0; i < 9; ++i) {
-    const double t = block_reduce<SumOp>(double(acc[i]), red);
-    if (threadIdx.x == 0) out[std::size_t(cg) * 9 + i] = S(t);
-  }
-}
-
 // -------------------------------------------------------- camera space ----
 // PCG scalars kept on the device so the recurrences never round-trip.
 template <class S>
@@ -527,6 +469,95 @@ struct PcgScal {
   int status;  // bit 1: rho breakdown, bit 2: pq breakdown
   int n;
 };
+
+// ----------------------------------------------------- DSE camera side ----
+// Halo slots after the all-reduce of their points' a_p: b_p = C_p^-1 a_p,
+// y_s = E_s b_p into the slot's own partial.
+template <class S>
+__global__ void k_halo_fix(std::int32_t n, const std::int32_t* __restrict__ halo_slot,
+                           const std::int32_t* __restrict__ slot_dpt, const std::int32_t* __restrict__ halo_of,
+                           const S* __restrict__ halo_buf, const S* __restrict__ Cinv, const S* __restrict__ E,
+                           const std::int32_t* __restrict__ slot_chunk, const std::int32_t* __restrict__ chunk_slot,
+                           const std::int32_t* __restrict__ halo_pos, S* __restrict__ part) {
+  const std::int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const std::int32_t s = halo_slot[i];
+  const std::int32_t p = slot_dpt[s];
+  S b[3];
+#pragma unroll
+  for (int j = 0; j < 3; ++j) b[j] = halo_buf[std::size_t(halo_of[p]) * 3 + j];
+  llt_solve<S, 3>(Cinv + std::size_t(p) * 9, b);
+  const S* e = E + rec_at<S>(slot_chunk, chunk_slot, s);
+#pragma unroll
+  for (int r = 0; r < 9; ++r)
+    part[std::size_t(halo_pos[i]) * 9 + r] =
+        (e[(r * 3) * kTile] * b[0] + e[(r * 3 + 1) * kTile] * b[1]) + e[(r * 3 + 2) * kTile] * b[2];
+}
+
+// c_cam = fold of the camera's partials in chunk order (warp per camera, lanes
+// strided, fixed shuffle tree), then per EPI:
+//   0: out = c (all m cameras written; the all-reduce follows for K > 1)
+//   1: out = q = B_d x - c and p.q -> alpha (DSE, K = 1, dba/solver.hpp:166)
+//   2: out = g = v - c (right-hand side, K = 1, dba/solver.hpp:363)
+template <class S, int EPI>
+__global__ void __launch_bounds__(kRedThreads) k_cam_reduce(std::int32_t m, const std::int32_t* __restrict__ cam_part_ptr,
+                                                            const std::int32_t* __restrict__ cam_part,
+                                                            const S* __restrict__ part, const S* __restrict__ Bd,
+                                                            const S* __restrict__ x, const S* __restrict__ v,
+                                                            S* __restrict__ out, RedWs ws, PcgScal<S>* sc) {
+  const int lane = threadIdx.x & 31;
+  const std::int32_t cam = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  double pq = 0.0;
+  if (cam < m) {
+    S acc[9];
+#pragma unroll
+    for (int i = 0; i < 9; ++i) acc[i] = S(0);
+    for (std::int32_t k = cam_part_ptr[cam] + lane; k < cam_part_ptr[cam + 1]; k += 32) {
+      const S* pp = part + std::size_t(k) * 9;
+#pragma unroll
+      for (int i = 0; i < 9; ++i) acc[i] += pp[i];
+    }
+#pragma unroll
+    for (int i = 0; i < 9; ++i) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) acc[i] += __shfl_down_sync(0xffffffffu, acc[i], o);
+      acc[i] = __shfl_sync(0xffffffffu, acc[i], 0);
+    }
+    if (lane < 9) {
+      S c = acc[0];
+#pragma unroll
+      for (int i = 1; i < 9; ++i)
+        if (lane == i) c = acc[i];
+      S o;
+      if (EPI == 0) {
+        o = c;
+      } else if (EPI == 2) {
+        o = v[std::size_t(cam) * 9 + lane] - c;
+      } else {
+        const S* b = Bd + std::size_t(cam) * 81 + lane * 9;
+        const S* xv = x + std::size_t(cam) * 9;
+        S d = S(0);
+#pragma unroll
+        for (int k = 0; k < 9; ++k) d += b[k] * xv[k];
+        o = d - c;
+        pq = double(xv[lane]) * double(o);
+      }
+      out[std::size_t(cam) * 9 + lane] = o;
+    }
+  }
+  if (EPI == 1) {
+    const double vv[1] = {pq};
+    __shared__ double fin[1];
+    if (grid_reduce<SumOp, 1>(vv, ws.partials, ws.counter, fin)) {
+      if (threadIdx.x == 0) {
+        const double r = fin[0];
+        sc->pq = r;
+        if (!(r > 0.0) || isinf(r)) sc->status |= 2;
+        sc->alpha = S(sc->rho / r);
+      }
+    }
+  }
+}
 
 // q = Bd x - c, and p.q in double when PQ (dba/solver.hpp:166-167, 238).
 template <class S, bool PQ>

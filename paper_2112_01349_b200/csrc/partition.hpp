@@ -14,6 +14,7 @@
 #pragma once
 
 #include <algorithm>
+#include <limits>
 #include <cstdint>
 #include <vector>
 
@@ -174,6 +175,129 @@ inline ShardPlan plan_shard(const std::int32_t* cam_id, const std::int32_t* pt_i
     }
   }
   return s;
+}
+
+// Device layout of one shard for the fused DSE (kernels.cuh k_dse_fused):
+//   * device points: the shard's local points ordered by their smallest
+//     camera id (ties by local id) so that a tile of consecutive points
+//     touches few cameras; each point keeps its slots in edge order, so
+//     per-point sums accumulate in the reference's order;
+//   * tiles of whole points (<= `tile` slots, or one long point), split in
+//     chunks of <= `tile` slots;
+//   * per chunk, the distinct cameras it touches with their slot lists: one
+//     9-wide partial per (chunk, camera), reduced per camera in chunk order
+//     (deterministic, no atomics);
+//   * halo slots (of points shared with other ranks) get their own partials.
+struct DeviceLayout {
+  std::vector<std::int32_t> dpt_lpt;      // device point -> local point
+  std::vector<std::int32_t> lpt_dpt;      // local point -> device point
+  std::vector<std::int32_t> slot_edge;    // device slot -> shard edge
+  std::vector<std::int32_t> dpt_ptr;      // device point -> slot range
+  std::vector<std::int32_t> slot_dpt;     // device slot -> device point
+  std::vector<std::int32_t> tile_pt;      // tile -> device point range
+  std::vector<std::int32_t> tile_chunk;   // tile -> chunk range
+  std::vector<std::int32_t> chunk_slot;   // chunk -> first slot
+  std::vector<std::int32_t> slot_chunk;   // slot -> chunk
+  std::vector<std::int32_t> chunk_ucam;   // chunk -> range of its (camera) partials
+  std::vector<std::int32_t> ucam_cam;     // partial -> global camera
+  std::vector<std::int32_t> ucam_ptr;     // partial -> range in ucam_slot
+  std::vector<std::int32_t> ucam_slot;    // slot offsets within the chunk
+  std::vector<std::int32_t> halo_slot;    // device slots of halo points
+  std::int32_t n_part = 0;                // chunk partials + halo partials
+  std::vector<std::int32_t> cam_part_ptr;  // global camera -> partial ids
+  std::vector<std::int32_t> cam_part;
+  std::vector<std::int32_t> part_pos;      // partial id -> camera-major position
+};
+
+inline DeviceLayout build_device_layout(const ShardPlan& s, const std::int32_t* cam_id_shard, int tile) {
+  DeviceLayout d;
+  const std::int32_t np = s.pts.size();
+  std::vector<std::int32_t> mincam(static_cast<std::size_t>(np), std::numeric_limits<std::int32_t>::max());
+  for (std::size_t e = 0; e < s.pt_of.size(); ++e) {
+    auto& mc = mincam[static_cast<std::size_t>(s.pt_of[e])];
+    mc = std::min(mc, cam_id_shard[e]);
+  }
+  d.dpt_lpt.resize(static_cast<std::size_t>(np));
+  for (std::int32_t i = 0; i < np; ++i) d.dpt_lpt[static_cast<std::size_t>(i)] = i;
+  std::stable_sort(d.dpt_lpt.begin(), d.dpt_lpt.end(), [&](std::int32_t a, std::int32_t b) {
+    return mincam[static_cast<std::size_t>(a)] < mincam[static_cast<std::size_t>(b)];
+  });
+  d.lpt_dpt.resize(static_cast<std::size_t>(np));
+  d.dpt_ptr.assign(static_cast<std::size_t>(np) + 1, 0);
+  d.slot_edge.reserve(s.pt_of.size());
+  d.slot_dpt.reserve(s.pt_of.size());
+  for (std::int32_t dp = 0; dp < np; ++dp) {
+    const std::int32_t lp = d.dpt_lpt[static_cast<std::size_t>(dp)];
+    d.lpt_dpt[static_cast<std::size_t>(lp)] = dp;
+    for (std::int64_t k = s.pt_ptr[static_cast<std::size_t>(lp)]; k < s.pt_ptr[static_cast<std::size_t>(lp) + 1]; ++k) {
+      d.slot_edge.push_back(static_cast<std::int32_t>(s.pt_blk[static_cast<std::size_t>(k)]));
+      d.slot_dpt.push_back(dp);
+    }
+    d.dpt_ptr[static_cast<std::size_t>(dp) + 1] = static_cast<std::int32_t>(d.slot_edge.size());
+  }
+  std::vector<std::int64_t> ptr64(d.dpt_ptr.begin(), d.dpt_ptr.end());
+  d.tile_pt = make_point_tiles(ptr64, tile);
+  const std::size_t nt = d.tile_pt.size() - 1;
+  d.tile_chunk.assign(nt + 1, 0);
+  d.chunk_ucam.push_back(0);
+  std::vector<std::int32_t> seen(static_cast<std::size_t>(s.m), -1), order;
+  for (std::size_t t = 0; t < nt; ++t) {
+    const std::int32_t s0 = d.dpt_ptr[static_cast<std::size_t>(d.tile_pt[t])];
+    const std::int32_t s1 = d.dpt_ptr[static_cast<std::size_t>(d.tile_pt[t + 1])];
+    for (std::int32_t c0 = s0; c0 < s1; c0 += tile) {
+      const std::int32_t c1 = std::min(s1, c0 + tile);
+      d.chunk_slot.push_back(c0);
+      for (std::int32_t sl = c0; sl < c1; ++sl) d.slot_chunk.push_back(static_cast<std::int32_t>(d.chunk_slot.size()) - 1);
+      // distinct cameras in first-appearance order, slots grouped per camera
+      order.clear();
+      std::vector<std::vector<std::int32_t>> lists;
+      for (std::int32_t sl = c0; sl < c1; ++sl) {
+        const std::int32_t cam = cam_id_shard[d.slot_edge[static_cast<std::size_t>(sl)]];
+        std::int32_t& u = seen[static_cast<std::size_t>(cam)];
+        if (u < 0) {
+          u = static_cast<std::int32_t>(order.size());
+          order.push_back(cam);
+          lists.emplace_back();
+        }
+        lists[static_cast<std::size_t>(u)].push_back(sl - c0);
+      }
+      for (std::size_t u = 0; u < order.size(); ++u) {
+        d.ucam_cam.push_back(order[u]);
+        d.ucam_ptr.push_back(static_cast<std::int32_t>(d.ucam_slot.size()));
+        d.ucam_slot.insert(d.ucam_slot.end(), lists[u].begin(), lists[u].end());
+        seen[static_cast<std::size_t>(order[u])] = -1;
+      }
+      d.chunk_ucam.push_back(static_cast<std::int32_t>(d.ucam_cam.size()));
+    }
+    d.tile_chunk[t + 1] = static_cast<std::int32_t>(d.chunk_slot.size());
+  }
+  d.ucam_ptr.push_back(static_cast<std::int32_t>(d.ucam_slot.size()));
+  // halo partials: one per slot of a shared point
+  const std::int32_t n_chunk_part = static_cast<std::int32_t>(d.ucam_cam.size());
+  std::vector<std::int32_t> halo_cam;
+  for (std::int32_t sl = 0; sl < static_cast<std::int32_t>(d.slot_edge.size()); ++sl) {
+    const std::int32_t lp = d.dpt_lpt[static_cast<std::size_t>(d.slot_dpt[static_cast<std::size_t>(sl)])];
+    if (s.halo_of_lpt[static_cast<std::size_t>(lp)] >= 0) {
+      d.halo_slot.push_back(sl);
+      halo_cam.push_back(cam_id_shard[d.slot_edge[static_cast<std::size_t>(sl)]]);
+    }
+  }
+  d.n_part = n_chunk_part + static_cast<std::int32_t>(d.halo_slot.size());
+  // camera -> partial ids (chunk partials in chunk order, then halo partials)
+  d.cam_part_ptr.assign(static_cast<std::size_t>(s.m) + 1, 0);
+  for (std::int32_t c : d.ucam_cam) ++d.cam_part_ptr[static_cast<std::size_t>(c) + 1];
+  for (std::int32_t c : halo_cam) ++d.cam_part_ptr[static_cast<std::size_t>(c) + 1];
+  for (std::int32_t c = 0; c < s.m; ++c) d.cam_part_ptr[static_cast<std::size_t>(c) + 1] += d.cam_part_ptr[static_cast<std::size_t>(c)];
+  d.cam_part.resize(static_cast<std::size_t>(d.n_part));
+  std::vector<std::int32_t> cur(d.cam_part_ptr.begin(), d.cam_part_ptr.end() - 1);
+  for (std::int32_t u = 0; u < n_chunk_part; ++u)
+    d.cam_part[static_cast<std::size_t>(cur[static_cast<std::size_t>(d.ucam_cam[static_cast<std::size_t>(u)])]++)] = u;
+  for (std::size_t h = 0; h < halo_cam.size(); ++h)
+    d.cam_part[static_cast<std::size_t>(cur[static_cast<std::size_t>(halo_cam[h])]++)] = n_chunk_part + static_cast<std::int32_t>(h);
+  // partials are stored camera-major: partial id -> its position
+  d.part_pos.resize(static_cast<std::size_t>(d.n_part));
+  for (std::int32_t k = 0; k < d.n_part; ++k) d.part_pos[static_cast<std::size_t>(d.cam_part[static_cast<std::size_t>(k)])] = k;
+  return d;
 }
 
 }  // namespace dbag

@@ -10,19 +10,27 @@
 //   dse                                              dse()           dba/solver.hpp:149-181
 //   dpcg                                             pcg()           dba/solver.hpp:202-257
 //   back-substitution + trial + model terms          backsub_trial() dba/solver.hpp:371-410
+//
+// Point-indexed device arrays use "device point" ids (DeviceLayout: local
+// points reordered for camera locality); host-facing accessors map them back
+// to global point ids.
 #pragma once
 
 #include <cuda_runtime.h>
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
+#include <string>
 #include <limits>
 #include <memory>
+#include <utility>
 #include <vector>
 
 #include "comm.hpp"
 #include "common.hpp"
+#include "dse.cuh"
 #include "kernels.cuh"
 #include "partition.hpp"
 
@@ -41,7 +49,7 @@ class DevBuf {
     if (n) DBAG_CUDA(cudaMalloc(&p_, n * sizeof(T)));
   }
   void upload(const T* h, std::size_t n) {
-    alloc(n);
+    alloc(std::max<std::size_t>(n, 1));
     if (n) DBAG_CUDA(cudaMemcpy(p_, h, n * sizeof(T), cudaMemcpyHostToDevice));
   }
   void upload(const std::vector<T>& v) { upload(v.data(), v.size()); }
@@ -113,6 +121,7 @@ class Rank {
   std::int64_t edges() const { return N_; }
   Tally& tally() { return tally_; }
   int last_dse_count() const { return dse_count_; }
+  std::int64_t launches() const { return launches_; }
 
   // ------------------------------------------------------------ upload ----
   void upload(const dbag_problem& p, int jac_mode) {
@@ -135,61 +144,77 @@ class Rank {
     N_ = plan_.range.count;
     H_ = plan_.n_shared;
     const std::int64_t base = plan_.range.start;
+    lay_ = build_device_layout(plan_, p.camera_id + base, dev::kTile);
     const S* px = static_cast<const S*>(p.pixel_x);
     const S* py = static_cast<const S*>(p.pixel_y);
     const S* wt = static_cast<const S*>(p.weight);
-    std::vector<std::int32_t> s_cam(N_), s_pt(N_), s_edge(N_);
+    std::vector<std::int32_t> s_cam(N_);
     std::vector<S> s_px(N_), s_py(N_), s_w(N_);
     for (std::int64_t s = 0; s < N_; ++s) {
-      const std::int64_t e = plan_.pt_blk[static_cast<std::size_t>(s)];
-      s_edge[s] = static_cast<std::int32_t>(e);
+      const std::int64_t e = lay_.slot_edge[static_cast<std::size_t>(s)];
       s_cam[s] = p.camera_id[base + e];
-      s_pt[s] = plan_.pt_of[static_cast<std::size_t>(e)];
       s_px[s] = px[base + e];
       s_py[s] = py[base + e];
       s_w[s] = wt ? wt[base + e] : S(1);
       if (!(s_w[s] >= S(0))) throw Error(DBAG_INVALID_ARGUMENT, "edge weight must be >= 0");
     }
     slot_cam_.upload(s_cam);
-    slot_pt_.upload(s_pt);
-    slot_edge_.upload(s_edge);
+    slot_dpt_.upload(lay_.slot_dpt);
+    slot_edge_.upload(lay_.slot_edge);
     slot_px_.upload(s_px);
     slot_py_.upload(s_py);
     slot_w_.upload(s_w);
-    std::vector<std::int32_t> ptr32(plan_.pt_ptr.begin(), plan_.pt_ptr.end());
-    pt_ptr_.upload(ptr32);
-    tile_pt_.upload(plan_.tile_pt);
-    n_tiles_ = static_cast<int>(plan_.tile_pt.size()) - 1;
+    dpt_ptr_.upload(lay_.dpt_ptr);
+    n_tiles_ = static_cast<int>(lay_.tile_pt.size()) - 1;
+    chunk_slot_.upload(lay_.chunk_slot);
+    cam_part_ptr_.upload(lay_.cam_part_ptr);
+    halo_slot_.upload(lay_.halo_slot);
+    slot_chunk_.upload(lay_.slot_chunk);
+    n_chunks_ = static_cast<std::int32_t>(lay_.chunk_slot.size());
+    n_chunk_part_ = static_cast<std::int32_t>(lay_.ucam_cam.size());
+    part_.alloc(std::max<std::size_t>(static_cast<std::size_t>(lay_.n_part) * 9, 1));
+    // camera-major view (assembly of B, v)
     std::vector<std::int32_t> cptr32(plan_.cam_ptr.begin(), plan_.cam_ptr.end());
     cam_ptr_.upload(cptr32);
     cam_glob_.upload(plan_.cams.to_global);
-    pt_glob_.upload(plan_.pts.to_global);
-    cslot_pslot_.upload(plan_.cslot_pslot);
-    std::vector<std::int32_t> cslot_pt(N_);
-    for (std::int64_t c = 0; c < N_; ++c) cslot_pt[c] = s_pt[plan_.cslot_pslot[static_cast<std::size_t>(c)]];
-    cslot_pt_.upload(cslot_pt);
-    owned_.upload(plan_.owned_lpt);
-    // halo
+    std::vector<std::int32_t> dslot_of_edge(static_cast<std::size_t>(N_));
+    for (std::int64_t s = 0; s < N_; ++s) dslot_of_edge[static_cast<std::size_t>(lay_.slot_edge[static_cast<std::size_t>(s)])] = static_cast<std::int32_t>(s);
+    std::vector<std::int32_t> cslot(static_cast<std::size_t>(N_));
+    for (std::int64_t c = 0; c < N_; ++c)
+      cslot[static_cast<std::size_t>(c)] = dslot_of_edge[static_cast<std::size_t>(plan_.cam_blk[static_cast<std::size_t>(c)])];
+    cslot_dslot_.upload(cslot);
+    // device points
+    dpt_glob_.resize(static_cast<std::size_t>(n_loc_));
+    std::vector<std::int32_t> halo_of(static_cast<std::size_t>(n_loc_), -1);
+    std::vector<std::uint8_t> owned(static_cast<std::size_t>(n_loc_), 1);
     std::vector<std::int32_t> hl, hi;
-    for (std::int32_t lp = 0; lp < n_loc_; ++lp)
-      if (plan_.halo_of_lpt[static_cast<std::size_t>(lp)] >= 0) {
-        hl.push_back(lp);
-        hi.push_back(plan_.halo_of_lpt[static_cast<std::size_t>(lp)]);
+    for (std::int32_t d = 0; d < n_loc_; ++d) {
+      const std::int32_t lp = lay_.dpt_lpt[static_cast<std::size_t>(d)];
+      dpt_glob_[static_cast<std::size_t>(d)] = plan_.pts.to_global[static_cast<std::size_t>(lp)];
+      halo_of[static_cast<std::size_t>(d)] = plan_.halo_of_lpt[static_cast<std::size_t>(lp)];
+      owned[static_cast<std::size_t>(d)] = plan_.owned_lpt[static_cast<std::size_t>(lp)];
+      if (halo_of[static_cast<std::size_t>(d)] >= 0) {
+        hl.push_back(d);
+        hi.push_back(halo_of[static_cast<std::size_t>(d)]);
       }
+    }
+    owned_h_ = owned;
+    dpt_glob_d_.upload(dpt_glob_);
+    halo_of_.upload(halo_of);
+    owned_.upload(owned);
     n_halo_loc_ = static_cast<std::int32_t>(hl.size());
-    halo_of_.upload(plan_.halo_of_lpt);
-    halo_lpt_.upload(hl);
+    halo_dpt_.upload(hl);
     halo_idx_.upload(hi);
     halo_buf_.alloc(static_cast<std::size_t>(std::max<std::int64_t>(H_, 1)) * 12);
     // state + system
     const std::size_t cm = static_cast<std::size_t>(m_) * 9, pl = static_cast<std::size_t>(n_loc_) * 3;
     for (DevBuf<S>* b : {&xc_, &xct_, &dxc_, &v_, &g_, &r_, &z_, &p_, &q_, &ctmp_}) b->alloc(std::max<std::size_t>(cm, 1));
-    for (DevBuf<S>* b : {&xp_, &xpt_, &dxp_, &w_, &bpt_}) b->alloc(std::max<std::size_t>(pl, 1));
+    for (DevBuf<S>* b : {&xp_, &xpt_, &dxp_, &w_}) b->alloc(std::max<std::size_t>(pl, 1));
     for (DevBuf<S>* b : {&B_, &Bd_, &Binv_}) b->alloc(std::max<std::size_t>(cm * 9, 1));
-    for (DevBuf<S>* b : {&C_, &Cd_, &Cinv_}) b->alloc(std::max<std::size_t>(pl * 3, 1));
+    for (DevBuf<S>* b : {&C_, &Cd_}) b->alloc(std::max<std::size_t>(pl * 3, 1));
+    Cinv_.alloc(pl * 3 + 16 / sizeof(S));  // slack for the 16-byte-rounded TMA reads
     Jb_.alloc(std::max<std::size_t>(static_cast<std::size_t>(N_) * 28, 1));
-    E_pm_.alloc(std::max<std::size_t>(static_cast<std::size_t>(N_) * 27, 1));
-    E_cm_.alloc(std::max<std::size_t>(static_cast<std::size_t>(N_) * 27, 1));
+    build_records(s_cam);
     set_state(static_cast<const S*>(p.cameras), static_cast<const S*>(p.points));
     have_system_ = false;
   }
@@ -199,25 +224,27 @@ class Rank {
     DBAG_CUDA(cudaSetDevice(device_));
     DBAG_CUDA(cudaMemcpyAsync(xc_.get(), xc, sizeof(S) * 9 * static_cast<std::size_t>(m_), cudaMemcpyHostToDevice, st_));
     std::vector<S> loc(static_cast<std::size_t>(n_loc_) * 3);
-    for (std::int32_t lp = 0; lp < n_loc_; ++lp) {
-      const std::size_t g = static_cast<std::size_t>(plan_.pts.to_global[static_cast<std::size_t>(lp)]);
-      for (int k = 0; k < 3; ++k) loc[static_cast<std::size_t>(lp) * 3 + k] = xp[g * 3 + k];
-    }
+    for (std::int32_t d = 0; d < n_loc_; ++d)
+      for (int k = 0; k < 3; ++k)
+        loc[static_cast<std::size_t>(d) * 3 + k] = xp[static_cast<std::size_t>(dpt_glob_[static_cast<std::size_t>(d)]) * 3 + k];
     DBAG_CUDA(cudaMemcpyAsync(xp_.get(), loc.data(), sizeof(S) * loc.size(), cudaMemcpyHostToDevice, st_));
     DBAG_CUDA(cudaStreamSynchronize(st_));
     have_system_ = false;
   }
 
-  void get_state(S* xc, S* xp) {
+  // Cameras and this rank's points (owned_only: points it owns) into
+  // full-size host vectors; other entries are left untouched.
+  void get_state(S* xc, S* xp, bool owned_only = false) {
     DBAG_CUDA(cudaSetDevice(device_));
     if (xc) DBAG_CUDA(cudaMemcpyAsync(xc, xc_.get(), sizeof(S) * 9 * static_cast<std::size_t>(m_), cudaMemcpyDeviceToHost, st_));
     std::vector<S> loc(static_cast<std::size_t>(n_loc_) * 3);
     DBAG_CUDA(cudaMemcpyAsync(loc.data(), xp_.get(), sizeof(S) * loc.size(), cudaMemcpyDeviceToHost, st_));
     DBAG_CUDA(cudaStreamSynchronize(st_));
     if (xp)
-      for (std::int32_t lp = 0; lp < n_loc_; ++lp) {
-        const std::size_t g = static_cast<std::size_t>(plan_.pts.to_global[static_cast<std::size_t>(lp)]);
-        for (int k = 0; k < 3; ++k) xp[g * 3 + k] = loc[static_cast<std::size_t>(lp) * 3 + k];
+      for (std::int32_t d = 0; d < n_loc_; ++d) {
+        if (owned_only && !owned_h_[static_cast<std::size_t>(d)]) continue;
+        for (int k = 0; k < 3; ++k)
+          xp[static_cast<std::size_t>(dpt_glob_[static_cast<std::size_t>(d)]) * 3 + k] = loc[static_cast<std::size_t>(d) * 3 + k];
       }
   }
 
@@ -227,11 +254,12 @@ class Rank {
   double cost(bool trial, std::int64_t* bad_edge) {
     DBAG_CUDA(cudaSetDevice(device_));
     DBAG_CUDA(cudaMemsetAsync(bad_.get(), 0xff, sizeof(unsigned long long), st_));
-    launch(dev::k_cost<S>, grid_for(N_, dev::kRedThreads, dev::kRedBlocksMax), dev::kRedThreads, 
-        N_, slot_cam_.get(), slot_pt_.get(), slot_edge_.get(), plan_.range.start, slot_px_.get(), slot_py_.get(),
-        slot_w_.get(), trial ? xct_.get() : xc_.get(), trial ? xpt_.get() : xp_.get(), red(), dsc_.get(),
-        bad_.get());
-        if (N_ == 0) DBAG_CUDA(cudaMemsetAsync(dsc_.get(), 0, sizeof(double), st_));
+    DBAG_CUDA(cudaMemsetAsync(dsc_.get(), 0, sizeof(double), st_));
+    if (N_ > 0)
+      launch(dev::k_cost<S>, grid_for(N_, dev::kRedThreads, dev::kRedBlocksMax), dev::kRedThreads, N_,
+             slot_cam_.get(), slot_dpt_.get(), slot_edge_.get(), plan_.range.start, slot_px_.get(), slot_py_.get(),
+             slot_w_.get(), trial ? xct_.get() : xc_.get(), trial ? xpt_.get() : xp_.get(), red(), dsc_.get(),
+             bad_.get());
     tally_.edges += static_cast<std::uint64_t>(N_);
     comm_->allreduce_sum(dsc_.get(), 1, DType::f64, st_);
     const std::int64_t bad = agree_min_index(bad_.get());
@@ -247,34 +275,24 @@ class Rank {
     DBAG_CUDA(cudaMemsetAsync(bad_.get(), 0xff, sizeof(unsigned long long), st_));
     if (N_ > 0) {
       const int blocks = static_cast<int>((N_ + 127) / 128);
-      if (jac_mode_ == 1)
-        launch(dev::k_linearize<S, 1>, blocks, 128, N_, slot_cam_.get(), slot_pt_.get(), slot_edge_.get(),
-                                                         plan_.range.start, slot_px_.get(), slot_py_.get(),
-                                                         slot_w_.get(), xc_.get(), xp_.get(), Jb_.get(), E_pm_.get(),
-                                                         bad_.get());
-      else
-        launch(dev::k_linearize<S, 0>, blocks, 128, N_, slot_cam_.get(), slot_pt_.get(), slot_edge_.get(),
-                                                         plan_.range.start, slot_px_.get(), slot_py_.get(),
-                                                         slot_w_.get(), xc_.get(), xp_.get(), Jb_.get(), E_pm_.get(),
-                                                         bad_.get());
-          }
+      auto kern = jac_mode_ == 1 ? dev::k_linearize<S, 1> : dev::k_linearize<S, 0>;
+      launch(kern, blocks, 128, N_, slot_cam_.get(), slot_dpt_.get(), slot_edge_.get(), plan_.range.start,
+             slot_px_.get(), slot_py_.get(), slot_w_.get(), xc_.get(), xp_.get(), Jb_.get(), E_.get(), slot_chunk_.get(),
+             chunk_slot_.get(), bad_.get());
+    }
     tally_.edges += static_cast<std::uint64_t>(N_);
     const std::int64_t bad = agree_min_index(bad_.get());
     if (bad >= 0) throw degenerate_depth(bad);
     DBAG_CUDA(cudaMemsetAsync(B_.get(), 0, B_.size() * sizeof(S), st_));
     DBAG_CUDA(cudaMemsetAsync(v_.get(), 0, v_.size() * sizeof(S), st_));
-    if (n_loc_ > 0) {
-      launch(dev::k_assemble_points<S>, grid_for(n_loc_, 128, 1 << 30), 128, n_loc_, pt_ptr_.get(), Jb_.get(),
-                                                                                 C_.get(), w_.get());
-          }
-    if (m_loc_ > 0) {
-      launch(dev::k_assemble_cameras<S, 256>, m_loc_, 256, cam_ptr_.get(), cam_glob_.get(), cslot_pslot_.get(),
-                                                               Jb_.get(), N_, E_pm_.get(), E_cm_.get(), B_.get(),
-                                                               v_.get());
-          }
+    if (n_loc_ > 0)
+      launch(dev::k_assemble_points<S>, grid_for(n_loc_, 128, 1 << 30), 128, n_loc_, dpt_ptr_.get(), Jb_.get(),
+             C_.get(), w_.get());
+    if (m_loc_ > 0)
+      launch(dev::k_assemble_cameras<S, 256>, m_loc_, 256, cam_ptr_.get(), cam_glob_.get(), cslot_dslot_.get(),
+             Jb_.get(), B_.get(), v_.get());
     comm_->allreduce_sum(B_.get(), static_cast<std::int64_t>(m_) * 81, kT, st_);
-    comm_->allreduce_sum(C_halo_exchange_begin(), halo_count(12), kT, st_);
-    C_halo_exchange_end();
+    halo_exchange_Cw();
     comm_->allreduce_sum(v_.get(), static_cast<std::int64_t>(m_) * 9, kT, st_);
     have_system_ = true;
   }
@@ -286,17 +304,15 @@ class Rank {
     policy_ = policy;
     DBAG_CUDA(cudaMemsetAsync(bad_.get(), 0xff, 2 * sizeof(unsigned long long), st_));
     const S lam = static_cast<S>(lambda);
-    if (n_loc_ > 0) {
-      launch(dev::k_damp_factor<S, 3>, grid_for(n_loc_, 128, 1 << 30), 128, 
-          n_loc_, C_.get(), lam, policy, Cd_.get(), Cinv_.get(), pt_glob_.get(), bad_.get());
-          }
-    if (m_ > 0) {
-      launch(dev::k_damp_factor<S, 9>, grid_for(m_, 64, 1 << 30), 64, m_, B_.get(), lam, policy, Bd_.get(),
-                                                                          Binv_.get(), nullptr, bad_.get() + 1);
-          }
     // C failures are reported by global point id: the reference factors the
     // full-size C in global order and names the first failing block, C
     // before B (dba/solver.hpp:354-355, dba/block_matrix.hpp:123-134).
+    if (n_loc_ > 0)
+      launch(dev::k_damp_factor<S, 3>, grid_for(n_loc_, 128, 1 << 30), 128, n_loc_, C_.get(), lam, policy, Cd_.get(),
+             Cinv_.get(), dpt_glob_d_.get(), bad_.get());
+    if (m_ > 0)
+      launch(dev::k_damp_factor<S, 9>, grid_for(m_, 64, 1 << 30), 64, m_, B_.get(), lam, policy, Bd_.get(),
+             Binv_.get(), static_cast<const std::int32_t*>(nullptr), bad_.get() + 1);
     DBAG_CUDA(cudaMemcpyAsync(hbuf_, bad_.get(), 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st_));
     DBAG_CUDA(cudaStreamSynchronize(st_));
     unsigned long long raw[2];
@@ -318,15 +334,16 @@ class Rank {
   // ---------------------------------------------------------------- rhs ----
   void rhs() {
     DBAG_CUDA(cudaSetDevice(device_));
-    if (n_loc_ > 0) {
-      launch(dev::k_point_solve<S>, grid_for(n_loc_, 128, 1 << 30), 128, n_loc_, Cinv_.get(), w_.get(), bpt_.get());
-          }
-    cam_apply(bpt_.get(), ctmp_.get());
+    fused_pass<2>(nullptr);
     tally_.block_ops += static_cast<std::uint64_t>(N_);
-    const std::int64_t len = static_cast<std::int64_t>(m_) * 9;
-    if (len > 0) {
-      launch(dev::k_sub<S>, grid_for(len, 256, 1 << 30), 256, len, v_.get(), ctmp_.get(), g_.get());
-          }
+    if (comm_->size() == 1) {
+      cam_reduce<2>(nullptr, g_.get());
+    } else {
+      cam_reduce<0>(nullptr, ctmp_.get());
+      comm_->allreduce_sum(ctmp_.get(), static_cast<std::int64_t>(m_) * 9, kT, st_);
+      const std::int64_t len = static_cast<std::int64_t>(m_) * 9;
+      if (len > 0) launch(dev::k_sub<S>, grid_for(len, 256, 1 << 30), 256, len, v_.get(), ctmp_.get(), g_.get());
+    }
   }
 
   // ---------------------------------------------------------------- DSE ----
@@ -335,37 +352,32 @@ class Rank {
   void dse(const S* x, S* q) {
     const bool prof = profiling_;
     if (prof) DBAG_CUDA(cudaEventRecord(prof_event(), st_));
-    if (H_ > 0) DBAG_CUDA(cudaMemsetAsync(halo_buf_.get(), 0, sizeof(S) * 3 * static_cast<std::size_t>(H_), st_));
-    if (n_tiles_ > 0) {
-      launch(dev::k_point_pass<S, 0>, n_tiles_, dev::kTile, N_, tile_pt_.get(), pt_ptr_.get(), slot_cam_.get(),
-                                                               E_pm_.get(), x, Cinv_.get(), nullptr,
-                                                               H_ > 0 ? halo_of_.get() : nullptr, halo_buf_.get(),
-                                                               bpt_.get());
-          }
+    fused_pass<0>(x);
     if (prof) DBAG_CUDA(cudaEventRecord(prof_event(), st_));
-    if (H_ > 0) {
-      comm_->allreduce_sum(halo_buf_.get(), 3 * H_, kT, st_);
-      if (n_halo_loc_ > 0) {
-        launch(dev::k_halo_finish<S, 0>, grid_for(n_halo_loc_, 128, 1 << 30), 128, 
-            n_halo_loc_, halo_lpt_.get(), halo_idx_.get(), halo_buf_.get(), Cinv_.get(), nullptr, bpt_.get());
-              }
+    if (comm_->size() == 1) {
+      if (PQ) {
+        cam_reduce<1>(x, q);
+      } else {
+        cam_reduce<0>(nullptr, ctmp_.get());
+        launch(dev::k_cam_epilogue<S, false>, grid_for(m_, dev::kRedThreads, dev::kRedBlocksMax), dev::kRedThreads,
+               m_, Bd_.get(), x, ctmp_.get(), q, red(), sc_.get());
+      }
+    } else {
+      cam_reduce<0>(nullptr, ctmp_.get());
+      comm_->allreduce_sum(ctmp_.get(), static_cast<std::int64_t>(m_) * 9, kT, st_);
+      launch(dev::k_cam_epilogue<S, PQ>, grid_for(m_, dev::kRedThreads, dev::kRedBlocksMax), dev::kRedThreads, m_,
+             Bd_.get(), x, ctmp_.get(), q, red(), sc_.get());
     }
     if (prof) DBAG_CUDA(cudaEventRecord(prof_event(), st_));
-    cam_apply(bpt_.get(), ctmp_.get());
-    if (prof) DBAG_CUDA(cudaEventRecord(prof_event(), st_));
-    if (m_ > 0) {
-      launch(dev::k_cam_epilogue<S, PQ>, grid_for(m_, dev::kRedThreads, dev::kRedBlocksMax), dev::kRedThreads, 
-          m_, Bd_.get(), x, ctmp_.get(), q, red(), sc_.get());
-          }
     tally_.block_ops += 2 * static_cast<std::uint64_t>(N_);
     ++dse_count_;
     ++dse_launches_;
   }
 
   // --------------------------------------------------------------- DPCG ----
-  PcgOut pcg(double tol, int max_iters, S* x_out_dev = nullptr) {
+  PcgOut pcg(double tol, int max_iters) {
     DBAG_CUDA(cudaSetDevice(device_));
-    S* x = x_out_dev ? x_out_dev : dxc_.get();
+    S* x = dxc_.get();
     const std::int64_t len = static_cast<std::int64_t>(m_) * 9;
     dse_count_ = 0;
     DBAG_CUDA(cudaMemsetAsync(x, 0, sizeof(S) * std::max<std::int64_t>(len, 1), st_));
@@ -388,19 +400,20 @@ class Rank {
       const std::uint64_t ops0 = tally_.block_ops;
       const int dse0 = dse_count_;
       launch(dev::k_pcg_precond<S>, rb, dev::kRedThreads, m_, Binv_.get(), r_.get(), z_.get(), red(), sc_.get());
-      launch(dev::k_pcg_p<S>, grid_for(len, 256, 1 << 30), 256, len, z_.get(), p_.get(), sc_.get());
-            dse<true>(p_.get(), q_.get());
+      launch(dev::k_pcg_p<S>, grid_for(len, 256, 1 << 30), 256, len, z_.get(), p_.get(),
+             static_cast<const Scal*>(sc_.get()));
+      dse<true>(p_.get(), q_.get());
       const std::uint64_t ops1 = tally_.block_ops;
       const int dse1 = dse_count_;
       const bool refresh = (n + 1) % 50 == 0;
       if (refresh) {
         launch(dev::k_pcg_xr<S, false>, vb, dev::kRedThreads, len, p_.get(), q_.get(), x, r_.get(), red(), sc_.get());
-                dse<false>(x, q_.get());
+        dse<false>(x, q_.get());
         launch(dev::k_pcg_refresh<S>, vb, dev::kRedThreads, len, g_.get(), q_.get(), r_.get(), red(), sc_.get(), 1);
       } else {
         launch(dev::k_pcg_xr<S, true>, vb, dev::kRedThreads, len, p_.get(), q_.get(), x, r_.get(), red(), sc_.get());
       }
-            read_scal();
+      read_scal();
       if (hsc_->status & 1) {  // rho breakdown: thrown before this iteration's DSE
         tally_.block_ops = ops0;
         dse_count_ = dse0;
@@ -423,31 +436,25 @@ class Rank {
   void backsub_trial() {
     DBAG_CUDA(cudaSetDevice(device_));
     if (H_ > 0) DBAG_CUDA(cudaMemsetAsync(halo_buf_.get(), 0, sizeof(S) * 3 * static_cast<std::size_t>(H_), st_));
-    if (n_tiles_ > 0) {
-      launch(dev::k_point_pass<S, 1>, n_tiles_, dev::kTile, N_, tile_pt_.get(), pt_ptr_.get(), slot_cam_.get(),
-                                                               E_pm_.get(), dxc_.get(), Cinv_.get(), w_.get(),
-                                                               H_ > 0 ? halo_of_.get() : nullptr, halo_buf_.get(),
-                                                               dxp_.get());
-          }
+    stream_pass<1>(dxc_.get());
     if (H_ > 0) {
       comm_->allreduce_sum(halo_buf_.get(), 3 * H_, kT, st_);
-      if (n_halo_loc_ > 0) {
-        launch(dev::k_halo_finish<S, 1>, grid_for(n_halo_loc_, 128, 1 << 30), 128, 
-            n_halo_loc_, halo_lpt_.get(), halo_idx_.get(), halo_buf_.get(), Cinv_.get(), w_.get(), dxp_.get());
-              }
+      if (n_halo_loc_ > 0)
+        launch(dev::k_halo_finish<S, 1>, grid_for(n_halo_loc_, 128, 1 << 30), 128, n_halo_loc_, halo_dpt_.get(),
+               halo_idx_.get(), static_cast<const S*>(halo_buf_.get()), static_cast<const S*>(Cinv_.get()),
+               static_cast<const S*>(w_.get()), dxp_.get());
     }
     tally_.block_ops += static_cast<std::uint64_t>(N_);
     double* d = dsc_.get();
     const int cb = grid_for(m_, dev::kRedThreads, dev::kRedBlocksMax);
     launch(dev::k_trial<S, 9>, cb, dev::kRedThreads, m_, xc_.get(), dxc_.get(), xct_.get(), B_.get(), v_.get(),
-                                                         nullptr, lambda_, policy_, red(), d + 16);
-        const int pb = grid_for(n_loc_, dev::kRedThreads, dev::kRedBlocksMax);
+           static_cast<const std::uint8_t*>(nullptr), lambda_, policy_, red(), d + 16);
     DBAG_CUDA(cudaMemsetAsync(d + 20, 0, 4 * sizeof(double), st_));
-    if (n_loc_ > 0) {
-      launch(dev::k_trial<S, 3>, pb, dev::kRedThreads, n_loc_, xp_.get(), dxp_.get(), xpt_.get(), C_.get(),
-                                                           w_.get(), owned_.get(), lambda_, policy_, red(), d + 20);
-          }
-    // point terms: [max, damp, gv] -> max over ranks for d[20], sum for d[21..22]
+    if (n_loc_ > 0)
+      launch(dev::k_trial<S, 3>, grid_for(n_loc_, dev::kRedThreads, dev::kRedBlocksMax), dev::kRedThreads, n_loc_,
+             xp_.get(), dxp_.get(), xpt_.get(), C_.get(), w_.get(), static_cast<const std::uint8_t*>(owned_.get()),
+             lambda_, policy_, red(), d + 20);
+    // point terms: max over ranks for d[20], sums for d[21..22]
     comm_->allreduce_max(d + 20, 1, DType::f64, st_);
     comm_->allreduce_sum(d + 21, 2, DType::f64, st_);
     DBAG_CUDA(cudaMemcpyAsync(hbuf_, d + 16, 8 * sizeof(double), cudaMemcpyDeviceToHost, st_));
@@ -481,14 +488,14 @@ class Rank {
     DBAG_CUDA(cudaStreamSynchronize(st_));
     double a = 0, b = 0;
     for (S v : hc) a = std::max(a, double(std::abs(v)));
-    for (std::int32_t lp = 0; lp < n_loc_; ++lp)
-      if (plan_.owned_lpt[static_cast<std::size_t>(lp)])
-        for (int k = 0; k < 3; ++k) b = std::max(b, double(std::abs(hp[static_cast<std::size_t>(lp) * 3 + k])));
-    double* d = dsc_.get();
+    for (std::int32_t d = 0; d < n_loc_; ++d)
+      if (owned_h_[static_cast<std::size_t>(d)])
+        for (int k = 0; k < 3; ++k) b = std::max(b, double(std::abs(hp[static_cast<std::size_t>(d) * 3 + k])));
+    double* dd = dsc_.get();
     hbuf_[0] = b;
-    DBAG_CUDA(cudaMemcpyAsync(d + 30, hbuf_, sizeof(double), cudaMemcpyHostToDevice, st_));
-    comm_->allreduce_max(d + 30, 1, DType::f64, st_);
-    DBAG_CUDA(cudaMemcpyAsync(hbuf_, d + 30, sizeof(double), cudaMemcpyDeviceToHost, st_));
+    DBAG_CUDA(cudaMemcpyAsync(dd + 30, hbuf_, sizeof(double), cudaMemcpyHostToDevice, st_));
+    comm_->allreduce_max(dd + 30, 1, DType::f64, st_);
+    DBAG_CUDA(cudaMemcpyAsync(hbuf_, dd + 30, sizeof(double), cudaMemcpyDeviceToHost, st_));
     DBAG_CUDA(cudaStreamSynchronize(st_));
     *ic = a;
     *ip = hbuf_[0];
@@ -512,7 +519,7 @@ class Rank {
     DevBuf<S> r;
     r.alloc(std::max<std::size_t>(static_cast<std::size_t>(N_) * 2, 1));
     if (N_ > 0)
-      launch(dev::k_residuals<S>, grid_for(N_, 128, 1 << 30), 128, N_, slot_cam_.get(), slot_pt_.get(),
+      launch(dev::k_residuals<S>, grid_for(N_, 128, 1 << 30), 128, N_, slot_cam_.get(), slot_dpt_.get(),
              slot_edge_.get(), slot_px_.get(), slot_py_.get(), trial ? xct_.get() : xc_.get(),
              trial ? xpt_.get() : xp_.get(), r.get());
     DBAG_CUDA(cudaMemcpyAsync(out, r.get(), sizeof(S) * 2 * static_cast<std::size_t>(N_), cudaMemcpyDeviceToHost, st_));
@@ -521,10 +528,11 @@ class Rank {
 
   void get_jacobians(S* res, S* jac) {
     DBAG_CUDA(cudaSetDevice(device_));
+    DBAG_CUDA(cudaStreamSynchronize(st_));
     std::vector<S> jb(static_cast<std::size_t>(N_) * 28);
     DBAG_CUDA(cudaMemcpy(jb.data(), Jb_.get(), sizeof(S) * jb.size(), cudaMemcpyDeviceToHost));
     for (std::int64_t s = 0; s < N_; ++s) {
-      const std::int64_t e = plan_.pt_blk[static_cast<std::size_t>(s)];
+      const std::int64_t e = lay_.slot_edge[static_cast<std::size_t>(s)];
       const S* row = jb.data() + static_cast<std::size_t>(s) * 28;
       res[e] = row[0];
       res[N_ + e] = row[1];
@@ -545,17 +553,18 @@ class Rank {
     DBAG_CUDA(cudaMemcpy(ww.data(), w_.get(), sizeof(S) * ww.size(), cudaMemcpyDeviceToHost));
     if (C) std::fill(C, C + static_cast<std::size_t>(n_glob_) * 9, S(0));
     if (w) std::fill(w, w + static_cast<std::size_t>(n_glob_) * 3, S(0));
-    for (std::int32_t lp = 0; lp < n_loc_; ++lp) {
-      const std::size_t g = static_cast<std::size_t>(plan_.pts.to_global[static_cast<std::size_t>(lp)]);
-      if (C) std::copy(c.begin() + lp * 9, c.begin() + lp * 9 + 9, C + g * 9);
-      if (w) std::copy(ww.begin() + lp * 3, ww.begin() + lp * 3 + 3, w + g * 3);
+    for (std::int32_t d = 0; d < n_loc_; ++d) {
+      const std::size_t g = static_cast<std::size_t>(dpt_glob_[static_cast<std::size_t>(d)]);
+      if (C) std::copy(c.begin() + d * 9, c.begin() + d * 9 + 9, C + g * 9);
+      if (w) std::copy(ww.begin() + d * 3, ww.begin() + d * 3 + 3, w + g * 3);
     }
     if (E) {
-      std::vector<S> e(static_cast<std::size_t>(N_) * 27);
-      DBAG_CUDA(cudaMemcpy(e.data(), E_pm_.get(), sizeof(S) * e.size(), cudaMemcpyDeviceToHost));
+      std::vector<S> e(E_.size());
+      DBAG_CUDA(cudaMemcpy(e.data(), E_.get(), sizeof(S) * e.size(), cudaMemcpyDeviceToHost));
       for (std::int64_t s = 0; s < N_; ++s) {
-        const std::int64_t ed = plan_.pt_blk[static_cast<std::size_t>(s)];
-        for (int k = 0; k < 27; ++k) E[ed * 27 + k] = e[static_cast<std::size_t>(k) * N_ + s];
+        const std::int64_t ed = lay_.slot_edge[static_cast<std::size_t>(s)];
+        const std::size_t at = rec_offset(s);
+        for (int k = 0; k < 27; ++k) E[ed * 27 + k] = e[at + static_cast<std::size_t>(k) * dev::kTile];
       }
     }
   }
@@ -569,32 +578,37 @@ class Rank {
     if (v) DBAG_CUDA(cudaMemcpy(v_.get(), v, sizeof(S) * 9 * static_cast<std::size_t>(m_), cudaMemcpyHostToDevice));
     if (C || w) {
       std::vector<S> c(static_cast<std::size_t>(n_loc_) * 9), ww(static_cast<std::size_t>(n_loc_) * 3);
-      for (std::int32_t lp = 0; lp < n_loc_; ++lp) {
-        const std::size_t g = static_cast<std::size_t>(plan_.pts.to_global[static_cast<std::size_t>(lp)]);
-        if (C) std::copy(C + g * 9, C + g * 9 + 9, c.begin() + lp * 9);
-        if (w) std::copy(w + g * 3, w + g * 3 + 3, ww.begin() + lp * 3);
+      DBAG_CUDA(cudaMemcpy(c.data(), C_.get(), sizeof(S) * c.size(), cudaMemcpyDeviceToHost));
+      DBAG_CUDA(cudaMemcpy(ww.data(), w_.get(), sizeof(S) * ww.size(), cudaMemcpyDeviceToHost));
+      for (std::int32_t d = 0; d < n_loc_; ++d) {
+        const std::size_t g = static_cast<std::size_t>(dpt_glob_[static_cast<std::size_t>(d)]);
+        if (C) std::copy(C + g * 9, C + g * 9 + 9, c.begin() + d * 9);
+        if (w) std::copy(w + g * 3, w + g * 3 + 3, ww.begin() + d * 3);
       }
-      if (C) DBAG_CUDA(cudaMemcpy(C_.get(), c.data(), sizeof(S) * c.size(), cudaMemcpyHostToDevice));
-      if (w) DBAG_CUDA(cudaMemcpy(w_.get(), ww.data(), sizeof(S) * ww.size(), cudaMemcpyHostToDevice));
+      DBAG_CUDA(cudaMemcpy(C_.get(), c.data(), sizeof(S) * c.size(), cudaMemcpyHostToDevice));
+      DBAG_CUDA(cudaMemcpy(w_.get(), ww.data(), sizeof(S) * ww.size(), cudaMemcpyHostToDevice));
     }
     if (E_table) {
-      std::vector<S> pm(static_cast<std::size_t>(N_) * 27), cmv(static_cast<std::size_t>(N_) * 27);
+      std::vector<S> e(E_.size());
+      DBAG_CUDA(cudaMemcpy(e.data(), E_.get(), sizeof(S) * e.size(), cudaMemcpyDeviceToHost));
       for (std::int64_t s = 0; s < N_; ++s) {
-        const std::int64_t ed = plan_.range.start + plan_.pt_blk[static_cast<std::size_t>(s)];
-        for (int k = 0; k < 27; ++k) pm[static_cast<std::size_t>(k) * N_ + s] = E_table[ed * 27 + k];
+        const std::int64_t ed = plan_.range.start + lay_.slot_edge[static_cast<std::size_t>(s)];
+        const std::size_t at = rec_offset(s);
+        for (int k = 0; k < 27; ++k) e[at + static_cast<std::size_t>(k) * dev::kTile] = E_table[ed * 27 + k];
       }
-      for (std::int64_t c = 0; c < N_; ++c) {
-        const std::int64_t s = plan_.cslot_pslot[static_cast<std::size_t>(c)];
-        for (int k = 0; k < 27; ++k) cmv[static_cast<std::size_t>(k) * N_ + c] = pm[static_cast<std::size_t>(k) * N_ + s];
-      }
-      DBAG_CUDA(cudaMemcpy(E_pm_.get(), pm.data(), sizeof(S) * pm.size(), cudaMemcpyHostToDevice));
-      DBAG_CUDA(cudaMemcpy(E_cm_.get(), cmv.data(), sizeof(S) * cmv.size(), cudaMemcpyHostToDevice));
+      DBAG_CUDA(cudaMemcpy(E_.get(), e.data(), sizeof(S) * e.size(), cudaMemcpyHostToDevice));
     }
     have_system_ = true;
   }
 
-  // Fabricated blocks are already damped: factor them as-is (lambda = 0,
-  // identity policy adds exactly 0 to every diagonal entry).
+  std::size_t rec_offset(std::int64_t s) const {
+    const std::int32_t c = lay_.slot_chunk[static_cast<std::size_t>(s)];
+    return static_cast<std::size_t>(c) * dev::Rec<S>::kLen +
+           static_cast<std::size_t>(s - lay_.chunk_slot[static_cast<std::size_t>(c)]);
+  }
+
+  // Fabricated blocks are already damped: factor them as-is (identity
+  // damping with lambda = 0 adds exactly 0 to every diagonal entry).
   void factor_as_is() { damp_factor(0.0, 0); }
 
   void dse_host(const S* x, S* out) {
@@ -639,9 +653,6 @@ class Rank {
   }
   void sync() { DBAG_CUDA(cudaStreamSynchronize(st_)); }
 
- public:
-  std::int64_t launches() const { return launches_; }
-
  private:
   template <class... KA, class... A>
   void launch(void (*k)(KA...), dim3 grid, dim3 block, A&&... args) {
@@ -649,6 +660,7 @@ class Rank {
     DBAG_LAUNCH_CHECK();
     ++launches_;
   }
+
   dev::RedWs red() { return dev::RedWs{red_part_.get(), red_cnt_.get()}; }
 
   void read_scal() {
@@ -659,18 +671,115 @@ class Rank {
 
   void launch_dot(const S* a, const S* b, std::int64_t len, double* out) {
     launch(dev::k_dot<S>, grid_for(len, dev::kRedThreads, dev::kRedBlocksMax), dev::kRedThreads, len, a, b, red(),
-                                                                                                     out);
-      }
+           out);
+  }
 
-  // c = E b over this rank's cameras, all-reduced (9m).
-  void cam_apply(const S* bpt, S* out) {
-    const std::size_t len = static_cast<std::size_t>(m_) * 9;
-    DBAG_CUDA(cudaMemsetAsync(out, 0, sizeof(S) * std::max<std::size_t>(len, 1), st_));
-    if (m_loc_ > 0) {
-      launch(dev::k_cam_pass<S, 256>, m_loc_, 256, cam_ptr_.get(), cam_glob_.get(), cslot_pt_.get(), N_,
-                                                       E_cm_.get(), bpt, out);
-          }
-    comm_->allreduce_sum(out, static_cast<std::int64_t>(len), kT, st_);
+  // The point-side half of the DSE (MODE 0) / rhs (MODE 2): one pass over E
+  // writing the per-(chunk, camera) partials; halo points are finished after
+  // their all-reduce.
+  template <int MODE>
+  void fused_pass(const S* x) {
+    const bool halo = MODE == 0 && H_ > 0;
+    if (halo) DBAG_CUDA(cudaMemsetAsync(halo_buf_.get(), 0, sizeof(S) * 3 * static_cast<std::size_t>(H_), st_));
+    stream_pass<MODE>(x);
+    const std::int32_t nh = static_cast<std::int32_t>(lay_.halo_slot.size());
+    if (MODE == 0 && H_ > 0) {
+      comm_->allreduce_sum(halo_buf_.get(), 3 * H_, kT, st_);
+      if (nh > 0)
+        launch(dev::k_halo_fix<S>, grid_for(nh, 128, 1 << 30), 128, nh, halo_slot_.get(), slot_dpt_.get(),
+               halo_of_.get(), static_cast<const S*>(halo_buf_.get()), static_cast<const S*>(Cinv_.get()),
+               static_cast<const S*>(E_.get()), slot_chunk_.get(), chunk_slot_.get(), halo_pos_.get(), part_.get());
+    } else if (MODE == 2 && nh > 0) {
+      // rhs: C and w are complete on every rank; halo slots still need
+      // their own partials (they were excluded from the chunk partials only
+      // in MODE 0, so here they duplicate nothing: zero them).
+      DBAG_CUDA(cudaMemsetAsync(part_.get() + static_cast<std::size_t>(n_chunk_part_) * 9, 0,
+                                sizeof(S) * 9 * static_cast<std::size_t>(nh), st_));
+    }
+  }
+
+  // E chunk records: zero E lanes plus each chunk's static metadata
+  // (kernels.cuh RecMeta); the E lanes are (re)written by k_linearize.
+  void build_records(const std::vector<std::int32_t>& s_cam) {
+    const std::size_t nc = static_cast<std::size_t>(std::max(n_chunks_, 1));
+    std::vector<S> recs(nc * dev::Rec<S>::kLen, S(0));
+    std::vector<std::int32_t> long_first;
+    const std::size_t nt = lay_.tile_pt.size() - 1;
+    for (std::size_t t = 0; t < nt; ++t) {
+      const std::int32_t p0 = lay_.tile_pt[t], p1 = lay_.tile_pt[t + 1];
+      const std::int32_t s0 = lay_.dpt_ptr[static_cast<std::size_t>(p0)];
+      const std::int32_t ch0 = lay_.tile_chunk[t], ch1 = lay_.tile_chunk[t + 1];
+      if (ch1 - ch0 > 1) long_first.push_back(ch0);
+      for (std::int32_t c = ch0; c < ch1; ++c) {
+        auto* M = reinterpret_cast<dev::RecMeta*>(recs.data() + static_cast<std::size_t>(c) * dev::Rec<S>::kLen +
+                                                  dev::Rec<S>::kE);
+        const std::int32_t c0 = lay_.chunk_slot[static_cast<std::size_t>(c)];
+        const std::int32_t c1 = (c + 1 < ch1) ? lay_.chunk_slot[static_cast<std::size_t>(c) + 1]
+                                              : lay_.dpt_ptr[static_cast<std::size_t>(p1)];
+        M->p0 = p0;
+        M->np = p1 - p0;
+        M->nslots = c1 - c0;
+        M->nchunk = ch1 - ch0;
+        M->ci = c - ch0;
+        for (std::int32_t sl = c0; sl < c1; ++sl) {
+          M->cam[sl - c0] = s_cam[static_cast<std::size_t>(sl)];
+          M->pt[sl - c0] = ch1 - ch0 > 1 ? 0
+                                          : static_cast<std::uint8_t>(lay_.slot_dpt[static_cast<std::size_t>(sl)] - p0);
+        }
+        if (ch1 - ch0 == 1)
+          for (std::int32_t i = 0; i <= p1 - p0; ++i)
+            M->pbeg[i] = static_cast<std::uint8_t>(lay_.dpt_ptr[static_cast<std::size_t>(p0 + i)] - s0);
+        const std::int32_t u0 = lay_.chunk_ucam[static_cast<std::size_t>(c)];
+        const std::int32_t u1 = lay_.chunk_ucam[static_cast<std::size_t>(c) + 1];
+        M->nu = u1 - u0;
+        const std::int32_t k0 = lay_.ucam_ptr[static_cast<std::size_t>(u0)];
+        for (std::int32_t u = u0; u <= u1; ++u) {
+          M->ubeg[u - u0] = static_cast<std::uint8_t>(lay_.ucam_ptr[static_cast<std::size_t>(u)] - k0);
+          if (u < u1) M->upart[u - u0] = lay_.part_pos[static_cast<std::size_t>(u)];
+        }
+        for (std::int32_t k = k0; k < lay_.ucam_ptr[static_cast<std::size_t>(u1)]; ++k)
+          M->uslot[k - k0] = static_cast<std::uint8_t>(lay_.ucam_slot[static_cast<std::size_t>(k)]);
+      }
+    }
+    E_.upload(recs);
+    n_long_ = static_cast<std::int32_t>(long_first.size());
+    long_chunk_.upload(long_first);
+    std::vector<std::int32_t> hpos(lay_.halo_slot.size());
+    for (std::size_t i = 0; i < hpos.size(); ++i)
+      hpos[i] = lay_.part_pos[static_cast<std::size_t>(n_chunk_part_) + i];
+    halo_pos_.upload(hpos);
+  }
+
+  dev::DseArgs<S> dse_args(const S* x) {
+    dev::DseArgs<S> a;
+    a.n_chunks = n_chunks_;
+    a.rec = E_.get();
+    a.x = x;
+    a.Cinv = Cinv_.get();
+    a.w = w_.get();
+    a.halo_of = H_ > 0 ? halo_of_.get() : nullptr;
+    a.halo_buf = halo_buf_.get();
+    a.part = part_.get();
+    a.out_pt = dxp_.get();
+    a.long_chunk = long_chunk_.get();
+    a.n_long = n_long_;
+    return a;
+  }
+
+  template <int MODE>
+  void stream_pass(const S* x) {
+    if (n_chunks_ == 0) return;
+    const dev::DseArgs<S> a = dse_args(x);
+    launch(dev::k_dse_chunk<S, MODE>, n_chunks_, dev::kTile, a);
+    if (n_long_ > 0) launch(dev::k_dse_long<S, MODE>, n_long_, dev::kTile, a);
+  }
+
+  template <int EPI>
+  void cam_reduce(const S* x, S* out) {
+    if (m_ == 0) return;
+    launch(dev::k_cam_reduce<S, EPI>, grid_for(static_cast<std::int64_t>(m_) * 32, dev::kRedThreads, 1 << 30),
+           dev::kRedThreads, m_, cam_part_ptr_.get(), static_cast<const std::int32_t*>(nullptr), static_cast<const S*>(part_.get()),
+           static_cast<const S*>(Bd_.get()), x, static_cast<const S*>(v_.get()), out, red(), sc_.get());
   }
 
   // Lowest index over ranks from a device u64 (all-ones = none); -1 if none.
@@ -680,7 +789,7 @@ class Rank {
     DBAG_CUDA(cudaStreamSynchronize(st_));
     std::memcpy(&raw, hbuf_, sizeof(raw));
     if (comm_->size() == 1) return raw == ~0ull ? -1 : static_cast<std::int64_t>(raw);
-    double neg = raw == ~0ull ? -std::numeric_limits<double>::infinity() : -double(raw);
+    const double neg = raw == ~0ull ? -std::numeric_limits<double>::infinity() : -double(raw);
     double* d = dsc_.get();
     hbuf_[0] = neg;
     DBAG_CUDA(cudaMemcpyAsync(d + 28, hbuf_, sizeof(double), cudaMemcpyHostToDevice, st_));
@@ -690,27 +799,30 @@ class Rank {
     return std::isfinite(hbuf_[0]) ? static_cast<std::int64_t>(-hbuf_[0]) : -1;
   }
 
-  std::int64_t halo_count(int width) const { return H_ > 0 ? H_ * width : 0; }
-  // C (9) and w (3) of shared points into the 12-wide halo buffer.
-  S* C_halo_exchange_begin() {
-    if (H_ == 0) return halo_buf_.get();
+  // C (9) and w (3) of shared points summed across ranks through the halo
+  // buffer (value-identical to the reference's full-size all-reduce).
+  void halo_exchange_Cw() {
+    if (H_ == 0) {
+      comm_->allreduce_sum(halo_buf_.get(), 0, kT, st_);  // keep the collective sequence aligned
+      return;
+    }
     DBAG_CUDA(cudaMemsetAsync(halo_buf_.get(), 0, sizeof(S) * 12 * static_cast<std::size_t>(H_), st_));
+    S* hw = halo_buf_.get() + 9 * static_cast<std::size_t>(H_);
+    const int g = grid_for(std::max(n_halo_loc_, 1), 128, 1 << 30);
     if (n_halo_loc_ > 0) {
-      // [C(9) | w(3)] per halo point: scatter C into a 9-wide view, w after it
-      launch(dev::k_halo_scatter<S, 9>, grid_for(n_halo_loc_, 128, 1 << 30), 128, 
-          n_halo_loc_, halo_lpt_.get(), halo_idx_.get(), C_.get(), halo_buf_.get());
-      launch(dev::k_halo_scatter<S, 3>, grid_for(n_halo_loc_, 128, 1 << 30), 128, 
-          n_halo_loc_, halo_lpt_.get(), halo_idx_.get(), w_.get(), halo_buf_.get() + 9 * static_cast<std::size_t>(H_));
-          }
-    return halo_buf_.get();
+      launch(dev::k_halo_scatter<S, 9>, g, 128, n_halo_loc_, halo_dpt_.get(), halo_idx_.get(),
+             static_cast<const S*>(C_.get()), halo_buf_.get());
+      launch(dev::k_halo_scatter<S, 3>, g, 128, n_halo_loc_, halo_dpt_.get(), halo_idx_.get(),
+             static_cast<const S*>(w_.get()), hw);
+    }
+    comm_->allreduce_sum(halo_buf_.get(), 12 * H_, kT, st_);
+    if (n_halo_loc_ > 0) {
+      launch(dev::k_halo_gather<S, 9>, g, 128, n_halo_loc_, halo_dpt_.get(), halo_idx_.get(),
+             static_cast<const S*>(halo_buf_.get()), C_.get());
+      launch(dev::k_halo_gather<S, 3>, g, 128, n_halo_loc_, halo_dpt_.get(), halo_idx_.get(),
+             static_cast<const S*>(hw), w_.get());
+    }
   }
-  void C_halo_exchange_end() {
-    if (H_ == 0 || n_halo_loc_ == 0) return;
-    launch(dev::k_halo_gather<S, 9>, grid_for(n_halo_loc_, 128, 1 << 30), 128, 
-        n_halo_loc_, halo_lpt_.get(), halo_idx_.get(), halo_buf_.get(), C_.get());
-    launch(dev::k_halo_gather<S, 3>, grid_for(n_halo_loc_, 128, 1 << 30), 128, 
-        n_halo_loc_, halo_lpt_.get(), halo_idx_.get(), halo_buf_.get() + 9 * static_cast<std::size_t>(H_), w_.get());
-      }
 
   cudaEvent_t prof_event() {
     if (prof_next_ == prof_ev_.size()) {
@@ -720,14 +832,14 @@ class Rank {
     }
     return prof_ev_[prof_next_++];
   }
-  // Events come in groups of 4 per DSE: [start, point done, halo done, cam done].
+  // Events come in groups of 3 per DSE: [start, point pass done, camera done].
   void collect_profile() {
     if (prof_next_ == 0) return;
     DBAG_CUDA(cudaStreamSynchronize(st_));
-    for (std::size_t i = 0; i + 3 < prof_next_; i += 4) {
+    for (std::size_t i = 0; i + 2 < prof_next_; i += 3) {
       float a = 0, b = 0;
       DBAG_CUDA(cudaEventElapsedTime(&a, prof_ev_[i], prof_ev_[i + 1]));
-      DBAG_CUDA(cudaEventElapsedTime(&b, prof_ev_[i + 2], prof_ev_[i + 3]));
+      DBAG_CUDA(cudaEventElapsedTime(&b, prof_ev_[i + 1], prof_ev_[i + 2]));
       prof_point_ms_ += a;
       prof_cam_ms_ += b;
     }
@@ -738,17 +850,19 @@ class Rank {
   Comm* comm_;
   cudaStream_t st_ = nullptr;
   ShardPlan plan_;
+  DeviceLayout lay_;
   int jac_mode_ = 0;
-  std::int32_t m_ = 0, n_glob_ = 0, n_loc_ = 0, m_loc_ = 0, n_halo_loc_ = 0;
+  std::int32_t m_ = 0, n_glob_ = 0, n_loc_ = 0, m_loc_ = 0, n_halo_loc_ = 0, n_chunk_part_ = 0;
   std::int64_t N_ = 0, H_ = 0;
   int n_tiles_ = 0;
+  std::int32_t n_long_ = 0;
+  std::int32_t n_chunks_ = 0;
   bool have_system_ = false;
   double lambda_ = 0;
   int policy_ = 1;
   double step_inf_ = 0, damp_term_ = 0, gv_ = 0;
   int dse_count_ = 0;
-  std::int64_t launches_ = 0;
-  std::int64_t dse_launches_ = 0;
+  std::int64_t dse_launches_ = 0, launches_ = 0;
   Tally tally_;
   Scal* hsc_ = nullptr;
   double* hbuf_ = nullptr;
@@ -757,18 +871,22 @@ class Rank {
   std::vector<cudaEvent_t> prof_ev_;
   std::size_t prof_next_ = 0;
   double prof_point_ms_ = 0, prof_cam_ms_ = 0;
+  std::vector<std::int32_t> dpt_glob_;
+  std::vector<std::uint8_t> owned_h_;
 
-  DevBuf<std::int32_t> slot_cam_, slot_pt_, slot_edge_, pt_ptr_, tile_pt_, cam_ptr_, cam_glob_, pt_glob_,
-      cslot_pslot_, cslot_pt_, halo_of_, halo_lpt_, halo_idx_;
+  DevBuf<std::int32_t> slot_cam_, slot_dpt_, slot_edge_, dpt_ptr_, chunk_slot_, cam_part_ptr_, halo_slot_, slot_chunk_,
+      long_chunk_, halo_pos_, cam_ptr_, cam_glob_, cslot_dslot_, dpt_glob_d_,
+      halo_of_, halo_dpt_, halo_idx_;
   DevBuf<std::uint8_t> owned_;
   DevBuf<S> slot_px_, slot_py_, slot_w_;
   DevBuf<S> xc_, xct_, dxc_, v_, g_, r_, z_, p_, q_, ctmp_;
-  DevBuf<S> xp_, xpt_, dxp_, w_, bpt_;
+  DevBuf<S> xp_, xpt_, dxp_, w_;
   DevBuf<S> B_, Bd_, Binv_, C_, Cd_, Cinv_;
-  DevBuf<S> Jb_, E_pm_, E_cm_, halo_buf_;
+  DevBuf<S> Jb_, E_, part_, halo_buf_;
   DevBuf<Scal> sc_;
   DevBuf<double> red_part_, dsc_, bounce_;
   DevBuf<unsigned> red_cnt_;
   DevBuf<unsigned long long> bad_;
 };
+
 }  // namespace dbag
