@@ -26,6 +26,7 @@
 #include <cstdint>
 
 #include "kernels.cuh"
+#include "tma.cuh"
 
 namespace dbag {
 namespace dev {
@@ -63,7 +64,8 @@ __device__ __forceinline__ const RecMeta& rec_meta(const S* R) {
 // Point finish: halo deposit or b = C^-1 a (MODE 0), dx_p = C^-1 (w - a)
 // (MODE 1), b = C^-1 w (MODE 2). Returns b (zero for halo points).
 template <class S, int MODE>
-__device__ __forceinline__ void finish_point(const DseArgs<S>& A, std::int32_t p, S* tt, S* b) {
+__device__ __forceinline__ void finish_point(const DseArgs<S>& A, std::int32_t p, const S* L, const S* wv, S* tt,
+                                             S* b) {
   const std::int32_t h = (MODE != 2 && A.halo_of) ? A.halo_of[p] : -1;
   if (h >= 0) {
 #pragma unroll
@@ -75,16 +77,26 @@ __device__ __forceinline__ void finish_point(const DseArgs<S>& A, std::int32_t p
   }
   if (MODE == 1)
 #pragma unroll
-    for (int j = 0; j < 3; ++j) tt[j] = A.w[std::size_t(p) * 3 + j] - tt[j];
+    for (int j = 0; j < 3; ++j) tt[j] = wv[j] - tt[j];
   if (MODE == 2)
 #pragma unroll
-    for (int j = 0; j < 3; ++j) tt[j] = A.w[std::size_t(p) * 3 + j];
-  llt_solve<S, 3>(A.Cinv + std::size_t(p) * 9, tt);
+    for (int j = 0; j < 3; ++j) tt[j] = wv[j];
+  llt_solve<S, 3>(L, tt);
 #pragma unroll
   for (int j = 0; j < 3; ++j) b[j] = tt[j];
   if (MODE == 1)
 #pragma unroll
     for (int j = 0; j < 3; ++j) A.out_pt[std::size_t(p) * 3 + j] = b[j];
+}
+
+// The point's C factor (and w for MODE 1/2), loaded early.
+template <class S, int MODE>
+__device__ __forceinline__ void load_point(const DseArgs<S>& A, std::int32_t p, S* L, S* wv) {
+#pragma unroll
+  for (int k = 0; k < 9; ++k) L[k] = A.Cinv[std::size_t(p) * 9 + k];
+  if (MODE != 0)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) wv[j] = A.w[std::size_t(p) * 3 + j];
 }
 
 // Folds sm.y per distinct camera of the chunk (warp per camera) into the
@@ -123,28 +135,54 @@ __device__ __forceinline__ void stage_meta(const RecMeta& M, DseWork<S>& sm) {
   if (tid < 8) sm.ubeg[kTile + tid] = M.ubeg[kTile + tid];
 }
 
-template <class S, int MODE>
-__global__ void __launch_bounds__(kTile, 4) k_dse_chunk(DseArgs<S> A) {
-  __shared__ DseWork<S> sm;
+// Camera-vector gathers of the a-phase: the plain vector x, or the PCG
+// search direction formed on the fly, p = z (first iteration) or
+// z + beta p_prev (dba/solver.hpp:231-236).
+template <class S>
+struct GatherX {
+  const S* x;
+  __device__ __forceinline__ S operator()(std::int32_t cam, int i) const { return __ldg(x + std::size_t(cam) * 9 + i); }
+};
+template <class S>
+struct GatherP {
+  const S* z;
+  const S* p_prev;
+  S beta;
+  bool first;
+  __device__ __forceinline__ S operator()(std::int32_t cam, int i) const {
+    const std::size_t k = std::size_t(cam) * 9 + i;
+    const S zv = __ldcg(z + k);
+    return first ? zv : zv + beta * __ldcg(p_prev + k);
+  }
+};
+
+// One 128-slot chunk whose record is at R (global or shared memory);
+// normal tiles only (long tiles return).
+template <class S, int MODE, class G>
+__device__ __forceinline__ void dse_chunk_at(const DseArgs<S>& A, DseWork<S>& sm, const S* R, const G& gx) {
   const int tid = threadIdx.x;
-  const S* R = A.rec + std::size_t(blockIdx.x) * Rec<S>::kLen;
   const RecMeta& M = rec_meta(R);
-  const std::int32_t p0 = M.p0, np = M.np, nslots = M.nslots, nchunk = M.nchunk, nu = M.nu;
-  if (nchunk > 1) return;  // long tile: k_dse_long
-  const bool mine = tid < nslots;
+  // Issue every independent load of the tile first: E lanes, header,
+  // metadata; then the loads that depend on them (C factors, x gathers).
   S e[27];
 #pragma unroll
   for (int k = 0; k < 27; ++k) e[k] = R[k * kTile + tid];  // padding slots hold zeros
+  const int4 hdr = *reinterpret_cast<const int4*>(&M.p0);  // p0, np, nslots, nchunk
+  const std::int32_t cam = M.cam[tid];
   const int pti = M.pt[tid];
   const int pb0 = M.pbeg[tid], pb1 = M.pbeg[tid + 1];
+  const int nu = M.nu;
   if (MODE != 1) stage_meta(M, sm);
+  if (hdr.w > 1) return;  // long tile: dse_long
+  const std::int32_t p0 = hdr.x, np = hdr.y;
+  S L[9], wv[3];
+  if (tid < np) load_point<S, MODE>(A, p0 + tid, L, wv);
   if (MODE != 2) {
     S a[3] = {S(0), S(0), S(0)};
-    if (mine) {
-      const S* xc = A.x + std::size_t(M.cam[tid]) * 9;
+    if (tid < hdr.z) {
 #pragma unroll
       for (int i = 0; i < 9; ++i) {
-        const S xv = __ldg(xc + i);
+        const S xv = gx(cam, i);
         a[0] += e[i * 3 + 0] * xv;
         a[1] += e[i * 3 + 1] * xv;
         a[2] += e[i * 3 + 2] * xv;
@@ -160,26 +198,37 @@ __global__ void __launch_bounds__(kTile, 4) k_dse_chunk(DseArgs<S> A) {
       for (int q = pb0; q < pb1; ++q)
 #pragma unroll
         for (int j = 0; j < 3; ++j) tt[j] += sm.a[q][j];
-    finish_point<S, MODE>(A, p0 + tid, tt, b);
+    finish_point<S, MODE>(A, p0 + tid, L, wv, tt, b);
 #pragma unroll
     for (int j = 0; j < 3; ++j) sm.b[tid][j] = b[j];
   }
+  __syncthreads();
   if constexpr (MODE != 1) {
-    __syncthreads();
     const S b0 = sm.b[pti][0], b1 = sm.b[pti][1], b2 = sm.b[pti][2];
 #pragma unroll
     for (int i = 0; i < 9; ++i) sm.y[tid][i] = (e[i * 3] * b0 + e[i * 3 + 1] * b1) + e[i * 3 + 2] * b2;
     __syncthreads();
     fold_cameras(A, sm, nu);
+    __syncthreads();
   }
 }
 
-// One CTA per long tile (a single point observed more than 128 times).
+template <class S, int MODE, class G>
+__device__ __forceinline__ void dse_chunk(const DseArgs<S>& A, DseWork<S>& sm, std::int32_t chunk, const G& gx) {
+  dse_chunk_at<S, MODE>(A, sm, A.rec + std::size_t(chunk) * Rec<S>::kLen, gx);
+}
+
 template <class S, int MODE>
-__global__ void __launch_bounds__(kTile) k_dse_long(DseArgs<S> A) {
+__global__ void __launch_bounds__(kTile, 5) k_dse_chunk(DseArgs<S> A) {
   __shared__ DseWork<S> sm;
+  dse_chunk<S, MODE>(A, sm, blockIdx.x, GatherX<S>{A.x});
+}
+
+// One CTA per long tile (a single point observed more than 128 times).
+template <class S, int MODE, class G>
+__device__ __forceinline__ void dse_long(const DseArgs<S>& A, DseWork<S>& sm, std::int32_t li, const G& gx) {
   const int tid = threadIdx.x;
-  const std::int32_t c0 = A.long_chunk[blockIdx.x];
+  const std::int32_t c0 = A.long_chunk[li];
   const RecMeta& M0 = rec_meta(A.rec + std::size_t(c0) * Rec<S>::kLen);
   const std::int32_t p = M0.p0, nchunk = M0.nchunk;
   S a[3] = {S(0), S(0), S(0)};
@@ -188,10 +237,10 @@ __global__ void __launch_bounds__(kTile) k_dse_long(DseArgs<S> A) {
       const S* R = A.rec + std::size_t(c) * Rec<S>::kLen;
       const RecMeta& M = rec_meta(R);
       if (tid < M.nslots) {
-        const S* xc = A.x + std::size_t(M.cam[tid]) * 9;
+        const std::int32_t cam = M.cam[tid];
 #pragma unroll
         for (int i = 0; i < 9; ++i) {
-          const S xv = __ldg(xc + i);
+          const S xv = gx(cam, i);
           a[0] += R[(i * 3 + 0) * kTile + tid] * xv;
           a[1] += R[(i * 3 + 1) * kTile + tid] * xv;
           a[2] += R[(i * 3 + 2) * kTile + tid] * xv;
@@ -208,7 +257,9 @@ __global__ void __launch_bounds__(kTile) k_dse_long(DseArgs<S> A) {
       for (int k = 0; k < kTile; ++k)
 #pragma unroll
         for (int j = 0; j < 3; ++j) tt[j] += sm.a[k][j];
-    finish_point<S, MODE>(A, p, tt, b);
+    S L[9], wv[3];
+    load_point<S, MODE>(A, p, L, wv);
+    finish_point<S, MODE>(A, p, L, wv, tt, b);
 #pragma unroll
     for (int j = 0; j < 3; ++j) sm.b[0][j] = b[j];
   }
@@ -227,6 +278,73 @@ __global__ void __launch_bounds__(kTile) k_dse_long(DseArgs<S> A) {
       fold_cameras(A, sm, M.nu);
     }
   }
+  __syncthreads();
+}
+
+template <class S, int MODE>
+__global__ void __launch_bounds__(kTile) k_dse_long(DseArgs<S> A) {
+  __shared__ DseWork<S> sm;
+  dse_long<S, MODE>(A, sm, blockIdx.x, GatherX<S>{A.x});
+}
+
+// ---- TMA-pipelined persistent variant ------------------------------------
+// Persistent CTAs walk chunks c = blockIdx.x, + gridDim.x, ...; one elected
+// thread has the TMA engine (cp.async.bulk + mbarrier complete_tx) bring the
+// next chunk's record into the other shared-memory stage while the CTA
+// computes the current one, so the HBM stream never waits on the compute
+// phases of a tile. The E chunk records are read-only during a solve.
+template <class S>
+struct DseStages {
+  S rec[2][Rec<S>::kLen];
+  alignas(8) std::uint64_t bar[2];
+};
+
+template <class S>
+__device__ __forceinline__ void stages_init(DseStages<S>& st) {
+  if (threadIdx.x == 0) {
+    mbar_init(&st.bar[0], 1);
+    mbar_init(&st.bar[1], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+}
+
+template <class S>
+__device__ __forceinline__ void stage_issue(const DseArgs<S>& A, DseStages<S>& st, std::int32_t c, int k) {
+  mbar_arrive_expect_tx(&st.bar[k], std::uint32_t(Rec<S>::kBytes));
+  bulk_g2s(st.rec[k], A.rec + std::size_t(c) * Rec<S>::kLen, std::uint32_t(Rec<S>::kBytes), &st.bar[k]);
+}
+
+// All chunks of this CTA, pipelined; `parity` carries the stage barriers'
+// phase bits across passes.
+template <class S, int MODE, class G>
+__device__ __forceinline__ void dse_stream_pass(const DseArgs<S>& A, DseWork<S>& sm, DseStages<S>& st,
+                                                unsigned& parity, const G& gx) {
+  const std::int32_t first = blockIdx.x, stride = gridDim.x;
+  if (first < A.n_chunks) {
+    __syncthreads();
+    if (threadIdx.x == 0) stage_issue(A, st, first, 0);
+    int k = 0;
+    for (std::int32_t c = first; c < A.n_chunks; c += stride) {
+      __syncthreads();  // stage k ^ 1 is free: its chunk is done
+      if (threadIdx.x == 0 && c + stride < A.n_chunks) stage_issue(A, st, c + stride, k ^ 1);
+      mbar_wait(&st.bar[k], (parity >> k) & 1u);
+      parity ^= 1u << k;
+      dse_chunk_at<S, MODE>(A, sm, st.rec[k], gx);
+      k ^= 1;
+    }
+  }
+  for (std::int32_t l = first; l < A.n_long; l += stride) dse_long<S, MODE>(A, sm, l, gx);
+}
+
+template <class S, int MODE>
+__global__ void __launch_bounds__(kTile) k_dse_stream(DseArgs<S> A) {
+  __shared__ DseWork<S> sm;
+  extern __shared__ __align__(128) unsigned char dse_dyn[];
+  DseStages<S>& st = *reinterpret_cast<DseStages<S>*>(dse_dyn);
+  stages_init(st);
+  unsigned parity = 0;
+  dse_stream_pass<S, MODE>(A, sm, st, parity, GatherX<S>{A.x});
 }
 
 }  // namespace dev

@@ -419,6 +419,41 @@ __device__ __forceinline__ void llt_solve(const S* __restrict__ L, S* x) {
   }
 }
 
+// Explicit inverse of SPD blocks from their stored factor (L with 1/L_kk in
+// the upper triangle): A^-1 = L^-T L^-1. Used for the block-Jacobi
+// preconditioner z = B^-1 r (dba/solver.hpp:224-225) as a 9x9 GEMV.
+template <class S, int BS>
+__global__ void k_block_inverse(std::int64_t nb, const S* __restrict__ L, S* __restrict__ out) {
+  const std::int64_t i = blockIdx.x * std::int64_t(blockDim.x) + threadIdx.x;
+  if (i >= nb) return;
+  const S* l = L + std::size_t(i) * BS * BS;
+  S li[BS][BS];
+#pragma unroll
+  for (int c = 0; c < BS; ++c)
+#pragma unroll
+    for (int r = 0; r < BS; ++r) {
+      if (r < c) {
+        li[r][c] = S(0);
+      } else {
+        S acc = (r == c) ? S(1) : S(0);
+#pragma unroll
+        for (int k = c; k < r; ++k) acc -= l[r * BS + k] * li[k][c];
+        li[r][c] = acc * l[rcp_at<BS>(r)];
+      }
+    }
+  S* o = out + std::size_t(i) * BS * BS;
+#pragma unroll
+  for (int r = 0; r < BS; ++r)
+#pragma unroll
+    for (int c = r; c < BS; ++c) {
+      S acc = S(0);
+#pragma unroll
+      for (int k = c; k < BS; ++k) acc += li[k][r] * li[k][c];
+      o[r * BS + c] = acc;
+      o[c * BS + r] = acc;
+    }
+}
+
 // -------------------------------------------------------------- halo ----
 // Finish of the MODE 1 pass (dse.cuh) for halo points after the all-reduce.
 template <class S, int MODE>
@@ -610,6 +645,37 @@ __global__ void __launch_bounds__(kRedThreads) k_pcg_precond(std::int32_t m, con
       z[std::size_t(cam) * 9 + i] = zv[i];
       acc += double(rv[i]) * double(zv[i]);
     }
+  }
+  const double v[1] = {acc};
+  __shared__ double fin[1];
+  if (grid_reduce<SumOp, 1>(v, ws.partials, ws.counter, fin)) {
+    if (threadIdx.x == 0) {
+      const double rho = fin[0];
+      sc->rho = rho;
+      if (!(rho > 0.0) || isinf(rho)) sc->status |= 1;
+      sc->beta = sc->n == 0 ? S(0) : S(rho / sc->rho_prev);
+    }
+  }
+}
+
+// z = B^-1 r with the explicit inverse (thread per element) and rho = r.z
+// in double; beta = (S)(rho / rho_prev) (dba/solver.hpp:224-236).
+template <class S>
+__global__ void __launch_bounds__(kRedThreads) k_pcg_precond_inv(std::int32_t m, const S* __restrict__ Binv,
+                                                                 const S* __restrict__ r, S* __restrict__ z, RedWs ws,
+                                                                 PcgScal<S>* sc) {
+  double acc = 0.0;
+  const std::int64_t len = std::int64_t(m) * 9;
+  for (std::int64_t i = blockIdx.x * std::int64_t(blockDim.x) + threadIdx.x; i < len;
+       i += std::int64_t(gridDim.x) * blockDim.x) {
+    const std::int64_t cam = i / 9, row = i % 9;
+    const S* bi = Binv + cam * 81 + row * 9;
+    const S* rc = r + cam * 9;
+    S zv = S(0);
+#pragma unroll
+    for (int k = 0; k < 9; ++k) zv += bi[k] * rc[k];
+    z[i] = zv;
+    acc += double(r[i]) * double(zv);
   }
   const double v[1] = {acc};
   __shared__ double fin[1];

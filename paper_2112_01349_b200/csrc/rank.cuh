@@ -31,6 +31,7 @@
 #include "comm.hpp"
 #include "common.hpp"
 #include "dse.cuh"
+#include "pcg.cuh"
 #include "kernels.cuh"
 #include "partition.hpp"
 
@@ -112,6 +113,7 @@ class Rank {
     cudaEventDestroy(mark_[1]);
     cudaFreeHost(hsc_);
     cudaFreeHost(hbuf_);
+    if (pcg_out_h_) cudaFreeHost(pcg_out_h_);
     cudaStreamDestroy(st_);
   }
 
@@ -210,7 +212,8 @@ class Rank {
     const std::size_t cm = static_cast<std::size_t>(m_) * 9, pl = static_cast<std::size_t>(n_loc_) * 3;
     for (DevBuf<S>* b : {&xc_, &xct_, &dxc_, &v_, &g_, &r_, &z_, &p_, &q_, &ctmp_}) b->alloc(std::max<std::size_t>(cm, 1));
     for (DevBuf<S>* b : {&xp_, &xpt_, &dxp_, &w_}) b->alloc(std::max<std::size_t>(pl, 1));
-    for (DevBuf<S>* b : {&B_, &Bd_, &Binv_}) b->alloc(std::max<std::size_t>(cm * 9, 1));
+    for (DevBuf<S>* b : {&B_, &Bd_, &Binv_, &Bexp_}) b->alloc(std::max<std::size_t>(cm * 9, 1));
+    p2_.alloc(std::max<std::size_t>(cm, 1));
     for (DevBuf<S>* b : {&C_, &Cd_}) b->alloc(std::max<std::size_t>(pl * 3, 1));
     Cinv_.alloc(pl * 3 + 16 / sizeof(S));  // slack for the 16-byte-rounded TMA reads
     Jb_.alloc(std::max<std::size_t>(static_cast<std::size_t>(N_) * 28, 1));
@@ -313,6 +316,9 @@ class Rank {
     if (m_ > 0)
       launch(dev::k_damp_factor<S, 9>, grid_for(m_, 64, 1 << 30), 64, m_, B_.get(), lam, policy, Bd_.get(),
              Binv_.get(), static_cast<const std::int32_t*>(nullptr), bad_.get() + 1);
+    if (m_ > 0)  // explicit B^-1 for the block-Jacobi preconditioner
+      launch(dev::k_block_inverse<S, 9>, grid_for(m_, 64, 1 << 30), 64, m_, static_cast<const S*>(Binv_.get()),
+             Bexp_.get());
     DBAG_CUDA(cudaMemcpyAsync(hbuf_, bad_.get(), 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st_));
     DBAG_CUDA(cudaStreamSynchronize(st_));
     unsigned long long raw[2];
@@ -377,6 +383,7 @@ class Rank {
   // --------------------------------------------------------------- DPCG ----
   PcgOut pcg(double tol, int max_iters) {
     DBAG_CUDA(cudaSetDevice(device_));
+    if (comm_->size() == 1 && persistent_grid() > 0) return pcg_persistent(tol, max_iters);
     S* x = dxc_.get();
     const std::int64_t len = static_cast<std::int64_t>(m_) * 9;
     dse_count_ = 0;
@@ -399,7 +406,8 @@ class Rank {
     while (r_norm > tol * rhs_norm && n < max_iters) {
       const std::uint64_t ops0 = tally_.block_ops;
       const int dse0 = dse_count_;
-      launch(dev::k_pcg_precond<S>, rb, dev::kRedThreads, m_, Binv_.get(), r_.get(), z_.get(), red(), sc_.get());
+      launch(dev::k_pcg_precond_inv<S>, vb, dev::kRedThreads, m_, static_cast<const S*>(Bexp_.get()),
+             static_cast<const S*>(r_.get()), z_.get(), red(), sc_.get());
       launch(dev::k_pcg_p<S>, grid_for(len, 256, 1 << 30), 256, len, z_.get(), p_.get(),
              static_cast<const Scal*>(sc_.get()));
       dse<true>(p_.get(), q_.get());
@@ -430,6 +438,84 @@ class Rank {
       r_norm = std::sqrt(hsc_->rnorm2);
     }
     return {n, r_norm <= tol * rhs_norm};
+  }
+
+  // Grid of the cooperative PCG kernel (0: unavailable -> host-driven loop).
+  // DBAG_PCG=host forces the host-driven loop; DBAG_DSE=direct|tma picks the
+  // DSE streaming variant (TMA-pipelined by default).
+  int persistent_grid() {
+    if (pcg_grid_ >= 0) return pcg_grid_;
+    const char* mode = std::getenv("DBAG_PCG");
+    const char* dse = std::getenv("DBAG_DSE");
+    use_tma_ = !(dse && std::string(dse) == "direct");
+    pcg_grid_ = 0;
+    if (mode && std::string(mode) == "host") return pcg_grid_;
+    int coop = 0, per_sm = 0, sms = 0;
+    DBAG_CUDA(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, device_));
+    DBAG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device_));
+    const int dyn = use_tma_ ? static_cast<int>(sizeof(dev::DseStages<S>)) : 0;
+    auto k = use_tma_ ? dev::k_pcg_persistent<S, true> : dev::k_pcg_persistent<S, false>;
+    DBAG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn));
+    DBAG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, dev::kTile, dyn));
+    if (!coop || per_sm < 1) return pcg_grid_;
+    pcg_grid_ = per_sm * sms;
+    pcg_part_.alloc(static_cast<std::size_t>(pcg_grid_) * 4);
+    pcg_bar_.alloc(2);
+    pcg_out_.alloc(1);
+    DBAG_CUDA(cudaMallocHost(&pcg_out_h_, sizeof(dev::PcgDevOut)));
+    return pcg_grid_;
+  }
+
+  // dpcg in one cooperative launch (pcg.cuh); same results, tallies and
+  // breakdown semantics as the host-driven loop below.
+  PcgOut pcg_persistent(double tol, int max_iters) {
+    dev::PcgPArgs<S> P;
+    P.dse = dse_args(nullptr);
+    P.m = m_;
+    P.cam_part_ptr = cam_part_ptr_.get();
+    P.Bd = Bd_.get();
+    P.Binv = Bexp_.get();
+    P.g = g_.get();
+    P.x = dxc_.get();
+    P.r = r_.get();
+    P.z = z_.get();
+    P.pa = p_.get();
+    P.pb = p2_.get();
+    P.q = q_.get();
+    P.tol = tol;
+    P.max_iters = max_iters;
+    P.bpart = pcg_part_.get();
+    P.bar = pcg_bar_.get();
+    P.out = pcg_out_.get();
+    DBAG_CUDA(cudaMemsetAsync(pcg_bar_.get(), 0, 2 * sizeof(unsigned), st_));
+    const bool prof = profiling_;
+    if (prof) DBAG_CUDA(cudaEventRecord(prof_event(), st_));
+    void* args[] = {&P};
+    if (use_tma_)
+      DBAG_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(dev::k_pcg_persistent<S, true>),
+                                            dim3(pcg_grid_), dim3(dev::kTile), args, sizeof(dev::DseStages<S>), st_));
+    else
+      DBAG_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(dev::k_pcg_persistent<S, false>),
+                                            dim3(pcg_grid_), dim3(dev::kTile), args, 0, st_));
+    ++launches_;
+    if (prof) {
+      DBAG_CUDA(cudaEventRecord(prof_event(), st_));
+      DBAG_CUDA(cudaEventRecord(prof_event(), st_));
+    }
+    DBAG_CUDA(cudaMemcpyAsync(pcg_out_h_, pcg_out_.get(), sizeof(dev::PcgDevOut), cudaMemcpyDeviceToHost, st_));
+    DBAG_CUDA(cudaStreamSynchronize(st_));
+    collect_profile();
+    const dev::PcgDevOut o = *pcg_out_h_;
+    dse_count_ = o.dse_count;
+    dse_launches_ += o.dse_count;
+    tally_.block_ops += 2 * static_cast<std::uint64_t>(N_) * static_cast<std::uint64_t>(o.dse_count);
+    if (o.status == 1)
+      throw Error(DBAG_PCG_BREAKDOWN, "preconditioned residual norm rho = " + std::to_string(o.rho) +
+                                          " at iteration " + std::to_string(o.iterations));
+    if (o.status == 2)
+      throw Error(DBAG_PCG_BREAKDOWN, "operator lost positive definiteness (p'q = " + std::to_string(o.pq) +
+                                          ") at iteration " + std::to_string(o.iterations));
+    return {o.iterations, o.converged != 0};
   }
 
   // ------------------------------------------- back-substitution + trial ----
@@ -770,8 +856,24 @@ class Rank {
   void stream_pass(const S* x) {
     if (n_chunks_ == 0) return;
     const dev::DseArgs<S> a = dse_args(x);
-    launch(dev::k_dse_chunk<S, MODE>, n_chunks_, dev::kTile, a);
-    if (n_long_ > 0) launch(dev::k_dse_long<S, MODE>, n_long_, dev::kTile, a);
+    persistent_grid();
+    if (use_tma_) {
+      if (stream_grid_ < 0) {
+        int per_sm = 0, sms = 0;
+        const int dyn = static_cast<int>(sizeof(dev::DseStages<S>));
+        for (auto k : {dev::k_dse_stream<S, 0>, dev::k_dse_stream<S, 1>, dev::k_dse_stream<S, 2>})
+          DBAG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn));
+        DBAG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dev::k_dse_stream<S, 0>, dev::kTile, dyn));
+        DBAG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device_));
+        stream_grid_ = std::max(1, std::min(n_chunks_ + n_long_, std::max(per_sm, 1) * sms));
+      }
+      dev::k_dse_stream<S, MODE><<<stream_grid_, dev::kTile, sizeof(dev::DseStages<S>), st_>>>(a);
+      DBAG_LAUNCH_CHECK();
+      ++launches_;
+    } else {
+      launch(dev::k_dse_chunk<S, MODE>, n_chunks_, dev::kTile, a);
+      if (n_long_ > 0) launch(dev::k_dse_long<S, MODE>, n_long_, dev::kTile, a);
+    }
   }
 
   template <int EPI>
@@ -881,7 +983,13 @@ class Rank {
   DevBuf<S> slot_px_, slot_py_, slot_w_;
   DevBuf<S> xc_, xct_, dxc_, v_, g_, r_, z_, p_, q_, ctmp_;
   DevBuf<S> xp_, xpt_, dxp_, w_;
-  DevBuf<S> B_, Bd_, Binv_, C_, Cd_, Cinv_;
+  DevBuf<S> B_, Bd_, Binv_, Bexp_, C_, Cd_, Cinv_, p2_;
+  DevBuf<double> pcg_part_;
+  DevBuf<unsigned> pcg_bar_;
+  DevBuf<dev::PcgDevOut> pcg_out_;
+  dev::PcgDevOut* pcg_out_h_ = nullptr;
+  int pcg_grid_ = -1, stream_grid_ = -1;
+  bool use_tma_ = true;
   DevBuf<S> Jb_, E_, part_, halo_buf_;
   DevBuf<Scal> sc_;
   DevBuf<double> red_part_, dsc_, bounce_;
