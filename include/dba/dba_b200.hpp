@@ -1,0 +1,374 @@
+// dba_b200.hpp — C++ drop-in facade of the reference's `dba` solver API over
+// the B200 C ABI (include/dbag.h).
+//
+// Same names, argument meaning and error behaviour as the reference's
+// header-only API, without its Eigen dependency:
+//   BAProblem<Scalar>::add_node / add_edge   dba/problem.hpp:171-261
+//   SolverConfig, IterationRecord, SolverState, TerminationReason
+//                                            dba/solver.hpp:39-85
+//   lm_solve(problem, config)                dba/solver.hpp:523-534
+//   partition_edges(problem, K)              dba/partition.hpp:76-103
+//   generate_synthetic(options)              dba/synthetic.hpp:70-146
+//   the exception hierarchy                  dba/errors.hpp:17-84
+// A reference user switches by including this header instead of
+// dba/solver.hpp and linking libdbag.so.
+#pragma once
+
+#include <array>
+#include <cmath>
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../dbag.h"
+
+namespace dba {
+
+// ---- errors (dba/errors.hpp) ------------------------------------------------
+class Error : public std::runtime_error {
+ public:
+  using std::runtime_error::runtime_error;
+};
+class InvalidArgumentError : public Error {
+ public:
+  using Error::Error;
+};
+class ShapeError : public Error {
+ public:
+  using Error::Error;
+};
+class CollectiveError : public Error {
+ public:
+  using Error::Error;
+};
+class PcgBreakdownError : public Error {
+ public:
+  using Error::Error;
+};
+class DegenerateDepthError : public Error {
+ public:
+  explicit DegenerateDepthError(std::int64_t edge_id = -1, const std::string& m = "degenerate depth (P_z = 0)")
+      : Error(m), edge_id_(edge_id) {}
+  std::int64_t edge_id() const { return edge_id_; }
+
+ private:
+  std::int64_t edge_id_;
+};
+class SingularBlockError : public Error {
+ public:
+  SingularBlockError(std::int64_t idx, int bs, const std::string& m) : Error(m), idx_(idx), bs_(bs) {}
+  std::int64_t block_index() const { return idx_; }
+  int block_size() const { return bs_; }
+
+ private:
+  std::int64_t idx_;
+  int bs_;
+};
+
+namespace detail {
+inline void check(int rc) {
+  if (rc == DBAG_OK) return;
+  const std::string msg = dbag_last_error();
+  switch (rc) {
+    case DBAG_DEGENERATE_DEPTH: throw DegenerateDepthError(dbag_last_error_index(), msg);
+    case DBAG_SINGULAR_BLOCK: throw SingularBlockError(dbag_last_error_index(), dbag_last_error_block_size(), msg);
+    case DBAG_PCG_BREAKDOWN: throw PcgBreakdownError(msg);
+    case DBAG_SHAPE: throw ShapeError(msg);
+    case DBAG_INVALID_ARGUMENT: throw InvalidArgumentError(msg);
+    case DBAG_COLLECTIVE: throw CollectiveError(msg);
+    default: throw Error(msg);
+  }
+}
+}  // namespace detail
+
+// ---- problem model (dba/problem.hpp) ----------------------------------------
+enum class MseConvention { per_observation, half_per_observation };
+enum class DampingPolicy { identity, diag_scaled };
+enum class JacobianMode { autodiff, analytic };
+enum class TerminationReason { converged, max_iterations, stalled };
+
+inline constexpr int kCameraParams = 9;
+inline constexpr int kPointParams = 3;
+
+template <typename Scalar>
+struct CameraState {
+  std::array<Scalar, 3> rotation{};
+  std::array<Scalar, 3> translation{};
+  Scalar focal = Scalar(1);
+  Scalar k1 = Scalar(0);
+  Scalar k2 = Scalar(0);
+  bool all_finite() const {
+    for (Scalar v : rotation)
+      if (!std::isfinite(double(v))) return false;
+    for (Scalar v : translation)
+      if (!std::isfinite(double(v))) return false;
+    return std::isfinite(double(focal)) && std::isfinite(double(k1)) && std::isfinite(double(k2));
+  }
+};
+
+template <typename Scalar>
+struct PointState {
+  std::array<Scalar, 3> position{};
+  bool all_finite() const {
+    for (Scalar v : position)
+      if (!std::isfinite(double(v))) return false;
+    return true;
+  }
+};
+
+template <typename Scalar>
+struct Observation {
+  std::int32_t camera_id = 0;
+  std::int32_t point_id = 0;
+  std::array<Scalar, 2> pixel{};
+  Scalar weight = Scalar(1);
+};
+
+template <typename Scalar>
+class BAProblem {
+ public:
+  std::int32_t add_node(const CameraState<Scalar>& c) {
+    if (!c.all_finite()) throw InvalidArgumentError("camera node has non-finite components");
+    cams_.insert(cams_.end(), c.rotation.begin(), c.rotation.end());
+    cams_.insert(cams_.end(), c.translation.begin(), c.translation.end());
+    cams_.push_back(c.focal);
+    cams_.push_back(c.k1);
+    cams_.push_back(c.k2);
+    return num_cameras() - 1;
+  }
+  std::int32_t add_node(const PointState<Scalar>& p) {
+    if (!p.all_finite()) throw InvalidArgumentError("point node has non-finite components");
+    pts_.insert(pts_.end(), p.position.begin(), p.position.end());
+    return num_points() - 1;
+  }
+  std::int32_t add_edge(const Observation<Scalar>& o) {
+    if (o.camera_id < 0 || o.camera_id >= num_cameras())
+      throw InvalidArgumentError("edge references unknown camera " + std::to_string(o.camera_id));
+    if (o.point_id < 0 || o.point_id >= num_points())
+      throw InvalidArgumentError("edge references unknown point " + std::to_string(o.point_id));
+    if (!(o.weight >= Scalar(0))) throw InvalidArgumentError("edge weight must be >= 0");
+    cam_id_.push_back(o.camera_id);
+    pt_id_.push_back(o.point_id);
+    px_.push_back(o.pixel[0]);
+    py_.push_back(o.pixel[1]);
+    w_.push_back(o.weight);
+    return static_cast<std::int32_t>(cam_id_.size()) - 1;
+  }
+  std::int32_t num_cameras() const { return static_cast<std::int32_t>(cams_.size() / kCameraParams); }
+  std::int32_t num_points() const { return static_cast<std::int32_t>(pts_.size() / kPointParams); }
+  std::int64_t num_observations() const { return static_cast<std::int64_t>(cam_id_.size()); }
+  const std::vector<Scalar>& packed_cameras() const { return cams_; }  // pack_cameras
+  const std::vector<Scalar>& packed_points() const { return pts_; }    // pack_points
+
+  dbag_problem c_view() const {
+    dbag_problem p;
+    p.num_cameras = num_cameras();
+    p.num_points = num_points();
+    p.num_observations = num_observations();
+    p.cameras = cams_.data();
+    p.points = pts_.data();
+    p.camera_id = cam_id_.data();
+    p.point_id = pt_id_.data();
+    p.pixel_x = px_.data();
+    p.pixel_y = py_.data();
+    p.weight = w_.data();
+    return p;
+  }
+
+ private:
+  std::vector<Scalar> cams_, pts_, px_, py_, w_;
+  std::vector<std::int32_t> cam_id_, pt_id_;
+};
+
+// ---- solver (dba/solver.hpp) ------------------------------------------------
+struct SolverConfig {
+  int workers = 1;
+  int max_iterations = 50;
+  double pcg_tol = 1e-6;
+  int pcg_max_iters = 500;
+  double lambda0 = 1e-4;
+  double lambda_max = 1e32;
+  double rel_tol = 1e-6;
+  double step_tol = 1e-8;
+  DampingPolicy damping = DampingPolicy::diag_scaled;
+  MseConvention mse = MseConvention::half_per_observation;
+  JacobianMode jacobian = JacobianMode::autodiff;
+  bool check_rank_identity = false;
+  std::vector<int> devices{0};  // B200 placement: rank r -> devices[r % size]
+
+  dbag_config c_view() const {
+    dbag_config c;
+    dbag_default_config(&c);
+    c.workers = workers;
+    c.max_iterations = max_iterations;
+    c.pcg_tol = pcg_tol;
+    c.pcg_max_iters = pcg_max_iters;
+    c.lambda0 = lambda0;
+    c.lambda_max = lambda_max;
+    c.rel_tol = rel_tol;
+    c.step_tol = step_tol;
+    c.damping = damping == DampingPolicy::diag_scaled ? 1 : 0;
+    c.mse_half = mse == MseConvention::half_per_observation ? 1 : 0;
+    c.jacobian = jacobian == JacobianMode::analytic ? 1 : 0;
+    c.check_rank_identity = check_rank_identity ? 1 : 0;
+    return c;
+  }
+};
+
+struct IterationRecord {
+  int iteration = 0;
+  double cost = 0, mse = 0, lambda = 0;
+  int pcg_iterations = 0;
+  bool accepted = false;
+  double wall_seconds = 0;
+  std::vector<std::uint64_t> worker_edges, worker_block_ops;
+};
+
+template <typename Scalar>
+struct SolverState {
+  std::vector<Scalar> x_c, x_p;
+  double lambda = 0, nu = 2;
+  int iteration = 0;
+  double cost = 0;
+  TerminationReason termination = TerminationReason::max_iterations;
+  std::vector<IterationRecord> history;
+};
+
+// dba::lm_solve on B200: config.workers ranks, rank 0's state.
+template <typename Scalar>
+SolverState<Scalar> lm_solve(const BAProblem<Scalar>& problem, const SolverConfig& config) {
+  static_assert(sizeof(Scalar) == 4 || sizeof(Scalar) == 8, "Scalar must be float or double");
+  const dbag_problem p = problem.c_view();
+  const dbag_config c = config.c_view();
+  const int cap = config.max_iterations, k = config.workers;
+  SolverState<Scalar> st;
+  st.x_c.resize(problem.packed_cameras().size());
+  st.x_p.resize(problem.packed_points().size());
+  std::vector<std::int32_t> it(cap), pcg(cap), acc(cap);
+  std::vector<double> cost(cap), mse(cap), lam(cap), wall(cap);
+  std::vector<std::uint64_t> we(static_cast<std::size_t>(cap) * k), wb(static_cast<std::size_t>(cap) * k);
+  dbag_result r{};
+  r.capacity = cap;
+  r.rec_iteration = it.data();
+  r.rec_cost = cost.data();
+  r.rec_mse = mse.data();
+  r.rec_lambda = lam.data();
+  r.rec_pcg = pcg.data();
+  r.rec_accepted = acc.data();
+  r.rec_wall = wall.data();
+  r.rec_worker_edges = we.data();
+  r.rec_worker_block_ops = wb.data();
+  r.x_c = st.x_c.data();
+  r.x_p = st.x_p.data();
+  detail::check(dbag_lm_solve(static_cast<int>(sizeof(Scalar)), &p, &c, config.devices.data(),
+                              static_cast<int>(config.devices.size()), &r));
+  st.lambda = r.lambda;
+  st.nu = r.nu;
+  st.iteration = r.iterations;
+  st.cost = r.cost;
+  st.termination = static_cast<TerminationReason>(r.termination);
+  for (int i = 0; i < std::min(cap, r.iterations); ++i) {
+    IterationRecord rec;
+    rec.iteration = it[static_cast<std::size_t>(i)];
+    rec.cost = cost[static_cast<std::size_t>(i)];
+    rec.mse = mse[static_cast<std::size_t>(i)];
+    rec.lambda = lam[static_cast<std::size_t>(i)];
+    rec.pcg_iterations = pcg[static_cast<std::size_t>(i)];
+    rec.accepted = acc[static_cast<std::size_t>(i)] != 0;
+    rec.wall_seconds = wall[static_cast<std::size_t>(i)];
+    rec.worker_edges.assign(we.begin() + i * k, we.begin() + (i + 1) * k);
+    rec.worker_block_ops.assign(wb.begin() + i * k, wb.begin() + (i + 1) * k);
+    st.history.push_back(rec);
+  }
+  return st;
+}
+
+// ---- partitioning (dba/partition.hpp) ----------------------------------------
+struct EdgePartition {
+  int worker_rank = 0;
+  std::vector<std::int32_t> edge_ids;
+  std::vector<std::int32_t> camera_to_global, point_to_global;  // LocalIndexMap::to_global
+};
+
+template <typename Scalar>
+std::vector<EdgePartition> partition_edges(const BAProblem<Scalar>& problem, int worker_count) {
+  const dbag_problem p = problem.c_view();
+  std::vector<EdgePartition> out;
+  if (worker_count < 1) throw InvalidArgumentError("worker count must be >= 1");
+  const std::size_t m = static_cast<std::size_t>(p.num_cameras), n = static_cast<std::size_t>(p.num_points),
+                    N = static_cast<std::size_t>(p.num_observations);
+  for (int r = 0; r < worker_count; ++r) {
+    std::int64_t start = 0, count = 0;
+    std::int32_t nc = 0, np = 0;
+    std::vector<std::int32_t> cg(std::max<std::size_t>(m, 1)), pg(std::max<std::size_t>(n, 1));
+    std::vector<std::int64_t> cptr(m + 1), pptr(n + 1), cblk(std::max<std::size_t>(N, 1)),
+        pblk(std::max<std::size_t>(N, 1));
+    detail::check(dbag_partition(&p, worker_count, r, &start, &count, &nc, cg.data(), &np, pg.data(), cptr.data(),
+                                 cblk.data(), pptr.data(), pblk.data()));
+    EdgePartition e;
+    e.worker_rank = r;
+    for (std::int64_t i = 0; i < count; ++i) e.edge_ids.push_back(static_cast<std::int32_t>(start + i));
+    e.camera_to_global.assign(cg.begin(), cg.begin() + nc);
+    e.point_to_global.assign(pg.begin(), pg.begin() + np);
+    out.push_back(std::move(e));
+  }
+  return out;
+}
+
+// ---- synthetic generator (dba/synthetic.hpp) ---------------------------------
+struct SyntheticOptions {
+  std::int32_t cameras = 20000, points = 80000, obs_per_point = 1000;
+  std::uint64_t seed = 1;
+  double circle_radius = 8.0, base_focal = 1000.0, pose_noise = 0.01, intrinsic_noise = 0.5, point_noise = 0.1;
+  std::int64_t num_observations = 0;  // > 0: count-exact extension
+  double pixel_noise = 0.0;
+};
+
+inline BAProblem<double> generate_synthetic(const SyntheticOptions& o) {
+  dbag_synthetic_options c{};
+  c.cameras = o.cameras;
+  c.points = o.points;
+  c.obs_per_point = o.obs_per_point;
+  c.seed = o.seed;
+  c.circle_radius = o.circle_radius;
+  c.base_focal = o.base_focal;
+  c.pose_noise = o.pose_noise;
+  c.intrinsic_noise = o.intrinsic_noise;
+  c.point_noise = o.point_noise;
+  c.num_observations = o.num_observations;
+  c.pixel_noise = o.pixel_noise;
+  std::int64_t N = 0;
+  detail::check(dbag_synthetic_count(&c, &N));
+  std::vector<double> cams(static_cast<std::size_t>(o.cameras) * 9), pts(static_cast<std::size_t>(o.points) * 3),
+      px(static_cast<std::size_t>(N)), py(static_cast<std::size_t>(N));
+  std::vector<std::int32_t> cid(static_cast<std::size_t>(N)), pid(static_cast<std::size_t>(N));
+  detail::check(dbag_generate_synthetic(&c, cams.data(), pts.data(), cid.data(), pid.data(), px.data(), py.data()));
+  BAProblem<double> p;
+  for (std::int32_t i = 0; i < o.cameras; ++i) {
+    CameraState<double> cs;
+    const double* q = cams.data() + static_cast<std::size_t>(i) * 9;
+    cs.rotation = {q[0], q[1], q[2]};
+    cs.translation = {q[3], q[4], q[5]};
+    cs.focal = q[6];
+    cs.k1 = q[7];
+    cs.k2 = q[8];
+    p.add_node(cs);
+  }
+  for (std::int32_t i = 0; i < o.points; ++i) {
+    PointState<double> ps;
+    ps.position = {pts[static_cast<std::size_t>(i) * 3], pts[static_cast<std::size_t>(i) * 3 + 1],
+                   pts[static_cast<std::size_t>(i) * 3 + 2]};
+    p.add_node(ps);
+  }
+  for (std::int64_t e = 0; e < N; ++e) {
+    Observation<double> ob;
+    ob.camera_id = cid[static_cast<std::size_t>(e)];
+    ob.point_id = pid[static_cast<std::size_t>(e)];
+    ob.pixel = {px[static_cast<std::size_t>(e)], py[static_cast<std::size_t>(e)]};
+    p.add_edge(ob);
+  }
+  return p;
+}
+
+}  // namespace dba
