@@ -169,6 +169,33 @@ def time_steps(ctx, cfg, steps, flush):
     return ms, pcg
 
 
+def dse_roofline(ctx, prof, b_dse, peak, steps, total_ms, world):
+    """Roofline of the dominant kernel, the DSE pass (B_DSE bytes
+    per pass). Single rank: the graph DPCG's k_g_pass, timed live with CUDA
+    events on the context's stream, launched alone back to back on the state
+    the timed steps left (its in-graph launches cannot carry events);
+    in_graph_ms_per_dse is the whole DPCG graph's device time per DSE
+    (pass + camera fold + step + loop overhead). Several ranks: the
+    host-driven loop's DSE launches (k_dse_stream), event-timed in place."""
+    dse_per_step = prof["dse_launches"] / max(steps, 1)
+    loop_ms_per_dse = prof["dse_ms"] / max(prof["dse_launches"], 1)
+    per, kernel = loop_ms_per_dse, "k_dse_stream (TMA DSE pass, host-driven DPCG)"
+    if world == 1:
+        try:
+            per = ctx.time_dse_pass(20)
+            kernel = "k_g_pass (DSE pass of the graph DPCG; launched alone, back to back)"
+        except Exception:  # DBAG_PCG selected a non-graph DPCG
+            kernel = "DPCG (DBAG_PCG=%s), device time per DSE" % os.environ.get("DBAG_PCG")
+    achieved = b_dse / (per / 1e3) / 1e9
+    return {"bound": "hbm", "kernel": kernel, "achieved": achieved, "peak": peak, "unit": "GB/s",
+            "frac": achieved / peak, "traffic": None, "bytes_per_launch": b_dse, "avg_launch_ms": per,
+            "launches_per_step": dse_per_step, "in_graph_ms_per_dse": loop_ms_per_dse,
+            "share_of_step": per * dse_per_step / max(total_ms / max(steps, 1), 1e-9),
+            "note": "achieved = algorithmic DSE bytes per pass (SURVEY 8d) / device ms per launch; "
+                    "trafalgar-257's E (49 MB) stays L2-resident across the passes of a step, "
+                    "see secondary (venice-1778, E 1.2 GB) for the HBM-bound size"}
+
+
 def run_ours(args):
     import torch
     import paper_2112_01349_b200 as dba
@@ -228,13 +255,12 @@ def run_ours(args):
     state_bytes = 8 * (9 * m + 3 * n)
 
     peak, peak_kind = load_peaks()
-    per_dse_ms = prof["dse_ms"] / max(prof["dse_launches"], 1)
     b_dse = dse_bytes(N // world, n, m, 8)
-    achieved = b_dse / (per_dse_ms / 1e3) / 1e9
-    traffic = None
+    roof = dse_roofline(ctx, prof, b_dse, peak, args.steps, total_ms, world)
+    roof["peak_kind"] = peak_kind
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
-            traffic = json.load(f).get(args.workload, {}).get("dram_bytes_per_launch")
+            roof["traffic"] = json.load(f).get(args.workload, {}).get("dram_bytes_per_launch")
     except Exception:
         pass
     line = {
@@ -246,17 +272,7 @@ def run_ours(args):
                    "solver": "SolverConfig defaults (diag_scaled, lambda0 1e-4, pcg_tol 1e-6, pcg_max_iters 500)",
                    "l2": "flushed (512 MiB write) between timed steps",
                    "step": "one LM iteration from x0 (linearize+assemble, factor, rhs, DPCG, backsub, trial cost)"},
-        "roofline": {"bound": "hbm", "kernel": "k_pcg_persistent (DPCG: fused DSE passes + camera-space ops)",
-                     "achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": traffic,
-                     "bytes_per_launch": b_dse * prof["dse_launches"] / max(args.steps, 1),
-                     "avg_launch_ms": prof["dse_ms"] / max(args.steps, 1),
-                     "bytes_per_dse": b_dse, "ms_per_dse": per_dse_ms,
-                     "dse_per_launch": prof["dse_launches"] / max(args.steps, 1),
-                     "share_of_step": prof["dse_ms"] / max(total_ms, 1e-9),
-                     "note": "achieved = algorithmic DSE bytes (SURVEY 8d B_DSE x DSE count) / device time of "
-                             "the PCG kernel; trafalgar-257's E (49 MB) is L2-resident inside a step, see secondary "
-                             "for an HBM-bound size"},
+        "roofline": roof,
         "e2e": {"value": N / e2e_s, "unit": "edges/s", "h2d_bytes_per_step": state_bytes,
                 "d2h_bytes_per_step": state_bytes},
         "clocks": clk.summary(),
@@ -288,23 +304,16 @@ def secondary(args, flush):
         ctx.profile(True)
         ms, pcg = time_steps(ctx, cfg, 3, flush)
         prof = ctx.profile()
-    t = sum(ms) / len(ms)
-    peak, _ = load_peaks()
-    per = prof["dse_ms"] / max(prof["dse_launches"], 1)
-    b = dse_bytes(N, n, m, 8)
-    traffic = None
+        t = sum(ms) / len(ms)
+        peak, _ = load_peaks()
+        roof = dse_roofline(ctx, prof, dse_bytes(N, n, m, 8), peak, len(ms), sum(ms), 1)
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
-            traffic = json.load(f).get(name, {}).get("dram_bytes_per_launch")
+            roof["traffic"] = json.load(f).get(name, {}).get("dram_bytes_per_launch")
     except Exception:
         pass
     return {"workload": name, "ms_per_step": t, "value": N / (t / 1e3), "unit": "edges/s",
-            "pcg_iterations_per_step": pcg,
-            "roofline": {"bound": "hbm", "kernel": "k_pcg_persistent", "achieved": b / (per / 1e3) / 1e9,
-                         "peak": peak, "unit": "GB/s", "frac": b / (per / 1e3) / 1e9 / peak, "traffic": traffic,
-                         "bytes_per_dse": b, "ms_per_dse": per, "dse_per_launch": prof["dse_launches"] / len(ms),
-                         "avg_launch_ms": prof["dse_ms"] / len(ms),
-                         "share_of_step": prof["dse_ms"] / max(sum(ms), 1e-9)}}
+            "pcg_iterations_per_step": pcg, "roofline": roof}
 
 
 def cpu_baseline(args, p):

@@ -195,6 +195,10 @@ int dbag_profile(dbag_ctx* ctx, int enable, double* dse_ms, int64_t* dse_launche
 int dbag_event_mark(dbag_ctx* ctx, int which);
 int dbag_event_elapsed(dbag_ctx* ctx, double* ms);
 int dbag_synchronize(dbag_ctx* ctx);
+/* Device ms per launch of the single-rank graph DPCG's DSE pass (k_g_pass),
+ * launched alone `reps` times back to back on the state the last dbag_pcg /
+ * probe step left (bench roofline; needs a preceding graph DPCG). */
+int dbag_time_dse_pass(dbag_ctx* ctx, int reps, double* ms_per_pass);
 /* Number of kernels this context has launched (bench: gpu_launches). */
 int dbag_launch_count(dbag_ctx* ctx, int64_t* out);
 

@@ -79,6 +79,7 @@ _SIGS = {
     "dbag_event_mark": (C.c_int, [vp, C.c_int]),
     "dbag_event_elapsed": (C.c_int, [vp, _P(f64)]),
     "dbag_synchronize": (C.c_int, [vp]),
+    "dbag_time_dse_pass": (C.c_int, [vp, C.c_int, _P(f64)]),
     "dbag_launch_count": (C.c_int, [vp, _P(i64)]),
     "dbag_residuals": (C.c_int, [vp, C.c_int, vp]),
     "dbag_get_jacobians": (C.c_int, [vp, vp, vp]),

@@ -470,6 +470,10 @@ int dbag_synchronize(dbag_ctx* ctx) {
   return guarded([&] { with_rank(ctx, [&](auto& rk) { rk.sync(); }); });
 }
 
+int dbag_time_dse_pass(dbag_ctx* ctx, int reps, double* ms_per_pass) {
+  return guarded([&] { with_rank(ctx, [&](auto& rk) { *ms_per_pass = rk.time_dse_pass(reps); }); });
+}
+
 int dbag_launch_count(dbag_ctx* ctx, int64_t* out) {
   return guarded([&] { with_rank(ctx, [&](auto& rk) { *out = rk.launches(); }); });
 }

@@ -143,7 +143,10 @@ struct GatherX {
   const S* x;
   __device__ __forceinline__ S operator()(std::int32_t cam, int i) const { return __ldg(x + std::size_t(cam) * 9 + i); }
 };
-template <class S>
+// COHERENT loads bypass L1 for vectors written earlier in the same
+// (persistent) launch; otherwise the gathers go through L1, where a tile's
+// repeated cameras hit.
+template <class S, bool COHERENT = true>
 struct GatherP {
   const S* z;
   const S* p_prev;
@@ -151,8 +154,12 @@ struct GatherP {
   bool first;
   __device__ __forceinline__ S operator()(std::int32_t cam, int i) const {
     const std::size_t k = std::size_t(cam) * 9 + i;
-    const S zv = __ldcg(z + k);
-    return first ? zv : zv + beta * __ldcg(p_prev + k);
+    if (COHERENT) {
+      const S zv = __ldcg(z + k);
+      return first ? zv : zv + beta * __ldcg(p_prev + k);
+    }
+    const S zv = __ldg(z + k);
+    return first ? zv : zv + beta * __ldg(p_prev + k);
   }
 };
 

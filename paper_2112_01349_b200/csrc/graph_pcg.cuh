@@ -1,0 +1,290 @@
+// graph_pcg.cuh — DPCG as a CUDA graph with device-side control flow.
+//
+// dpcg (dba/solver.hpp:202-257) for a single rank, every recurrence on the
+// device and the loop itself in the graph: one conditional WHILE node whose
+// body is three kernels,
+//   k_g_pass    the fused DSE pass over E (one CTA per chunk, long tiles
+//               first) gathering p formed on the fly from z and the previous
+//               p, writing camera-major partials;
+//   k_g_camera  warp per camera: c = fold(partials) in chunk order, p stored,
+//               q = B_d p - c, the camera's p.q term;
+//   k_g_step    alpha = rho / sum(p.q) (camera order), x += alpha p,
+//               r -= alpha q, z = B^-1 r, rho, |r|^2 and the loop decision
+//               (cudaGraphSetConditional) from a deterministic grid reduction.
+// Every 50th iteration the body runs once more as a residual-refresh pass
+// (DSE on x, r = g - S x), selected by a device-side phase flag. One graph
+// launch runs the whole inner solve with no host round trip, no
+// persistent-kernel grid barriers and full-occupancy DSE tiles.
+//
+// Loop control matches the reference: stop when |r| <= tol |g| or
+// n == max_iters; rho (after z = B^-1 r) and p'q breakdowns stop with status
+// 1 / 2 in the reference's order (rho checked before the DSE, p'q after).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "dse.cuh"
+
+namespace dbag {
+namespace dev {
+
+template <class S>
+struct GScal {
+  double rho, rho_prev, pq, rnorm2, rhs_norm2, tol;
+  S alpha, beta;
+  int n, max_iters, status, dse_count;
+  int phase;  // 0: PCG pass, 1: residual-refresh pass (DSE on x)
+};
+
+template <class S>
+struct GBufs {
+  std::int32_t m;
+  const S* Bd;
+  const S* Binv;
+  const S* g;
+  S* x;
+  S* r;
+  S* z;
+  S* p0;  // p buffers: iteration n writes p[n & 1]
+  S* p1;
+  S* q;
+  const std::int32_t* cam_part_ptr;
+  const S* part;
+  double* pq_cam;  // per-camera p.q of the running pass
+};
+
+template <class S>
+__device__ __forceinline__ S* p_cur(const GBufs<S>& B, int n) {
+  return (n & 1) ? B.p1 : B.p0;
+}
+
+// Loop decision after rho / |r|^2 of iteration state n (dba/solver.hpp:223-230).
+template <class S>
+__device__ __forceinline__ bool continue_loop(GScal<S>* sc) {
+  bool loop = sqrt(sc->rnorm2) > sc->tol * sqrt(sc->rhs_norm2) && sc->n < sc->max_iters;
+  if (loop && (!(sc->rho > 0.0) || isinf(sc->rho))) {
+    sc->status = 1;
+    loop = false;
+  }
+  return loop;
+}
+
+// Lanes 0..26 of each warp: 3 cameras x 9 rows (thread = row of a camera).
+__device__ __forceinline__ bool camera_lane(std::int32_t m, std::int32_t& cam, int& row, int& base) {
+  const int lane = threadIdx.x & 31;
+  const std::int64_t warp = (blockIdx.x * std::int64_t(blockDim.x) + threadIdx.x) >> 5;
+  row = lane % 9;
+  base = lane - row;
+  cam = std::int32_t(warp * 3 + lane / 9);
+  return lane < 27 && cam < m;
+}
+
+// z = B^-1 r for a camera whose 9 rows sit in lanes base..base+8.
+template <class S>
+__device__ __forceinline__ S precond_lane(const S* Binv, std::int32_t cam, int row, int base, S rrow) {
+  const S* bi = Binv + std::size_t(cam) * 81 + row * 9;
+  S z = S(0);
+#pragma unroll
+  for (int k = 0; k < 9; ++k) z += bi[k] * __shfl_sync(0xffffffffu, rrow, base + k);
+  return z;
+}
+
+// x = 0, r = g, z = B^-1 g, rho, |g|^2; sets the WHILE condition.
+template <class S>
+__global__ void __launch_bounds__(kRedThreads) k_g_init(GBufs<S> B, RedWs ws, GScal<S>* sc,
+                                                        cudaGraphConditionalHandle h_while) {
+  std::int32_t cam;
+  int row, base;
+  const bool on = camera_lane(B.m, cam, row, base);
+  double rho = 0.0, rn = 0.0;
+  const std::size_t i = on ? std::size_t(cam) * 9 + row : 0;
+  const S gi = on ? B.g[i] : S(0);
+  const S zi = precond_lane(B.Binv, on ? cam : 0, row, base, gi);
+  if (on) {
+    B.x[i] = S(0);
+    B.r[i] = gi;
+    B.z[i] = zi;
+    rho = double(gi) * double(zi);
+    rn = double(gi) * double(gi);
+  }
+  const double v[2] = {rho, rn};
+  __shared__ double fin[2];
+  if (grid_reduce<SumOp, 2>(v, ws.partials, ws.counter, fin) && threadIdx.x == 0) {
+    sc->rho = fin[0];
+    sc->rnorm2 = fin[1];
+    sc->rhs_norm2 = fin[1];
+    sc->rho_prev = 0.0;
+    sc->n = 0;
+    sc->status = 0;
+    sc->beta = S(0);
+    sc->phase = 0;
+    sc->dse_count = fin[1] != 0.0 ? 1 : 0;  // the reference's DSE on x0 (dba/solver.hpp:217)
+    cudaGraphSetConditional(h_while, fin[1] != 0.0 && continue_loop(sc) ? 1u : 0u);
+  }
+}
+
+// One camera, one warp: c = fold of the camera's partials in chunk order
+// (lanes strided, fixed shuffle tree); v = p = z + beta p_prev (PCG pass,
+// stored as p) or x (refresh pass); q = B_d v - c; the p.q term in double.
+template <class S>
+__global__ void __launch_bounds__(kRedThreads) k_g_camera(GBufs<S> B, const GScal<S>* sc) {
+  const int lane = threadIdx.x & 31;
+  const std::int32_t cam = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (cam >= B.m) return;
+  const int n = sc->n;
+  const bool pcg = sc->phase == 0;
+  S acc[9];
+#pragma unroll
+  for (int i = 0; i < 9; ++i) acc[i] = S(0);
+  for (std::int32_t k = B.cam_part_ptr[cam] + lane; k < B.cam_part_ptr[cam + 1]; k += 32) {
+    const S* pp = B.part + std::size_t(k) * 9;
+#pragma unroll
+    for (int i = 0; i < 9; ++i) acc[i] += pp[i];
+  }
+#pragma unroll
+  for (int i = 0; i < 9; ++i) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc[i] += __shfl_down_sync(0xffffffffu, acc[i], o);
+    acc[i] = __shfl_sync(0xffffffffu, acc[i], 0);
+  }
+  const std::size_t at = std::size_t(cam) * 9;
+  const int row = lane < 9 ? lane : 0;
+  S v;
+  if (pcg) {
+    const S zr = B.z[at + row];
+    v = n == 0 ? zr : zr + sc->beta * p_cur(B, n + 1)[at + row];
+    if (lane < 9) p_cur(B, n)[at + row] = v;
+  } else {
+    v = B.x[at + row];
+  }
+  S d = S(0);
+#pragma unroll
+  for (int k = 0; k < 9; ++k) d += B.Bd[std::size_t(cam) * 81 + row * 9 + k] * __shfl_sync(0xffffffffu, v, k);
+  S c = acc[0];
+#pragma unroll
+  for (int i = 1; i < 9; ++i)
+    if (row == i) c = acc[i];
+  const S qv = d - c;
+  double pq = 0.0;
+  if (lane < 9) {
+    B.q[at + row] = qv;
+    pq = double(v) * double(qv);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) pq += __shfl_down_sync(0xffffffffu, pq, o);
+  if (lane == 0) B.pq_cam[cam] = pq;
+}
+
+// The body's DSE pass: CTAs [0, n_long) take the long tiles, the rest one
+// chunk each; the gathered vector is p formed on the fly from z and the
+// previous p (PCG pass) or x (refresh pass).
+template <class S>
+__global__ void __launch_bounds__(kTile, 5) k_g_pass(DseArgs<S> A, GBufs<S> B, const GScal<S>* sc) {
+  __shared__ DseWork<S> sm;
+  const int n = sc->n;
+  const S beta = sc->beta;
+  const bool pcg = sc->phase == 0;
+  const std::int32_t blk = blockIdx.x;
+  if (blk < A.n_long) {
+    if (pcg)
+      dse_long<S, 0>(A, sm, blk, GatherP<S, false>{B.z, p_cur(B, n + 1), beta, n == 0});
+    else
+      dse_long<S, 0>(A, sm, blk, GatherX<S>{B.x});
+    return;
+  }
+  const std::int32_t chunk = blk - A.n_long;
+  if (pcg)
+    dse_chunk<S, 0>(A, sm, chunk, GatherP<S, false>{B.z, p_cur(B, n + 1), beta, n == 0});
+  else
+    dse_chunk<S, 0>(A, sm, chunk, GatherX<S>{B.x});
+}
+
+// Finish of an iteration: rho_prev, rho, |r|^2, n + 1, beta, loop decision.
+template <class S>
+__device__ __forceinline__ void finish_iteration(GScal<S>* sc, double rho, double rn2,
+                                                 cudaGraphConditionalHandle h_while) {
+  sc->rho_prev = sc->rho;
+  sc->rho = rho;
+  sc->rnorm2 = rn2;
+  sc->n += 1;
+  sc->beta = S(rho / sc->rho_prev);
+  cudaGraphSetConditional(h_while, continue_loop(sc) ? 1u : 0u);
+}
+
+// End of a body pass (dba/solver.hpp:238-254). PCG pass: p'q = sum of the
+// per-camera terms (every CTA folds them in camera order: same value
+// everywhere), breakdown check, alpha; x += alpha p; then either
+// r -= alpha q, z = B^-1 r, rho, |r|^2 and the loop decision, or (every 50th
+// iteration) hand over to a refresh pass. Refresh pass (q = S x): r = g - q,
+// z, rho, |r|^2 and the loop decision. sc is written only by the CTA that
+// finishes the grid reduction, after every CTA has read it.
+template <class S>
+__global__ void __launch_bounds__(kRedThreads) k_g_step(GBufs<S> B, RedWs ws, GScal<S>* sc,
+                                                        cudaGraphConditionalHandle h_while) {
+  __shared__ double red[32];
+  __shared__ double pq_all;
+  const int n = sc->n;
+  const bool refresh_pass = sc->phase != 0;
+  S alpha = S(0);
+  double pq = 0.0;
+  if (!refresh_pass) {
+    for (std::int32_t c = threadIdx.x; c < B.m; c += blockDim.x) pq += __ldcg(B.pq_cam + c);
+    pq = block_reduce<SumOp>(pq, red);
+    if (threadIdx.x == 0) pq_all = pq;
+    __syncthreads();
+    pq = pq_all;
+    if (!(pq > 0.0) || isinf(pq)) {  // p'q breakdown (uniform across the grid)
+      if (blockIdx.x == 0 && threadIdx.x == 0) {
+        sc->pq = pq;
+        sc->status = 2;
+        sc->dse_count += 1;
+        cudaGraphSetConditional(h_while, 0u);
+      }
+      return;
+    }
+    alpha = S(sc->rho / pq);
+  }
+  const bool hand_over = !refresh_pass && (n + 1) % 50 == 0;
+  std::int32_t cam;
+  int row, base;
+  const bool on = camera_lane(B.m, cam, row, base);
+  const std::size_t i = on ? std::size_t(cam) * 9 + row : 0;
+  S ri = S(0);
+  if (refresh_pass) {
+    if (on) ri = B.g[i] - B.q[i];
+  } else if (on) {
+    B.x[i] = B.x[i] + alpha * p_cur(B, n)[i];
+    if (!hand_over) ri = B.r[i] - alpha * B.q[i];
+  }
+  double rho = 0.0, rn = 0.0;
+  if (!hand_over) {
+    const S zi = precond_lane(B.Binv, on ? cam : 0, row, base, ri);
+    if (on) {
+      B.r[i] = ri;
+      B.z[i] = zi;
+      rho = double(ri) * double(zi);
+      rn = double(ri) * double(ri);
+    }
+  }
+  const double v[2] = {rho, rn};
+  __shared__ double fin[2];
+  if (grid_reduce<SumOp, 2>(v, ws.partials, ws.counter, fin) && threadIdx.x == 0) {
+    sc->dse_count += 1;
+    if (!refresh_pass) {
+      sc->pq = pq;
+      sc->alpha = alpha;
+    }
+    if (hand_over) {
+      sc->phase = 1;
+      cudaGraphSetConditional(h_while, 1u);
+    } else {
+      sc->phase = 0;
+      finish_iteration(sc, fin[0], fin[1], h_while);
+    }
+  }
+}
+
+}  // namespace dev
+}  // namespace dbag

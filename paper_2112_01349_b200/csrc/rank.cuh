@@ -31,6 +31,7 @@
 #include "comm.hpp"
 #include "common.hpp"
 #include "dse.cuh"
+#include "graph_pcg.cuh"
 #include "pcg.cuh"
 #include "kernels.cuh"
 #include "partition.hpp"
@@ -114,6 +115,8 @@ class Rank {
     cudaFreeHost(hsc_);
     cudaFreeHost(hbuf_);
     if (pcg_out_h_) cudaFreeHost(pcg_out_h_);
+    if (gsc_h_) cudaFreeHost(gsc_h_);
+    destroy_graph();
     cudaStreamDestroy(st_);
   }
 
@@ -137,6 +140,7 @@ class Rank {
         throw Error(DBAG_INVALID_ARGUMENT, "edge references unknown point " + std::to_string(p.point_id[e]));
     }
     jac_mode_ = jac_mode;
+    destroy_graph();
     plan_ = plan_shard(p.camera_id, p.point_id, p.num_observations, p.num_cameras, p.num_points, comm_->size(),
                        comm_->rank(), dev::kTile);
     m_ = plan_.m;
@@ -208,6 +212,8 @@ class Rank {
     halo_dpt_.upload(hl);
     halo_idx_.upload(hi);
     halo_buf_.alloc(static_cast<std::size_t>(std::max<std::int64_t>(H_, 1)) * 12);
+    // grid-reduction partials: enough for one warp per camera
+    red_part_.alloc(std::max<std::size_t>(8 * dev::kRedBlocksMax, 2 * (static_cast<std::size_t>(p.num_cameras) * 32 / 256 + 64)));
     // state + system
     const std::size_t cm = static_cast<std::size_t>(m_) * 9, pl = static_cast<std::size_t>(n_loc_) * 3;
     for (DevBuf<S>* b : {&xc_, &xct_, &dxc_, &v_, &g_, &r_, &z_, &p_, &q_, &ctmp_}) b->alloc(std::max<std::size_t>(cm, 1));
@@ -383,7 +389,12 @@ class Rank {
   // --------------------------------------------------------------- DPCG ----
   PcgOut pcg(double tol, int max_iters) {
     DBAG_CUDA(cudaSetDevice(device_));
-    if (comm_->size() == 1 && persistent_grid() > 0) return pcg_persistent(tol, max_iters);
+    if (comm_->size() == 1) {
+      const char* mode = std::getenv("DBAG_PCG");
+      const std::string m = mode ? mode : "graph";
+      if (m == "graph" && n_chunks_ > 0 && m_ > 0) return pcg_graph(tol, max_iters);
+      if (m == "persistent" && persistent_grid() > 0) return pcg_persistent(tol, max_iters);
+    }
     S* x = dxc_.get();
     const std::int64_t len = static_cast<std::int64_t>(m_) * 9;
     dse_count_ = 0;
@@ -439,6 +450,144 @@ class Rank {
     }
     return {n, r_norm <= tol * rhs_norm};
   }
+
+  // ---- DPCG as one CUDA graph with conditional WHILE / IF nodes (K = 1) ----
+  dev::GBufs<S> gbufs() {
+    dev::GBufs<S> b;
+    b.m = m_;
+    b.Bd = Bd_.get();
+    b.Binv = Bexp_.get();
+    b.g = g_.get();
+    b.x = dxc_.get();
+    b.r = r_.get();
+    b.z = z_.get();
+    b.p0 = p_.get();
+    b.p1 = p2_.get();
+    b.q = q_.get();
+    b.cam_part_ptr = cam_part_ptr_.get();
+    b.part = part_.get();
+    b.pq_cam = g_pq_cam_.get();
+    return b;
+  }
+
+  static cudaGraphNode_t add_kernel(cudaGraph_t g, const cudaGraphNode_t* dep, void* func, int grid, int block,
+                                    void** args) {
+    cudaKernelNodeParams kp{};
+    kp.func = func;
+    kp.gridDim = dim3(static_cast<unsigned>(std::max(grid, 1)));
+    kp.blockDim = dim3(static_cast<unsigned>(block));
+    kp.sharedMemBytes = 0;
+    kp.kernelParams = args;
+    cudaGraphNode_t n;
+    DBAG_CUDA(cudaGraphAddKernelNode(&n, g, dep, dep ? 1 : 0, &kp));
+    return n;
+  }
+
+  static cudaGraph_t add_conditional(cudaGraph_t g, const cudaGraphNode_t* dep, cudaGraphConditionalHandle h,
+                                     cudaGraphConditionalNodeType type, cudaGraphNode_t* node) {
+    cudaGraphNodeParams np{};
+    np.type = cudaGraphNodeTypeConditional;
+    np.conditional.handle = h;
+    np.conditional.type = type;
+    np.conditional.size = 1;
+    DBAG_CUDA(cudaGraphAddNode(node, g, dep, dep ? 1 : 0, &np));
+    return np.conditional.phGraph_out[0];
+  }
+
+  void destroy_graph() {
+    if (g_exec_) cudaGraphExecDestroy(g_exec_);
+    if (g_graph_) cudaGraphDestroy(g_graph_);
+    g_exec_ = nullptr;
+    g_graph_ = nullptr;
+  }
+
+  void build_graph() {
+    destroy_graph();
+    if (!gsc_.get()) {
+      gsc_.alloc(1);
+      DBAG_CUDA(cudaMallocHost(&gsc_h_, sizeof(dev::GScal<S>)));
+    }
+    g_pq_cam_.alloc(std::max<std::size_t>(m_, 1));
+    dev::GBufs<S> B = gbufs();
+    dev::RedWs ws = red();
+    dev::GScal<S>* sc = gsc_.get();
+    dev::DseArgs<S> A = dse_args(nullptr);
+    const int cam_lane_blocks = static_cast<int>((static_cast<std::int64_t>(m_) * 32 / 3 + 255) / 256 + 1);
+    DBAG_CUDA(cudaGraphCreate(&g_graph_, 0));
+    cudaGraphConditionalHandle hw;
+    DBAG_CUDA(cudaGraphConditionalHandleCreate(&hw, g_graph_, 0, 0));
+    void* a_init[] = {&B, &ws, &sc, &hw};
+    cudaGraphNode_t n_init = add_kernel(g_graph_, nullptr, reinterpret_cast<void*>(dev::k_g_init<S>), cam_lane_blocks,
+                                        dev::kRedThreads, a_init);
+    cudaGraphNode_t n_while;
+    cudaGraph_t body = add_conditional(g_graph_, &n_init, hw, cudaGraphCondTypeWhile, &n_while);
+    const dev::GScal<S>* csc = sc;
+    void* a_pass[] = {&A, &B, &csc};
+    cudaGraphNode_t cur = add_kernel(body, nullptr, reinterpret_cast<void*>(dev::k_g_pass<S>), n_long_ + n_chunks_,
+                                     dev::kTile, a_pass);
+    void* a_cam[] = {&B, &csc};
+    const int cam_warp_blocks = static_cast<int>((static_cast<std::int64_t>(m_) * 32 + 255) / 256);
+    cur = add_kernel(body, &cur, reinterpret_cast<void*>(dev::k_g_camera<S>), cam_warp_blocks, dev::kRedThreads,
+                     a_cam);
+    void* a_step[] = {&B, &ws, &sc, &hw};
+    add_kernel(body, &cur, reinterpret_cast<void*>(dev::k_g_step<S>), cam_lane_blocks, dev::kRedThreads, a_step);
+    DBAG_CUDA(cudaGraphInstantiate(&g_exec_, g_graph_, 0));
+  }
+
+  PcgOut pcg_graph(double tol, int max_iters) {
+    if (!g_exec_) build_graph();
+    dev::GScal<S> init{};
+    init.tol = tol;
+    init.max_iters = max_iters;
+    *gsc_h_ = init;
+    DBAG_CUDA(cudaMemcpyAsync(gsc_.get(), gsc_h_, sizeof(init), cudaMemcpyHostToDevice, st_));
+    const bool prof = profiling_;
+    if (prof) DBAG_CUDA(cudaEventRecord(prof_event(), st_));
+    DBAG_CUDA(cudaGraphLaunch(g_exec_, st_));
+    if (prof) {
+      DBAG_CUDA(cudaEventRecord(prof_event(), st_));
+      DBAG_CUDA(cudaEventRecord(prof_event(), st_));
+    }
+    DBAG_CUDA(cudaMemcpyAsync(gsc_h_, gsc_.get(), sizeof(init), cudaMemcpyDeviceToHost, st_));
+    DBAG_CUDA(cudaStreamSynchronize(st_));
+    collect_profile();
+    const dev::GScal<S> o = *gsc_h_;
+    launches_ += 1 + 3 * static_cast<std::int64_t>(std::max(o.dse_count - 1, 0));  // k_g_init + 3 per body pass
+    dse_count_ = o.dse_count;
+    dse_launches_ += o.dse_count;
+    tally_.block_ops += 2 * static_cast<std::uint64_t>(N_) * static_cast<std::uint64_t>(o.dse_count);
+    if (o.status == 1)
+      throw Error(DBAG_PCG_BREAKDOWN, "preconditioned residual norm rho = " + std::to_string(o.rho) +
+                                          " at iteration " + std::to_string(o.n));
+    if (o.status == 2)
+      throw Error(DBAG_PCG_BREAKDOWN, "operator lost positive definiteness (p'q = " + std::to_string(o.pq) +
+                                          ") at iteration " + std::to_string(o.n));
+    return {o.n, std::sqrt(o.rnorm2) <= tol * std::sqrt(o.rhs_norm2)};
+  }
+  // Device time of the graph body's DSE pass (k_g_pass) launched alone,
+  // back to back, on the state the last graph DPCG left (bench roofline).
+  double time_dse_pass(int reps) {
+    DBAG_CUDA(cudaSetDevice(device_));
+    if (!g_exec_) throw Error(DBAG_INVALID_ARGUMENT, "time_dse_pass needs a preceding graph DPCG");
+    const dev::DseArgs<S> A = dse_args(nullptr);
+    const dev::GBufs<S> B = gbufs();
+    const dev::GScal<S>* sc = gsc_.get();
+    const int grid = n_long_ + n_chunks_;
+    cudaEvent_t e0, e1;
+    DBAG_CUDA(cudaEventCreate(&e0));
+    DBAG_CUDA(cudaEventCreate(&e1));
+    launch(dev::k_g_pass<S>, grid, dev::kTile, A, B, sc);  // warm-up
+    DBAG_CUDA(cudaEventRecord(e0, st_));
+    for (int r = 0; r < reps; ++r) launch(dev::k_g_pass<S>, grid, dev::kTile, A, B, sc);
+    DBAG_CUDA(cudaEventRecord(e1, st_));
+    DBAG_CUDA(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    DBAG_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    return static_cast<double>(ms) / std::max(reps, 1);
+  }
+
 
   // Grid of the cooperative PCG kernel (0: unavailable -> host-driven loop).
   // DBAG_PCG=host forces the host-driven loop; DBAG_DSE=direct|tma picks the
@@ -987,6 +1136,11 @@ class Rank {
   DevBuf<double> pcg_part_;
   DevBuf<unsigned> pcg_bar_;
   DevBuf<dev::PcgDevOut> pcg_out_;
+  DevBuf<dev::GScal<S>> gsc_;
+  DevBuf<double> g_pq_cam_;
+  dev::GScal<S>* gsc_h_ = nullptr;
+  cudaGraph_t g_graph_ = nullptr;
+  cudaGraphExec_t g_exec_ = nullptr;
   dev::PcgDevOut* pcg_out_h_ = nullptr;
   int pcg_grid_ = -1, stream_grid_ = -1;
   bool use_tma_ = true;

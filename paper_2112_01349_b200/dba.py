@@ -637,6 +637,12 @@ class RankContext:
     def synchronize(self):
         _check(N.lib().dbag_synchronize(self.h))
 
+    def time_dse_pass(self, reps: int = 20) -> float:
+        """Device ms per launch of the graph DPCG's DSE pass launched alone."""
+        t = C.c_double()
+        _check(N.lib().dbag_time_dse_pass(self.h, int(reps), C.byref(t)))
+        return t.value
+
     def launch_count(self) -> int:
         n = C.c_int64()
         _check(N.lib().dbag_launch_count(self.h, C.byref(n)))
