@@ -10,7 +10,7 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libdbag.so")
+LIB_PATH = os.environ.get("DBAG_LIB") or os.path.join(_HERE, "libdbag.so")
 
 i32, i64, u64, f64 = C.c_int32, C.c_int64, C.c_uint64, C.c_double
 vp, cvp = C.c_void_p, C.c_void_p

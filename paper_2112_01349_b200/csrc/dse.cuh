@@ -99,30 +99,36 @@ __device__ __forceinline__ void load_point(const DseArgs<S>& A, std::int32_t p, 
     for (int j = 0; j < 3; ++j) wv[j] = A.w[std::size_t(p) * 3 + j];
 }
 
-// Folds sm.y per distinct camera of the chunk (warp per camera) into the
-// camera-major partials.
+// Folds sm.y per distinct camera of the chunk into the camera-major
+// partials. A chunk holds few cameras with many slots each, so each camera
+// gets a group of G lanes (G = the largest power of two with nu * G <= 128,
+// at most 32; groups never straddle a warp): lane j of the group sums slots
+// j, j + G, ... in slot order, an xor butterfly combines the group (fixed
+// order: deterministic), and the group's lanes share the 9 stores.
 template <class S>
 __device__ __forceinline__ void fold_cameras(const DseArgs<S>& A, DseWork<S>& sm, int nu) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int u = warp; u < nu; u += kTile / 32) {
-    S acc[9];
+  const int tid = threadIdx.x;
+  const int G = min(32, 1 << (31 - __clz(kTile / max(nu, 1))));
+  const int u = tid / G, j = tid & (G - 1);
+  S acc[9];
 #pragma unroll
-    for (int i = 0; i < 9; ++i) acc[i] = S(0);
-    for (int k = sm.ubeg[u] + lane; k < sm.ubeg[u + 1]; k += 32) {
+  for (int i = 0; i < 9; ++i) acc[i] = S(0);
+  if (u < nu) {
+    for (int k = sm.ubeg[u] + j; k < sm.ubeg[u + 1]; k += G) {
       const int o = sm.uslot[k];
 #pragma unroll
       for (int i = 0; i < 9; ++i) acc[i] += sm.y[o][i];
     }
+  }
+  for (int o = 1; o < G; o <<= 1) {
 #pragma unroll
-    for (int i = 0; i < 9; ++i) {
+    for (int i = 0; i < 9; ++i) acc[i] += __shfl_xor_sync(0xffffffffu, acc[i], o);
+  }
+  if (u < nu) {
+    S* out = A.part + std::size_t(sm.upart[u]) * 9;
 #pragma unroll
-      for (int off = 16; off > 0; off >>= 1) acc[i] += __shfl_down_sync(0xffffffffu, acc[i], off);
-    }
-    if (lane == 0) {
-      S* out = A.part + std::size_t(sm.upart[u]) * 9;
-#pragma unroll
-      for (int i = 0; i < 9; ++i) out[i] = acc[i];
-    }
+    for (int i = 0; i < 9; ++i)
+      if ((i & (G - 1)) == j) out[i] = acc[i];
   }
 }
 
@@ -138,9 +144,12 @@ __device__ __forceinline__ void stage_meta(const RecMeta& M, DseWork<S>& sm) {
 // Camera-vector gathers of the a-phase: the plain vector x, or the PCG
 // search direction formed on the fly, p = z (first iteration) or
 // z + beta p_prev (dba/solver.hpp:231-236).
+// ready() runs once per tile after the tile's own (constant) loads are in
+// flight and before the first gather; false skips the tile.
 template <class S>
 struct GatherX {
   const S* x;
+  __device__ __forceinline__ bool ready() { return true; }
   __device__ __forceinline__ S operator()(std::int32_t cam, int i) const { return __ldg(x + std::size_t(cam) * 9 + i); }
 };
 // COHERENT loads bypass L1 for vectors written earlier in the same
@@ -152,6 +161,7 @@ struct GatherP {
   const S* p_prev;
   S beta;
   bool first;
+  __device__ __forceinline__ bool ready() { return true; }
   __device__ __forceinline__ S operator()(std::int32_t cam, int i) const {
     const std::size_t k = std::size_t(cam) * 9 + i;
     if (COHERENT) {
@@ -166,7 +176,7 @@ struct GatherP {
 // One 128-slot chunk whose record is at R (global or shared memory);
 // normal tiles only (long tiles return).
 template <class S, int MODE, class G>
-__device__ __forceinline__ void dse_chunk_at(const DseArgs<S>& A, DseWork<S>& sm, const S* R, const G& gx) {
+__device__ __forceinline__ void dse_chunk_at(const DseArgs<S>& A, DseWork<S>& sm, const S* R, G gx) {
   const int tid = threadIdx.x;
   const RecMeta& M = rec_meta(R);
   // Issue every independent load of the tile first: E lanes, header,
@@ -184,6 +194,7 @@ __device__ __forceinline__ void dse_chunk_at(const DseArgs<S>& A, DseWork<S>& sm
   const std::int32_t p0 = hdr.x, np = hdr.y;
   S L[9], wv[3];
   if (tid < np) load_point<S, MODE>(A, p0 + tid, L, wv);
+  if (!gx.ready()) return;
   if (MODE != 2) {
     S a[3] = {S(0), S(0), S(0)};
     if (tid < hdr.z) {
@@ -233,7 +244,8 @@ __global__ void __launch_bounds__(kTile, 5) k_dse_chunk(DseArgs<S> A) {
 
 // One CTA per long tile (a single point observed more than 128 times).
 template <class S, int MODE, class G>
-__device__ __forceinline__ void dse_long(const DseArgs<S>& A, DseWork<S>& sm, std::int32_t li, const G& gx) {
+__device__ __forceinline__ void dse_long(const DseArgs<S>& A, DseWork<S>& sm, std::int32_t li, G gx) {
+  if (!gx.ready()) return;
   const int tid = threadIdx.x;
   const std::int32_t c0 = A.long_chunk[li];
   const RecMeta& M0 = rec_meta(A.rec + std::size_t(c0) * Rec<S>::kLen);

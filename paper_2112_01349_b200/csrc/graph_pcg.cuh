@@ -2,19 +2,21 @@
 //
 // dpcg (dba/solver.hpp:202-257) for a single rank, every recurrence on the
 // device and the loop itself in the graph: one conditional WHILE node whose
-// body is three kernels,
-//   k_g_pass    the fused DSE pass over E (one CTA per chunk, long tiles
-//               first) gathering p formed on the fly from z and the previous
-//               p, writing camera-major partials;
-//   k_g_camera  warp per camera: c = fold(partials) in chunk order, p stored,
-//               q = B_d p - c, the camera's p.q term;
-//   k_g_step    alpha = rho / sum(p.q) (camera order), x += alpha p,
-//               r -= alpha q, z = B^-1 r, rho, |r|^2 and the loop decision
-//               (cudaGraphSetConditional) from a deterministic grid reduction.
+// body is kGraphUnroll copies of three kernels,
+//   k_g_pass  the fused DSE pass over E (one CTA per chunk, long tiles first)
+//             gathering p formed on the fly from z and the previous p,
+//             writing camera-major partials;
+//   k_g_fold  warp per camera: c = fold(partials) in chunk order, p stored,
+//             q = B_d p - c, the camera's p.q term;
+//   k_g_step  alpha = rho / sum(p.q) (camera order), x += alpha p,
+//             r -= alpha q, z = B^-1 r, rho, |r|^2 and the loop decision
+//             (cudaGraphSetConditional) from a deterministic grid reduction.
 // Every 50th iteration the body runs once more as a residual-refresh pass
-// (DSE on x, r = g - S x), selected by a device-side phase flag. One graph
-// launch runs the whole inner solve with no host round trip, no
-// persistent-kernel grid barriers and full-occupancy DSE tiles.
+// (DSE on x, r = g - S x), selected by a device-side phase flag. Unrolling
+// amortises the WHILE node's relaunch; once the loop is decided the copies
+// left in the body return at entry (done flag). One graph launch runs the
+// whole inner solve with no host round trip, no persistent-kernel grid
+// barriers and full-occupancy DSE tiles.
 //
 // Loop control matches the reference: stop when |r| <= tol |g| or
 // n == max_iters; rho (after z = B^-1 r) and p'q breakdowns stop with status
@@ -27,8 +29,30 @@
 
 #include "dse.cuh"
 
+#ifndef DBAG_GRAPH_UNROLL
+#define DBAG_GRAPH_UNROLL 4  // PCG iterations per WHILE-body launch
+#endif
+#ifndef DBAG_PASS_MINB
+#define DBAG_PASS_MINB 5  // resident CTAs per SM the pass is compiled for
+#endif
+
 namespace dbag {
 namespace dev {
+
+#if DBAG_GTIMING  // per-iteration timeline of the graph body (development builds)
+__device__ unsigned long long g_tl[4 * 1024];
+__device__ __forceinline__ void tl_mark(int n, int k) {
+  if (n < 1024) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_tl[n * 4 + k] = t;
+  }
+}
+#define DBAG_TL(n, k, cond) \
+  if (cond) tl_mark(n, k)
+#else
+#define DBAG_TL(n, k, cond)
+#endif
 
 template <class S>
 struct GScal {
@@ -36,6 +60,7 @@ struct GScal {
   S alpha, beta;
   int n, max_iters, status, dse_count;
   int phase;  // 0: PCG pass, 1: residual-refresh pass (DSE on x)
+  int done;   // loop finished: the remaining kernels of an unrolled body return at once
 };
 
 template <class S>
@@ -59,6 +84,45 @@ template <class S>
 __device__ __forceinline__ S* p_cur(const GBufs<S>& B, int n) {
   return (n & 1) ? B.p1 : B.p0;
 }
+
+// Programmatic dependent launch (graph edges of type programmatic): a kernel
+// lets its dependent start launching early, and the dependent waits for the
+// full completion (and memory) of its prerequisite only where it first needs
+// it. Both are no-ops for kernels launched without such an edge.
+__device__ __forceinline__ void pdl_allow_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+// Gather of the graph's DSE pass: the tile's E, metadata and C factors (all
+// constant during the solve) are loaded before waiting on the previous
+// kernel; then p = z + beta p_prev (PCG pass) or x (refresh pass).
+template <class S>
+struct GatherGraph {
+  const GScal<S>* sc;
+  const S* z;
+  const S* x;
+  const S* p0;
+  const S* p1;
+  const S* v;  // x (refresh) or z (PCG), set by ready()
+  const S* pprev;
+  S beta;
+  bool first, pcg;
+  __device__ __forceinline__ bool ready() {
+    pdl_wait();
+    if (sc->done) return false;
+    const int n = sc->n;
+    pcg = sc->phase == 0;
+    beta = sc->beta;
+    first = n == 0;
+    v = pcg ? z : x;
+    pprev = ((n + 1) & 1) ? p1 : p0;
+    return true;
+  }
+  __device__ __forceinline__ S operator()(std::int32_t cam, int i) const {
+    const std::size_t k = std::size_t(cam) * 9 + i;
+    const S a = __ldg(v + k);
+    return (!pcg || first) ? a : a + beta * __ldg(pprev + k);
+  }
+};
 
 // Loop decision after rho / |r|^2 of iteration state n (dba/solver.hpp:223-230).
 template <class S>
@@ -121,7 +185,9 @@ __global__ void __launch_bounds__(kRedThreads) k_g_init(GBufs<S> B, RedWs ws, GS
     sc->beta = S(0);
     sc->phase = 0;
     sc->dse_count = fin[1] != 0.0 ? 1 : 0;  // the reference's DSE on x0 (dba/solver.hpp:217)
-    cudaGraphSetConditional(h_while, fin[1] != 0.0 && continue_loop(sc) ? 1u : 0u);
+    const bool loop = fin[1] != 0.0 && continue_loop(sc);
+    sc->done = loop ? 0 : 1;
+    cudaGraphSetConditional(h_while, loop ? 1u : 0u);
   }
 }
 
@@ -129,12 +195,7 @@ __global__ void __launch_bounds__(kRedThreads) k_g_init(GBufs<S> B, RedWs ws, GS
 // (lanes strided, fixed shuffle tree); v = p = z + beta p_prev (PCG pass,
 // stored as p) or x (refresh pass); q = B_d v - c; the p.q term in double.
 template <class S>
-__global__ void __launch_bounds__(kRedThreads) k_g_camera(GBufs<S> B, const GScal<S>* sc) {
-  const int lane = threadIdx.x & 31;
-  const std::int32_t cam = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  if (cam >= B.m) return;
-  const int n = sc->n;
-  const bool pcg = sc->phase == 0;
+__device__ __forceinline__ void camera_fold(const GBufs<S>& B, std::int32_t cam, int lane, int n, S beta, bool pcg) {
   S acc[9];
 #pragma unroll
   for (int i = 0; i < 9; ++i) acc[i] = S(0);
@@ -154,7 +215,7 @@ __global__ void __launch_bounds__(kRedThreads) k_g_camera(GBufs<S> B, const GSca
   S v;
   if (pcg) {
     const S zr = B.z[at + row];
-    v = n == 0 ? zr : zr + sc->beta * p_cur(B, n + 1)[at + row];
+    v = n == 0 ? zr : zr + beta * p_cur(B, n + 1)[at + row];
     if (lane < 9) p_cur(B, n)[at + row] = v;
   } else {
     v = B.x[at + row];
@@ -178,27 +239,23 @@ __global__ void __launch_bounds__(kRedThreads) k_g_camera(GBufs<S> B, const GSca
 }
 
 // The body's DSE pass: CTAs [0, n_long) take the long tiles, the rest one
-// chunk each; the gathered vector is p formed on the fly from z and the
-// previous p (PCG pass) or x (refresh pass).
+// chunk each (GatherGraph).
 template <class S>
-__global__ void __launch_bounds__(kTile, 5) k_g_pass(DseArgs<S> A, GBufs<S> B, const GScal<S>* sc) {
+__global__ void __launch_bounds__(kTile, DBAG_PASS_MINB) k_g_pass(DseArgs<S> A, GBufs<S> B, const GScal<S>* sc) {
   __shared__ DseWork<S> sm;
-  const int n = sc->n;
-  const S beta = sc->beta;
-  const bool pcg = sc->phase == 0;
+  pdl_allow_dependents();
   const std::int32_t blk = blockIdx.x;
-  if (blk < A.n_long) {
-    if (pcg)
-      dse_long<S, 0>(A, sm, blk, GatherP<S, false>{B.z, p_cur(B, n + 1), beta, n == 0});
-    else
-      dse_long<S, 0>(A, sm, blk, GatherX<S>{B.x});
-    return;
+  const GatherGraph<S> gx{sc, B.z, B.x, B.p0, B.p1, nullptr, nullptr, S(0), false, true};
+#if DBAG_GTIMING
+  if (blk == 0 && threadIdx.x == 0) {
+    pdl_wait();
+    tl_mark(sc->n, 0);
   }
-  const std::int32_t chunk = blk - A.n_long;
-  if (pcg)
-    dse_chunk<S, 0>(A, sm, chunk, GatherP<S, false>{B.z, p_cur(B, n + 1), beta, n == 0});
+#endif
+  if (blk < A.n_long)
+    dse_long<S, 0>(A, sm, blk, gx);
   else
-    dse_chunk<S, 0>(A, sm, chunk, GatherX<S>{B.x});
+    dse_chunk<S, 0>(A, sm, blk - A.n_long, gx);
 }
 
 // Finish of an iteration: rho_prev, rho, |r|^2, n + 1, beta, loop decision.
@@ -210,7 +267,21 @@ __device__ __forceinline__ void finish_iteration(GScal<S>* sc, double rho, doubl
   sc->rnorm2 = rn2;
   sc->n += 1;
   sc->beta = S(rho / sc->rho_prev);
-  cudaGraphSetConditional(h_while, continue_loop(sc) ? 1u : 0u);
+  const bool loop = continue_loop(sc);
+  sc->done = loop ? 0 : 1;
+  cudaGraphSetConditional(h_while, loop ? 1u : 0u);
+}
+
+// Camera fold of the pass: warp per camera (camera_fold).
+template <class S>
+__global__ void __launch_bounds__(kRedThreads) k_g_fold(GBufs<S> B, const GScal<S>* sc) {
+  pdl_allow_dependents();
+  pdl_wait();
+  if (sc->done) return;
+  const int n = sc->n;
+  DBAG_TL(n, 1, blockIdx.x == 0 && threadIdx.x == 0);
+  const std::int32_t cam = std::int32_t((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  if (cam < B.m) camera_fold(B, cam, threadIdx.x & 31, n, sc->beta, sc->phase == 0);
 }
 
 // End of a body pass (dba/solver.hpp:238-254). PCG pass: p'q = sum of the
@@ -225,7 +296,11 @@ __global__ void __launch_bounds__(kRedThreads) k_g_step(GBufs<S> B, RedWs ws, GS
                                                         cudaGraphConditionalHandle h_while) {
   __shared__ double red[32];
   __shared__ double pq_all;
+  pdl_allow_dependents();
+  pdl_wait();
+  if (sc->done) return;
   const int n = sc->n;
+  DBAG_TL(n, 2, blockIdx.x == 0 && threadIdx.x == 0);
   const bool refresh_pass = sc->phase != 0;
   S alpha = S(0);
   double pq = 0.0;
@@ -240,6 +315,7 @@ __global__ void __launch_bounds__(kRedThreads) k_g_step(GBufs<S> B, RedWs ws, GS
         sc->pq = pq;
         sc->status = 2;
         sc->dse_count += 1;
+        sc->done = 1;
         cudaGraphSetConditional(h_while, 0u);
       }
       return;
@@ -271,6 +347,7 @@ __global__ void __launch_bounds__(kRedThreads) k_g_step(GBufs<S> B, RedWs ws, GS
   const double v[2] = {rho, rn};
   __shared__ double fin[2];
   if (grid_reduce<SumOp, 2>(v, ws.partials, ws.counter, fin) && threadIdx.x == 0) {
+    DBAG_TL(n, 3, true);
     sc->dse_count += 1;
     if (!refresh_pass) {
       sc->pq = pq;

@@ -483,6 +483,19 @@ class Rank {
     return n;
   }
 
+  // Kernel node depending on `dep` through a programmatic edge (the
+  // dependent may launch once every CTA of `dep` allowed it, and waits for
+  // dep's completion at its griddepcontrol.wait).
+  static cudaGraphNode_t add_kernel_pdl(cudaGraph_t g, cudaGraphNode_t dep, void* func, int grid, int block,
+                                        void** args) {
+    cudaGraphNode_t n = add_kernel(g, nullptr, func, grid, block, args);
+    cudaGraphEdgeData e{};
+    e.from_port = cudaGraphKernelNodePortProgrammatic;
+    e.type = cudaGraphDependencyTypeProgrammatic;
+    DBAG_CUDA(cudaGraphAddDependencies_v2(g, &dep, &n, &e, 1));
+    return n;
+  }
+
   static cudaGraph_t add_conditional(cudaGraph_t g, const cudaGraphNode_t* dep, cudaGraphConditionalHandle h,
                                      cudaGraphConditionalNodeType type, cudaGraphNode_t* node) {
     cudaGraphNodeParams np{};
@@ -523,14 +536,19 @@ class Rank {
     cudaGraph_t body = add_conditional(g_graph_, &n_init, hw, cudaGraphCondTypeWhile, &n_while);
     const dev::GScal<S>* csc = sc;
     void* a_pass[] = {&A, &B, &csc};
-    cudaGraphNode_t cur = add_kernel(body, nullptr, reinterpret_cast<void*>(dev::k_g_pass<S>), n_long_ + n_chunks_,
-                                     dev::kTile, a_pass);
-    void* a_cam[] = {&B, &csc};
-    const int cam_warp_blocks = static_cast<int>((static_cast<std::int64_t>(m_) * 32 + 255) / 256);
-    cur = add_kernel(body, &cur, reinterpret_cast<void*>(dev::k_g_camera<S>), cam_warp_blocks, dev::kRedThreads,
-                     a_cam);
+    void* a_fold[] = {&B, &csc};
     void* a_step[] = {&B, &ws, &sc, &hw};
-    add_kernel(body, &cur, reinterpret_cast<void*>(dev::k_g_step<S>), cam_lane_blocks, dev::kRedThreads, a_step);
+    const int cam_warp_blocks = static_cast<int>((static_cast<std::int64_t>(m_) * 32 + 255) / 256);
+    cudaGraphNode_t cur = nullptr;
+    for (int u = 0; u < DBAG_GRAPH_UNROLL; ++u) {
+      void* pass = reinterpret_cast<void*>(dev::k_g_pass<S>);
+      cur = u ? add_kernel_pdl(body, cur, pass, n_long_ + n_chunks_, dev::kTile, a_pass)
+              : add_kernel(body, nullptr, pass, n_long_ + n_chunks_, dev::kTile, a_pass);
+      cur = add_kernel_pdl(body, cur, reinterpret_cast<void*>(dev::k_g_fold<S>), cam_warp_blocks, dev::kRedThreads,
+                           a_fold);
+      cur = add_kernel_pdl(body, cur, reinterpret_cast<void*>(dev::k_g_step<S>), cam_lane_blocks, dev::kRedThreads,
+                           a_step);
+    }
     DBAG_CUDA(cudaGraphInstantiate(&g_exec_, g_graph_, 0));
   }
 
@@ -551,8 +569,31 @@ class Rank {
     DBAG_CUDA(cudaMemcpyAsync(gsc_h_, gsc_.get(), sizeof(init), cudaMemcpyDeviceToHost, st_));
     DBAG_CUDA(cudaStreamSynchronize(st_));
     collect_profile();
+#if DBAG_GTIMING
+    {
+      static unsigned long long t[4 * 1024];
+      DBAG_CUDA(cudaMemcpyFromSymbol(t, dev::g_tl, sizeof(t)));
+      const int nn = std::min(gsc_h_->n, 1023);
+      double a = 0, b = 0, c = 0, d = 0;
+      int cnt = 0;
+      for (int k = 1; k + 1 < nn; ++k) {
+        if ((k + 1) % 50 == 0 || k % 50 == 0) continue;
+        a += double(t[k * 4 + 1] - t[k * 4 + 0]);
+        b += double(t[k * 4 + 2] - t[k * 4 + 1]);
+        c += double(t[k * 4 + 3] - t[k * 4 + 2]);
+        d += double(t[(k + 1) * 4 + 0] - t[k * 4 + 3]);
+        ++cnt;
+      }
+      if (cnt)
+        std::fprintf(stderr, "GTIMING n=%d pass %.2f fold %.2f step %.2f loop %.2f us\n", nn, a / cnt / 1e3,
+                     b / cnt / 1e3, c / cnt / 1e3, d / cnt / 1e3);
+    }
+#endif
     const dev::GScal<S> o = *gsc_h_;
-    launches_ += 1 + 3 * static_cast<std::int64_t>(std::max(o.dse_count - 1, 0));  // k_g_init + 3 per body pass
+    // k_g_init + 3 kernels per body pass (the no-op copies of the last
+    // unrolled body launch too)
+    const std::int64_t passes = std::max(o.dse_count - 1, 0);
+    launches_ += 1 + 3 * ((passes + DBAG_GRAPH_UNROLL - 1) / DBAG_GRAPH_UNROLL) * DBAG_GRAPH_UNROLL;
     dse_count_ = o.dse_count;
     dse_launches_ += o.dse_count;
     tally_.block_ops += 2 * static_cast<std::uint64_t>(N_) * static_cast<std::uint64_t>(o.dse_count);
@@ -573,6 +614,10 @@ class Rank {
     const dev::GBufs<S> B = gbufs();
     const dev::GScal<S>* sc = gsc_.get();
     const int grid = n_long_ + n_chunks_;
+    dev::GScal<S> live = *gsc_h_;  // the finished solve's scalars, reopened
+    live.done = 0;
+    *gsc_h_ = live;
+    DBAG_CUDA(cudaMemcpyAsync(gsc_.get(), gsc_h_, sizeof(live), cudaMemcpyHostToDevice, st_));
     cudaEvent_t e0, e1;
     DBAG_CUDA(cudaEventCreate(&e0));
     DBAG_CUDA(cudaEventCreate(&e1));
