@@ -51,6 +51,7 @@ struct DseWork {
   S a[kTile][3];
   S b[kTile][3];
   S y[kTile][9];
+  S xs[kXsCams * 9];  // the chunk's camera vectors, gathered once per distinct camera
   std::int32_t upart[kTile];
   std::uint8_t uslot[kTile];
   std::uint8_t ubeg[kTile + 8];
@@ -99,38 +100,49 @@ __device__ __forceinline__ void load_point(const DseArgs<S>& A, std::int32_t p, 
     for (int j = 0; j < 3; ++j) wv[j] = A.w[std::size_t(p) * 3 + j];
 }
 
-// Folds sm.y per distinct camera of the chunk into the camera-major
-// partials. A chunk holds few cameras with many slots each, so each camera
-// gets a group of G lanes (G = the largest power of two with nu * G <= 128,
-// at most 32; groups never straddle a warp): lane j of the group sums slots
-// j, j + G, ... in slot order, an xor butterfly combines the group (fixed
-// order: deterministic), and the group's lanes share the 9 stores.
-template <class S>
-__device__ __forceinline__ void fold_cameras(const DseArgs<S>& A, DseWork<S>& sm, int nu) {
+// Folds y per distinct camera of the chunk into the camera-major partials
+// with a single warp when nu <= 32: camera u gets G lanes (the largest power
+// of two with nu * G <= 32); lane j of the group sums slots j, j + G, ... of
+// the camera in slot-list order, an xor butterfly over the G lanes combines
+// them (fixed order: deterministic) and the group's lanes share the 9
+// stores. nu > 32: one thread per camera, sequential. Few lanes and few
+// butterfly levels keep the fold's shuffle count small (it dominated the
+// instruction mix with a warp per camera).
+template <class S, class Y>
+__device__ __forceinline__ void fold_cameras(const DseArgs<S>& A, int nu, const std::uint8_t* ubeg,
+                                             const std::uint8_t* uslot, const std::int32_t* upart, const Y& y) {
   const int tid = threadIdx.x;
-  const int G = min(32, 1 << (31 - __clz(kTile / max(nu, 1))));
+  const int G = nu <= 32 ? (1 << (31 - __clz(32 / max(nu, 1)))) : 1;
+  const int nact = nu * G;
+  if ((tid & ~31) >= nact) return;  // the warp has no camera
   const int u = tid / G, j = tid & (G - 1);
   S acc[9];
 #pragma unroll
   for (int i = 0; i < 9; ++i) acc[i] = S(0);
-  if (u < nu) {
-    for (int k = sm.ubeg[u] + j; k < sm.ubeg[u + 1]; k += G) {
-      const int o = sm.uslot[k];
+  if (tid < nact) {
+    for (int k = ubeg[u] + j; k < ubeg[u + 1]; k += G) {
+      const int o = uslot[k];
 #pragma unroll
-      for (int i = 0; i < 9; ++i) acc[i] += sm.y[o][i];
+      for (int i = 0; i < 9; ++i) acc[i] += y(o, i);
     }
   }
-  for (int o = 1; o < G; o <<= 1) {
+  for (int o = 1; o < G; o <<= 1) {  // G > 1 only when nact <= 32: the whole warp is here
 #pragma unroll
     for (int i = 0; i < 9; ++i) acc[i] += __shfl_xor_sync(0xffffffffu, acc[i], o);
   }
-  if (u < nu) {
-    S* out = A.part + std::size_t(sm.upart[u]) * 9;
+  if (tid < nact) {
+    S* out = A.part + std::size_t(upart[u]) * 9;
 #pragma unroll
     for (int i = 0; i < 9; ++i)
       if ((i & (G - 1)) == j) out[i] = acc[i];
   }
 }
+
+template <class S>
+struct YRows {  // y[slot][9] rows (DseWork)
+  const S (*y)[9];
+  __device__ __forceinline__ S operator()(int o, int i) const { return y[o][i]; }
+};
 
 template <class S>
 __device__ __forceinline__ void stage_meta(const RecMeta& M, DseWork<S>& sm) {
@@ -185,7 +197,7 @@ __device__ __forceinline__ void dse_chunk_at(const DseArgs<S>& A, DseWork<S>& sm
 #pragma unroll
   for (int k = 0; k < 27; ++k) e[k] = R[k * kTile + tid];  // padding slots hold zeros
   const int4 hdr = *reinterpret_cast<const int4*>(&M.p0);  // p0, np, nslots, nchunk
-  const std::int32_t cam = M.cam[tid];
+  const int su = M.su[tid];
   const int pti = M.pt[tid];
   const int pb0 = M.pbeg[tid], pb1 = M.pbeg[tid + 1];
   const int nu = M.nu;
@@ -196,11 +208,17 @@ __device__ __forceinline__ void dse_chunk_at(const DseArgs<S>& A, DseWork<S>& sm
   if (tid < np) load_point<S, MODE>(A, p0 + tid, L, wv);
   if (!gx.ready()) return;
   if (MODE != 2) {
+    const bool staged = nu <= kXsCams;
+    if (staged) {  // the chunk's camera vectors, once per (camera, row)
+      for (int t = tid; t < nu * 9; t += kTile) sm.xs[t] = gx(M.ucam[t / 9], t % 9);
+      __syncthreads();
+    }
     S a[3] = {S(0), S(0), S(0)};
     if (tid < hdr.z) {
+      const std::int32_t cam = staged ? 0 : M.cam[tid];
 #pragma unroll
       for (int i = 0; i < 9; ++i) {
-        const S xv = gx(cam, i);
+        const S xv = staged ? sm.xs[su * 9 + i] : gx(cam, i);
         a[0] += e[i * 3 + 0] * xv;
         a[1] += e[i * 3 + 1] * xv;
         a[2] += e[i * 3 + 2] * xv;
@@ -226,7 +244,7 @@ __device__ __forceinline__ void dse_chunk_at(const DseArgs<S>& A, DseWork<S>& sm
 #pragma unroll
     for (int i = 0; i < 9; ++i) sm.y[tid][i] = (e[i * 3] * b0 + e[i * 3 + 1] * b1) + e[i * 3 + 2] * b2;
     __syncthreads();
-    fold_cameras(A, sm, nu);
+    fold_cameras(A, nu, sm.ubeg, sm.uslot, sm.upart, YRows<S>{sm.y});
     __syncthreads();
   }
 }
@@ -294,7 +312,7 @@ __device__ __forceinline__ void dse_long(const DseArgs<S>& A, DseWork<S>& sm, st
         sm.y[tid][i] = (R[(i * 3) * kTile + tid] * b0 + R[(i * 3 + 1) * kTile + tid] * b1) +
                        R[(i * 3 + 2) * kTile + tid] * b2;
       __syncthreads();
-      fold_cameras(A, sm, M.nu);
+      fold_cameras(A, M.nu, sm.ubeg, sm.uslot, sm.upart, YRows<S>{sm.y});
     }
   }
   __syncthreads();

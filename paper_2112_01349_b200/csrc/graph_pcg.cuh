@@ -28,9 +28,10 @@
 #include <cstdint>
 
 #include "dse.cuh"
+#include "pipe.cuh"
 
 #ifndef DBAG_GRAPH_UNROLL
-#define DBAG_GRAPH_UNROLL 4  // PCG iterations per WHILE-body launch
+#define DBAG_GRAPH_UNROLL 8  // PCG iterations per WHILE-body launch (DBAG_UNROLL overrides)
 #endif
 #ifndef DBAG_PASS_MINB
 #define DBAG_PASS_MINB 5  // resident CTAs per SM the pass is compiled for
@@ -40,12 +41,12 @@ namespace dbag {
 namespace dev {
 
 #if DBAG_GTIMING  // per-iteration timeline of the graph body (development builds)
-__device__ unsigned long long g_tl[4 * 1024];
+__device__ unsigned long long g_tl[8 * 1024];
 __device__ __forceinline__ void tl_mark(int n, int k) {
   if (n < 1024) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    g_tl[n * 4 + k] = t;
+    g_tl[n * 8 + k] = t;
   }
 }
 #define DBAG_TL(n, k, cond) \
@@ -121,6 +122,25 @@ struct GatherGraph {
     const std::size_t k = std::size_t(cam) * 9 + i;
     const S a = __ldg(v + k);
     return (!pcg || first) ? a : a + beta * __ldg(pprev + k);
+  }
+};
+
+// GatherGraph split for the pipelined pass (pipe.cuh): load() issues the z
+// (or x) and p_prev loads one chunk ahead, combine() forms p = z + beta p_prev.
+template <class S>
+struct PipeGatherGraph : GatherGraph<S> {
+  struct Raw {
+    S v, pp;
+  };
+  __device__ __forceinline__ Raw load(std::int32_t cam, int i) const {
+    const std::size_t k = std::size_t(cam) * 9 + i;
+    Raw r;
+    r.v = __ldg(this->v + k);
+    r.pp = (!this->pcg || this->first) ? S(0) : __ldg(this->pprev + k);
+    return r;
+  }
+  __device__ __forceinline__ S combine(const Raw& r) const {
+    return (!this->pcg || this->first) ? r.v : r.v + this->beta * r.pp;
   }
 };
 
@@ -258,6 +278,33 @@ __global__ void __launch_bounds__(kTile, DBAG_PASS_MINB) k_g_pass(DseArgs<S> A, 
     dse_chunk<S, 0>(A, sm, blk - A.n_long, gx);
 }
 
+// The body's DSE pass, pipelined (pipe.cuh): persistent CTAs, TMA-fed
+// records, camera gathers and point factors one chunk ahead.
+template <class S>
+__global__ void __launch_bounds__(kTile) k_g_pipe(DseArgs<S> A, GBufs<S> B, const GScal<S>* sc) {
+  extern __shared__ __align__(128) unsigned char pipe_dyn[];
+  PipeSmem<S>& sm = *reinterpret_cast<PipeSmem<S>*>(pipe_dyn);
+  pdl_allow_dependents();
+  PipeGatherGraph<S> gx;
+  gx.sc = sc;
+  gx.z = B.z;
+  gx.x = B.x;
+  gx.p0 = B.p0;
+  gx.p1 = B.p1;
+  gx.v = nullptr;
+  gx.pprev = nullptr;
+  gx.beta = S(0);
+  gx.first = false;
+  gx.pcg = true;
+#if DBAG_GTIMING
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    pdl_wait();
+    tl_mark(sc->n, 0);
+  }
+#endif
+  pipe_pass<S, 0>(A, sm, gx);
+}
+
 // Finish of an iteration: rho_prev, rho, |r|^2, n + 1, beta, loop decision.
 template <class S>
 __device__ __forceinline__ void finish_iteration(GScal<S>* sc, double rho, double rn2,
@@ -350,6 +397,165 @@ __global__ void __launch_bounds__(kRedThreads) k_g_step(GBufs<S> B, RedWs ws, GS
     DBAG_TL(n, 3, true);
     sc->dse_count += 1;
     if (!refresh_pass) {
+      sc->pq = pq;
+      sc->alpha = alpha;
+    }
+    if (hand_over) {
+      sc->phase = 1;
+      cudaGraphSetConditional(h_while, 1u);
+    } else {
+      sc->phase = 0;
+      finish_iteration(sc, fin[0], fin[1], h_while);
+    }
+  }
+}
+
+// Software grid barrier (generation counter). Only for kernels whose CTAs
+// are all co-resident: k_g_fs runs at most one CTA per SM slot it can hold
+// (checked at graph build) and its PDL dependents cannot launch before every
+// one of its CTAs has started.
+__device__ __forceinline__ void grid_barrier(unsigned* count, unsigned* gen) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned g = *reinterpret_cast<volatile unsigned*>(gen);
+    __threadfence();
+    if (atomicAdd(count, 1u) == gridDim.x - 1) {
+      atomicExch(count, 0u);
+      __threadfence();
+      atomicAdd(gen, 1u);
+    } else {
+      while (*reinterpret_cast<volatile unsigned*>(gen) == g) {
+      }
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+// Camera fold + PCG step in one kernel (m <= 8 x grid): one warp per camera,
+// lane = row. The camera's B_d and B^-1 rows and its partial range are
+// constant during the solve and are loaded before waiting on the pass; after
+// it, every vector row the camera needs is loaded in one round trip and
+// stays in registers:
+//   c = fold(partials), v = p = z + beta p_prev (stored) or x (refresh),
+//   q = B_d v - c, p.q -> pq_cam; grid barrier; p'q = sum over cameras (the
+//   same fixed order in every CTA), alpha; x += alpha p; r -= alpha q (or
+//   r = g - q after a refresh pass); z = B^-1 r; rho, |r|^2 -> grid reduce;
+//   the last CTA advances the scalars and sets the WHILE condition.
+// Same arithmetic (and association) as k_g_fold + k_g_step except the final
+// rho / |r|^2 block reductions (one camera per warp here).
+template <class S>
+__global__ void __launch_bounds__(kRedThreads) k_g_fs(GBufs<S> B, RedWs ws, GScal<S>* sc,
+                                                      cudaGraphConditionalHandle h_while, unsigned* bar) {
+  __shared__ double red[32];
+  __shared__ double pq_all;
+  pdl_allow_dependents();
+  const int lane = threadIdx.x & 31;
+  const int row = lane < 9 ? lane : 0;
+  const std::int32_t cam = std::int32_t((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  const bool on = cam < B.m;
+  const std::int32_t c = on ? cam : 0;
+  const std::int32_t k0 = B.cam_part_ptr[c], k1 = on ? B.cam_part_ptr[c + 1] : k0;
+  S bd[9], bi[9];
+#pragma unroll
+  for (int k = 0; k < 9; ++k) {
+    bd[k] = B.Bd[std::size_t(c) * 81 + row * 9 + k];
+    bi[k] = B.Binv[std::size_t(c) * 81 + row * 9 + k];
+  }
+  pdl_wait();
+#if DBAG_GTIMING
+  unsigned long long t_w;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_w));
+#endif
+  const int done = __ldcg(&sc->done), n = __ldcg(&sc->n), phase = __ldcg(&sc->phase);
+  const S beta = __ldcg(&sc->beta);
+  const double rho_cur = __ldcg(&sc->rho);
+  if (done) return;
+#if DBAG_GTIMING
+  if (blockIdx.x == 0 && threadIdx.x == 0 && n < 1024) g_tl[n * 8 + 1] = t_w;
+#endif
+  DBAG_TL(n, 2, blockIdx.x == 0 && threadIdx.x == 0);
+  const bool pcg = phase == 0;
+  const std::size_t at = std::size_t(c) * 9 + row;
+  const S zr = __ldcg(B.z + at), pp = __ldcg(p_cur(B, n + 1) + at), xr = __ldcg(B.x + at);
+  const S rr = __ldcg(B.r + at), gr = __ldcg(B.g + at);
+  S acc[9];
+#pragma unroll
+  for (int i = 0; i < 9; ++i) acc[i] = S(0);
+  for (std::int32_t k = k0 + lane; k < k1; k += 32) {
+    const S* p = B.part + std::size_t(k) * 9;
+#pragma unroll
+    for (int i = 0; i < 9; ++i) acc[i] += __ldcg(p + i);
+  }
+#pragma unroll
+  for (int i = 0; i < 9; ++i) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc[i] += __shfl_down_sync(0xffffffffu, acc[i], o);
+    acc[i] = __shfl_sync(0xffffffffu, acc[i], 0);
+  }
+  S cr = acc[0];
+#pragma unroll
+  for (int i = 1; i < 9; ++i)
+    if (row == i) cr = acc[i];
+  const S v = pcg ? (n == 0 ? zr : zr + beta * pp) : xr;
+  if (pcg && on && lane < 9) p_cur(B, n)[at] = v;
+  S d = S(0);
+#pragma unroll
+  for (int k = 0; k < 9; ++k) d += bd[k] * __shfl_sync(0xffffffffu, v, k);
+  const S qv = d - cr;
+  S alpha = S(0);
+  double pq = 0.0;
+  bool hand_over = false;
+  S ri = S(0);
+  if (pcg) {
+    double t = lane < 9 ? double(v) * double(qv) : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_down_sync(0xffffffffu, t, o);
+    if (lane == 0 && on) B.pq_cam[cam] = t;
+    DBAG_TL(n, 3, blockIdx.x == 0 && threadIdx.x == 0);
+    grid_barrier(bar, bar + 1);
+    DBAG_TL(n, 4, blockIdx.x == 0 && threadIdx.x == 0);
+    for (std::int32_t k = threadIdx.x; k < B.m; k += blockDim.x) pq += __ldcg(B.pq_cam + k);
+    pq = block_reduce<SumOp>(pq, red);
+    if (threadIdx.x == 0) pq_all = pq;
+    __syncthreads();
+    pq = pq_all;
+    DBAG_TL(n, 5, blockIdx.x == 0 && threadIdx.x == 0);
+    if (!(pq > 0.0) || isinf(pq)) {  // p'q breakdown (uniform across the grid)
+      if (blockIdx.x == 0 && threadIdx.x == 0) {
+        sc->pq = pq;
+        sc->status = 2;
+        sc->dse_count += 1;
+        sc->done = 1;
+        cudaGraphSetConditional(h_while, 0u);
+      }
+      return;
+    }
+    alpha = S(rho_cur / pq);
+    hand_over = (n + 1) % 50 == 0;
+    if (on && lane < 9) B.x[at] = xr + alpha * v;
+    if (!hand_over) ri = rr - alpha * qv;
+  } else {
+    ri = gr - qv;
+  }
+  double rho = 0.0, rn = 0.0;
+  if (!hand_over) {
+    S zi = S(0);
+#pragma unroll
+    for (int k = 0; k < 9; ++k) zi += bi[k] * __shfl_sync(0xffffffffu, ri, k);
+    if (on && lane < 9) {
+      B.r[at] = ri;
+      B.z[at] = zi;
+      rho = double(ri) * double(zi);
+      rn = double(ri) * double(ri);
+    }
+  }
+  const double vv[2] = {rho, rn};
+  __shared__ double fin[2];
+  if (grid_reduce<SumOp, 2>(vv, ws.partials, ws.counter, fin) && threadIdx.x == 0) {
+    DBAG_TL(n, 6, true);
+    sc->dse_count += 1;
+    if (pcg) {
       sc->pq = pq;
       sc->alpha = alpha;
     }

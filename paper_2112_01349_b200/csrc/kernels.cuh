@@ -28,6 +28,7 @@ namespace dev {
 constexpr int kTile = 128;        // point-pass tile (slots) == block size
 constexpr int kRedThreads = 256;  // reduction kernels' block size
 constexpr int kRedBlocksMax = 592;  // 4 x 148 SMs
+constexpr int kXsCams = 32;  // distinct cameras of a chunk whose vectors are gathered once into shared memory
 
 // Static per-chunk metadata stored after the E lanes of its record, so one
 // coalesced read of a record brings every index a tile needs (no pointer
@@ -37,10 +38,12 @@ struct RecMeta {
   std::int32_t nu, ci, pad0, pad1;      // distinct cameras; chunk index inside its tile
   std::int32_t cam[kTile];              // camera of each slot (padding: 0)
   std::int32_t upart[kTile];            // camera-major partial position of each distinct camera
+  std::int32_t ucam[kXsCams];           // camera id of distinct camera u < kXsCams
   std::uint8_t pt[kTile];               // slot -> point index in the tile
   std::uint8_t uslot[kTile];            // slots grouped by camera
   std::uint8_t ubeg[kTile + 8];         // camera u's slots: uslot[ubeg[u] .. ubeg[u+1])
   std::uint8_t pbeg[kTile + 8];         // point i's slots: [pbeg[i], pbeg[i+1])
+  std::uint8_t su[kTile];               // slot -> its distinct camera u (inverse of uslot / ubeg)
 };
 static_assert(sizeof(RecMeta) % 16 == 0, "record metadata must keep 16-byte alignment");
 

@@ -471,12 +471,12 @@ class Rank {
   }
 
   static cudaGraphNode_t add_kernel(cudaGraph_t g, const cudaGraphNode_t* dep, void* func, int grid, int block,
-                                    void** args) {
+                                    void** args, int smem = 0) {
     cudaKernelNodeParams kp{};
     kp.func = func;
     kp.gridDim = dim3(static_cast<unsigned>(std::max(grid, 1)));
     kp.blockDim = dim3(static_cast<unsigned>(block));
-    kp.sharedMemBytes = 0;
+    kp.sharedMemBytes = static_cast<unsigned>(smem);
     kp.kernelParams = args;
     cudaGraphNode_t n;
     DBAG_CUDA(cudaGraphAddKernelNode(&n, g, dep, dep ? 1 : 0, &kp));
@@ -487,8 +487,8 @@ class Rank {
   // dependent may launch once every CTA of `dep` allowed it, and waits for
   // dep's completion at its griddepcontrol.wait).
   static cudaGraphNode_t add_kernel_pdl(cudaGraph_t g, cudaGraphNode_t dep, void* func, int grid, int block,
-                                        void** args) {
-    cudaGraphNode_t n = add_kernel(g, nullptr, func, grid, block, args);
+                                        void** args, int smem = 0) {
+    cudaGraphNode_t n = add_kernel(g, nullptr, func, grid, block, args, smem);
     cudaGraphEdgeData e{};
     e.from_port = cudaGraphKernelNodePortProgrammatic;
     e.type = cudaGraphDependencyTypeProgrammatic;
@@ -516,6 +516,7 @@ class Rank {
 
   void build_graph() {
     destroy_graph();
+    pipe_grid();
     if (!gsc_.get()) {
       gsc_.alloc(1);
       DBAG_CUDA(cudaMallocHost(&gsc_h_, sizeof(dev::GScal<S>)));
@@ -539,11 +540,32 @@ class Rank {
     void* a_fold[] = {&B, &csc};
     void* a_step[] = {&B, &ws, &sc, &hw};
     const int cam_warp_blocks = static_cast<int>((static_cast<std::int64_t>(m_) * 32 + 255) / 256);
+    // fused fold + step (k_g_fs) when its warp-per-camera grid is co-resident
+    int fs_per_sm = 0, sms = 0;
+    DBAG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&fs_per_sm, dev::k_g_fs<S>, dev::kRedThreads, 0));
+    DBAG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device_));
+    const char* fse = std::getenv("DBAG_FS");
+    g_fused_ = !(fse && std::string(fse) == "0") && cam_warp_blocks <= fs_per_sm * sms &&
+               cam_warp_blocks <= dev::kRedBlocksMax;
+    if (!g_bar_.get()) g_bar_.alloc(2);
+    DBAG_CUDA(cudaMemset(g_bar_.get(), 0, 2 * sizeof(unsigned)));
+    unsigned* bar = g_bar_.get();
+    void* a_fs[] = {&B, &ws, &sc, &hw, &bar};
     cudaGraphNode_t cur = nullptr;
-    for (int u = 0; u < DBAG_GRAPH_UNROLL; ++u) {
-      void* pass = reinterpret_cast<void*>(dev::k_g_pass<S>);
-      cur = u ? add_kernel_pdl(body, cur, pass, n_long_ + n_chunks_, dev::kTile, a_pass)
-              : add_kernel(body, nullptr, pass, n_long_ + n_chunks_, dev::kTile, a_pass);
+    g_unroll_ = DBAG_GRAPH_UNROLL;
+    if (const char* ue = std::getenv("DBAG_UNROLL")) g_unroll_ = std::max(1, std::atoi(ue));
+    for (int u = 0; u < g_unroll_; ++u) {
+      const bool piped = dse_kind() == 0;
+      void* pass = piped ? reinterpret_cast<void*>(dev::k_g_pipe<S>) : reinterpret_cast<void*>(dev::k_g_pass<S>);
+      const int pgrid = piped ? pipe_grid_for_pass() : n_long_ + n_chunks_;
+      const int psmem = piped ? static_cast<int>(sizeof(dev::PipeSmem<S>)) : 0;
+      cur = u ? add_kernel_pdl(body, cur, pass, pgrid, dev::kTile, a_pass, psmem)
+              : add_kernel(body, nullptr, pass, pgrid, dev::kTile, a_pass, psmem);
+      if (g_fused_) {
+        cur = add_kernel_pdl(body, cur, reinterpret_cast<void*>(dev::k_g_fs<S>), cam_warp_blocks, dev::kRedThreads,
+                             a_fs);
+        continue;
+      }
       cur = add_kernel_pdl(body, cur, reinterpret_cast<void*>(dev::k_g_fold<S>), cam_warp_blocks, dev::kRedThreads,
                            a_fold);
       cur = add_kernel_pdl(body, cur, reinterpret_cast<void*>(dev::k_g_step<S>), cam_lane_blocks, dev::kRedThreads,
@@ -571,29 +593,31 @@ class Rank {
     collect_profile();
 #if DBAG_GTIMING
     {
-      static unsigned long long t[4 * 1024];
+      static unsigned long long t[8 * 1024];
       DBAG_CUDA(cudaMemcpyFromSymbol(t, dev::g_tl, sizeof(t)));
       const int nn = std::min(gsc_h_->n, 1023);
-      double a = 0, b = 0, c = 0, d = 0;
+      double acc[8] = {0};
       int cnt = 0;
       for (int k = 1; k + 1 < nn; ++k) {
         if ((k + 1) % 50 == 0 || k % 50 == 0) continue;
-        a += double(t[k * 4 + 1] - t[k * 4 + 0]);
-        b += double(t[k * 4 + 2] - t[k * 4 + 1]);
-        c += double(t[k * 4 + 3] - t[k * 4 + 2]);
-        d += double(t[(k + 1) * 4 + 0] - t[k * 4 + 3]);
+        bool ok = true;
+        for (int q = 0; q < 7; ++q) ok = ok && t[k * 8 + q] != 0;
+        if (!ok) continue;
+        for (int q = 0; q < 6; ++q) acc[q] += double(t[k * 8 + q + 1]) - double(t[k * 8 + q]);
+        acc[6] += double(t[(k + 1) * 8]) - double(t[k * 8 + 6]);
         ++cnt;
       }
       if (cnt)
-        std::fprintf(stderr, "GTIMING n=%d pass %.2f fold %.2f step %.2f loop %.2f us\n", nn, a / cnt / 1e3,
-                     b / cnt / 1e3, c / cnt / 1e3, d / cnt / 1e3);
+        std::fprintf(stderr, "GTIMING n=%d marks(us): pass->fs %.2f sc %.2f fold %.2f barrier %.2f pqsum %.2f step %.2f loop %.2f\n",
+                     nn, acc[0] / cnt / 1e3, acc[1] / cnt / 1e3, acc[2] / cnt / 1e3, acc[3] / cnt / 1e3, acc[4] / cnt / 1e3,
+                     acc[5] / cnt / 1e3, acc[6] / cnt / 1e3);
     }
 #endif
     const dev::GScal<S> o = *gsc_h_;
     // k_g_init + 3 kernels per body pass (the no-op copies of the last
     // unrolled body launch too)
     const std::int64_t passes = std::max(o.dse_count - 1, 0);
-    launches_ += 1 + 3 * ((passes + DBAG_GRAPH_UNROLL - 1) / DBAG_GRAPH_UNROLL) * DBAG_GRAPH_UNROLL;
+    launches_ += 1 + (g_fused_ ? 2 : 3) * ((passes + g_unroll_ - 1) / g_unroll_) * g_unroll_;
     dse_count_ = o.dse_count;
     dse_launches_ += o.dse_count;
     tally_.block_ops += 2 * static_cast<std::uint64_t>(N_) * static_cast<std::uint64_t>(o.dse_count);
@@ -621,9 +645,18 @@ class Rank {
     cudaEvent_t e0, e1;
     DBAG_CUDA(cudaEventCreate(&e0));
     DBAG_CUDA(cudaEventCreate(&e1));
-    launch(dev::k_g_pass<S>, grid, dev::kTile, A, B, sc);  // warm-up
+    auto one = [&] {
+      if (dse_kind() == 0) {
+        dev::k_g_pipe<S><<<pipe_grid_for_pass(), dev::kTile, sizeof(dev::PipeSmem<S>), st_>>>(A, B, sc);
+        DBAG_LAUNCH_CHECK();
+        ++launches_;
+      } else {
+        launch(dev::k_g_pass<S>, grid, dev::kTile, A, B, sc);
+      }
+    };
+    one();  // warm-up
     DBAG_CUDA(cudaEventRecord(e0, st_));
-    for (int r = 0; r < reps; ++r) launch(dev::k_g_pass<S>, grid, dev::kTile, A, B, sc);
+    for (int r = 0; r < reps; ++r) one();
     DBAG_CUDA(cudaEventRecord(e1, st_));
     DBAG_CUDA(cudaEventSynchronize(e1));
     float ms = 0.f;
@@ -1016,9 +1049,15 @@ class Rank {
         for (std::int32_t u = u0; u <= u1; ++u) {
           M->ubeg[u - u0] = static_cast<std::uint8_t>(lay_.ucam_ptr[static_cast<std::size_t>(u)] - k0);
           if (u < u1) M->upart[u - u0] = lay_.part_pos[static_cast<std::size_t>(u)];
+          if (u < u1 && u - u0 < dev::kXsCams) M->ucam[u - u0] = lay_.ucam_cam[static_cast<std::size_t>(u)];
         }
-        for (std::int32_t k = k0; k < lay_.ucam_ptr[static_cast<std::size_t>(u1)]; ++k)
-          M->uslot[k - k0] = static_cast<std::uint8_t>(lay_.ucam_slot[static_cast<std::size_t>(k)]);
+        for (std::int32_t u = u0; u < u1; ++u)
+          for (std::int32_t k = lay_.ucam_ptr[static_cast<std::size_t>(u)]; k < lay_.ucam_ptr[static_cast<std::size_t>(u) + 1];
+               ++k) {
+            const std::int32_t sl = lay_.ucam_slot[static_cast<std::size_t>(k)];
+            M->uslot[k - k0] = static_cast<std::uint8_t>(sl);
+            M->su[sl] = static_cast<std::uint8_t>(u - u0);
+          }
       }
     }
     E_.upload(recs);
@@ -1046,12 +1085,39 @@ class Rank {
     return a;
   }
 
+  // Grid of the pipelined DSE pass (pipe.cuh): resident CTAs per SM x SMs.
+  int pipe_grid() {
+    if (pipe_grid_ > 0) return pipe_grid_;
+    const int dyn = static_cast<int>(sizeof(dev::PipeSmem<S>));
+    auto attrs = [&](const void* k) {
+      DBAG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn));
+      DBAG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    };
+    attrs(reinterpret_cast<const void*>(dev::k_dse_pipe<S, 0>));
+    attrs(reinterpret_cast<const void*>(dev::k_dse_pipe<S, 1>));
+    attrs(reinterpret_cast<const void*>(dev::k_dse_pipe<S, 2>));
+    attrs(reinterpret_cast<const void*>(dev::k_g_pipe<S>));
+    int per_sm = 0, sms = 0;
+    DBAG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dev::k_g_pipe<S>, dev::kTile, dyn));
+    DBAG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device_));
+    pipe_grid_ = std::max(1, std::max(per_sm, 1) * sms);
+    if (std::getenv("DBAG_VERBOSE"))
+      std::fprintf(stderr, "dbag: pipelined DSE pass: %d CTAs/SM x %d SMs, %d B shared per CTA\n", per_sm, sms, dyn);
+    return pipe_grid_;
+  }
+  int pipe_grid_for_pass() { return std::max(1, std::min(pipe_grid(), std::max(n_chunks_, n_long_))); }
+
   template <int MODE>
   void stream_pass(const S* x) {
     if (n_chunks_ == 0) return;
     const dev::DseArgs<S> a = dse_args(x);
     persistent_grid();
-    if (use_tma_) {
+    if (dse_kind() == 0) {
+      const int grid = pipe_grid_for_pass();
+      dev::k_dse_pipe<S, MODE><<<grid, dev::kTile, sizeof(dev::PipeSmem<S>), st_>>>(a);
+      DBAG_LAUNCH_CHECK();
+      ++launches_;
+    } else if (use_tma_) {
       if (stream_grid_ < 0) {
         int per_sm = 0, sms = 0;
         const int dyn = static_cast<int>(sizeof(dev::DseStages<S>));
@@ -1183,11 +1249,20 @@ class Rank {
   DevBuf<dev::PcgDevOut> pcg_out_;
   DevBuf<dev::GScal<S>> gsc_;
   DevBuf<double> g_pq_cam_;
+  DevBuf<unsigned> g_bar_;  // k_g_fs grid barrier (count, generation)
+  bool g_fused_ = false;
+  int g_unroll_ = DBAG_GRAPH_UNROLL;
   dev::GScal<S>* gsc_h_ = nullptr;
   cudaGraph_t g_graph_ = nullptr;
   cudaGraphExec_t g_exec_ = nullptr;
   dev::PcgDevOut* pcg_out_h_ = nullptr;
-  int pcg_grid_ = -1, stream_grid_ = -1;
+  int pcg_grid_ = -1, stream_grid_ = -1, pipe_grid_ = -1;
+  // DBAG_DSE: direct (default; k_dse_chunk / k_g_pass) | pipe (pipe.cuh) | tma (k_dse_stream)
+  static int dse_kind() {
+    const char* d = std::getenv("DBAG_DSE");
+    if (!d || std::string(d) == "direct") return 2;
+    return std::string(d) == "tma" ? 1 : 0;
+  }
   bool use_tma_ = true;
   DevBuf<S> Jb_, E_, part_, halo_buf_;
   DevBuf<Scal> sc_;
