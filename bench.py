@@ -176,10 +176,10 @@ def dse_roofline(ctx, prof, b_dse, peak, steps, total_ms, world):
     the timed steps left (its in-graph launches cannot carry events);
     in_graph_ms_per_dse is the whole DPCG graph's device time per DSE
     (pass + camera fold + step + loop overhead). Several ranks: the
-    host-driven loop's DSE launches (k_dse_stream), event-timed in place."""
+    host-driven loop's DSE launches (k_dse_chunk), event-timed in place."""
     dse_per_step = prof["dse_launches"] / max(steps, 1)
     loop_ms_per_dse = prof["dse_ms"] / max(prof["dse_launches"], 1)
-    per, kernel = loop_ms_per_dse, "k_dse_stream (TMA DSE pass, host-driven DPCG)"
+    per, kernel = loop_ms_per_dse, "k_dse_chunk (DSE pass, host-driven DPCG)"
     if world == 1:
         try:
             per = ctx.time_dse_pass(20)

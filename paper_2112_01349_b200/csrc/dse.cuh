@@ -26,7 +26,6 @@
 #include <cstdint>
 
 #include "kernels.cuh"
-#include "tma.cuh"
 
 namespace dbag {
 namespace dev {
@@ -164,27 +163,6 @@ struct GatherX {
   __device__ __forceinline__ bool ready() { return true; }
   __device__ __forceinline__ S operator()(std::int32_t cam, int i) const { return __ldg(x + std::size_t(cam) * 9 + i); }
 };
-// COHERENT loads bypass L1 for vectors written earlier in the same
-// (persistent) launch; otherwise the gathers go through L1, where a tile's
-// repeated cameras hit.
-template <class S, bool COHERENT = true>
-struct GatherP {
-  const S* z;
-  const S* p_prev;
-  S beta;
-  bool first;
-  __device__ __forceinline__ bool ready() { return true; }
-  __device__ __forceinline__ S operator()(std::int32_t cam, int i) const {
-    const std::size_t k = std::size_t(cam) * 9 + i;
-    if (COHERENT) {
-      const S zv = __ldcg(z + k);
-      return first ? zv : zv + beta * __ldcg(p_prev + k);
-    }
-    const S zv = __ldg(z + k);
-    return first ? zv : zv + beta * __ldg(p_prev + k);
-  }
-};
-
 // One 128-slot chunk whose record is at R (global or shared memory);
 // normal tiles only (long tiles return).
 template <class S, int MODE, class G>
@@ -322,66 +300,6 @@ template <class S, int MODE>
 __global__ void __launch_bounds__(kTile) k_dse_long(DseArgs<S> A) {
   __shared__ DseWork<S> sm;
   dse_long<S, MODE>(A, sm, blockIdx.x, GatherX<S>{A.x});
-}
-
-// ---- TMA-pipelined persistent variant ------------------------------------
-// Persistent CTAs walk chunks c = blockIdx.x, + gridDim.x, ...; one elected
-// thread has the TMA engine (cp.async.bulk + mbarrier complete_tx) bring the
-// next chunk's record into the other shared-memory stage while the CTA
-// computes the current one, so the HBM stream never waits on the compute
-// phases of a tile. The E chunk records are read-only during a solve.
-template <class S>
-struct DseStages {
-  S rec[2][Rec<S>::kLen];
-  alignas(8) std::uint64_t bar[2];
-};
-
-template <class S>
-__device__ __forceinline__ void stages_init(DseStages<S>& st) {
-  if (threadIdx.x == 0) {
-    mbar_init(&st.bar[0], 1);
-    mbar_init(&st.bar[1], 1);
-    fence_mbar_init();
-  }
-  __syncthreads();
-}
-
-template <class S>
-__device__ __forceinline__ void stage_issue(const DseArgs<S>& A, DseStages<S>& st, std::int32_t c, int k) {
-  mbar_arrive_expect_tx(&st.bar[k], std::uint32_t(Rec<S>::kBytes));
-  bulk_g2s(st.rec[k], A.rec + std::size_t(c) * Rec<S>::kLen, std::uint32_t(Rec<S>::kBytes), &st.bar[k]);
-}
-
-// All chunks of this CTA, pipelined; `parity` carries the stage barriers'
-// phase bits across passes.
-template <class S, int MODE, class G>
-__device__ __forceinline__ void dse_stream_pass(const DseArgs<S>& A, DseWork<S>& sm, DseStages<S>& st,
-                                                unsigned& parity, const G& gx) {
-  const std::int32_t first = blockIdx.x, stride = gridDim.x;
-  if (first < A.n_chunks) {
-    __syncthreads();
-    if (threadIdx.x == 0) stage_issue(A, st, first, 0);
-    int k = 0;
-    for (std::int32_t c = first; c < A.n_chunks; c += stride) {
-      __syncthreads();  // stage k ^ 1 is free: its chunk is done
-      if (threadIdx.x == 0 && c + stride < A.n_chunks) stage_issue(A, st, c + stride, k ^ 1);
-      mbar_wait(&st.bar[k], (parity >> k) & 1u);
-      parity ^= 1u << k;
-      dse_chunk_at<S, MODE>(A, sm, st.rec[k], gx);
-      k ^= 1;
-    }
-  }
-  for (std::int32_t l = first; l < A.n_long; l += stride) dse_long<S, MODE>(A, sm, l, gx);
-}
-
-template <class S, int MODE>
-__global__ void __launch_bounds__(kTile) k_dse_stream(DseArgs<S> A) {
-  __shared__ DseWork<S> sm;
-  extern __shared__ __align__(128) unsigned char dse_dyn[];
-  DseStages<S>& st = *reinterpret_cast<DseStages<S>*>(dse_dyn);
-  stages_init(st);
-  unsigned parity = 0;
-  dse_stream_pass<S, MODE>(A, sm, st, parity, GatherX<S>{A.x});
 }
 
 }  // namespace dev

@@ -25,6 +25,7 @@
 #include <cstdint>
 
 #include "dse.cuh"
+#include "tma.cuh"
 
 namespace dbag {
 namespace dev {

@@ -32,7 +32,6 @@
 #include "common.hpp"
 #include "dse.cuh"
 #include "graph_pcg.cuh"
-#include "pcg.cuh"
 #include "kernels.cuh"
 #include "partition.hpp"
 
@@ -114,7 +113,6 @@ class Rank {
     cudaEventDestroy(mark_[1]);
     cudaFreeHost(hsc_);
     cudaFreeHost(hbuf_);
-    if (pcg_out_h_) cudaFreeHost(pcg_out_h_);
     if (gsc_h_) cudaFreeHost(gsc_h_);
     destroy_graph();
     cudaStreamDestroy(st_);
@@ -393,7 +391,6 @@ class Rank {
       const char* mode = std::getenv("DBAG_PCG");
       const std::string m = mode ? mode : "graph";
       if (m == "graph" && n_chunks_ > 0 && m_ > 0) return pcg_graph(tol, max_iters);
-      if (m == "persistent" && persistent_grid() > 0) return pcg_persistent(tol, max_iters);
     }
     S* x = dxc_.get();
     const std::int64_t len = static_cast<std::int64_t>(m_) * 9;
@@ -666,84 +663,6 @@ class Rank {
     return static_cast<double>(ms) / std::max(reps, 1);
   }
 
-
-  // Grid of the cooperative PCG kernel (0: unavailable -> host-driven loop).
-  // DBAG_PCG=host forces the host-driven loop; DBAG_DSE=direct|tma picks the
-  // DSE streaming variant (TMA-pipelined by default).
-  int persistent_grid() {
-    if (pcg_grid_ >= 0) return pcg_grid_;
-    const char* mode = std::getenv("DBAG_PCG");
-    const char* dse = std::getenv("DBAG_DSE");
-    use_tma_ = !(dse && std::string(dse) == "direct");
-    pcg_grid_ = 0;
-    if (mode && std::string(mode) == "host") return pcg_grid_;
-    int coop = 0, per_sm = 0, sms = 0;
-    DBAG_CUDA(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, device_));
-    DBAG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device_));
-    const int dyn = use_tma_ ? static_cast<int>(sizeof(dev::DseStages<S>)) : 0;
-    auto k = use_tma_ ? dev::k_pcg_persistent<S, true> : dev::k_pcg_persistent<S, false>;
-    DBAG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn));
-    DBAG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, dev::kTile, dyn));
-    if (!coop || per_sm < 1) return pcg_grid_;
-    pcg_grid_ = per_sm * sms;
-    pcg_part_.alloc(static_cast<std::size_t>(pcg_grid_) * 4);
-    pcg_bar_.alloc(2);
-    pcg_out_.alloc(1);
-    DBAG_CUDA(cudaMallocHost(&pcg_out_h_, sizeof(dev::PcgDevOut)));
-    return pcg_grid_;
-  }
-
-  // dpcg in one cooperative launch (pcg.cuh); same results, tallies and
-  // breakdown semantics as the host-driven loop below.
-  PcgOut pcg_persistent(double tol, int max_iters) {
-    dev::PcgPArgs<S> P;
-    P.dse = dse_args(nullptr);
-    P.m = m_;
-    P.cam_part_ptr = cam_part_ptr_.get();
-    P.Bd = Bd_.get();
-    P.Binv = Bexp_.get();
-    P.g = g_.get();
-    P.x = dxc_.get();
-    P.r = r_.get();
-    P.z = z_.get();
-    P.pa = p_.get();
-    P.pb = p2_.get();
-    P.q = q_.get();
-    P.tol = tol;
-    P.max_iters = max_iters;
-    P.bpart = pcg_part_.get();
-    P.bar = pcg_bar_.get();
-    P.out = pcg_out_.get();
-    DBAG_CUDA(cudaMemsetAsync(pcg_bar_.get(), 0, 2 * sizeof(unsigned), st_));
-    const bool prof = profiling_;
-    if (prof) DBAG_CUDA(cudaEventRecord(prof_event(), st_));
-    void* args[] = {&P};
-    if (use_tma_)
-      DBAG_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(dev::k_pcg_persistent<S, true>),
-                                            dim3(pcg_grid_), dim3(dev::kTile), args, sizeof(dev::DseStages<S>), st_));
-    else
-      DBAG_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(dev::k_pcg_persistent<S, false>),
-                                            dim3(pcg_grid_), dim3(dev::kTile), args, 0, st_));
-    ++launches_;
-    if (prof) {
-      DBAG_CUDA(cudaEventRecord(prof_event(), st_));
-      DBAG_CUDA(cudaEventRecord(prof_event(), st_));
-    }
-    DBAG_CUDA(cudaMemcpyAsync(pcg_out_h_, pcg_out_.get(), sizeof(dev::PcgDevOut), cudaMemcpyDeviceToHost, st_));
-    DBAG_CUDA(cudaStreamSynchronize(st_));
-    collect_profile();
-    const dev::PcgDevOut o = *pcg_out_h_;
-    dse_count_ = o.dse_count;
-    dse_launches_ += o.dse_count;
-    tally_.block_ops += 2 * static_cast<std::uint64_t>(N_) * static_cast<std::uint64_t>(o.dse_count);
-    if (o.status == 1)
-      throw Error(DBAG_PCG_BREAKDOWN, "preconditioned residual norm rho = " + std::to_string(o.rho) +
-                                          " at iteration " + std::to_string(o.iterations));
-    if (o.status == 2)
-      throw Error(DBAG_PCG_BREAKDOWN, "operator lost positive definiteness (p'q = " + std::to_string(o.pq) +
-                                          ") at iteration " + std::to_string(o.iterations));
-    return {o.iterations, o.converged != 0};
-  }
 
   // ------------------------------------------- back-substitution + trial ----
   void backsub_trial() {
@@ -1111,23 +1030,8 @@ class Rank {
   void stream_pass(const S* x) {
     if (n_chunks_ == 0) return;
     const dev::DseArgs<S> a = dse_args(x);
-    persistent_grid();
     if (dse_kind() == 0) {
-      const int grid = pipe_grid_for_pass();
-      dev::k_dse_pipe<S, MODE><<<grid, dev::kTile, sizeof(dev::PipeSmem<S>), st_>>>(a);
-      DBAG_LAUNCH_CHECK();
-      ++launches_;
-    } else if (use_tma_) {
-      if (stream_grid_ < 0) {
-        int per_sm = 0, sms = 0;
-        const int dyn = static_cast<int>(sizeof(dev::DseStages<S>));
-        for (auto k : {dev::k_dse_stream<S, 0>, dev::k_dse_stream<S, 1>, dev::k_dse_stream<S, 2>})
-          DBAG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn));
-        DBAG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dev::k_dse_stream<S, 0>, dev::kTile, dyn));
-        DBAG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device_));
-        stream_grid_ = std::max(1, std::min(n_chunks_ + n_long_, std::max(per_sm, 1) * sms));
-      }
-      dev::k_dse_stream<S, MODE><<<stream_grid_, dev::kTile, sizeof(dev::DseStages<S>), st_>>>(a);
+      dev::k_dse_pipe<S, MODE><<<pipe_grid_for_pass(), dev::kTile, sizeof(dev::PipeSmem<S>), st_>>>(a);
       DBAG_LAUNCH_CHECK();
       ++launches_;
     } else {
@@ -1244,9 +1148,6 @@ class Rank {
   DevBuf<S> xc_, xct_, dxc_, v_, g_, r_, z_, p_, q_, ctmp_;
   DevBuf<S> xp_, xpt_, dxp_, w_;
   DevBuf<S> B_, Bd_, Binv_, Bexp_, C_, Cd_, Cinv_, p2_;
-  DevBuf<double> pcg_part_;
-  DevBuf<unsigned> pcg_bar_;
-  DevBuf<dev::PcgDevOut> pcg_out_;
   DevBuf<dev::GScal<S>> gsc_;
   DevBuf<double> g_pq_cam_;
   DevBuf<unsigned> g_bar_;  // k_g_fs grid barrier (count, generation)
@@ -1255,15 +1156,12 @@ class Rank {
   dev::GScal<S>* gsc_h_ = nullptr;
   cudaGraph_t g_graph_ = nullptr;
   cudaGraphExec_t g_exec_ = nullptr;
-  dev::PcgDevOut* pcg_out_h_ = nullptr;
-  int pcg_grid_ = -1, stream_grid_ = -1, pipe_grid_ = -1;
-  // DBAG_DSE: direct (default; k_dse_chunk / k_g_pass) | pipe (pipe.cuh) | tma (k_dse_stream)
+  int pipe_grid_ = -1;
+  // DBAG_DSE: direct (default; k_dse_chunk / k_g_pass) | pipe (pipe.cuh)
   static int dse_kind() {
     const char* d = std::getenv("DBAG_DSE");
-    if (!d || std::string(d) == "direct") return 2;
-    return std::string(d) == "tma" ? 1 : 0;
+    return d && std::string(d) == "pipe" ? 0 : 1;
   }
-  bool use_tma_ = true;
   DevBuf<S> Jb_, E_, part_, halo_buf_;
   DevBuf<Scal> sc_;
   DevBuf<double> red_part_, dsc_, bounce_;
