@@ -410,22 +410,19 @@ __global__ void __launch_bounds__(kRedThreads) k_g_step(GBufs<S> B, RedWs ws, GS
   }
 }
 
-// Software grid barrier (generation counter). Only for kernels whose CTAs
-// are all co-resident: k_g_fs runs at most one CTA per SM slot it can hold
-// (checked at graph build) and its PDL dependents cannot launch before every
-// one of its CTAs has started.
-__device__ __forceinline__ void grid_barrier(unsigned* count, unsigned* gen) {
+// Software grid barrier over co-resident CTAs: one monotonically increasing
+// 64-bit arrival counter (never reset), so a barrier costs one atomic and
+// the polls; the target is the next multiple of gridDim.x. Only for kernels
+// whose CTAs are all co-resident: k_g_fs runs at most as many CTAs as the
+// SMs hold (checked at graph build) and its PDL dependents cannot launch
+// before every one of its CTAs has started.
+__device__ __forceinline__ void grid_barrier(unsigned long long* count) {
   __syncthreads();
   if (threadIdx.x == 0) {
-    const unsigned g = *reinterpret_cast<volatile unsigned*>(gen);
     __threadfence();
-    if (atomicAdd(count, 1u) == gridDim.x - 1) {
-      atomicExch(count, 0u);
-      __threadfence();
-      atomicAdd(gen, 1u);
-    } else {
-      while (*reinterpret_cast<volatile unsigned*>(gen) == g) {
-      }
+    const unsigned long long old = atomicAdd(count, 1ull);
+    const unsigned long long target = (old / gridDim.x + 1) * gridDim.x;
+    while (*reinterpret_cast<volatile unsigned long long*>(count) < target) {
     }
     __threadfence();
   }
@@ -446,7 +443,7 @@ __device__ __forceinline__ void grid_barrier(unsigned* count, unsigned* gen) {
 // rho / |r|^2 block reductions (one camera per warp here).
 template <class S>
 __global__ void __launch_bounds__(kRedThreads) k_g_fs(GBufs<S> B, RedWs ws, GScal<S>* sc,
-                                                      cudaGraphConditionalHandle h_while, unsigned* bar) {
+                                                      cudaGraphConditionalHandle h_while, unsigned long long* bar) {
   __shared__ double red[32];
   __shared__ double pq_all;
   pdl_allow_dependents();
@@ -513,7 +510,7 @@ __global__ void __launch_bounds__(kRedThreads) k_g_fs(GBufs<S> B, RedWs ws, GSca
     for (int o = 16; o > 0; o >>= 1) t += __shfl_down_sync(0xffffffffu, t, o);
     if (lane == 0 && on) B.pq_cam[cam] = t;
     DBAG_TL(n, 3, blockIdx.x == 0 && threadIdx.x == 0);
-    grid_barrier(bar, bar + 1);
+    grid_barrier(bar);
     DBAG_TL(n, 4, blockIdx.x == 0 && threadIdx.x == 0);
     for (std::int32_t k = threadIdx.x; k < B.m; k += blockDim.x) pq += __ldcg(B.pq_cam + k);
     pq = block_reduce<SumOp>(pq, red);

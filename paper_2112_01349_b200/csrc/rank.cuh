@@ -544,9 +544,9 @@ class Rank {
     const char* fse = std::getenv("DBAG_FS");
     g_fused_ = !(fse && std::string(fse) == "0") && cam_warp_blocks <= fs_per_sm * sms &&
                cam_warp_blocks <= dev::kRedBlocksMax;
-    if (!g_bar_.get()) g_bar_.alloc(2);
-    DBAG_CUDA(cudaMemset(g_bar_.get(), 0, 2 * sizeof(unsigned)));
-    unsigned* bar = g_bar_.get();
+    if (!g_bar_.get()) g_bar_.alloc(1);
+    DBAG_CUDA(cudaMemset(g_bar_.get(), 0, sizeof(unsigned long long)));
+    unsigned long long* bar = g_bar_.get();
     void* a_fs[] = {&B, &ws, &sc, &hw, &bar};
     cudaGraphNode_t cur = nullptr;
     g_unroll_ = DBAG_GRAPH_UNROLL;
@@ -1150,7 +1150,7 @@ class Rank {
   DevBuf<S> B_, Bd_, Binv_, Bexp_, C_, Cd_, Cinv_, p2_;
   DevBuf<dev::GScal<S>> gsc_;
   DevBuf<double> g_pq_cam_;
-  DevBuf<unsigned> g_bar_;  // k_g_fs grid barrier (count, generation)
+  DevBuf<unsigned long long> g_bar_;  // k_g_fs grid barrier arrivals (monotonic)
   bool g_fused_ = false;
   int g_unroll_ = DBAG_GRAPH_UNROLL;
   dev::GScal<S>* gsc_h_ = nullptr;
