@@ -9,6 +9,7 @@
 //   lm_solve(problem, config)                dba/solver.hpp:523-534
 //   partition_edges(problem, K)              dba/partition.hpp:76-103
 //   generate_synthetic(options)              dba/synthetic.hpp:70-146
+//   parse_bal / serialize_bal                dba/bal_io.hpp:78-209
 //   the exception hierarchy                  dba/errors.hpp:17-84
 // A reference user switches by including this header instead of
 // dba/solver.hpp and linking libdbag.so.
@@ -17,6 +18,9 @@
 #include <array>
 #include <cmath>
 #include <cstdint>
+#include <istream>
+#include <iterator>
+#include <ostream>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -29,6 +33,14 @@ namespace dba {
 class Error : public std::runtime_error {
  public:
   using std::runtime_error::runtime_error;
+};
+class ParseError : public Error {  // message "line L: ..." (dba/errors.hpp:17-26)
+ public:
+  ParseError(const std::string& m, std::int64_t line) : Error(m), line_(line) {}
+  std::int64_t line() const { return line_; }
+
+ private:
+  std::int64_t line_;
 };
 class InvalidArgumentError : public Error {
  public:
@@ -77,6 +89,7 @@ inline void check(int rc) {
     case DBAG_SHAPE: throw ShapeError(msg);
     case DBAG_INVALID_ARGUMENT: throw InvalidArgumentError(msg);
     case DBAG_COLLECTIVE: throw CollectiveError(msg);
+    case DBAG_PARSE: throw ParseError(msg, dbag_last_error_index());
     default: throw Error(msg);
   }
 }
@@ -369,6 +382,83 @@ inline BAProblem<double> generate_synthetic(const SyntheticOptions& o) {
     p.add_edge(ob);
   }
   return p;
+}
+
+// ---- BAL text (dba/bal_io.hpp) ---------------------------------------------
+// parse_bal<Scalar>: reals parsed in double and cast to Scalar, observations
+// with weight 1; ParseError("line L: ...") on malformed text; validate()-style
+// warnings (unreferenced nodes, non-positive focal) appended to `warnings`.
+template <typename Scalar>
+BAProblem<Scalar> parse_bal(std::istream& in, std::vector<std::string>* warnings = nullptr) {
+  const std::string text((std::istreambuf_iterator<char>(in)), std::istreambuf_iterator<char>());
+  dbag_bal* h = nullptr;
+  detail::check(dbag_bal_parse(text.data(), static_cast<std::int64_t>(text.size()), &h));
+  std::int32_t m = 0, n = 0;
+  std::int64_t N = 0;
+  std::vector<double> cams, pts, px, py;
+  std::vector<std::int32_t> cid, pid;
+  try {
+    detail::check(dbag_bal_counts(h, &m, &n, &N));
+    cams.resize(static_cast<std::size_t>(m) * 9);
+    pts.resize(static_cast<std::size_t>(n) * 3);
+    px.resize(static_cast<std::size_t>(N));
+    py.resize(static_cast<std::size_t>(N));
+    cid.resize(static_cast<std::size_t>(N));
+    pid.resize(static_cast<std::size_t>(N));
+    detail::check(dbag_bal_copy(h, cams.data(), pts.data(), cid.data(), pid.data(), px.data(), py.data()));
+  } catch (...) {
+    dbag_bal_free(h);
+    throw;
+  }
+  dbag_bal_free(h);
+  BAProblem<Scalar> p;
+  std::vector<bool> cam_used(static_cast<std::size_t>(m)), pt_used(static_cast<std::size_t>(n));
+  for (std::int32_t i = 0; i < m; ++i) {
+    const double* q = cams.data() + static_cast<std::size_t>(i) * 9;
+    CameraState<Scalar> c;
+    for (int j = 0; j < 3; ++j) c.rotation[j] = static_cast<Scalar>(q[j]);
+    for (int j = 0; j < 3; ++j) c.translation[j] = static_cast<Scalar>(q[3 + j]);
+    c.focal = static_cast<Scalar>(q[6]);
+    c.k1 = static_cast<Scalar>(q[7]);
+    c.k2 = static_cast<Scalar>(q[8]);
+    p.add_node(c);
+  }
+  for (std::int32_t i = 0; i < n; ++i) {
+    PointState<Scalar> ps;
+    for (int j = 0; j < 3; ++j) ps.position[j] = static_cast<Scalar>(pts[static_cast<std::size_t>(i) * 3 + j]);
+    p.add_node(ps);
+  }
+  for (std::int64_t e = 0; e < N; ++e) {
+    Observation<Scalar> o;
+    o.camera_id = cid[static_cast<std::size_t>(e)];
+    o.point_id = pid[static_cast<std::size_t>(e)];
+    o.pixel = {static_cast<Scalar>(px[static_cast<std::size_t>(e)]), static_cast<Scalar>(py[static_cast<std::size_t>(e)])};
+    p.add_edge(o);
+    cam_used[static_cast<std::size_t>(o.camera_id)] = true;
+    pt_used[static_cast<std::size_t>(o.point_id)] = true;
+  }
+  if (warnings) {  // BAProblem::validate (dba/problem.hpp:231-255)
+    for (std::int32_t i = 0; i < m; ++i)
+      if (!cam_used[static_cast<std::size_t>(i)])
+        warnings->push_back("camera " + std::to_string(i) + " is not referenced by any observation");
+    for (std::int32_t i = 0; i < n; ++i)
+      if (!pt_used[static_cast<std::size_t>(i)])
+        warnings->push_back("point " + std::to_string(i) + " is not referenced by any observation");
+    for (std::int32_t i = 0; i < m; ++i)
+      if (!(p.packed_cameras()[static_cast<std::size_t>(i) * 9 + 6] > Scalar(0)))
+        warnings->push_back("camera " + std::to_string(i) + " has non-positive focal length");
+  }
+  return p;
+}
+
+template <typename Scalar>
+void serialize_bal(const BAProblem<Scalar>& problem, std::ostream& out) {
+  const dbag_problem v = problem.c_view();
+  char* text = nullptr;
+  std::int64_t len = 0;
+  detail::check(dbag_bal_format(static_cast<int>(sizeof(Scalar)), &v, &text, &len));
+  out.write(text, static_cast<std::streamsize>(len));
+  dbag_free_text(text);
 }
 
 }  // namespace dba

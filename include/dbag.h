@@ -35,6 +35,7 @@ extern "C" {
 #define DBAG_CUDA_ERROR 7
 #define DBAG_NCCL_ERROR 8
 #define DBAG_INTERNAL 9
+#define DBAG_PARSE 10             /* ParseError(msg, line): line via dbag_last_error_index  errors.hpp:17-26 */
 
 /* ---- problem / config / result ----------------------------------------- */
 
@@ -129,6 +130,23 @@ int dbag_shared_points(const dbag_problem* p, int k, int64_t* n_shared, int32_t*
 int dbag_synthetic_count(const dbag_synthetic_options* o, int64_t* n_obs);
 int dbag_generate_synthetic(const dbag_synthetic_options* o, double* cameras, double* points, int32_t* camera_id,
                             int32_t* point_id, double* pixel_x, double* pixel_y);
+
+/* ---- BAL text: dba::parse_bal / serialize_bal (dba/bal_io.hpp:78-209) ----
+ * dbag_bal_parse scans `len` bytes of BAL text (header, observations,
+ * cameras, points) with the reference's validation and messages; on
+ * malformed input it returns DBAG_PARSE, dbag_last_error() reads
+ * "line L: <msg>" and dbag_last_error_index() the line L. Values are fp64;
+ * callers cast to their Scalar exactly as parse_bal<Scalar> does.
+ * dbag_bal_format emits the same text serialize_bal writes ("%.16e" reals);
+ * free it with dbag_free_text. */
+typedef struct dbag_bal dbag_bal;
+int dbag_bal_parse(const char* text, int64_t len, dbag_bal** out);
+int dbag_bal_counts(const dbag_bal* b, int32_t* num_cameras, int32_t* num_points, int64_t* num_observations);
+int dbag_bal_copy(const dbag_bal* b, double* cameras, double* points, int32_t* camera_id, int32_t* point_id,
+                  double* pixel_x, double* pixel_y);
+int dbag_bal_free(dbag_bal* b);
+int dbag_bal_format(int precision, const dbag_problem* p, char** text, int64_t* len);
+int dbag_free_text(char* text);
 
 /* ---- one-shot solve: dba::lm_solve (dba/solver.hpp:523-534) -------------- */
 

@@ -90,6 +90,12 @@ _SIGS = {
     "dbag_group_operator": (C.c_int, [C.c_int, _P(Problem), C.c_int, C.c_int, f64, C.c_int, vp, vp, vp, C.c_int,
                                       vp, f64, C.c_int, vp, _P(C.c_int), _P(C.c_int)]),
     "dbag_group_allreduce": (C.c_int, [C.c_int, C.c_int, i64, vp]),
+    "dbag_bal_parse": (C.c_int, [C.c_char_p, i64, _P(vp)]),
+    "dbag_bal_counts": (C.c_int, [vp, _P(i32), _P(i32), _P(i64)]),
+    "dbag_bal_copy": (C.c_int, [vp, vp, vp, vp, vp, vp, vp]),
+    "dbag_bal_free": (C.c_int, [vp]),
+    "dbag_bal_format": (C.c_int, [C.c_int, _P(Problem), _P(C.c_void_p), _P(i64)]),
+    "dbag_free_text": (C.c_int, [vp]),
 }
 
 EXPORTED = tuple(_SIGS)

@@ -7,6 +7,8 @@
 #include <cuda_runtime.h>
 #include <nccl.h>
 
+#include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <exception>
 #include <memory>
@@ -16,6 +18,7 @@
 
 #include "comm.hpp"
 #include "common.hpp"
+#include "bal.hpp"
 #include "partition.hpp"
 #include "rank.cuh"
 #include "solver.cuh"
@@ -276,6 +279,74 @@ int dbag_synthetic_count(const dbag_synthetic_options* o, int64_t* n_obs) {
 int dbag_generate_synthetic(const dbag_synthetic_options* o, double* cameras, double* points, int32_t* camera_id,
                             int32_t* point_id, double* pixel_x, double* pixel_y) {
   return guarded([&] { generate_synthetic(*o, cameras, points, camera_id, point_id, pixel_x, pixel_y); });
+}
+
+struct dbag_bal {
+  dbag::BalData d;
+};
+
+int dbag_bal_parse(const char* text, int64_t len, dbag_bal** out) {
+  return guarded([&] {
+    if (!out || (!text && len > 0) || len < 0) throw Error(DBAG_INVALID_ARGUMENT, "dbag_bal_parse: bad arguments");
+    auto b = std::make_unique<dbag_bal>();
+    b->d = dbag::parse_bal_text(text, static_cast<std::size_t>(len));
+    *out = b.release();
+  });
+}
+
+int dbag_bal_counts(const dbag_bal* b, int32_t* m, int32_t* n, int64_t* N) {
+  return guarded([&] {
+    if (!b) throw Error(DBAG_INVALID_ARGUMENT, "dbag_bal_counts: null handle");
+    *m = b->d.m;
+    *n = b->d.n;
+    *N = b->d.N;
+  });
+}
+
+int dbag_bal_copy(const dbag_bal* b, double* cameras, double* points, int32_t* camera_id, int32_t* point_id,
+                  double* pixel_x, double* pixel_y) {
+  return guarded([&] {
+    if (!b) throw Error(DBAG_INVALID_ARGUMENT, "dbag_bal_copy: null handle");
+    const auto& d = b->d;
+    std::copy(d.cameras.begin(), d.cameras.end(), cameras);
+    std::copy(d.points.begin(), d.points.end(), points);
+    std::copy(d.cam.begin(), d.cam.end(), camera_id);
+    std::copy(d.pt.begin(), d.pt.end(), point_id);
+    std::copy(d.px.begin(), d.px.end(), pixel_x);
+    std::copy(d.py.begin(), d.py.end(), pixel_y);
+  });
+}
+
+int dbag_bal_free(dbag_bal* b) {
+  return guarded([&] { delete b; });
+}
+
+int dbag_bal_format(int precision, const dbag_problem* p, char** text, int64_t* len) {
+  return guarded([&] {
+    if (!p || !text || !len) throw Error(DBAG_INVALID_ARGUMENT, "dbag_bal_format: bad arguments");
+    std::string s;
+    if (precision == 8)
+      s = dbag::format_bal(p->num_cameras, p->num_points, p->num_observations, static_cast<const double*>(p->cameras),
+                           static_cast<const double*>(p->points), p->camera_id, p->point_id,
+                           static_cast<const double*>(p->pixel_x), static_cast<const double*>(p->pixel_y));
+    else if (precision == 4)
+      s = dbag::format_bal(p->num_cameras, p->num_points, p->num_observations, static_cast<const float*>(p->cameras),
+                           static_cast<const float*>(p->points), p->camera_id, p->point_id,
+                           static_cast<const float*>(p->pixel_x), static_cast<const float*>(p->pixel_y));
+    else
+      throw Error(DBAG_INVALID_ARGUMENT, "precision must be 4 or 8");
+    char* buf = static_cast<char*>(std::malloc(s.size() + 1));
+    if (!buf) throw Error(DBAG_INTERNAL, "out of host memory");
+    std::memcpy(buf, s.data(), s.size());
+    buf[s.size()] = '\0';
+    *text = buf;
+    *len = static_cast<int64_t>(s.size());
+  });
+}
+
+int dbag_free_text(char* text) {
+  std::free(text);
+  return DBAG_OK;
 }
 
 int dbag_lm_solve(int precision, const dbag_problem* p, const dbag_config* c, const int* devices, int n_devices,

@@ -32,7 +32,11 @@ class Error(RuntimeError):
 
 
 class ParseError(Error):
-    pass
+    """Malformed input text (dba/errors.hpp:17-26); ``line`` is 1-based, 0 if unknown."""
+
+    def __init__(self, msg: str, line: int = 0):
+        super().__init__(msg)
+        self.line = line
 
 
 class InvalidArgumentError(Error):
@@ -82,6 +86,8 @@ def _check(rc: int) -> None:
         raise DegenerateDepthError(msg, idx)
     if rc == 2:
         raise SingularBlockError(msg, idx, int(lib.dbag_last_error_block_size()))
+    if rc == 10:
+        raise ParseError(msg, max(idx, 0))
     raise {3: PcgBreakdownError, 4: ShapeError, 5: InvalidArgumentError, 6: CollectiveError, 7: CudaError,
            8: NcclError}.get(rc, Error)(msg)
 

@@ -4,6 +4,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <sstream>
 
 #include "dba/dba_b200.hpp"
 
@@ -33,6 +34,26 @@ int main(int argc, char** argv) {
     dba::partition_edges(problem, 0);
   } catch (const dba::InvalidArgumentError&) {
     threw = true;
+  }
+  CHECK(threw);
+  // BAL text round trip and the ParseError contract (tests/test_problem.cpp:35-80)
+  std::ostringstream bal;
+  dba::serialize_bal(problem, bal);
+  CHECK(bal.str().substr(0, bal.str().find('\n')) == "20 80 800");
+  std::istringstream back(bal.str());
+  std::vector<std::string> warnings;
+  const auto again = dba::parse_bal<double>(back, &warnings);
+  CHECK(warnings.empty());
+  CHECK(again.num_observations() == 800 && again.packed_cameras() == problem.packed_cameras());
+  std::ostringstream bal2;
+  dba::serialize_bal(again, bal2);
+  CHECK(bal2.str() == bal.str());
+  std::istringstream bad("2 1 1\n5 0 0 0\n");
+  threw = false;
+  try {
+    dba::parse_bal<float>(bad);
+  } catch (const dba::ParseError& e) {
+    threw = e.line() == 2 && std::string(e.what()).find("camera index 5") != std::string::npos;
   }
   CHECK(threw);
   if (gpu) {
