@@ -280,6 +280,7 @@ def run_ours(args):
     }
     if world == 1 and rank == 0 and not args.no_secondary:
         line["secondary"] = secondary(args, flush)
+        line["fp32"] = secondary(args, flush, args.workload, np.float32)
     if world == 1 and rank == 0 and not args.no_cpu:
         line["cpu_baseline"] = cpu_baseline(args, p)
     ctx.close()
@@ -290,13 +291,15 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
-def secondary(args, flush):
-    """The same step on the Venice-shaped problem (inputs larger than L2)."""
+def secondary(args, flush, name=SECONDARY_WORKLOAD, dtype=np.float64):
+    """The same step on another configuration: the Venice-shaped problem
+    (inputs larger than L2), or the headline workload in FP32 (BASELINE.json
+    configs[1] is quoted FP32/FP64)."""
     import paper_2112_01349_b200 as dba
-    name = SECONDARY_WORKLOAD
     m, n, N = WORKLOADS[name]
-    p = make_problem(name)
-    with dba.RankContext(0, 8) as ctx:
+    s = np.dtype(dtype).itemsize
+    p = make_problem(name, dtype)
+    with dba.RankContext(0, s) as ctx:
         ctx.upload(p)
         cfg = dba.SolverConfig()
         for _ in range(2):
@@ -306,14 +309,15 @@ def secondary(args, flush):
         prof = ctx.profile()
         t = sum(ms) / len(ms)
         peak, _ = load_peaks()
-        roof = dse_roofline(ctx, prof, dse_bytes(N, n, m, 8), peak, len(ms), sum(ms), 1)
+        roof = dse_roofline(ctx, prof, dse_bytes(N, n, m, s), peak, len(ms), sum(ms), 1)
     try:
-        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
-            roof["traffic"] = json.load(f).get(name, {}).get("dram_bytes_per_launch")
+        if s == 8:  # the committed captures are FP64
+            with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+                roof["traffic"] = json.load(f).get(name, {}).get("dram_bytes_per_launch")
     except Exception:
         pass
-    return {"workload": name, "ms_per_step": t, "value": N / (t / 1e3), "unit": "edges/s",
-            "pcg_iterations_per_step": pcg, "roofline": roof}
+    return {"workload": name, "dtype": "f64" if s == 8 else "f32", "ms_per_step": t, "value": N / (t / 1e3),
+            "unit": "edges/s", "pcg_iterations_per_step": pcg, "roofline": roof}
 
 
 def cpu_baseline(args, p):
