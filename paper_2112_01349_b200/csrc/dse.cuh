@@ -162,6 +162,12 @@ struct GatherX {
   const S* x;
   __device__ __forceinline__ bool ready() { return true; }
   __device__ __forceinline__ S operator()(std::int32_t cam, int i) const { return __ldg(x + std::size_t(cam) * 9 + i); }
+  // split access: raw() issues the loads, combine() forms the value
+  struct Raw {
+    S v;
+  };
+  __device__ __forceinline__ Raw raw(std::int32_t cam, int i) const { return {__ldg(x + std::size_t(cam) * 9 + i)}; }
+  __device__ __forceinline__ S combine(const Raw& r) const { return r.v; }
 };
 // One 128-slot chunk whose record is at R (global or shared memory);
 // normal tiles only (long tiles return).
@@ -169,11 +175,11 @@ template <class S, int MODE, class G>
 __device__ __forceinline__ void dse_chunk_at(const DseArgs<S>& A, DseWork<S>& sm, const S* R, G gx) {
   const int tid = threadIdx.x;
   const RecMeta& M = rec_meta(R);
-  // Issue every independent load of the tile first: E lanes, header,
-  // metadata; then the loads that depend on them (C factors, x gathers).
-  S e[27];
-#pragma unroll
-  for (int k = 0; k < 27; ++k) e[k] = R[k * kTile + tid];  // padding slots hold zeros
+  // Load order (measured): header and metadata first; then the loads that
+  // depend on them and sit on the tile's critical path (C factors, then the
+  // camera gathers after the producer wait); the 27-lane E stream, needed
+  // only from the a-phase on, is issued behind the gathers so it does not
+  // queue ahead of them.
   const int4 hdr = *reinterpret_cast<const int4*>(&M.p0);  // p0, np, nslots, nchunk
   const int su = M.su[tid];
   const int pti = M.pt[tid];
@@ -185,10 +191,23 @@ __device__ __forceinline__ void dse_chunk_at(const DseArgs<S>& A, DseWork<S>& sm
   S L[9], wv[3];
   if (tid < np) load_point<S, MODE>(A, p0 + tid, L, wv);
   if (!gx.ready()) return;
+  const bool staged = nu <= kXsCams;
+  typename G::Raw graw[3];  // the chunk's camera vectors, once per (camera, row)
+  if (MODE != 2 && staged) {
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      const int t = tid + kTile * j;
+      if (t < nu * 9) graw[j] = gx.raw(M.ucam[t / 9], t - (t / 9) * 9);
+    }
+  }
+  S e[27];
+#pragma unroll
+  for (int k = 0; k < 27; ++k) e[k] = R[k * kTile + tid];  // padding slots hold zeros
   if (MODE != 2) {
-    const bool staged = nu <= kXsCams;
-    if (staged) {  // the chunk's camera vectors, once per (camera, row)
-      for (int t = tid; t < nu * 9; t += kTile) sm.xs[t] = gx(M.ucam[t / 9], t % 9);
+    if (staged) {
+#pragma unroll
+      for (int j = 0; j < 3; ++j)
+        if (tid + kTile * j < nu * 9) sm.xs[tid + kTile * j] = gx.combine(graw[j]);
       __syncthreads();
     }
     S a[3] = {S(0), S(0), S(0)};

@@ -123,6 +123,14 @@ struct GatherGraph {
     const S a = __ldg(v + k);
     return (!pcg || first) ? a : a + beta * __ldg(pprev + k);
   }
+  struct Raw {
+    S v, pp;
+  };
+  __device__ __forceinline__ Raw raw(std::int32_t cam, int i) const {
+    const std::size_t k = std::size_t(cam) * 9 + i;
+    return {__ldg(v + k), (!pcg || first) ? S(0) : __ldg(pprev + k)};
+  }
+  __device__ __forceinline__ S combine(const Raw& r) const { return (!pcg || first) ? r.v : r.v + beta * r.pp; }
 };
 
 // GatherGraph split for the pipelined pass (pipe.cuh): load() issues the z
