@@ -31,7 +31,7 @@
 #include "pipe.cuh"
 
 #ifndef DBAG_GRAPH_UNROLL
-#define DBAG_GRAPH_UNROLL 8  // PCG iterations per WHILE-body launch (DBAG_UNROLL overrides)
+#define DBAG_GRAPH_UNROLL 16  // PCG iterations per WHILE-body launch (DBAG_UNROLL overrides)
 #endif
 #ifndef DBAG_PASS_MINB
 #define DBAG_PASS_MINB 5  // resident CTAs per SM the pass is compiled for
