@@ -196,6 +196,9 @@ void group_operator(const dbag_problem* p, int k, int device, double lambda, int
     }
     if (mode == 0) {
       rk.dse_host(static_cast<const S*>(x), outs[static_cast<std::size_t>(r)].data());
+    } else if (mode >= 2) {  // diagnostics of one LM trial's pieces
+      S* o = outs[static_cast<std::size_t>(r)].data();
+      rk.trial_probe(mode, tol, max_iters, o);
     } else {
       its[static_cast<std::size_t>(r)] =
           rk.dpcg_host(static_cast<const S*>(x), tol, max_iters, outs[static_cast<std::size_t>(r)].data()).iterations;

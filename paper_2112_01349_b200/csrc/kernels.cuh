@@ -532,6 +532,15 @@ __global__ void k_halo_fix(std::int32_t n, const std::int32_t* __restrict__ halo
         (e[(r * 3) * kTile] * b[0] + e[(r * 3 + 1) * kTile] * b[1]) + e[(r * 3 + 2) * kTile] * b[2];
 }
 
+// rows[idx[i]] = 0 for W-wide rows.
+template <class S, int W>
+__global__ void k_zero_rows(std::int32_t n, const std::int32_t* __restrict__ idx, S* __restrict__ rows) {
+  const std::int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+#pragma unroll
+  for (int k = 0; k < W; ++k) rows[std::size_t(idx[i]) * W + k] = S(0);
+}
+
 // c_cam = fold of the camera's partials in chunk order (warp per camera, lanes
 // strided, fixed shuffle tree), then per EPI:
 //   0: out = c (all m cameras written; the all-reduce follows for K > 1)

@@ -852,6 +852,38 @@ class Rank {
     DBAG_CUDA(cudaStreamSynchronize(st_));
   }
 
+  // One trial's intermediate results for the cross-K tests (group_operator
+  // modes): 2 g (rhs), 3 dx_c after DPCG, 4 [cost_new, step_inf, damping
+  // term, dx.v + dx.w], 5 v.
+  void trial_probe(int mode, double tol, int max_iters, S* out) {
+    DBAG_CUDA(cudaSetDevice(device_));
+    const std::size_t len = static_cast<std::size_t>(m_) * 9;
+    if (mode == 5) {
+      DBAG_CUDA(cudaMemcpyAsync(out, v_.get(), sizeof(S) * len, cudaMemcpyDeviceToHost, st_));
+      DBAG_CUDA(cudaStreamSynchronize(st_));
+      return;
+    }
+    rhs();
+    if (mode == 2) {
+      DBAG_CUDA(cudaMemcpyAsync(out, g_.get(), sizeof(S) * len, cudaMemcpyDeviceToHost, st_));
+      DBAG_CUDA(cudaStreamSynchronize(st_));
+      return;
+    }
+    pcg(tol, max_iters);
+    if (mode == 3) {
+      DBAG_CUDA(cudaMemcpyAsync(out, dxc_.get(), sizeof(S) * len, cudaMemcpyDeviceToHost, st_));
+      DBAG_CUDA(cudaStreamSynchronize(st_));
+      return;
+    }
+    backsub_trial();
+    std::int64_t bad = -1;
+    const double c = cost(true, &bad);
+    out[0] = S(c);
+    out[1] = S(step_inf_);
+    out[2] = S(damp_term_);
+    out[3] = S(gv_);
+  }
+
   PcgOut dpcg_host(const S* rhs, double tol, int max_iters, S* x_out) {
     DBAG_CUDA(cudaSetDevice(device_));
     const std::size_t len = static_cast<std::size_t>(m_) * 9;
@@ -922,11 +954,12 @@ class Rank {
                halo_of_.get(), static_cast<const S*>(halo_buf_.get()), static_cast<const S*>(Cinv_.get()),
                static_cast<const S*>(E_.get()), slot_chunk_.get(), chunk_slot_.get(), halo_pos_.get(), part_.get());
     } else if (MODE == 2 && nh > 0) {
-      // rhs: C and w are complete on every rank; halo slots still need
-      // their own partials (they were excluded from the chunk partials only
-      // in MODE 0, so here they duplicate nothing: zero them).
-      DBAG_CUDA(cudaMemsetAsync(part_.get() + static_cast<std::size_t>(n_chunk_part_) * 9, 0,
-                                sizeof(S) * 9 * static_cast<std::size_t>(nh), st_));
+      // rhs: C and w are complete on every rank, so the chunk partials
+      // already hold the halo slots' E_s C^-1 w; the halo slots' own
+      // partials (camera-major positions halo_pos) must add nothing: zero
+      // them (they still hold the last DSE's values).
+      launch(dev::k_zero_rows<S, 9>, grid_for(nh, 128, 1 << 30), 128, nh, static_cast<const std::int32_t*>(halo_pos_.get()),
+             part_.get());
     }
   }
 

@@ -702,7 +702,10 @@ class RankContext:
 def group_operator(problem: BAProblem, k: int, x, mode: int = 0, lam: float = 0.0, policy: int = DAMPING_IDENTITY,
                    blocks=None, tol: float = 1e-12, max_iters: int = 500, device: int = 0):
     """K in-process ranks on one device: mode 0 -> dse(x), mode 1 -> dpcg(rhs=x)
-    on the problem's own damped system, or on fabricated (B, C, E_table)."""
+    on the problem's own damped system, or on fabricated (B, C, E_table);
+    modes 2-5 expose one LM trial's pieces on the problem's system (rank 0's
+    values): 2 the right-hand side g, 3 dx_c after DPCG(tol, max_iters),
+    4 [trial cost, step_inf, damping term, dx.v + dx.w], 5 the gradient v."""
     s = problem.c_struct()
     d = problem.dtype
     x = np.ascontiguousarray(x, d)

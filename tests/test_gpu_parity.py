@@ -224,6 +224,38 @@ def test_lm_trajectory_tight_pcg(k):
     assert max(np.abs(g.x_c - o.x_c).max(), np.abs(g.x_p - o.x_p).max()) / scale < 1e-8
 
 
+@pytest.mark.parametrize("k", [2, 3, 4])
+def test_lm_trajectory_with_shared_points(k):
+    """Count-exact edge totals that split points across shard boundaries
+    (SURVEY.md §8e halo: <= K - 1 shared points, exchanged instead of the
+    reference's full point-space all-reduce). Same protocol as above."""
+    p = ring(40, 400, 8, radius=1.0, noise=0.5, seed=2024, nobs=3197)
+    assert len(dba.shared_points(p, k)) > 0
+    cfg = dba.SolverConfig(max_iterations=6, workers=k, check_rank_identity=True, pcg_tol=1e-12, pcg_max_iters=2000)
+    g = dba.lm_solve(p, cfg)
+    o = O.lm_solve(p, cfg)
+    _compare_histories(g, o, 1e-9)
+    for a, b in zip(g.history, o.history):
+        assert a.worker_edges == b.worker_edges
+
+
+@pytest.mark.parametrize("nobs", [3197, 3203])
+def test_trial_pieces_across_k_with_shared_points(nobs):
+    """One LM trial's pieces on K in-process ranks (group_operator modes 2-5):
+    rhs g, DPCG dx_c, trial cost and model terms equal K = 1 to reassociation
+    level when shard boundaries split points."""
+    p = ring(40, 400, 8, radius=1.0, noise=0.5, seed=2024, nobs=nobs)
+    z = np.zeros(9 * p.num_cameras)
+    base = {m: dba.group_operator(p, 1, z, mode=m, lam=1e-4, policy=1, tol=1e-12, max_iters=2000)[0] for m in (2, 3, 4, 5)}
+    for k in (2, 3, 4):
+        assert len(dba.shared_points(p, k)) > 0
+        for m, tol in ((5, 1e-14), (2, 1e-12), (3, 1e-10), (4, 1e-10)):
+            out, _, ident = dba.group_operator(p, k, z, mode=m, lam=1e-4, policy=1, tol=1e-12, max_iters=2000)
+            assert ident
+            a, b = (out[:4], base[m][:4]) if m == 4 else (out, base[m])
+            assert rel(a, b) < tol, (k, m, rel(a, b))
+
+
 @pytest.mark.parametrize("k", [1, 2])
 def test_lm_trajectory_defaults(k):
     """SolverConfig defaults (pcg_tol 1e-6): same accept/reject sequence; costs
@@ -364,3 +396,37 @@ def test_probe_step_matches_first_iteration():
             cost, it, acc = c.probe_step(cfg.lambda0, cfg)
             assert acc == st.history[0].accepted and it == st.history[0].pcg_iterations
             assert cost == pytest.approx(st.history[0].cost, rel=1e-12)
+
+
+def test_full_size_venice_operator_properties():
+    """venice-1778-shaped instance (5.0 M observations, E 1.2 GB, the bench's
+    HBM-bound secondary): properties that hold at any size, where the oracle
+    would take minutes. The reduced camera operator S of the graph path is
+    symmetric, linear and positive definite; DPCG's answer satisfies the true
+    residual bound; the first LM iteration agrees between K = 1 (graph DPCG)
+    and K = 2 (host-driven DPCG over the in-process group) to the reference's
+    own cross-K noise at pcg_tol 1e-6."""
+    p = dba.generate_synthetic(dba.SyntheticOptions(cameras=1778, points=993923, num_observations=5001946, seed=1,
+                                                    pixel_noise=0.5))
+    m = p.num_cameras
+    rng = np.random.default_rng(5)
+    with dba.RankContext(0, 8) as c:
+        c.upload(p)
+        c.linearize()
+        c.damp_factor(10.0, dba.DAMPING_DIAG_SCALED)  # well conditioned: DPCG converges tightly
+        x, y = rng.standard_normal(9 * m), rng.standard_normal(9 * m)
+        Sx, Sy = c.dse(x), c.dse(y)
+        assert abs(y @ Sx - x @ Sy) <= 1e-12 * np.linalg.norm(y) * np.linalg.norm(Sx)
+        assert rel(c.dse(2.0 * x - 3.0 * y), 2.0 * Sx - 3.0 * Sy) < 1e-12
+        assert x @ Sx > 0 and y @ Sy > 0
+        g = rng.standard_normal(9 * m)
+        sol, it, conv = c.dpcg(g, 1e-10, 2000)
+        assert conv and 0 < it < 2000
+        assert np.linalg.norm(g - c.dse(sol)) <= 1e-8 * np.linalg.norm(g)
+    s1 = dba.lm_solve(p, dba.SolverConfig(max_iterations=1))
+    s2 = dba.lm_solve(p, dba.SolverConfig(max_iterations=1, workers=2), devices=[0])
+    h1, h2 = s1.history[0], s2.history[0]
+    assert len(dba.shared_points(p, 2)) == 1  # the boundary splits a point: the halo path runs
+    assert h1.accepted == h2.accepted and h1.pcg_iterations == h2.pcg_iterations == 500
+    assert abs(h1.cost - h2.cost) <= 1e-5 * h1.cost
+    assert h2.worker_edges == [2 * 2500973, 2 * 2500973]
