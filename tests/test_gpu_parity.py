@@ -430,3 +430,18 @@ def test_full_size_venice_operator_properties():
     assert h1.accepted == h2.accepted and h1.pcg_iterations == h2.pcg_iterations == 500
     assert abs(h1.cost - h2.cost) <= 1e-5 * h1.cost
     assert h2.worker_edges == [2 * 2500973, 2 * 2500973]
+
+
+@pytest.mark.parametrize("k", [1, 2, 3])
+def test_long_tiles_dse_and_lm(k):
+    """Points observed by more than 128 cameras take the long-tile path
+    (dse_long: one CTA per point, chunks of one tile), here mixed with shard
+    boundaries inside such points: DSE vs the oracle at 1e-12, LM trajectory
+    vs the oracle at the same K."""
+    p = ring(220, 30, 150, seed=7, radius=1.0, noise=0.5, nobs=30 * 150 + 17)
+    x = np.random.default_rng(2).standard_normal(9 * p.num_cameras)
+    out, _, ident = dba.group_operator(p, k, x, mode=0, lam=1e-3, policy=0)
+    orc, _ = O.dse(p, k, 1e-3, 0, x)
+    assert ident and rel(out, orc) < 1e-12
+    cfg = dba.SolverConfig(max_iterations=4, workers=k, pcg_tol=1e-12, pcg_max_iters=2000)
+    _compare_histories(dba.lm_solve(p, cfg), O.lm_solve(p, cfg), 1e-9)
