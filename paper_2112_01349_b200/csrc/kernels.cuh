@@ -532,6 +532,23 @@ __global__ void k_halo_fix(std::int32_t n, const std::int32_t* __restrict__ halo
         (e[(r * 3) * kTile] * b[0] + e[(r * 3 + 1) * kTile] * b[1]) + e[(r * 3 + 2) * kTile] * b[2];
 }
 
+// Point rows between global order and device-point order:
+// SCATTER = false: dev[d] = glob[idx[d]]; true: glob[idx[d]] = dev[d].
+template <class S, bool SCATTER>
+__global__ void k_point_rows(std::int32_t n, const std::int32_t* __restrict__ idx, const S* __restrict__ src,
+                             S* __restrict__ dst) {
+  const std::int32_t d = blockIdx.x * blockDim.x + threadIdx.x;
+  if (d >= n) return;
+  const std::size_t g = std::size_t(idx[d]) * 3, l = std::size_t(d) * 3;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    if (SCATTER)
+      dst[g + k] = src[l + k];
+    else
+      dst[l + k] = src[g + k];
+  }
+}
+
 // rows[idx[i]] = 0 for W-wide rows.
 template <class S, int W>
 __global__ void k_zero_rows(std::int32_t n, const std::int32_t* __restrict__ idx, S* __restrict__ rows) {

@@ -227,14 +227,18 @@ class Rank {
   }
 
   // Full-size host x_c (9m) and x_p (3n); this rank keeps its local points.
+  // The full x_p goes to the device as is (one copy from the caller's
+  // buffer, DMA-direct when it is pinned) and is permuted into device-point
+  // order there.
   void set_state(const S* xc, const S* xp) {
     DBAG_CUDA(cudaSetDevice(device_));
     DBAG_CUDA(cudaMemcpyAsync(xc_.get(), xc, sizeof(S) * 9 * static_cast<std::size_t>(m_), cudaMemcpyHostToDevice, st_));
-    std::vector<S> loc(static_cast<std::size_t>(n_loc_) * 3);
-    for (std::int32_t d = 0; d < n_loc_; ++d)
-      for (int k = 0; k < 3; ++k)
-        loc[static_cast<std::size_t>(d) * 3 + k] = xp[static_cast<std::size_t>(dpt_glob_[static_cast<std::size_t>(d)]) * 3 + k];
-    DBAG_CUDA(cudaMemcpyAsync(xp_.get(), loc.data(), sizeof(S) * loc.size(), cudaMemcpyHostToDevice, st_));
+    const std::size_t full = static_cast<std::size_t>(n_glob_) * 3;
+    if (xp_full_.size() < std::max<std::size_t>(full, 1)) xp_full_.alloc(std::max<std::size_t>(full, 1));
+    DBAG_CUDA(cudaMemcpyAsync(xp_full_.get(), xp, sizeof(S) * full, cudaMemcpyHostToDevice, st_));
+    if (n_loc_ > 0)
+      launch(dev::k_point_rows<S, false>, grid_for(n_loc_, 256, 1 << 30), 256, n_loc_,
+             static_cast<const std::int32_t*>(dpt_glob_d_.get()), xp_full_.get(), xp_.get());
     DBAG_CUDA(cudaStreamSynchronize(st_));
     have_system_ = false;
   }
@@ -244,6 +248,16 @@ class Rank {
   void get_state(S* xc, S* xp, bool owned_only = false) {
     DBAG_CUDA(cudaSetDevice(device_));
     if (xc) DBAG_CUDA(cudaMemcpyAsync(xc, xc_.get(), sizeof(S) * 9 * static_cast<std::size_t>(m_), cudaMemcpyDeviceToHost, st_));
+    if (xp && n_loc_ == n_glob_) {  // every point is local: un-permute on the device, one copy out
+      const std::size_t full = static_cast<std::size_t>(n_glob_) * 3;
+      if (xp_full_.size() < std::max<std::size_t>(full, 1)) xp_full_.alloc(std::max<std::size_t>(full, 1));
+      if (n_loc_ > 0)
+        launch(dev::k_point_rows<S, true>, grid_for(n_loc_, 256, 1 << 30), 256, n_loc_,
+               static_cast<const std::int32_t*>(dpt_glob_d_.get()), xp_.get(), xp_full_.get());
+      DBAG_CUDA(cudaMemcpyAsync(xp, xp_full_.get(), sizeof(S) * full, cudaMemcpyDeviceToHost, st_));
+      DBAG_CUDA(cudaStreamSynchronize(st_));
+      return;
+    }
     std::vector<S> loc(static_cast<std::size_t>(n_loc_) * 3);
     DBAG_CUDA(cudaMemcpyAsync(loc.data(), xp_.get(), sizeof(S) * loc.size(), cudaMemcpyDeviceToHost, st_));
     DBAG_CUDA(cudaStreamSynchronize(st_));
@@ -1183,6 +1197,7 @@ class Rank {
   DevBuf<S> B_, Bd_, Binv_, Bexp_, C_, Cd_, Cinv_, p2_;
   DevBuf<dev::GScal<S>> gsc_;
   DevBuf<double> g_pq_cam_;
+  DevBuf<S> xp_full_;  // x_p in global point order (state transfers)
   DevBuf<unsigned long long> g_bar_;  // k_g_fs grid barrier arrivals (monotonic)
   bool g_fused_ = false;
   int g_unroll_ = DBAG_GRAPH_UNROLL;

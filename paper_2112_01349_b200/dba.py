@@ -583,9 +583,17 @@ class RankContext:
         xp = np.ascontiguousarray(x_p, self.dtype)
         _check(N.lib().dbag_set_state(self.h, xc.ctypes.data, xp.ctypes.data))
 
-    def get_state(self):
-        xc = np.zeros(9 * self.m, self.dtype)
-        xp = np.zeros(max(3 * self.n, 1), self.dtype)
+    def get_state(self, out=None):
+        """(x_c, x_p); ``out`` = preallocated (9m, >= 3n) arrays of the context
+        dtype (e.g. pinned) to copy into."""
+        if out is None:
+            xc = np.zeros(9 * self.m, self.dtype)
+            xp = np.zeros(max(3 * self.n, 1), self.dtype)
+        else:
+            xc, xp = out
+            if xc.dtype != self.dtype or xp.dtype != self.dtype or xc.size < 9 * self.m or xp.size < 3 * self.n \
+                    or not (xc.flags.c_contiguous and xp.flags.c_contiguous):
+                raise InvalidArgumentError("get_state out arrays must be contiguous, sized and of the context dtype")
         _check(N.lib().dbag_get_state(self.h, xc.ctypes.data, xp.ctypes.data))
         return xc, xp[:3 * self.n]
 
