@@ -99,34 +99,59 @@ __device__ __forceinline__ double block_reduce(double v, double* smem) {
   return v;
 }
 
+// NV block reductions in one pass (one shared round trip for all values);
+// results valid in thread 0. smem: >= NV * 32 doubles.
+template <class Op, int NV>
+__device__ __forceinline__ void block_reduce_n(double (&v)[NV], double* smem) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+#pragma unroll
+  for (int k = 0; k < NV; ++k) v[k] = warp_reduce<Op>(v[k]);
+  __syncthreads();
+  if (lane == 0)
+#pragma unroll
+    for (int k = 0; k < NV; ++k) smem[k * 32 + warp] = v[k];
+  __syncthreads();
+  if (warp == 0)
+#pragma unroll
+    for (int k = 0; k < NV; ++k) v[k] = warp_reduce<Op>(lane < nw ? smem[k * 32 + lane] : Op::id());
+}
+
 // Grid-wide deterministic reduction of NV values: every block calls this
 // once; the last block to arrive reduces the per-block partials in block
 // order and writes out[0..NV). Returns true in the finalizing block (all
-// threads), after out[] is written and visible to that block.
+// threads), after out[] is written and visible to that block. Only the
+// partials' writer (thread 0) fences before arriving: the callers' other
+// stores are for later kernels, which the kernel boundary orders.
 template <class Op, int NV>
 __device__ __forceinline__ bool grid_reduce(const double (&v)[NV], double* partials, unsigned* counter,
                                             double* out) {
-  __shared__ double red[32];
+  __shared__ double red[NV * 32];
   __shared__ bool last;
+  double b[NV];
 #pragma unroll
-  for (int k = 0; k < NV; ++k) {
-    const double b = block_reduce<Op>(v[k], red);
-    if (threadIdx.x == 0) partials[k * gridDim.x + blockIdx.x] = b;
+  for (int k = 0; k < NV; ++k) b[k] = v[k];
+  block_reduce_n<Op, NV>(b, red);
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int k = 0; k < NV; ++k) partials[k * gridDim.x + blockIdx.x] = b[k];
+    __threadfence();
+    last = (atomicAdd(counter, 1u) == gridDim.x - 1);
   }
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) last = (atomicAdd(counter, 1u) == gridDim.x - 1);
   __syncthreads();
   if (!last) return false;
   __threadfence();
+  double acc[NV];
 #pragma unroll
   for (int k = 0; k < NV; ++k) {
-    double acc = Op::id();
-    for (unsigned i = threadIdx.x; i < gridDim.x; i += blockDim.x) acc = Op::op(acc, __ldcg(partials + k * gridDim.x + i));
-    acc = block_reduce<Op>(acc, red);
-    if (threadIdx.x == 0) out[k] = acc;
+    acc[k] = Op::id();
+    for (unsigned i = threadIdx.x; i < gridDim.x; i += blockDim.x) acc[k] = Op::op(acc[k], __ldcg(partials + k * gridDim.x + i));
   }
-  if (threadIdx.x == 0) *counter = 0u;
+  block_reduce_n<Op, NV>(acc, red);
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int k = 0; k < NV; ++k) out[k] = acc[k];
+    *counter = 0u;
+  }
   __threadfence();
   __syncthreads();
   return true;
