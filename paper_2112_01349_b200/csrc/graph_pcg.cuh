@@ -23,6 +23,7 @@
 // 1 / 2 in the reference's order (rho checked before the DSE, p'q after).
 #pragma once
 
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -574,6 +575,193 @@ __global__ void __launch_bounds__(kRedThreads) k_g_fs(GBufs<S> B, RedWs ws, GSca
       finish_iteration(sc, fin[0], fin[1], h_while);
     }
   }
+}
+
+
+// Camera fold + PCG step for small m as ONE thread-block cluster (<= 16 CTAs
+// of 544 threads, warp per camera, CPW cameras per warp): the p'q and
+// rho / |r|^2 reductions go through distributed shared memory and hardware
+// cluster barriers instead of global atomics, a software grid barrier and a
+// last-block pass. Same per-camera arithmetic as k_g_fs; the cross-camera
+// sums are taken in fixed (CTA, warp, camera) order, so deterministic.
+constexpr int kFscThreads = 544;  // 17 warps: a 16-CTA cluster covers 272 cameras with one camera per warp
+constexpr int kFscWarps = kFscThreads / 32;
+
+template <class S, int CPW>
+__global__ void __launch_bounds__(kFscThreads, 1) k_g_fsc(GBufs<S> B, GScal<S>* sc, cudaGraphConditionalHandle h_while) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cluster = cg::this_cluster();
+  __shared__ double w_pq[kFscWarps], w_rho[kFscWarps], w_rn[kFscWarps];
+  __shared__ double cta_sum[3];  // this CTA's p'q, rho, |r|^2 (read by the cluster)
+  __shared__ double pq_all;
+  pdl_allow_dependents();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int row = lane < 9 ? lane : 0;
+  const int rank = int(cluster.block_rank()), ncta = int(cluster.num_blocks());
+  std::int32_t cam[CPW], k0[CPW], k1[CPW];
+  bool on[CPW];
+  S bd[CPW][9], bi[CPW][9];
+#pragma unroll
+  for (int j = 0; j < CPW; ++j) {
+    const std::int32_t c = (rank * kFscWarps + warp) + j * ncta * kFscWarps;
+    on[j] = c < B.m;
+    cam[j] = on[j] ? c : 0;
+    k0[j] = B.cam_part_ptr[cam[j]];
+    k1[j] = on[j] ? B.cam_part_ptr[cam[j] + 1] : k0[j];
+#pragma unroll
+    for (int k = 0; k < 9; ++k) {
+      bd[j][k] = B.Bd[std::size_t(cam[j]) * 81 + row * 9 + k];
+      bi[j][k] = B.Binv[std::size_t(cam[j]) * 81 + row * 9 + k];
+    }
+  }
+  pdl_wait();
+  const int done = sc->done, n = sc->n, phase = sc->phase;
+  const S beta = sc->beta;
+  const double rho_cur = sc->rho;
+  if (done) return;  // uniform over the cluster
+  DBAG_TL(n, 1, rank == 0 && threadIdx.x == 0);
+  DBAG_TL(n, 2, rank == 0 && threadIdx.x == 0);
+  const bool pcg = phase == 0;
+  S v[CPW], qv[CPW], xr[CPW], rr[CPW], gr[CPW];
+  double pq_w = 0.0;
+#pragma unroll
+  for (int j = 0; j < CPW; ++j) {
+    const std::size_t at = std::size_t(cam[j]) * 9 + row;
+    const S zr = B.z[at], pp = p_cur(B, n + 1)[at];
+    xr[j] = B.x[at];
+    rr[j] = B.r[at];
+    gr[j] = B.g[at];
+    S acc[9];
+#pragma unroll
+    for (int i = 0; i < 9; ++i) acc[i] = S(0);
+    for (std::int32_t k = k0[j] + lane; k < k1[j]; k += 32) {
+      const S* pa = B.part + std::size_t(k) * 9;
+#pragma unroll
+      for (int i = 0; i < 9; ++i) acc[i] += pa[i];
+    }
+#pragma unroll
+    for (int i = 0; i < 9; ++i) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) acc[i] += __shfl_down_sync(0xffffffffu, acc[i], o);
+      acc[i] = __shfl_sync(0xffffffffu, acc[i], 0);
+    }
+    S cr = acc[0];
+#pragma unroll
+    for (int i = 1; i < 9; ++i)
+      if (row == i) cr = acc[i];
+    v[j] = pcg ? (n == 0 ? zr : zr + beta * pp) : xr[j];
+    if (pcg && on[j] && lane < 9) p_cur(B, n)[at] = v[j];
+    S d = S(0);
+#pragma unroll
+    for (int k = 0; k < 9; ++k) d += bd[j][k] * __shfl_sync(0xffffffffu, v[j], k);
+    qv[j] = d - cr;
+    double t = (lane < 9 && on[j]) ? double(v[j]) * double(qv[j]) : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_down_sync(0xffffffffu, t, o);
+    pq_w += t;  // lane 0: this warp's cameras in order
+  }
+  S alpha = S(0);
+  double pq = 0.0;
+  bool hand_over = false;
+  if (pcg) {
+    if (lane == 0) w_pq[warp] = pq_w;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double b = 0.0;
+      for (int w = 0; w < kFscWarps; ++w) b += w_pq[w];
+      cta_sum[0] = b;
+    }
+    DBAG_TL(n, 3, rank == 0 && threadIdx.x == 0);
+    cluster.sync();
+    DBAG_TL(n, 4, rank == 0 && threadIdx.x == 0);
+    if (threadIdx.x == 0) {
+      double a = 0.0;
+      for (int r = 0; r < ncta; ++r) a += *cluster.map_shared_rank(&cta_sum[0], r);
+      pq_all = a;
+    }
+    cluster.sync();  // every CTA has read every cta_sum[0]
+    pq = pq_all;
+    DBAG_TL(n, 5, rank == 0 && threadIdx.x == 0);
+    if (!(pq > 0.0) || isinf(pq)) {  // p'q breakdown (uniform over the cluster)
+      if (rank == 0 && threadIdx.x == 0) {
+        sc->pq = pq;
+        sc->status = 2;
+        sc->dse_count += 1;
+        sc->done = 1;
+        cudaGraphSetConditional(h_while, 0u);
+      }
+      return;
+    }
+    alpha = S(rho_cur / pq);
+    hand_over = (n + 1) % 50 == 0;
+  }
+  double rho_w = 0.0, rn_w = 0.0;
+#pragma unroll
+  for (int j = 0; j < CPW; ++j) {
+    const std::size_t at = std::size_t(cam[j]) * 9 + row;
+    S ri = S(0);
+    if (pcg) {
+      if (on[j] && lane < 9) B.x[at] = xr[j] + alpha * v[j];
+      if (!hand_over) ri = rr[j] - alpha * qv[j];
+    } else {
+      ri = gr[j] - qv[j];
+    }
+    if (!hand_over) {
+      S zi = S(0);
+#pragma unroll
+      for (int k = 0; k < 9; ++k) zi += bi[j][k] * __shfl_sync(0xffffffffu, ri, k);
+      double rho = 0.0, rn = 0.0;
+      if (on[j] && lane < 9) {
+        B.r[at] = ri;
+        B.z[at] = zi;
+        rho = double(ri) * double(zi);
+        rn = double(ri) * double(ri);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        rho += __shfl_down_sync(0xffffffffu, rho, o);
+        rn += __shfl_down_sync(0xffffffffu, rn, o);
+      }
+      rho_w += rho;
+      rn_w += rn;
+    }
+  }
+  if (lane == 0) {
+    w_rho[warp] = rho_w;
+    w_rn[warp] = rn_w;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double a = 0.0, b = 0.0;
+    for (int w = 0; w < kFscWarps; ++w) {
+      a += w_rho[w];
+      b += w_rn[w];
+    }
+    cta_sum[1] = a;
+    cta_sum[2] = b;
+  }
+  cluster.sync();
+  if (rank == 0 && threadIdx.x == 0) {
+    double rho = 0.0, rn = 0.0;
+    for (int r = 0; r < ncta; ++r) {
+      rho += *cluster.map_shared_rank(&cta_sum[1], r);
+      rn += *cluster.map_shared_rank(&cta_sum[2], r);
+    }
+    DBAG_TL(n, 6, true);
+    sc->dse_count += 1;
+    if (pcg) {
+      sc->pq = pq;
+      sc->alpha = alpha;
+    }
+    if (hand_over) {
+      sc->phase = 1;
+      cudaGraphSetConditional(h_while, 1u);
+    } else {
+      sc->phase = 0;
+      finish_iteration(sc, rho, rn, h_while);
+    }
+  }
+  cluster.sync();  // CTA 0 has read every CTA's sums
 }
 
 }  // namespace dev

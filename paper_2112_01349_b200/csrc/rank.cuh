@@ -562,6 +562,29 @@ class Rank {
     DBAG_CUDA(cudaMemset(g_bar_.get(), 0, sizeof(unsigned long long)));
     unsigned long long* bar = g_bar_.get();
     void* a_fs[] = {&B, &ws, &sc, &hw, &bar};
+    void* a_fsc[] = {&B, &sc, &hw};
+    // small m: fold + step as one thread-block cluster (k_g_fsc)
+    const char* fcl = std::getenv("DBAG_FSC");
+    g_cluster_ = 0;
+    g_cpw_ = m_ <= 16 * dev::kFscWarps ? 1 : 2;
+    const int fsc_ctas = static_cast<int>((m_ + g_cpw_ * dev::kFscWarps - 1) / (g_cpw_ * dev::kFscWarps));
+    void* fsc_fn = g_cpw_ == 1 ? reinterpret_cast<void*>(dev::k_g_fsc<S, 1>) : reinterpret_cast<void*>(dev::k_g_fsc<S, 2>);
+    if (!(fcl && std::string(fcl) == "0") && m_ > 0 && fsc_ctas <= 16) {
+      DBAG_CUDA(cudaFuncSetAttribute(fsc_fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+      cudaLaunchConfig_t lc{};
+      lc.gridDim = dim3(static_cast<unsigned>(fsc_ctas));
+      lc.blockDim = dim3(dev::kFscThreads);
+      cudaLaunchAttribute at{};
+      at.id = cudaLaunchAttributeClusterDimension;
+      at.val.clusterDim.x = static_cast<unsigned>(fsc_ctas);
+      at.val.clusterDim.y = 1;
+      at.val.clusterDim.z = 1;
+      lc.attrs = &at;
+      lc.numAttrs = 1;
+      int clusters = 0;
+      if (cudaOccupancyMaxActiveClusters(&clusters, fsc_fn, &lc) == cudaSuccess && clusters > 0) g_cluster_ = fsc_ctas;
+      cudaGetLastError();
+    }
     cudaGraphNode_t cur = nullptr;
     g_unroll_ = DBAG_GRAPH_UNROLL;
     if (const char* ue = std::getenv("DBAG_UNROLL")) g_unroll_ = std::max(1, std::atoi(ue));
@@ -572,6 +595,15 @@ class Rank {
       const int psmem = piped ? static_cast<int>(sizeof(dev::PipeSmem<S>)) : 0;
       cur = u ? add_kernel_pdl(body, cur, pass, pgrid, dev::kTile, a_pass, psmem)
               : add_kernel(body, nullptr, pass, pgrid, dev::kTile, a_pass, psmem);
+      if (g_cluster_ > 0) {
+        cur = add_kernel_pdl(body, cur, fsc_fn, g_cluster_, dev::kFscThreads, a_fsc);
+        cudaLaunchAttributeValue cv{};
+        cv.clusterDim.x = static_cast<unsigned>(g_cluster_);
+        cv.clusterDim.y = 1;
+        cv.clusterDim.z = 1;
+        DBAG_CUDA(cudaGraphKernelNodeSetAttribute(cur, cudaLaunchAttributeClusterDimension, &cv));
+        continue;
+      }
       if (g_fused_) {
         cur = add_kernel_pdl(body, cur, reinterpret_cast<void*>(dev::k_g_fs<S>), cam_warp_blocks, dev::kRedThreads,
                              a_fs);
@@ -628,7 +660,7 @@ class Rank {
     // k_g_init + 3 kernels per body pass (the no-op copies of the last
     // unrolled body launch too)
     const std::int64_t passes = std::max(o.dse_count - 1, 0);
-    launches_ += 1 + (g_fused_ ? 2 : 3) * ((passes + g_unroll_ - 1) / g_unroll_) * g_unroll_;
+    launches_ += 1 + (g_fused_ || g_cluster_ > 0 ? 2 : 3) * ((passes + g_unroll_ - 1) / g_unroll_) * g_unroll_;
     dse_count_ = o.dse_count;
     dse_launches_ += o.dse_count;
     tally_.block_ops += 2 * static_cast<std::uint64_t>(N_) * static_cast<std::uint64_t>(o.dse_count);
@@ -1200,6 +1232,7 @@ class Rank {
   DevBuf<S> xp_full_;  // x_p in global point order (state transfers)
   DevBuf<unsigned long long> g_bar_;  // k_g_fs grid barrier arrivals (monotonic)
   bool g_fused_ = false;
+  int g_cluster_ = 0, g_cpw_ = 1;  // k_g_fsc cluster size (0: not used), cameras per warp
   int g_unroll_ = DBAG_GRAPH_UNROLL;
   dev::GScal<S>* gsc_h_ = nullptr;
   cudaGraph_t g_graph_ = nullptr;
