@@ -29,7 +29,6 @@
 #include <cstdint>
 
 #include "dse.cuh"
-#include "pipe.cuh"
 
 #ifndef DBAG_GRAPH_UNROLL
 #define DBAG_GRAPH_UNROLL 16  // PCG iterations per WHILE-body launch (DBAG_UNROLL overrides)
@@ -132,25 +131,6 @@ struct GatherGraph {
     return {__ldg(v + k), (!pcg || first) ? S(0) : __ldg(pprev + k)};
   }
   __device__ __forceinline__ S combine(const Raw& r) const { return (!pcg || first) ? r.v : r.v + beta * r.pp; }
-};
-
-// GatherGraph split for the pipelined pass (pipe.cuh): load() issues the z
-// (or x) and p_prev loads one chunk ahead, combine() forms p = z + beta p_prev.
-template <class S>
-struct PipeGatherGraph : GatherGraph<S> {
-  struct Raw {
-    S v, pp;
-  };
-  __device__ __forceinline__ Raw load(std::int32_t cam, int i) const {
-    const std::size_t k = std::size_t(cam) * 9 + i;
-    Raw r;
-    r.v = __ldg(this->v + k);
-    r.pp = (!this->pcg || this->first) ? S(0) : __ldg(this->pprev + k);
-    return r;
-  }
-  __device__ __forceinline__ S combine(const Raw& r) const {
-    return (!this->pcg || this->first) ? r.v : r.v + this->beta * r.pp;
-  }
 };
 
 // Loop decision after rho / |r|^2 of iteration state n (dba/solver.hpp:223-230).
@@ -285,33 +265,6 @@ __global__ void __launch_bounds__(kTile, DBAG_PASS_MINB) k_g_pass(DseArgs<S> A, 
     dse_long<S, 0>(A, sm, blk, gx);
   else
     dse_chunk<S, 0>(A, sm, blk - A.n_long, gx);
-}
-
-// The body's DSE pass, pipelined (pipe.cuh): persistent CTAs, TMA-fed
-// records, camera gathers and point factors one chunk ahead.
-template <class S>
-__global__ void __launch_bounds__(kTile) k_g_pipe(DseArgs<S> A, GBufs<S> B, const GScal<S>* sc) {
-  extern __shared__ __align__(128) unsigned char pipe_dyn[];
-  PipeSmem<S>& sm = *reinterpret_cast<PipeSmem<S>*>(pipe_dyn);
-  pdl_allow_dependents();
-  PipeGatherGraph<S> gx;
-  gx.sc = sc;
-  gx.z = B.z;
-  gx.x = B.x;
-  gx.p0 = B.p0;
-  gx.p1 = B.p1;
-  gx.v = nullptr;
-  gx.pprev = nullptr;
-  gx.beta = S(0);
-  gx.first = false;
-  gx.pcg = true;
-#if DBAG_GTIMING
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    pdl_wait();
-    tl_mark(sc->n, 0);
-  }
-#endif
-  pipe_pass<S, 0>(A, sm, gx);
 }
 
 // Finish of an iteration: rho_prev, rho, |r|^2, n + 1, beta, loop decision.

@@ -527,7 +527,6 @@ class Rank {
 
   void build_graph() {
     destroy_graph();
-    pipe_grid();
     if (!gsc_.get()) {
       gsc_.alloc(1);
       DBAG_CUDA(cudaMallocHost(&gsc_h_, sizeof(dev::GScal<S>)));
@@ -589,10 +588,9 @@ class Rank {
     g_unroll_ = DBAG_GRAPH_UNROLL;
     if (const char* ue = std::getenv("DBAG_UNROLL")) g_unroll_ = std::max(1, std::atoi(ue));
     for (int u = 0; u < g_unroll_; ++u) {
-      const bool piped = dse_kind() == 0;
-      void* pass = piped ? reinterpret_cast<void*>(dev::k_g_pipe<S>) : reinterpret_cast<void*>(dev::k_g_pass<S>);
-      const int pgrid = piped ? pipe_grid_for_pass() : n_long_ + n_chunks_;
-      const int psmem = piped ? static_cast<int>(sizeof(dev::PipeSmem<S>)) : 0;
+      void* pass = reinterpret_cast<void*>(dev::k_g_pass<S>);
+      const int pgrid = n_long_ + n_chunks_;
+      const int psmem = 0;
       cur = u ? add_kernel_pdl(body, cur, pass, pgrid, dev::kTile, a_pass, psmem)
               : add_kernel(body, nullptr, pass, pgrid, dev::kTile, a_pass, psmem);
       if (g_cluster_ > 0) {
@@ -688,15 +686,7 @@ class Rank {
     cudaEvent_t e0, e1;
     DBAG_CUDA(cudaEventCreate(&e0));
     DBAG_CUDA(cudaEventCreate(&e1));
-    auto one = [&] {
-      if (dse_kind() == 0) {
-        dev::k_g_pipe<S><<<pipe_grid_for_pass(), dev::kTile, sizeof(dev::PipeSmem<S>), st_>>>(A, B, sc);
-        DBAG_LAUNCH_CHECK();
-        ++launches_;
-      } else {
-        launch(dev::k_g_pass<S>, grid, dev::kTile, A, B, sc);
-      }
-    };
+    auto one = [&] { launch(dev::k_g_pass<S>, grid, dev::kTile, A, B, sc); };
     one();  // warm-up
     DBAG_CUDA(cudaEventRecord(e0, st_));
     for (int r = 0; r < reps; ++r) one();
@@ -1083,40 +1073,12 @@ class Rank {
     return a;
   }
 
-  // Grid of the pipelined DSE pass (pipe.cuh): resident CTAs per SM x SMs.
-  int pipe_grid() {
-    if (pipe_grid_ > 0) return pipe_grid_;
-    const int dyn = static_cast<int>(sizeof(dev::PipeSmem<S>));
-    auto attrs = [&](const void* k) {
-      DBAG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn));
-      DBAG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-    };
-    attrs(reinterpret_cast<const void*>(dev::k_dse_pipe<S, 0>));
-    attrs(reinterpret_cast<const void*>(dev::k_dse_pipe<S, 1>));
-    attrs(reinterpret_cast<const void*>(dev::k_dse_pipe<S, 2>));
-    attrs(reinterpret_cast<const void*>(dev::k_g_pipe<S>));
-    int per_sm = 0, sms = 0;
-    DBAG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dev::k_g_pipe<S>, dev::kTile, dyn));
-    DBAG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device_));
-    pipe_grid_ = std::max(1, std::max(per_sm, 1) * sms);
-    if (std::getenv("DBAG_VERBOSE"))
-      std::fprintf(stderr, "dbag: pipelined DSE pass: %d CTAs/SM x %d SMs, %d B shared per CTA\n", per_sm, sms, dyn);
-    return pipe_grid_;
-  }
-  int pipe_grid_for_pass() { return std::max(1, std::min(pipe_grid(), std::max(n_chunks_, n_long_))); }
-
   template <int MODE>
   void stream_pass(const S* x) {
     if (n_chunks_ == 0) return;
     const dev::DseArgs<S> a = dse_args(x);
-    if (dse_kind() == 0) {
-      dev::k_dse_pipe<S, MODE><<<pipe_grid_for_pass(), dev::kTile, sizeof(dev::PipeSmem<S>), st_>>>(a);
-      DBAG_LAUNCH_CHECK();
-      ++launches_;
-    } else {
-      launch(dev::k_dse_chunk<S, MODE>, n_chunks_, dev::kTile, a);
-      if (n_long_ > 0) launch(dev::k_dse_long<S, MODE>, n_long_, dev::kTile, a);
-    }
+    launch(dev::k_dse_chunk<S, MODE>, n_chunks_, dev::kTile, a);
+    if (n_long_ > 0) launch(dev::k_dse_long<S, MODE>, n_long_, dev::kTile, a);
   }
 
   template <int EPI>
@@ -1237,12 +1199,6 @@ class Rank {
   dev::GScal<S>* gsc_h_ = nullptr;
   cudaGraph_t g_graph_ = nullptr;
   cudaGraphExec_t g_exec_ = nullptr;
-  int pipe_grid_ = -1;
-  // DBAG_DSE: direct (default; k_dse_chunk / k_g_pass) | pipe (pipe.cuh)
-  static int dse_kind() {
-    const char* d = std::getenv("DBAG_DSE");
-    return d && std::string(d) == "pipe" ? 0 : 1;
-  }
   DevBuf<S> Jb_, E_, part_, halo_buf_;
   DevBuf<Scal> sc_;
   DevBuf<double> red_part_, dsc_, bounce_;

@@ -3,8 +3,17 @@
 #include <cstdio>
 #include <cstdint>
 #include <cuda_runtime.h>
-#include "../../paper_2112_01349_b200/csrc/tma.cuh"
-using namespace dbag::dev;
+// minimal TMA bulk-copy helpers (cp.async.bulk + mbarrier)
+__device__ __forceinline__ unsigned smem_addr(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* b, unsigned n) { asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(b)), "r"(n) : "memory"); }
+__device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* b, unsigned bytes) { asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(b)), "r"(bytes) : "memory"); }
+__device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned ph) {
+  asm volatile("{\n\t.reg .pred P;\nW_%=:\n\tmbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n\t@!P bra W_%=;\n}" ::"r"(smem_addr(b)), "r"(ph) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* d, const void* s, unsigned bytes, uint64_t* b) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_addr(d)), "l"(s), "r"(bytes), "r"(smem_addr(b)) : "memory");
+}
 constexpr int kRec = 29232 / 8;  // doubles per record (E + meta)
 
 __global__ void k_vec(const double2* __restrict__ a, size_t n, double* out) {

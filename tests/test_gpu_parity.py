@@ -445,3 +445,19 @@ def test_long_tiles_dse_and_lm(k):
     assert ident and rel(out, orc) < 1e-12
     cfg = dba.SolverConfig(max_iterations=4, workers=k, pcg_tol=1e-12, pcg_max_iters=2000)
     _compare_histories(dba.lm_solve(p, cfg), O.lm_solve(p, cfg), 1e-9)
+
+
+@pytest.mark.parametrize("variant", ["cluster-2-per-warp", "grid-barrier", "fold+step kernels"])
+def test_graph_fold_step_variants(variant, monkeypatch):
+    """The three fold + step forms of the graph DPCG (k_g_fsc for m <= 544,
+    k_g_fs up to 4736 cameras, k_g_fold + k_g_step beyond) give the oracle's
+    trajectory. m = 300 makes k_g_fsc fold two cameras per warp; the
+    environment switches force the larger-m forms on the same instance."""
+    if variant == "grid-barrier":
+        monkeypatch.setenv("DBAG_FSC", "0")
+    elif variant == "fold+step kernels":
+        monkeypatch.setenv("DBAG_FSC", "0")
+        monkeypatch.setenv("DBAG_FS", "0")
+    p = ring(300, 900, 4, radius=1.0, noise=0.5, seed=11)
+    cfg = dba.SolverConfig(max_iterations=4, pcg_tol=1e-12, pcg_max_iters=2000)
+    _compare_histories(dba.lm_solve(p, cfg), O.lm_solve(p, cfg), 1e-9)
