@@ -59,7 +59,8 @@ typedef struct dbag_problem {
 typedef struct dbag_config {
   int32_t workers, max_iterations;
   double pcg_tol;
-  int32_t pcg_max_iters, _pad0;
+  int32_t pcg_max_iters;
+  int32_t coupling_fp32;       /* B200 extension: FP64 solve with the E blocks stored in FP32; 0 = off */
   double lambda0, lambda_max, rel_tol, step_tol;
   int32_t damping;             /* 0 identity, 1 diag_scaled (default) */
   int32_t mse_half;            /* 1 half_per_observation (default), 0 per_observation */
@@ -168,6 +169,10 @@ typedef struct dbag_ctx dbag_ctx;
 
 /* K = 1 context on `device` (single rank, no collectives). */
 int dbag_create(int device, int precision, dbag_ctx** out);
+/* Same, with the memory-lean variant: precision 8 and
+ * coupling_fp32 != 0 keep every vector, block and reduction in FP64 and store
+ * only the coupling blocks E in FP32 (half the DSE stream). */
+int dbag_create_ex(int device, int precision, int coupling_fp32, dbag_ctx** out);
 /* Context for rank `rank` of an NCCL communicator (multi-process). */
 int dbag_create_nccl(int device, int rank, int nranks, const unsigned char* nccl_id128, int precision,
                      dbag_ctx** out);

@@ -24,7 +24,7 @@ class Problem(C.Structure):
 
 class Config(C.Structure):
     _fields_ = [("workers", i32), ("max_iterations", i32), ("pcg_tol", f64), ("pcg_max_iters", i32),
-                ("_pad0", i32), ("lambda0", f64), ("lambda_max", f64), ("rel_tol", f64), ("step_tol", f64),
+                ("coupling_fp32", i32), ("lambda0", f64), ("lambda_max", f64), ("rel_tol", f64), ("step_tol", f64),
                 ("damping", i32), ("mse_half", i32), ("jacobian", i32), ("check_rank_identity", i32)]
 
 
@@ -61,6 +61,7 @@ _SIGS = {
     "dbag_lm_solve_rank": (C.c_int, [C.c_int, _P(Problem), _P(Config), C.c_int, C.c_int, vp, C.c_int,
                                      _P(Result)]),
     "dbag_create": (C.c_int, [C.c_int, C.c_int, _P(vp)]),
+    "dbag_create_ex": (C.c_int, [C.c_int, C.c_int, C.c_int, _P(vp)]),
     "dbag_create_nccl": (C.c_int, [C.c_int, C.c_int, C.c_int, vp, C.c_int, _P(vp)]),
     "dbag_destroy": (C.c_int, [vp]),
     "dbag_upload_problem": (C.c_int, [vp, _P(Problem), C.c_int]),

@@ -36,6 +36,7 @@ struct dbag_ctx {
   std::unique_ptr<Comm> comm;
   std::unique_ptr<Rank<float>> r32;
   std::unique_ptr<Rank<double>> r64;
+  std::unique_ptr<Rank<double, float>> r64l;  // FP64 arithmetic, FP32 coupling blocks (coupling_fp32)
   std::int64_t num_obs = 0;
   bool cost_valid = false;
   double cost = 0;
@@ -70,14 +71,15 @@ void check_precision(int p) {
 }
 
 void check_ctx(dbag_ctx* c) {
-  if (!c || (!c->r32 && !c->r64)) throw Error(DBAG_INVALID_ARGUMENT, "null or empty context");
+  if (!c || (!c->r32 && !c->r64 && !c->r64l)) throw Error(DBAG_INVALID_ARGUMENT, "null or empty context");
 }
 
-// Calls fn(Rank<S>&) on the context's typed rank.
+// Calls fn(Rank<S, T>&) on the context's typed rank.
 template <class Fn>
 void with_rank(dbag_ctx* c, Fn&& fn) {
   check_ctx(c);
   if (c->r64) fn(*c->r64);
+  else if (c->r64l) fn(*c->r64l);
   else fn(*c->r32);
 }
 
@@ -108,8 +110,8 @@ void fill_result(const Outcome& o, int K, dbag_result* out) {
 
 // Writes this rank's owned points (and, on rank 0, the cameras) of the
 // current state into full-size host vectors.
-template <class S>
-void export_state(Rank<S>& rk, S* xc, S* xp) {
+template <class R, class S = typename R::Scalar>
+void export_state(R& rk, S* xc, S* xp) {
   const ShardPlan& pl = rk.plan();
   std::vector<S> cams(static_cast<std::size_t>(pl.m) * 9);
   rk.get_state(cams.data(), xp, /*owned_only=*/true);
@@ -142,7 +144,7 @@ void run_ranks(Group& g, Fn&& body) {
   if (first) std::rethrow_exception(first);
 }
 
-template <class S>
+template <class S, class T = S>
 void lm_group(const dbag_problem* p, const dbag_config* c, const int* devices, int n_devices, dbag_result* out) {
   const int K = c->workers;
   std::vector<int> devs(devices, devices + std::max(n_devices, 0));
@@ -152,7 +154,7 @@ void lm_group(const dbag_problem* p, const dbag_config* c, const int* devices, i
   if (out->x_p) std::memcpy(out->x_p, p->points, sizeof(S) * 3 * static_cast<std::size_t>(p->num_points));
   run_ranks(g, [&](int r) {
     GroupComm comm(&g, r);
-    Rank<S> rk(g.device_of(r), &comm);
+    Rank<S, T> rk(g.device_of(r), &comm);
     rk.upload(*p, c->jacobian);
     const Outcome o = lm_solve_rank(rk, *c, p->num_observations);
     export_state(rk, static_cast<S*>(out->x_c), static_cast<S*>(out->x_p));
@@ -160,13 +162,13 @@ void lm_group(const dbag_problem* p, const dbag_config* c, const int* devices, i
   });
 }
 
-template <class S>
+template <class S, class T = S>
 void lm_nccl(const dbag_problem* p, const dbag_config* c, int rank, int nranks, const unsigned char* id, int device,
              dbag_result* out) {
   DBAG_CUDA(cudaSetDevice(device));
   if (c->workers != nranks) throw Error(DBAG_INVALID_ARGUMENT, "config.workers must equal nranks");
   NcclComm comm(rank, nranks, id);
-  Rank<S> rk(device, &comm);
+  Rank<S, T> rk(device, &comm);
   rk.upload(*p, c->jacobian);
   const Outcome o = lm_solve_rank(rk, *c, p->num_observations);
   if (out->x_p) std::memcpy(out->x_p, p->points, sizeof(S) * 3 * static_cast<std::size_t>(p->num_points));
@@ -356,7 +358,8 @@ int dbag_lm_solve(int precision, const dbag_problem* p, const dbag_config* c, co
                   dbag_result* out) {
   return guarded([&] {
     check_precision(precision);
-    if (precision == 8) lm_group<double>(p, c, devices, n_devices, out);
+    if (precision == 8 && c->coupling_fp32) lm_group<double, float>(p, c, devices, n_devices, out);
+    else if (precision == 8) lm_group<double>(p, c, devices, n_devices, out);
     else lm_group<float>(p, c, devices, n_devices, out);
   });
 }
@@ -374,22 +377,26 @@ int dbag_lm_solve_rank(int precision, const dbag_problem* p, const dbag_config* 
                        const unsigned char* id, int device, dbag_result* out) {
   return guarded([&] {
     check_precision(precision);
-    if (precision == 8) lm_nccl<double>(p, c, rank, nranks, id, device, out);
+    if (precision == 8 && c->coupling_fp32) lm_nccl<double, float>(p, c, rank, nranks, id, device, out);
+    else if (precision == 8) lm_nccl<double>(p, c, rank, nranks, id, device, out);
     else lm_nccl<float>(p, c, rank, nranks, id, device, out);
   });
 }
 
-int dbag_create(int device, int precision, dbag_ctx** out) {
+int dbag_create_ex(int device, int precision, int coupling_fp32, dbag_ctx** out) {
   return guarded([&] {
     check_precision(precision);
     auto ctx = std::make_unique<dbag_ctx>();
     ctx->precision = precision;
     ctx->comm = std::make_unique<SelfComm>();
-    if (precision == 8) ctx->r64 = std::make_unique<Rank<double>>(device, ctx->comm.get());
+    if (precision == 8 && coupling_fp32) ctx->r64l = std::make_unique<Rank<double, float>>(device, ctx->comm.get());
+    else if (precision == 8) ctx->r64 = std::make_unique<Rank<double>>(device, ctx->comm.get());
     else ctx->r32 = std::make_unique<Rank<float>>(device, ctx->comm.get());
     *out = ctx.release();
   });
 }
+
+int dbag_create(int device, int precision, dbag_ctx** out) { return dbag_create_ex(device, precision, 0, out); }
 
 int dbag_create_nccl(int device, int rank, int nranks, const unsigned char* id, int precision, dbag_ctx** out) {
   return guarded([&] {
@@ -420,7 +427,7 @@ int dbag_set_state(dbag_ctx* ctx, const void* x_c, const void* x_p) {
   return guarded([&] {
     with_rank(ctx, [&](auto& rk) {
       using S = std::remove_reference_t<decltype(rk)>;
-      using T = std::conditional_t<std::is_same_v<S, Rank<double>>, double, float>;
+      using T = typename S::Scalar;
       rk.set_state(static_cast<const T*>(x_c), static_cast<const T*>(x_p));
     });
     ctx->cost_valid = false;
@@ -431,7 +438,7 @@ int dbag_get_state(dbag_ctx* ctx, void* x_c, void* x_p) {
   return guarded([&] {
     with_rank(ctx, [&](auto& rk) {
       using S = std::remove_reference_t<decltype(rk)>;
-      using T = std::conditional_t<std::is_same_v<S, Rank<double>>, double, float>;
+      using T = typename S::Scalar;
       rk.get_state(static_cast<T*>(x_c), static_cast<T*>(x_p));
     });
   });
@@ -556,7 +563,7 @@ int dbag_residuals(dbag_ctx* ctx, int use_trial, void* out) {
   return guarded([&] {
     with_rank(ctx, [&](auto& rk) {
       using S = std::remove_reference_t<decltype(rk)>;
-      using T = std::conditional_t<std::is_same_v<S, Rank<double>>, double, float>;
+      using T = typename S::Scalar;
       rk.residuals(use_trial != 0, static_cast<T*>(out));
     });
   });
@@ -566,7 +573,7 @@ int dbag_get_jacobians(dbag_ctx* ctx, void* res, void* jac) {
   return guarded([&] {
     with_rank(ctx, [&](auto& rk) {
       using S = std::remove_reference_t<decltype(rk)>;
-      using T = std::conditional_t<std::is_same_v<S, Rank<double>>, double, float>;
+      using T = typename S::Scalar;
       rk.get_jacobians(static_cast<T*>(res), static_cast<T*>(jac));
     });
   });
@@ -576,7 +583,7 @@ int dbag_get_system(dbag_ctx* ctx, void* B, void* C, void* E, void* v, void* w) 
   return guarded([&] {
     with_rank(ctx, [&](auto& rk) {
       using S = std::remove_reference_t<decltype(rk)>;
-      using T = std::conditional_t<std::is_same_v<S, Rank<double>>, double, float>;
+      using T = typename S::Scalar;
       rk.get_system(static_cast<T*>(B), static_cast<T*>(C), static_cast<T*>(E), static_cast<T*>(v),
                     static_cast<T*>(w));
     });
@@ -587,7 +594,7 @@ int dbag_set_system(dbag_ctx* ctx, const void* B, const void* C, const void* E_t
   return guarded([&] {
     with_rank(ctx, [&](auto& rk) {
       using S = std::remove_reference_t<decltype(rk)>;
-      using T = std::conditional_t<std::is_same_v<S, Rank<double>>, double, float>;
+      using T = typename S::Scalar;
       rk.set_system(static_cast<const T*>(B), static_cast<const T*>(C), static_cast<const T*>(E_table),
                     static_cast<const T*>(v), static_cast<const T*>(w));
     });
@@ -598,7 +605,7 @@ int dbag_dse(dbag_ctx* ctx, const void* x, void* out) {
   return guarded([&] {
     with_rank(ctx, [&](auto& rk) {
       using S = std::remove_reference_t<decltype(rk)>;
-      using T = std::conditional_t<std::is_same_v<S, Rank<double>>, double, float>;
+      using T = typename S::Scalar;
       rk.dse_host(static_cast<const T*>(x), static_cast<T*>(out));
     });
   });
@@ -609,7 +616,7 @@ int dbag_dpcg(dbag_ctx* ctx, const void* rhs, double tol, int max_iters, void* x
   return guarded([&] {
     with_rank(ctx, [&](auto& rk) {
       using S = std::remove_reference_t<decltype(rk)>;
-      using T = std::conditional_t<std::is_same_v<S, Rank<double>>, double, float>;
+      using T = typename S::Scalar;
       const PcgOut o = rk.dpcg_host(static_cast<const T*>(rhs), tol, max_iters, static_cast<T*>(x_out));
       if (iterations) *iterations = o.iterations;
       if (converged) *converged = o.converged ? 1 : 0;

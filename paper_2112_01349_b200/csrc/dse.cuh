@@ -30,10 +30,12 @@
 namespace dbag {
 namespace dev {
 
-template <class S>
+// S: arithmetic type; T: storage type of the E lanes in the records (T = S,
+// or float under FP64 arithmetic: SolverConfig coupling_fp32, row f4).
+template <class S, class T = S>
 struct DseArgs {
   std::int32_t n_chunks;
-  const S* rec;
+  const T* rec;
   const S* x;
   const S* Cinv;
   const S* w;
@@ -56,15 +58,15 @@ struct DseWork {
   std::uint8_t ubeg[kTile + 8];
 };
 
-template <class S>
-__device__ __forceinline__ const RecMeta& rec_meta(const S* R) {
-  return *reinterpret_cast<const RecMeta*>(R + Rec<S>::kE);
+template <class T>
+__device__ __forceinline__ const RecMeta& rec_meta(const T* R) {
+  return *reinterpret_cast<const RecMeta*>(R + Rec<T>::kE);
 }
 
 // Point finish: halo deposit or b = C^-1 a (MODE 0), dx_p = C^-1 (w - a)
 // (MODE 1), b = C^-1 w (MODE 2). Returns b (zero for halo points).
-template <class S, int MODE>
-__device__ __forceinline__ void finish_point(const DseArgs<S>& A, std::int32_t p, const S* L, const S* wv, S* tt,
+template <class S, int MODE, class T>
+__device__ __forceinline__ void finish_point(const DseArgs<S, T>& A, std::int32_t p, const S* L, const S* wv, S* tt,
                                              S* b) {
   const std::int32_t h = (MODE != 2 && A.halo_of) ? A.halo_of[p] : -1;
   if (h >= 0) {
@@ -90,8 +92,8 @@ __device__ __forceinline__ void finish_point(const DseArgs<S>& A, std::int32_t p
 }
 
 // The point's C factor (and w for MODE 1/2), loaded early.
-template <class S, int MODE>
-__device__ __forceinline__ void load_point(const DseArgs<S>& A, std::int32_t p, S* L, S* wv) {
+template <class S, int MODE, class T>
+__device__ __forceinline__ void load_point(const DseArgs<S, T>& A, std::int32_t p, S* L, S* wv) {
 #pragma unroll
   for (int k = 0; k < 9; ++k) L[k] = A.Cinv[std::size_t(p) * 9 + k];
   if (MODE != 0)
@@ -107,8 +109,8 @@ __device__ __forceinline__ void load_point(const DseArgs<S>& A, std::int32_t p, 
 // stores. nu > 32: one thread per camera, sequential. Few lanes and few
 // butterfly levels keep the fold's shuffle count small (it dominated the
 // instruction mix with a warp per camera).
-template <class S, class Y>
-__device__ __forceinline__ void fold_cameras(const DseArgs<S>& A, int nu, const std::uint8_t* ubeg,
+template <class S, class Y, class T>
+__device__ __forceinline__ void fold_cameras(const DseArgs<S, T>& A, int nu, const std::uint8_t* ubeg,
                                              const std::uint8_t* uslot, const std::int32_t* upart, const Y& y) {
   const int tid = threadIdx.x;
   const int G = nu <= 32 ? (1 << (31 - __clz(32 / max(nu, 1)))) : 1;
@@ -171,8 +173,8 @@ struct GatherX {
 };
 // One 128-slot chunk whose record is at R (global or shared memory);
 // normal tiles only (long tiles return).
-template <class S, int MODE, class G>
-__device__ __forceinline__ void dse_chunk_at(const DseArgs<S>& A, DseWork<S>& sm, const S* R, G gx) {
+template <class S, int MODE, class G, class T>
+__device__ __forceinline__ void dse_chunk_at(const DseArgs<S, T>& A, DseWork<S>& sm, const T* R, G gx) {
   const int tid = threadIdx.x;
   const RecMeta& M = rec_meta(R);
   // Load order (measured): header and metadata first; then the loads that
@@ -202,7 +204,7 @@ __device__ __forceinline__ void dse_chunk_at(const DseArgs<S>& A, DseWork<S>& sm
   }
   S e[27];
 #pragma unroll
-  for (int k = 0; k < 27; ++k) e[k] = R[k * kTile + tid];  // padding slots hold zeros
+  for (int k = 0; k < 27; ++k) e[k] = S(R[k * kTile + tid]);  // padding slots hold zeros
   if (MODE != 2) {
     if (staged) {
 #pragma unroll
@@ -246,38 +248,38 @@ __device__ __forceinline__ void dse_chunk_at(const DseArgs<S>& A, DseWork<S>& sm
   }
 }
 
-template <class S, int MODE, class G>
-__device__ __forceinline__ void dse_chunk(const DseArgs<S>& A, DseWork<S>& sm, std::int32_t chunk, const G& gx) {
-  dse_chunk_at<S, MODE>(A, sm, A.rec + std::size_t(chunk) * Rec<S>::kLen, gx);
+template <class S, int MODE, class G, class T>
+__device__ __forceinline__ void dse_chunk(const DseArgs<S, T>& A, DseWork<S>& sm, std::int32_t chunk, const G& gx) {
+  dse_chunk_at<S, MODE>(A, sm, A.rec + std::size_t(chunk) * Rec<T>::kLen, gx);
 }
 
-template <class S, int MODE>
-__global__ void __launch_bounds__(kTile, 5) k_dse_chunk(DseArgs<S> A) {
+template <class S, int MODE, class T = S>
+__global__ void __launch_bounds__(kTile, 5) k_dse_chunk(DseArgs<S, T> A) {
   __shared__ DseWork<S> sm;
   dse_chunk<S, MODE>(A, sm, blockIdx.x, GatherX<S>{A.x});
 }
 
 // One CTA per long tile (a single point observed more than 128 times).
-template <class S, int MODE, class G>
-__device__ __forceinline__ void dse_long(const DseArgs<S>& A, DseWork<S>& sm, std::int32_t li, G gx) {
+template <class S, int MODE, class G, class T>
+__device__ __forceinline__ void dse_long(const DseArgs<S, T>& A, DseWork<S>& sm, std::int32_t li, G gx) {
   if (!gx.ready()) return;
   const int tid = threadIdx.x;
   const std::int32_t c0 = A.long_chunk[li];
-  const RecMeta& M0 = rec_meta(A.rec + std::size_t(c0) * Rec<S>::kLen);
+  const RecMeta& M0 = rec_meta(A.rec + std::size_t(c0) * Rec<T>::kLen);
   const std::int32_t p = M0.p0, nchunk = M0.nchunk;
   S a[3] = {S(0), S(0), S(0)};
   if (MODE != 2) {
     for (std::int32_t c = c0; c < c0 + nchunk; ++c) {
-      const S* R = A.rec + std::size_t(c) * Rec<S>::kLen;
+      const T* R = A.rec + std::size_t(c) * Rec<T>::kLen;
       const RecMeta& M = rec_meta(R);
       if (tid < M.nslots) {
         const std::int32_t cam = M.cam[tid];
 #pragma unroll
         for (int i = 0; i < 9; ++i) {
           const S xv = gx(cam, i);
-          a[0] += R[(i * 3 + 0) * kTile + tid] * xv;
-          a[1] += R[(i * 3 + 1) * kTile + tid] * xv;
-          a[2] += R[(i * 3 + 2) * kTile + tid] * xv;
+          a[0] += S(R[(i * 3 + 0) * kTile + tid]) * xv;
+          a[1] += S(R[(i * 3 + 1) * kTile + tid]) * xv;
+          a[2] += S(R[(i * 3 + 2) * kTile + tid]) * xv;
         }
       }
     }
@@ -299,15 +301,15 @@ __device__ __forceinline__ void dse_long(const DseArgs<S>& A, DseWork<S>& sm, st
   }
   if constexpr (MODE != 1) {
     for (std::int32_t c = c0; c < c0 + nchunk; ++c) {
-      const S* R = A.rec + std::size_t(c) * Rec<S>::kLen;
+      const T* R = A.rec + std::size_t(c) * Rec<T>::kLen;
       const RecMeta& M = rec_meta(R);
       __syncthreads();
       stage_meta(M, sm);
       const S b0 = sm.b[0][0], b1 = sm.b[0][1], b2 = sm.b[0][2];
 #pragma unroll
       for (int i = 0; i < 9; ++i)
-        sm.y[tid][i] = (R[(i * 3) * kTile + tid] * b0 + R[(i * 3 + 1) * kTile + tid] * b1) +
-                       R[(i * 3 + 2) * kTile + tid] * b2;
+        sm.y[tid][i] = (S(R[(i * 3) * kTile + tid]) * b0 + S(R[(i * 3 + 1) * kTile + tid]) * b1) +
+                       S(R[(i * 3 + 2) * kTile + tid]) * b2;
       __syncthreads();
       fold_cameras(A, M.nu, sm.ubeg, sm.uslot, sm.upart, YRows<S>{sm.y});
     }
@@ -315,8 +317,8 @@ __device__ __forceinline__ void dse_long(const DseArgs<S>& A, DseWork<S>& sm, st
   __syncthreads();
 }
 
-template <class S, int MODE>
-__global__ void __launch_bounds__(kTile) k_dse_long(DseArgs<S> A) {
+template <class S, int MODE, class T = S>
+__global__ void __launch_bounds__(kTile) k_dse_long(DseArgs<S, T> A) {
   __shared__ DseWork<S> sm;
   dse_long<S, MODE>(A, sm, blockIdx.x, GatherX<S>{A.x});
 }

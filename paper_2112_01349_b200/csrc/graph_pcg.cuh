@@ -249,8 +249,8 @@ __device__ __forceinline__ void camera_fold(const GBufs<S>& B, std::int32_t cam,
 
 // The body's DSE pass: CTAs [0, n_long) take the long tiles, the rest one
 // chunk each (GatherGraph).
-template <class S>
-__global__ void __launch_bounds__(kTile, DBAG_PASS_MINB) k_g_pass(DseArgs<S> A, GBufs<S> B, const GScal<S>* sc) {
+template <class S, class T = S>
+__global__ void __launch_bounds__(kTile, DBAG_PASS_MINB) k_g_pass(DseArgs<S, T> A, GBufs<S> B, const GScal<S>* sc) {
   __shared__ DseWork<S> sm;
   pdl_allow_dependents();
   const std::int32_t blk = blockIdx.x;

@@ -221,14 +221,14 @@ __global__ void k_residuals(std::int64_t N, const std::int32_t* __restrict__ slo
 // ---------------------------------------------------------- linearize ----
 // Fused K1+K2(+K3)+K5-E: gather, jets (or closed form), residual, Jacobian,
 // E = w Jc^T Jp. Jb row: [r0 r1 | J0[12] | J1[12] | w pad].
-template <class S, int MODE>
+template <class S, int MODE, class T = S>
 __global__ void __launch_bounds__(128) k_linearize(std::int64_t N, const std::int32_t* __restrict__ slot_cam,
                                                    const std::int32_t* __restrict__ slot_pt,
                                                    const std::int32_t* __restrict__ slot_edge,
                                                    std::int64_t edge_base, const S* __restrict__ px,
                                                    const S* __restrict__ py, const S* __restrict__ w,
                                                    const S* __restrict__ xc, const S* __restrict__ xp,
-                                                   S* __restrict__ Jb, S* __restrict__ E,
+                                                   S* __restrict__ Jb, T* __restrict__ E,
                                                    const std::int32_t* __restrict__ slot_chunk,
                                                    const std::int32_t* __restrict__ chunk_slot,
                                                    unsigned long long* bad_edge) {
@@ -257,12 +257,12 @@ __global__ void __launch_bounds__(128) k_linearize(std::int64_t N, const std::in
   }
   row[26] = wt;
   row[27] = S(0);
-  const std::size_t base = rec_at<S>(slot_chunk, chunk_slot, s);
+  const std::size_t base = rec_at<T>(slot_chunk, chunk_slot, s);
 #pragma unroll
   for (int i = 0; i < 9; ++i)
 #pragma unroll
     for (int j = 0; j < 3; ++j)
-      E[base + std::size_t(i * 3 + j) * kTile] = fm(wt, fa(fm(J[0][i], J[0][9 + j]), fm(J[1][i], J[1][9 + j])));
+      E[base + std::size_t(i * 3 + j) * kTile] = T(fm(wt, fa(fm(J[0][i], J[0][9 + j]), fm(J[1][i], J[1][9 + j]))));
 }
 
 // C[p] += w Jp^T Jp, w[p] -= w Jp^T r over the point's slots in edge order
@@ -536,10 +536,10 @@ struct PcgScal {
 // ----------------------------------------------------- DSE camera side ----
 // Halo slots after the all-reduce of their points' a_p: b_p = C_p^-1 a_p,
 // y_s = E_s b_p into the slot's own partial.
-template <class S>
+template <class S, class T = S>
 __global__ void k_halo_fix(std::int32_t n, const std::int32_t* __restrict__ halo_slot,
                            const std::int32_t* __restrict__ slot_dpt, const std::int32_t* __restrict__ halo_of,
-                           const S* __restrict__ halo_buf, const S* __restrict__ Cinv, const S* __restrict__ E,
+                           const S* __restrict__ halo_buf, const S* __restrict__ Cinv, const T* __restrict__ E,
                            const std::int32_t* __restrict__ slot_chunk, const std::int32_t* __restrict__ chunk_slot,
                            const std::int32_t* __restrict__ halo_pos, S* __restrict__ part) {
   const std::int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -550,11 +550,11 @@ __global__ void k_halo_fix(std::int32_t n, const std::int32_t* __restrict__ halo
 #pragma unroll
   for (int j = 0; j < 3; ++j) b[j] = halo_buf[std::size_t(halo_of[p]) * 3 + j];
   llt_solve<S, 3>(Cinv + std::size_t(p) * 9, b);
-  const S* e = E + rec_at<S>(slot_chunk, chunk_slot, s);
+  const T* e = E + rec_at<T>(slot_chunk, chunk_slot, s);
 #pragma unroll
   for (int r = 0; r < 9; ++r)
     part[std::size_t(halo_pos[i]) * 9 + r] =
-        (e[(r * 3) * kTile] * b[0] + e[(r * 3 + 1) * kTile] * b[1]) + e[(r * 3 + 2) * kTile] * b[2];
+        (S(e[(r * 3) * kTile]) * b[0] + S(e[(r * 3 + 1) * kTile]) * b[1]) + S(e[(r * 3 + 2) * kTile]) * b[2];
 }
 
 // Point rows between global order and device-point order:

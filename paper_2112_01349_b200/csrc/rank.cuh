@@ -85,9 +85,12 @@ struct Tally {  // dba/counters.hpp:11-24
   std::uint64_t edges = 0, block_ops = 0;
 };
 
-template <class S>
+// S: arithmetic and state type; T: storage type of the E lanes (T = S, or
+// float under FP64 arithmetic: the memory-lean variant).
+template <class S, class T = S>
 class Rank {
  public:
+  using Scalar = S;
   using Scal = dev::PcgScal<S>;
   static constexpr DType kT = sizeof(S) == 8 ? DType::f64 : DType::f32;
 
@@ -296,7 +299,7 @@ class Rank {
     DBAG_CUDA(cudaMemsetAsync(bad_.get(), 0xff, sizeof(unsigned long long), st_));
     if (N_ > 0) {
       const int blocks = static_cast<int>((N_ + 127) / 128);
-      auto kern = jac_mode_ == 1 ? dev::k_linearize<S, 1> : dev::k_linearize<S, 0>;
+      auto kern = jac_mode_ == 1 ? dev::k_linearize<S, 1, T> : dev::k_linearize<S, 0, T>;
       launch(kern, blocks, 128, N_, slot_cam_.get(), slot_dpt_.get(), slot_edge_.get(), plan_.range.start,
              slot_px_.get(), slot_py_.get(), slot_w_.get(), xc_.get(), xp_.get(), Jb_.get(), E_.get(), slot_chunk_.get(),
              chunk_slot_.get(), bad_.get());
@@ -535,7 +538,7 @@ class Rank {
     dev::GBufs<S> B = gbufs();
     dev::RedWs ws = red();
     dev::GScal<S>* sc = gsc_.get();
-    dev::DseArgs<S> A = dse_args(nullptr);
+    dev::DseArgs<S, T> A = dse_args(nullptr);
     const int cam_lane_blocks = static_cast<int>((static_cast<std::int64_t>(m_) * 32 / 3 + 255) / 256 + 1);
     DBAG_CUDA(cudaGraphCreate(&g_graph_, 0));
     cudaGraphConditionalHandle hw;
@@ -588,7 +591,7 @@ class Rank {
     g_unroll_ = DBAG_GRAPH_UNROLL;
     if (const char* ue = std::getenv("DBAG_UNROLL")) g_unroll_ = std::max(1, std::atoi(ue));
     for (int u = 0; u < g_unroll_; ++u) {
-      void* pass = reinterpret_cast<void*>(dev::k_g_pass<S>);
+      void* pass = reinterpret_cast<void*>(dev::k_g_pass<S, T>);
       const int pgrid = n_long_ + n_chunks_;
       const int psmem = 0;
       cur = u ? add_kernel_pdl(body, cur, pass, pgrid, dev::kTile, a_pass, psmem)
@@ -675,7 +678,7 @@ class Rank {
   double time_dse_pass(int reps) {
     DBAG_CUDA(cudaSetDevice(device_));
     if (!g_exec_) throw Error(DBAG_INVALID_ARGUMENT, "time_dse_pass needs a preceding graph DPCG");
-    const dev::DseArgs<S> A = dse_args(nullptr);
+    const dev::DseArgs<S, T> A = dse_args(nullptr);
     const dev::GBufs<S> B = gbufs();
     const dev::GScal<S>* sc = gsc_.get();
     const int grid = n_long_ + n_chunks_;
@@ -686,7 +689,7 @@ class Rank {
     cudaEvent_t e0, e1;
     DBAG_CUDA(cudaEventCreate(&e0));
     DBAG_CUDA(cudaEventCreate(&e1));
-    auto one = [&] { launch(dev::k_g_pass<S>, grid, dev::kTile, A, B, sc); };
+    auto one = [&] { launch(dev::k_g_pass<S, T>, grid, dev::kTile, A, B, sc); };
     one();  // warm-up
     DBAG_CUDA(cudaEventRecord(e0, st_));
     for (int r = 0; r < reps; ++r) one();
@@ -827,12 +830,12 @@ class Rank {
       if (w) std::copy(ww.begin() + d * 3, ww.begin() + d * 3 + 3, w + g * 3);
     }
     if (E) {
-      std::vector<S> e(E_.size());
-      DBAG_CUDA(cudaMemcpy(e.data(), E_.get(), sizeof(S) * e.size(), cudaMemcpyDeviceToHost));
+      std::vector<T> e(E_.size());
+      DBAG_CUDA(cudaMemcpy(e.data(), E_.get(), sizeof(T) * e.size(), cudaMemcpyDeviceToHost));
       for (std::int64_t s = 0; s < N_; ++s) {
         const std::int64_t ed = lay_.slot_edge[static_cast<std::size_t>(s)];
         const std::size_t at = rec_offset(s);
-        for (int k = 0; k < 27; ++k) E[ed * 27 + k] = e[at + static_cast<std::size_t>(k) * dev::kTile];
+        for (int k = 0; k < 27; ++k) E[ed * 27 + k] = S(e[at + static_cast<std::size_t>(k) * dev::kTile]);
       }
     }
   }
@@ -857,21 +860,21 @@ class Rank {
       DBAG_CUDA(cudaMemcpy(w_.get(), ww.data(), sizeof(S) * ww.size(), cudaMemcpyHostToDevice));
     }
     if (E_table) {
-      std::vector<S> e(E_.size());
-      DBAG_CUDA(cudaMemcpy(e.data(), E_.get(), sizeof(S) * e.size(), cudaMemcpyDeviceToHost));
+      std::vector<T> e(E_.size());
+      DBAG_CUDA(cudaMemcpy(e.data(), E_.get(), sizeof(T) * e.size(), cudaMemcpyDeviceToHost));
       for (std::int64_t s = 0; s < N_; ++s) {
         const std::int64_t ed = plan_.range.start + lay_.slot_edge[static_cast<std::size_t>(s)];
         const std::size_t at = rec_offset(s);
-        for (int k = 0; k < 27; ++k) e[at + static_cast<std::size_t>(k) * dev::kTile] = E_table[ed * 27 + k];
+        for (int k = 0; k < 27; ++k) e[at + static_cast<std::size_t>(k) * dev::kTile] = T(E_table[ed * 27 + k]);
       }
-      DBAG_CUDA(cudaMemcpy(E_.get(), e.data(), sizeof(S) * e.size(), cudaMemcpyHostToDevice));
+      DBAG_CUDA(cudaMemcpy(E_.get(), e.data(), sizeof(T) * e.size(), cudaMemcpyHostToDevice));
     }
     have_system_ = true;
   }
 
   std::size_t rec_offset(std::int64_t s) const {
     const std::int32_t c = lay_.slot_chunk[static_cast<std::size_t>(s)];
-    return static_cast<std::size_t>(c) * dev::Rec<S>::kLen +
+    return static_cast<std::size_t>(c) * dev::Rec<T>::kLen +
            static_cast<std::size_t>(s - lay_.chunk_slot[static_cast<std::size_t>(c)]);
   }
 
@@ -986,9 +989,9 @@ class Rank {
     if (MODE == 0 && H_ > 0) {
       comm_->allreduce_sum(halo_buf_.get(), 3 * H_, kT, st_);
       if (nh > 0)
-        launch(dev::k_halo_fix<S>, grid_for(nh, 128, 1 << 30), 128, nh, halo_slot_.get(), slot_dpt_.get(),
+        launch(dev::k_halo_fix<S, T>, grid_for(nh, 128, 1 << 30), 128, nh, halo_slot_.get(), slot_dpt_.get(),
                halo_of_.get(), static_cast<const S*>(halo_buf_.get()), static_cast<const S*>(Cinv_.get()),
-               static_cast<const S*>(E_.get()), slot_chunk_.get(), chunk_slot_.get(), halo_pos_.get(), part_.get());
+               static_cast<const T*>(E_.get()), slot_chunk_.get(), chunk_slot_.get(), halo_pos_.get(), part_.get());
     } else if (MODE == 2 && nh > 0) {
       // rhs: C and w are complete on every rank, so the chunk partials
       // already hold the halo slots' E_s C^-1 w; the halo slots' own
@@ -1003,7 +1006,7 @@ class Rank {
   // (kernels.cuh RecMeta); the E lanes are (re)written by k_linearize.
   void build_records(const std::vector<std::int32_t>& s_cam) {
     const std::size_t nc = static_cast<std::size_t>(std::max(n_chunks_, 1));
-    std::vector<S> recs(nc * dev::Rec<S>::kLen, S(0));
+    std::vector<T> recs(nc * dev::Rec<T>::kLen, T(0));
     std::vector<std::int32_t> long_first;
     const std::size_t nt = lay_.tile_pt.size() - 1;
     for (std::size_t t = 0; t < nt; ++t) {
@@ -1012,8 +1015,8 @@ class Rank {
       const std::int32_t ch0 = lay_.tile_chunk[t], ch1 = lay_.tile_chunk[t + 1];
       if (ch1 - ch0 > 1) long_first.push_back(ch0);
       for (std::int32_t c = ch0; c < ch1; ++c) {
-        auto* M = reinterpret_cast<dev::RecMeta*>(recs.data() + static_cast<std::size_t>(c) * dev::Rec<S>::kLen +
-                                                  dev::Rec<S>::kE);
+        auto* M = reinterpret_cast<dev::RecMeta*>(recs.data() + static_cast<std::size_t>(c) * dev::Rec<T>::kLen +
+                                                  dev::Rec<T>::kE);
         const std::int32_t c0 = lay_.chunk_slot[static_cast<std::size_t>(c)];
         const std::int32_t c1 = (c + 1 < ch1) ? lay_.chunk_slot[static_cast<std::size_t>(c) + 1]
                                               : lay_.dpt_ptr[static_cast<std::size_t>(p1)];
@@ -1057,8 +1060,8 @@ class Rank {
     halo_pos_.upload(hpos);
   }
 
-  dev::DseArgs<S> dse_args(const S* x) {
-    dev::DseArgs<S> a;
+  dev::DseArgs<S, T> dse_args(const S* x) {
+    dev::DseArgs<S, T> a;
     a.n_chunks = n_chunks_;
     a.rec = E_.get();
     a.x = x;
@@ -1076,9 +1079,9 @@ class Rank {
   template <int MODE>
   void stream_pass(const S* x) {
     if (n_chunks_ == 0) return;
-    const dev::DseArgs<S> a = dse_args(x);
-    launch(dev::k_dse_chunk<S, MODE>, n_chunks_, dev::kTile, a);
-    if (n_long_ > 0) launch(dev::k_dse_long<S, MODE>, n_long_, dev::kTile, a);
+    const dev::DseArgs<S, T> a = dse_args(x);
+    launch(dev::k_dse_chunk<S, MODE, T>, n_chunks_, dev::kTile, a);
+    if (n_long_ > 0) launch(dev::k_dse_long<S, MODE, T>, n_long_, dev::kTile, a);
   }
 
   template <int EPI>
@@ -1199,7 +1202,8 @@ class Rank {
   dev::GScal<S>* gsc_h_ = nullptr;
   cudaGraph_t g_graph_ = nullptr;
   cudaGraphExec_t g_exec_ = nullptr;
-  DevBuf<S> Jb_, E_, part_, halo_buf_;
+  DevBuf<S> Jb_, part_, halo_buf_;
+  DevBuf<T> E_;  // chunk records: E lanes (T) + RecMeta
   DevBuf<Scal> sc_;
   DevBuf<double> red_part_, dsc_, bounce_;
   DevBuf<unsigned> red_cnt_;

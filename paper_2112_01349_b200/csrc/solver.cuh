@@ -64,8 +64,8 @@ struct Trial {
   double shrink = 1.0;  // lambda factor on accept
 };
 
-template <class S>
-Trial run_trial(Rank<S>& rk, const dbag_config& c, double lambda, double cost) {
+template <class R>
+Trial run_trial(R& rk, const dbag_config& c, double lambda, double cost) {
   Trial t;
   try {
     rk.damp_factor(lambda, c.damping);
@@ -95,8 +95,8 @@ Trial run_trial(Rank<S>& rk, const dbag_config& c, double lambda, double cost) {
   return t;
 }
 
-template <class S>
-Outcome lm_solve_rank(Rank<S>& rk, const dbag_config& c, std::int64_t num_obs) {
+template <class R>
+Outcome lm_solve_rank(R& rk, const dbag_config& c, std::int64_t num_obs) {
   const auto t0 = std::chrono::steady_clock::now();
   const int K = rk.plan().ranks, me = rk.plan().rank;
   Outcome st;
@@ -181,8 +181,8 @@ Outcome lm_solve_rank(Rank<S>& rk, const dbag_config& c, std::int64_t num_obs) {
 
 // One LM iteration from the current state (relinearized) without committing
 // it: the bench "step" (identical work every call).
-template <class S>
-Trial probe_step(Rank<S>& rk, const dbag_config& c, double lambda) {
+template <class R>
+Trial probe_step(R& rk, const dbag_config& c, double lambda) {
   std::int64_t bad = -1;
   const double cost = rk.cost(false, &bad);
   if (!std::isfinite(cost)) throw degenerate_depth(bad);

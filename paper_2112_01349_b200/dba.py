@@ -366,6 +366,9 @@ class SolverConfig:
     mse: int = MSE_HALF_PER_OBSERVATION
     jacobian: int = JACOBIAN_AUTODIFF
     check_rank_identity: bool = False
+    # B200 extension: FP64 solve with the coupling blocks E
+    # stored in FP32 (half the DSE stream; not the reference's numerics)
+    coupling_fp32: bool = False
 
     def c_struct(self) -> N.Config:
         c = N.Config()
@@ -373,6 +376,7 @@ class SolverConfig:
         c.pcg_max_iters, c.lambda0, c.lambda_max = self.pcg_max_iters, self.lambda0, self.lambda_max
         c.rel_tol, c.step_tol, c.damping = self.rel_tol, self.step_tol, self.damping
         c.mse_half, c.jacobian, c.check_rank_identity = self.mse, self.jacobian, int(self.check_rank_identity)
+        c.coupling_fp32 = int(self.coupling_fp32)
         return c
 
 
@@ -541,12 +545,12 @@ class RankContext:
     """One rank's device context (include/dbag.h "rank context"): the operator
     level of lm_solve_rank. K = 1 unless created with ``nccl=(rank, nranks, uid)``."""
 
-    def __init__(self, device: int = 0, precision: int = 8, nccl=None):
+    def __init__(self, device: int = 0, precision: int = 8, nccl=None, coupling_fp32: bool = False):
         self.precision = precision
         self.dtype = np.float64 if precision == 8 else np.float32
         h = C.c_void_p()
         if nccl is None:
-            _check(N.lib().dbag_create(device, precision, C.byref(h)))
+            _check(N.lib().dbag_create_ex(device, precision, int(coupling_fp32), C.byref(h)))
         else:
             rank, nranks, uid = nccl
             _check(N.lib().dbag_create_nccl(device, rank, nranks, C.create_string_buffer(bytes(uid), 128), precision,

@@ -461,3 +461,29 @@ def test_graph_fold_step_variants(variant, monkeypatch):
     p = ring(300, 900, 4, radius=1.0, noise=0.5, seed=11)
     cfg = dba.SolverConfig(max_iterations=4, pcg_tol=1e-12, pcg_max_iters=2000)
     _compare_histories(dba.lm_solve(p, cfg), O.lm_solve(p, cfg), 1e-9)
+
+
+def test_coupling_fp32_memory_lean_variant():
+    """Row f4: FP64 solve with the coupling blocks stored in
+    FP32. Not the reference's numerics — E carries ~6e-8 relative rounding,
+    which this ill-conditioned ring amplifies to a few 1e-6 in the cost — so
+    the bar is closeness to the FP64 path: S x within 1e-6, the same
+    accept/reject sequence and costs within 1e-4 relative (the north star's
+    FP32 bar) at tight PCG; K = 2 reproduces K = 1 of the same variant."""
+    p = ring(40, 400, 8, radius=1.0, noise=0.5, seed=2024, nobs=3197)
+    x = np.random.default_rng(3).standard_normal(9 * p.num_cameras)
+    outs = []
+    for lean in (False, True):
+        with dba.RankContext(0, 8, coupling_fp32=lean) as c:
+            c.upload(p)
+            c.linearize()
+            c.damp_factor(1e-3, dba.DAMPING_DIAG_SCALED)
+            outs.append(c.dse(x))
+    assert 0 < rel(outs[1], outs[0]) < 1e-6
+    cfg = dba.SolverConfig(max_iterations=6, pcg_tol=1e-12, pcg_max_iters=2000)
+    a = dba.lm_solve(p, cfg)
+    b = dba.lm_solve(p, dba.SolverConfig(max_iterations=6, pcg_tol=1e-12, pcg_max_iters=2000, coupling_fp32=True))
+    _compare_histories(b, a, 1e-4, check_lambda=False)
+    b2 = dba.lm_solve(p, dba.SolverConfig(max_iterations=6, pcg_tol=1e-12, pcg_max_iters=2000, coupling_fp32=True,
+                                          workers=2))
+    _compare_histories(b2, b, 1e-6, check_lambda=False)
