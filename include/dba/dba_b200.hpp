@@ -209,6 +209,7 @@ struct SolverConfig {
   JacobianMode jacobian = JacobianMode::autodiff;
   bool check_rank_identity = false;
   std::vector<int> devices{0};  // B200 placement: rank r -> devices[r % size]
+  bool coupling_fp32 = false;     // B200 extension (row f4): E blocks stored in FP32 under an FP64 solve
 
   dbag_config c_view() const {
     dbag_config c;
@@ -225,6 +226,7 @@ struct SolverConfig {
     c.mse_half = mse == MseConvention::half_per_observation ? 1 : 0;
     c.jacobian = jacobian == JacobianMode::analytic ? 1 : 0;
     c.check_rank_identity = check_rank_identity ? 1 : 0;
+    c.coupling_fp32 = coupling_fp32 ? 1 : 0;
     return c;
   }
 };
