@@ -253,8 +253,18 @@ __device__ __forceinline__ void dse_chunk(const DseArgs<S, T>& A, DseWork<S>& sm
   dse_chunk_at<S, MODE>(A, sm, A.rec + std::size_t(chunk) * Rec<T>::kLen, gx);
 }
 
+// Resident CTAs per SM the chunk pass is compiled for (register budget):
+// measured best 5 with FP64 E lanes in registers, 7 with FP32 lanes.
+#ifndef DBAG_PASS_MINB_F32E
+#define DBAG_PASS_MINB_F32E 7
+#endif
+template <class T>
+constexpr int pass_min_blocks() {
+  return sizeof(T) == 4 ? DBAG_PASS_MINB_F32E : 5;
+}
+
 template <class S, int MODE, class T = S>
-__global__ void __launch_bounds__(kTile, 5) k_dse_chunk(DseArgs<S, T> A) {
+__global__ void __launch_bounds__(kTile, pass_min_blocks<T>()) k_dse_chunk(DseArgs<S, T> A) {
   __shared__ DseWork<S> sm;
   dse_chunk<S, MODE>(A, sm, blockIdx.x, GatherX<S>{A.x});
 }
