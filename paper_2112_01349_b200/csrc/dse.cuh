@@ -47,16 +47,22 @@ struct DseArgs {
   std::int32_t n_long;
 };
 
+// Shared work area of a chunk pass. a (3 x kTile), b (3 x kTile) and the
+// staged camera vectors xs live only through the point solves; y (9 x kTile)
+// only from then on, so y overlays them (a smaller footprint leaves L1 room
+// for the in-flight E lines of more resident CTAs).
 template <class S>
 struct DseWork {
-  S a[kTile][3];
-  S b[kTile][3];
-  S y[kTile][9];
-  S xs[kXsCams * 9];  // the chunk's camera vectors, gathered once per distinct camera
+  S buf[kTile * 9];
   std::int32_t upart[kTile];
   std::uint8_t uslot[kTile];
   std::uint8_t ubeg[kTile + 8];
+  __device__ __forceinline__ S (*a())[3] { return reinterpret_cast<S(*)[3]>(buf); }
+  __device__ __forceinline__ S (*b())[3] { return reinterpret_cast<S(*)[3]>(buf + 3 * kTile); }
+  __device__ __forceinline__ S* xs() { return buf + 6 * kTile; }
+  __device__ __forceinline__ S (*y())[9] { return reinterpret_cast<S(*)[9]>(buf); }
 };
+static_assert(6 * kTile + kXsCams * 9 <= 9 * kTile, "a, b and xs must fit under y");
 
 template <class T>
 __device__ __forceinline__ const RecMeta& rec_meta(const T* R) {
@@ -209,7 +215,7 @@ __device__ __forceinline__ void dse_chunk_at(const DseArgs<S, T>& A, DseWork<S>&
     if (staged) {
 #pragma unroll
       for (int j = 0; j < 3; ++j)
-        if (tid + kTile * j < nu * 9) sm.xs[tid + kTile * j] = gx.combine(graw[j]);
+        if (tid + kTile * j < nu * 9) sm.xs()[tid + kTile * j] = gx.combine(graw[j]);
       __syncthreads();
     }
     S a[3] = {S(0), S(0), S(0)};
@@ -217,14 +223,14 @@ __device__ __forceinline__ void dse_chunk_at(const DseArgs<S, T>& A, DseWork<S>&
       const std::int32_t cam = staged ? 0 : M.cam[tid];
 #pragma unroll
       for (int i = 0; i < 9; ++i) {
-        const S xv = staged ? sm.xs[su * 9 + i] : gx(cam, i);
+        const S xv = staged ? sm.xs()[su * 9 + i] : gx(cam, i);
         a[0] += e[i * 3 + 0] * xv;
         a[1] += e[i * 3 + 1] * xv;
         a[2] += e[i * 3 + 2] * xv;
       }
     }
 #pragma unroll
-    for (int j = 0; j < 3; ++j) sm.a[tid][j] = a[j];
+    for (int j = 0; j < 3; ++j) sm.a()[tid][j] = a[j];
   }
   __syncthreads();
   if (tid < np) {
@@ -232,18 +238,19 @@ __device__ __forceinline__ void dse_chunk_at(const DseArgs<S, T>& A, DseWork<S>&
     if (MODE != 2)
       for (int q = pb0; q < pb1; ++q)
 #pragma unroll
-        for (int j = 0; j < 3; ++j) tt[j] += sm.a[q][j];
+        for (int j = 0; j < 3; ++j) tt[j] += sm.a()[q][j];
     finish_point<S, MODE>(A, p0 + tid, L, wv, tt, b);
 #pragma unroll
-    for (int j = 0; j < 3; ++j) sm.b[tid][j] = b[j];
+    for (int j = 0; j < 3; ++j) sm.b()[tid][j] = b[j];
   }
   __syncthreads();
   if constexpr (MODE != 1) {
-    const S b0 = sm.b[pti][0], b1 = sm.b[pti][1], b2 = sm.b[pti][2];
+    const S b0 = sm.b()[pti][0], b1 = sm.b()[pti][1], b2 = sm.b()[pti][2];
+    __syncthreads();  // y overlays b
 #pragma unroll
-    for (int i = 0; i < 9; ++i) sm.y[tid][i] = (e[i * 3] * b0 + e[i * 3 + 1] * b1) + e[i * 3 + 2] * b2;
+    for (int i = 0; i < 9; ++i) sm.y()[tid][i] = (e[i * 3] * b0 + e[i * 3 + 1] * b1) + e[i * 3 + 2] * b2;
     __syncthreads();
-    fold_cameras(A, nu, sm.ubeg, sm.uslot, sm.upart, YRows<S>{sm.y});
+    fold_cameras(A, nu, sm.ubeg, sm.uslot, sm.upart, YRows<S>{sm.y()});
     __syncthreads();
   }
 }
@@ -258,9 +265,12 @@ __device__ __forceinline__ void dse_chunk(const DseArgs<S, T>& A, DseWork<S>& sm
 #ifndef DBAG_PASS_MINB_F32E
 #define DBAG_PASS_MINB_F32E 7
 #endif
+#ifndef DBAG_PASS_MINB_F64E
+#define DBAG_PASS_MINB_F64E 5
+#endif
 template <class T>
 constexpr int pass_min_blocks() {
-  return sizeof(T) == 4 ? DBAG_PASS_MINB_F32E : 5;
+  return sizeof(T) == 4 ? DBAG_PASS_MINB_F32E : DBAG_PASS_MINB_F64E;
 }
 
 template <class S, int MODE, class T = S>
@@ -295,33 +305,34 @@ __device__ __forceinline__ void dse_long(const DseArgs<S, T>& A, DseWork<S>& sm,
     }
   }
 #pragma unroll
-  for (int j = 0; j < 3; ++j) sm.a[tid][j] = a[j];
+  for (int j = 0; j < 3; ++j) sm.a()[tid][j] = a[j];
   __syncthreads();
   if (tid == 0) {
     S tt[3] = {S(0), S(0), S(0)}, b[3];
     if (MODE != 2)
       for (int k = 0; k < kTile; ++k)
 #pragma unroll
-        for (int j = 0; j < 3; ++j) tt[j] += sm.a[k][j];
+        for (int j = 0; j < 3; ++j) tt[j] += sm.a()[k][j];
     S L[9], wv[3];
     load_point<S, MODE>(A, p, L, wv);
     finish_point<S, MODE>(A, p, L, wv, tt, b);
 #pragma unroll
-    for (int j = 0; j < 3; ++j) sm.b[0][j] = b[j];
+    for (int j = 0; j < 3; ++j) sm.b()[0][j] = b[j];
   }
   if constexpr (MODE != 1) {
+    __syncthreads();
+    const S b0 = sm.b()[0][0], b1 = sm.b()[0][1], b2 = sm.b()[0][2];  // y overlays b below
     for (std::int32_t c = c0; c < c0 + nchunk; ++c) {
       const T* R = A.rec + std::size_t(c) * Rec<T>::kLen;
       const RecMeta& M = rec_meta(R);
       __syncthreads();
       stage_meta(M, sm);
-      const S b0 = sm.b[0][0], b1 = sm.b[0][1], b2 = sm.b[0][2];
 #pragma unroll
       for (int i = 0; i < 9; ++i)
-        sm.y[tid][i] = (S(R[(i * 3) * kTile + tid]) * b0 + S(R[(i * 3 + 1) * kTile + tid]) * b1) +
+        sm.y()[tid][i] = (S(R[(i * 3) * kTile + tid]) * b0 + S(R[(i * 3 + 1) * kTile + tid]) * b1) +
                        S(R[(i * 3 + 2) * kTile + tid]) * b2;
       __syncthreads();
-      fold_cameras(A, M.nu, sm.ubeg, sm.uslot, sm.upart, YRows<S>{sm.y});
+      fold_cameras(A, M.nu, sm.ubeg, sm.uslot, sm.upart, YRows<S>{sm.y()});
     }
   }
   __syncthreads();
