@@ -487,3 +487,24 @@ def test_coupling_fp32_memory_lean_variant():
     b2 = dba.lm_solve(p, dba.SolverConfig(max_iterations=6, pcg_tol=1e-12, pcg_max_iters=2000, coupling_fp32=True,
                                           workers=2))
     _compare_histories(b2, b, 1e-6, check_lambda=False)
+
+
+@pytest.mark.parametrize("k", [1, 2])
+def test_unobserved_camera_and_point(k):
+    """A camera and a point no observation references (BAProblem::validate
+    warns, dba/problem.hpp:231-255): their parameters stay untouched and the
+    trajectory matches the oracle; an edge-less problem fails like
+    partition_edges (K > N, dba/partition.hpp:76-103)."""
+    base = ring(12, 80, 4, seed=9, radius=1.0, noise=0.5)
+    cams, pts, cid, pid, px, py, _ = base.arrays()
+    cams2, pts2 = np.vstack([cams, cams[0] + 0.01]), np.vstack([pts, pts[0] + 0.02])
+    p = dba.BAProblem.from_arrays(cams2, pts2, cid, pid, np.stack([px, py], 1))
+    assert len(p.validate()) == 2
+    cfg = dba.SolverConfig(max_iterations=4, workers=k, pcg_tol=1e-12, pcg_max_iters=2000)
+    g, o = dba.lm_solve(p, cfg), O.lm_solve(p, cfg)
+    _compare_histories(g, o, 1e-9)
+    assert np.array_equal(g.x_c.reshape(-1, 9)[12], cams2[12]) and np.array_equal(g.x_p.reshape(-1, 3)[80], pts2[80])
+    assert np.abs(g.x_c - o.x_c).max() < 1e-6 and np.abs(g.x_p - o.x_p).max() < 1e-8
+    empty = dba.BAProblem.from_arrays(cams[:2], pts[:3], np.zeros(0, np.int32), np.zeros(0, np.int32), np.zeros((0, 2)))
+    with pytest.raises(dba.InvalidArgumentError):
+        dba.lm_solve(empty, dba.SolverConfig(max_iterations=3))
