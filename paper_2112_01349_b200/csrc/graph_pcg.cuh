@@ -1,22 +1,26 @@
 // graph_pcg.cuh — DPCG as a CUDA graph with device-side control flow.
 //
 // dpcg (dba/solver.hpp:202-257) for a single rank, every recurrence on the
-// device and the loop itself in the graph: one conditional WHILE node whose
-// body is kGraphUnroll copies of three kernels,
-//   k_g_pass  the fused DSE pass over E (one CTA per chunk, long tiles first)
-//             gathering p formed on the fly from z and the previous p,
-//             writing camera-major partials;
-//   k_g_fold  warp per camera: c = fold(partials) in chunk order, p stored,
-//             q = B_d p - c, the camera's p.q term;
-//   k_g_step  alpha = rho / sum(p.q) (camera order), x += alpha p,
-//             r -= alpha q, z = B^-1 r, rho, |r|^2 and the loop decision
-//             (cudaGraphSetConditional) from a deterministic grid reduction.
-// Every 50th iteration the body runs once more as a residual-refresh pass
-// (DSE on x, r = g - S x), selected by a device-side phase flag. Unrolling
-// amortises the WHILE node's relaunch; once the loop is decided the copies
-// left in the body return at entry (done flag). One graph launch runs the
-// whole inner solve with no host round trip, no persistent-kernel grid
-// barriers and full-occupancy DSE tiles.
+// device and the loop itself in the graph: k_g_init, then one conditional
+// WHILE node whose body is DBAG_GRAPH_UNROLL copies of
+//   k_g_pass   the DSE pass over E (one CTA per chunk, long tiles first),
+//              gathering p = z + beta p_prev (or x) once per (chunk,
+//              camera) and writing camera-major partials;
+// followed by the camera fold + PCG step, in one of three forms chosen by m:
+//   k_g_fsc    m <= 544: one thread-block cluster (<= 16 CTAs), warp per
+//              camera; p'q and rho, |r|^2 over distributed shared memory;
+//   k_g_fs     m <= 4736: warp per camera, software grid barrier for p'q,
+//              last-block grid reduction for rho, |r|^2;
+//   k_g_fold + k_g_step  beyond: the fold and the step as two kernels.
+// Each computes c = fold(partials) in chunk order, q = B_d p - c, p'q (camera
+// order), alpha, x += alpha p, r -= alpha q, z = B^-1 r, rho, |r|^2 and the
+// loop decision (cudaGraphSetConditional). Consecutive kernels are linked by
+// programmatic-dependent-launch edges: a kernel's constant loads run before
+// it waits on its predecessor. Every 50th iteration the body runs once more
+// as a residual-refresh pass (DSE on x, r = g - S x), selected by a device
+// phase flag; once the loop is decided the copies left in the body return at
+// entry (done flag). One graph launch runs the whole inner solve with no host
+// round trip.
 //
 // Loop control matches the reference: stop when |r| <= tol |g| or
 // n == max_iters; rho (after z = B^-1 r) and p'q breakdowns stop with status

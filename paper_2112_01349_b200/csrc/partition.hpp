@@ -177,7 +177,7 @@ inline ShardPlan plan_shard(const std::int32_t* cam_id, const std::int32_t* pt_i
   return s;
 }
 
-// Device layout of one shard for the fused DSE (kernels.cuh k_dse_fused):
+// Device layout of one shard for the DSE chunk pass (dse.cuh):
 //   * device points: the shard's local points ordered by their smallest
 //     camera id (ties by local id) so that a tile of consecutive points
 //     touches few cameras; each point keeps its slots in edge order, so

@@ -10,4 +10,4 @@ with dba.RankContext(0, 8) as ctx:
     ctx.upload(p)
     cfg = dba.SolverConfig()
     ctx.probe_step(cfg.lambda0, cfg)
-    print(name, os.environ.get("DBAG_DSE", "pipe"), "pass ms", ctx.time_dse_pass(20), flush=True)
+    print(name, "k_g_pass ms", ctx.time_dse_pass(20), flush=True)
