@@ -192,8 +192,9 @@ def dse_roofline(ctx, prof, b_dse, peak, steps, total_ms, world):
             "launches_per_step": dse_per_step, "in_graph_ms_per_dse": loop_ms_per_dse,
             "share_of_step": per * dse_per_step / max(total_ms / max(steps, 1), 1e-9),
             "note": "achieved = algorithmic DSE bytes per pass (SURVEY 8d) / device ms per launch; "
-                    "trafalgar-257's E (49 MB) stays L2-resident across the passes of a step, "
-                    "see secondary (venice-1778, E 1.2 GB) for the HBM-bound size"}
+                    "the pass re-reads E from HBM each PCG iteration (ncu, warm caches: L2 hit rate ~20 %) "
+                    "and is latency-bound at trafalgar-257's 1780 chunk CTAs (2.4 waves); "
+                    "traffic = ncu dram bytes of one standalone launch (profiles/ncu_traffic.json)"}
 
 
 def run_ours(args):
