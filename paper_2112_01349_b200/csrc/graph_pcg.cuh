@@ -569,19 +569,18 @@ __global__ void __launch_bounds__(kFscThreads, 1) k_g_fsc(GBufs<S> B, GScal<S>* 
     }
   }
   pdl_wait();
+  // the scalars, every vector row (both p buffers: n picks one) and the
+  // partials go out in one round trip; the done check follows the fold
   const int done = sc->done, n = sc->n, phase = sc->phase;
   const S beta = sc->beta;
   const double rho_cur = sc->rho;
-  if (done) return;  // uniform over the cluster
-  DBAG_TL(n, 1, rank == 0 && threadIdx.x == 0);
-  DBAG_TL(n, 2, rank == 0 && threadIdx.x == 0);
-  const bool pcg = phase == 0;
-  S v[CPW], qv[CPW], xr[CPW], rr[CPW], gr[CPW];
-  double pq_w = 0.0;
+  S v[CPW], qv[CPW], xr[CPW], rr[CPW], gr[CPW], zr[CPW], pa[CPW], pb[CPW], cr[CPW];
 #pragma unroll
   for (int j = 0; j < CPW; ++j) {
     const std::size_t at = std::size_t(cam[j]) * 9 + row;
-    const S zr = B.z[at], pp = p_cur(B, n + 1)[at];
+    zr[j] = B.z[at];
+    pa[j] = B.p0[at];
+    pb[j] = B.p1[at];
     xr[j] = B.x[at];
     rr[j] = B.r[at];
     gr[j] = B.g[at];
@@ -599,16 +598,26 @@ __global__ void __launch_bounds__(kFscThreads, 1) k_g_fsc(GBufs<S> B, GScal<S>* 
       for (int o = 16; o > 0; o >>= 1) acc[i] += __shfl_down_sync(0xffffffffu, acc[i], o);
       acc[i] = __shfl_sync(0xffffffffu, acc[i], 0);
     }
-    S cr = acc[0];
+    cr[j] = acc[0];
 #pragma unroll
     for (int i = 1; i < 9; ++i)
-      if (row == i) cr = acc[i];
-    v[j] = pcg ? (n == 0 ? zr : zr + beta * pp) : xr[j];
+      if (row == i) cr[j] = acc[i];
+  }
+  if (done != 0 || n < 0 || beta != beta) return;  // uniform over the cluster (n < 0, NaN beta: never)
+  DBAG_TL(n, 1, rank == 0 && threadIdx.x == 0);
+  DBAG_TL(n, 2, rank == 0 && threadIdx.x == 0);
+  const bool pcg = phase == 0;
+  double pq_w = 0.0;
+#pragma unroll
+  for (int j = 0; j < CPW; ++j) {
+    const std::size_t at = std::size_t(cam[j]) * 9 + row;
+    const S pp = ((n + 1) & 1) ? pb[j] : pa[j];  // p_cur(B, n + 1)
+    v[j] = pcg ? (n == 0 ? zr[j] : zr[j] + beta * pp) : xr[j];
     if (pcg && on[j] && lane < 9) p_cur(B, n)[at] = v[j];
     S d = S(0);
 #pragma unroll
     for (int k = 0; k < 9; ++k) d += bd[j][k] * __shfl_sync(0xffffffffu, v[j], k);
-    qv[j] = d - cr;
+    qv[j] = d - cr[j];
     double t = (lane < 9 && on[j]) ? double(v[j]) * double(qv[j]) : 0.0;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) t += __shfl_down_sync(0xffffffffu, t, o);
