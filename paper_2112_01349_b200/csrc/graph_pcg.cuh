@@ -80,7 +80,15 @@ struct GBufs {
   const std::int32_t* cam_part_ptr;
   const S* part;
   double* pq_cam;  // per-camera p.q of the running pass
+  const S* c_total;  // K > 1: E C^-1 E^T p summed over ranks (k_g_fold reads it instead of the partials)
 };
+
+// The WHILE node's condition; kNoCond outside a graph (the run-ahead
+// stream loop of K > 1 ranks, Rank::pcg_stream).
+constexpr cudaGraphConditionalHandle kNoCond = ~0ull;
+__device__ __forceinline__ void set_conditional(cudaGraphConditionalHandle h, unsigned v) {
+  if (h != kNoCond) cudaGraphSetConditional(h, v);
+}
 
 template <class S>
 __device__ __forceinline__ S* p_cur(const GBufs<S>& B, int n) {
@@ -197,7 +205,7 @@ __global__ void __launch_bounds__(kRedThreads) k_g_init(GBufs<S> B, RedWs ws, GS
     sc->dse_count = fin[1] != 0.0 ? 1 : 0;  // the reference's DSE on x0 (dba/solver.hpp:217)
     const bool loop = fin[1] != 0.0 && continue_loop(sc);
     sc->done = loop ? 0 : 1;
-    cudaGraphSetConditional(h_while, loop ? 1u : 0u);
+    set_conditional(h_while, loop ? 1u : 0u);
   }
 }
 
@@ -209,19 +217,23 @@ __device__ __forceinline__ void camera_fold(const GBufs<S>& B, std::int32_t cam,
   S acc[9];
 #pragma unroll
   for (int i = 0; i < 9; ++i) acc[i] = S(0);
-  for (std::int32_t k = B.cam_part_ptr[cam] + lane; k < B.cam_part_ptr[cam + 1]; k += 32) {
-    const S* pp = B.part + std::size_t(k) * 9;
-#pragma unroll
-    for (int i = 0; i < 9; ++i) acc[i] += pp[i];
-  }
-#pragma unroll
-  for (int i = 0; i < 9; ++i) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) acc[i] += __shfl_down_sync(0xffffffffu, acc[i], o);
-    acc[i] = __shfl_sync(0xffffffffu, acc[i], 0);
-  }
   const std::size_t at = std::size_t(cam) * 9;
   const int row = lane < 9 ? lane : 0;
+  if (B.c_total) {  // already folded and summed over ranks
+    acc[0] = B.c_total[at + row];
+  } else {
+    for (std::int32_t k = B.cam_part_ptr[cam] + lane; k < B.cam_part_ptr[cam + 1]; k += 32) {
+      const S* pp = B.part + std::size_t(k) * 9;
+#pragma unroll
+      for (int i = 0; i < 9; ++i) acc[i] += pp[i];
+    }
+#pragma unroll
+    for (int i = 0; i < 9; ++i) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) acc[i] += __shfl_down_sync(0xffffffffu, acc[i], o);
+      acc[i] = __shfl_sync(0xffffffffu, acc[i], 0);
+    }
+  }
   S v;
   if (pcg) {
     const S zr = B.z[at + row];
@@ -234,9 +246,10 @@ __device__ __forceinline__ void camera_fold(const GBufs<S>& B, std::int32_t cam,
 #pragma unroll
   for (int k = 0; k < 9; ++k) d += B.Bd[std::size_t(cam) * 81 + row * 9 + k] * __shfl_sync(0xffffffffu, v, k);
   S c = acc[0];
+  if (!B.c_total)
 #pragma unroll
-  for (int i = 1; i < 9; ++i)
-    if (row == i) c = acc[i];
+    for (int i = 1; i < 9; ++i)
+      if (row == i) c = acc[i];
   const S qv = d - c;
   double pq = 0.0;
   if (lane < 9) {
@@ -279,7 +292,7 @@ __device__ __forceinline__ void finish_iteration(GScal<S>* sc, double rho, doubl
   sc->beta = S(rho / sc->rho_prev);
   const bool loop = continue_loop(sc);
   sc->done = loop ? 0 : 1;
-  cudaGraphSetConditional(h_while, loop ? 1u : 0u);
+  set_conditional(h_while, loop ? 1u : 0u);
 }
 
 // Camera fold of the pass: warp per camera (camera_fold).
@@ -326,7 +339,7 @@ __global__ void __launch_bounds__(kRedThreads) k_g_step(GBufs<S> B, RedWs ws, GS
         sc->status = 2;
         sc->dse_count += 1;
         sc->done = 1;
-        cudaGraphSetConditional(h_while, 0u);
+        set_conditional(h_while, 0u);
       }
       return;
     }
@@ -365,7 +378,7 @@ __global__ void __launch_bounds__(kRedThreads) k_g_step(GBufs<S> B, RedWs ws, GS
     }
     if (hand_over) {
       sc->phase = 1;
-      cudaGraphSetConditional(h_while, 1u);
+      set_conditional(h_while, 1u);
     } else {
       sc->phase = 0;
       finish_iteration(sc, fin[0], fin[1], h_while);
@@ -489,7 +502,7 @@ __global__ void __launch_bounds__(kRedThreads) k_g_fs(GBufs<S> B, RedWs ws, GSca
         sc->status = 2;
         sc->dse_count += 1;
         sc->done = 1;
-        cudaGraphSetConditional(h_while, 0u);
+        set_conditional(h_while, 0u);
       }
       return;
     }
@@ -523,7 +536,7 @@ __global__ void __launch_bounds__(kRedThreads) k_g_fs(GBufs<S> B, RedWs ws, GSca
     }
     if (hand_over) {
       sc->phase = 1;
-      cudaGraphSetConditional(h_while, 1u);
+      set_conditional(h_while, 1u);
     } else {
       sc->phase = 0;
       finish_iteration(sc, fin[0], fin[1], h_while);
@@ -651,7 +664,7 @@ __global__ void __launch_bounds__(kFscThreads, 1) k_g_fsc(GBufs<S> B, GScal<S>* 
         sc->status = 2;
         sc->dse_count += 1;
         sc->done = 1;
-        cudaGraphSetConditional(h_while, 0u);
+        set_conditional(h_while, 0u);
       }
       return;
     }
@@ -718,7 +731,7 @@ __global__ void __launch_bounds__(kFscThreads, 1) k_g_fsc(GBufs<S> B, GScal<S>* 
     }
     if (hand_over) {
       sc->phase = 1;
-      cudaGraphSetConditional(h_while, 1u);
+      set_conditional(h_while, 1u);
     } else {
       sc->phase = 0;
       finish_iteration(sc, rho, rn, h_while);

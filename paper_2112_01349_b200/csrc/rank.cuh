@@ -409,6 +409,10 @@ class Rank {
       const std::string m = mode ? mode : "graph";
       if (m == "graph" && n_chunks_ > 0 && m_ > 0) return pcg_graph(tol, max_iters);
     }
+    if (comm_->size() > 1 && n_chunks_ > 0 && m_ > 0) {
+      const char* mode = std::getenv("DBAG_PCG");
+      if (!(mode && std::string(mode) == "host")) return pcg_stream(tol, max_iters);
+    }
     S* x = dxc_.get();
     const std::int64_t len = static_cast<std::int64_t>(m_) * 9;
     dse_count_ = 0;
@@ -465,6 +469,79 @@ class Rank {
     return {n, r_norm <= tol * rhs_norm};
   }
 
+  // ---- DPCG for K > 1 ranks: the graph body's kernels, run ahead ----------
+  // The same device-side state machine as the graph (k_g_init, k_g_pass,
+  // k_g_fold, k_g_step; scalars, loop decision, breakdowns and refresh
+  // passes all on the device), with the cross-rank steps between them: the
+  // halo all-reduce + k_halo_fix after the pass, the camera fold
+  // (k_cam_reduce) + its all-reduce before k_g_fold. The host enqueues
+  // kRunAhead body passes at a time and reads the scalars once per batch
+  // (instead of once per PCG iteration); passes after the loop decision
+  // return at entry, and every rank enqueues the same collectives, so the
+  // call sequence stays aligned across ranks.
+  PcgOut pcg_stream(double tol, int max_iters) {
+    constexpr int kRunAhead = 8;
+    if (!gsc_.get()) {
+      gsc_.alloc(1);
+      DBAG_CUDA(cudaMallocHost(&gsc_h_, sizeof(dev::GScal<S>)));
+    }
+    if (g_pq_cam_.size() < static_cast<std::size_t>(std::max(m_, 1))) g_pq_cam_.alloc(std::max<std::size_t>(m_, 1));
+    dev::GBufs<S> B = gbufs();
+    B.c_total = ctmp_.get();
+    const dev::RedWs ws = red();
+    dev::GScal<S>* sc = gsc_.get();
+    const dev::GScal<S>* csc = sc;
+    const dev::DseArgs<S, T> A = dse_args(nullptr);
+    dev::GScal<S> init{};
+    init.tol = tol;
+    init.max_iters = max_iters;
+    *gsc_h_ = init;
+    DBAG_CUDA(cudaMemcpyAsync(sc, gsc_h_, sizeof(init), cudaMemcpyHostToDevice, st_));
+    const int lane_blocks = static_cast<int>((static_cast<std::int64_t>(m_) * 32 / 3 + 255) / 256 + 1);
+    const int warp_blocks = static_cast<int>((static_cast<std::int64_t>(m_) * 32 + 255) / 256);
+    const bool prof = profiling_;
+    if (prof) DBAG_CUDA(cudaEventRecord(prof_event(), st_));
+    launch(dev::k_g_init<S>, lane_blocks, dev::kRedThreads, B, ws, sc, dev::kNoCond);
+    const std::int32_t nh = static_cast<std::int32_t>(lay_.halo_slot.size());
+    std::int64_t passes = 0;
+    for (;;) {
+      for (int u = 0; u < kRunAhead; ++u, ++passes) {
+        if (H_ > 0) DBAG_CUDA(cudaMemsetAsync(halo_buf_.get(), 0, sizeof(S) * 3 * static_cast<std::size_t>(H_), st_));
+        launch(dev::k_g_pass<S, T>, n_long_ + n_chunks_, dev::kTile, A, B, csc);
+        if (H_ > 0) {
+          comm_->allreduce_sum(halo_buf_.get(), 3 * H_, kT, st_);
+          if (nh > 0)
+            launch(dev::k_halo_fix<S, T>, grid_for(nh, 128, 1 << 30), 128, nh, halo_slot_.get(), slot_dpt_.get(),
+                   halo_of_.get(), static_cast<const S*>(halo_buf_.get()), static_cast<const S*>(Cinv_.get()),
+                   static_cast<const T*>(E_.get()), slot_chunk_.get(), chunk_slot_.get(), halo_pos_.get(), part_.get());
+        }
+        cam_reduce<0>(nullptr, ctmp_.get());
+        comm_->allreduce_sum(ctmp_.get(), static_cast<std::int64_t>(m_) * 9, kT, st_);
+        launch(dev::k_g_fold<S>, warp_blocks, dev::kRedThreads, B, csc);
+        launch(dev::k_g_step<S>, lane_blocks, dev::kRedThreads, B, ws, sc, dev::kNoCond);
+      }
+      DBAG_CUDA(cudaMemcpyAsync(gsc_h_, sc, sizeof(dev::GScal<S>), cudaMemcpyDeviceToHost, st_));
+      DBAG_CUDA(cudaStreamSynchronize(st_));
+      if (gsc_h_->done) break;
+    }
+    if (prof) {
+      DBAG_CUDA(cudaEventRecord(prof_event(), st_));
+      DBAG_CUDA(cudaEventRecord(prof_event(), st_));
+    }
+    collect_profile();
+    const dev::GScal<S> o = *gsc_h_;
+    dse_count_ = o.dse_count;
+    dse_launches_ += o.dse_count;
+    tally_.block_ops += 2 * static_cast<std::uint64_t>(N_) * static_cast<std::uint64_t>(o.dse_count);
+    if (o.status == 1)
+      throw Error(DBAG_PCG_BREAKDOWN, "preconditioned residual norm rho = " + std::to_string(o.rho) +
+                                          " at iteration " + std::to_string(o.n));
+    if (o.status == 2)
+      throw Error(DBAG_PCG_BREAKDOWN, "operator lost positive definiteness (p'q = " + std::to_string(o.pq) +
+                                          ") at iteration " + std::to_string(o.n));
+    return {o.n, std::sqrt(o.rnorm2) <= tol * std::sqrt(o.rhs_norm2)};
+  }
+
   // ---- DPCG as one CUDA graph with conditional WHILE / IF nodes (K = 1) ----
   dev::GBufs<S> gbufs() {
     dev::GBufs<S> b;
@@ -481,6 +558,7 @@ class Rank {
     b.cam_part_ptr = cam_part_ptr_.get();
     b.part = part_.get();
     b.pq_cam = g_pq_cam_.get();
+    b.c_total = nullptr;
     return b;
   }
 
