@@ -508,3 +508,14 @@ def test_unobserved_camera_and_point(k):
     empty = dba.BAProblem.from_arrays(cams[:2], pts[:3], np.zeros(0, np.int32), np.zeros(0, np.int32), np.zeros((0, 2)))
     with pytest.raises(dba.InvalidArgumentError):
         dba.lm_solve(empty, dba.SolverConfig(max_iterations=3))
+
+
+@pytest.mark.parametrize("k", [1, 2])
+def test_host_driven_dpcg_loop(k, monkeypatch):
+    """DBAG_PCG=host: the one-launch-per-step DPCG loop (a host round trip per
+    PCG iteration) kept as the reference implementation of the device-driven
+    forms; same oracle trajectory, split points included."""
+    monkeypatch.setenv("DBAG_PCG", "host")
+    p = ring(40, 400, 8, radius=1.0, noise=0.5, seed=2024, nobs=3197)
+    cfg = dba.SolverConfig(max_iterations=4, workers=k, pcg_tol=1e-12, pcg_max_iters=2000)
+    _compare_histories(dba.lm_solve(p, cfg), O.lm_solve(p, cfg), 1e-9)
