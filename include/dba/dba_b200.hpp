@@ -331,6 +331,19 @@ std::vector<EdgePartition> partition_edges(const BAProblem<Scalar>& problem, int
   return out;
 }
 
+// ---- predicted-size memory pool (B200 extension) ------------
+// Device bytes rank `rank` of `worker_count` reserves in its one pool
+// allocation when lm_solve uploads its shard; host-only, no GPU needed.
+template <typename Scalar>
+std::uint64_t predict_memory(const BAProblem<Scalar>& problem, int worker_count = 1, int rank = 0,
+                             bool coupling_fp32 = false) {
+  const dbag_problem p = problem.c_view();
+  std::uint64_t bytes = 0;
+  detail::check(dbag_predict_memory(&p, static_cast<int>(sizeof(Scalar)), coupling_fp32 ? 1 : 0, worker_count, rank,
+                                    &bytes));
+  return bytes;
+}
+
 // ---- synthetic generator (dba/synthetic.hpp) ---------------------------------
 struct SyntheticOptions {
   std::int32_t cameras = 20000, points = 80000, obs_per_point = 1000;

@@ -125,6 +125,15 @@ int dbag_partition(const dbag_problem* p, int k, int rank, int64_t* start, int64
  * NULL to query the count. */
 int dbag_shared_points(const dbag_problem* p, int k, int64_t* n_shared, int32_t* ids);
 
+/* Predicted-size memory pool: the exact
+ * device bytes rank `rank` of `k` reserves in ONE allocation when the problem
+ * is uploaded (E chunk records, shard arrays, state and system blocks, PCG
+ * vectors), computed on the host from the partition and layout alone — no
+ * GPU needed — so a caller can pick K or the FP32-E variant before
+ * uploading. precision 4|8; coupling_fp32 as in dbag_create_ex. Not
+ * included: the per-context fixed scratch (< 64 KB) and NCCL's buffers. */
+int dbag_predict_memory(const dbag_problem* p, int precision, int coupling_fp32, int k, int rank, uint64_t* bytes);
+
 /* generate_synthetic (dba/synthetic.hpp:70-146), fp64 output. Query the edge
  * count first with dbag_synthetic_count. Outputs: cameras[9m], points[3n],
  * camera_id/point_id/pixel_x/pixel_y[N]. */
@@ -224,6 +233,9 @@ int dbag_synchronize(dbag_ctx* ctx);
 int dbag_time_dse_pass(dbag_ctx* ctx, int reps, double* ms_per_pass);
 /* Number of kernels this context has launched (bench: gpu_launches). */
 int dbag_launch_count(dbag_ctx* ctx, int64_t* out);
+/* The context's pool after dbag_upload_problem: reserved == the prediction,
+ * used == reserved (upload fails with DBAG_INTERNAL otherwise). */
+int dbag_memory_pool(dbag_ctx* ctx, uint64_t* reserved, uint64_t* used);
 
 /* ---- test hooks (operator-level parity) ------------------- */
 /* Scalar-model residuals (dba/problem.hpp:151-165) of the current (0) or

@@ -54,6 +54,8 @@ _SIGS = {
     "dbag_partition": (C.c_int, [_P(Problem), C.c_int, C.c_int, _P(i64), _P(i64), _P(i32), vp, _P(i32), vp, vp,
                                  vp, vp, vp]),
     "dbag_shared_points": (C.c_int, [_P(Problem), C.c_int, _P(i64), vp]),
+    "dbag_predict_memory": (C.c_int, [_P(Problem), C.c_int, C.c_int, C.c_int, C.c_int, _P(u64)]),
+    "dbag_memory_pool": (C.c_int, [vp, _P(u64), _P(u64)]),
     "dbag_synthetic_count": (C.c_int, [_P(SynthOptions), _P(i64)]),
     "dbag_generate_synthetic": (C.c_int, [_P(SynthOptions), vp, vp, vp, vp, vp, vp]),
     "dbag_lm_solve": (C.c_int, [C.c_int, _P(Problem), _P(Config), _P(C.c_int), C.c_int, _P(Result)]),

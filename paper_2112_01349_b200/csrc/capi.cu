@@ -277,6 +277,28 @@ int dbag_shared_points(const dbag_problem* p, int k, int64_t* n_shared, int32_t*
   });
 }
 
+int dbag_predict_memory(const dbag_problem* p, int precision, int coupling_fp32, int k, int rank, uint64_t* bytes) {
+  return guarded([&] {
+    check_precision(precision);
+    check_problem(*p);
+    const ShardPlan s = plan_shard(p->camera_id, p->point_id, p->num_observations, p->num_cameras, p->num_points, k,
+                                   rank, dev::kTile);
+    const DeviceLayout d = build_device_layout(s, p->camera_id + s.range.start, dev::kTile);
+    if (precision == 8 && coupling_fp32) *bytes = Rank<double, float>::predict_bytes(Rank<double, float>::shard_sizes(s, d));
+    else if (precision == 8) *bytes = Rank<double>::predict_bytes(Rank<double>::shard_sizes(s, d));
+    else *bytes = Rank<float>::predict_bytes(Rank<float>::shard_sizes(s, d));
+  });
+}
+
+int dbag_memory_pool(dbag_ctx* ctx, uint64_t* reserved, uint64_t* used) {
+  return guarded([&] {
+    with_rank(ctx, [&](auto& rk) {
+      *reserved = rk.pool_bytes();
+      *used = rk.pool_used();
+    });
+  });
+}
+
 int dbag_synthetic_count(const dbag_synthetic_options* o, int64_t* n_obs) {
   return guarded([&] { *n_obs = synthetic_count(*o); });
 }

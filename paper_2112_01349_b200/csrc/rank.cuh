@@ -25,6 +25,7 @@
 #include <string>
 #include <limits>
 #include <memory>
+#include <type_traits>
 #include <utility>
 #include <vector>
 
@@ -37,9 +38,49 @@
 
 namespace dbag {
 
+// One device allocation per rank, sized in advance from the shard's layout:
+// the paper's predicted-size memory pool (SURVEY.md §8f
+// f4). upload() reserves it once and carves every shard buffer from it, so a
+// problem that does not fit fails at one cudaMalloc, before any copy, and
+// nothing is allocated inside the LM loop.
+class Arena {
+ public:
+  static constexpr std::size_t kAlign = 256;
+  static std::size_t round(std::size_t b) { return (b + kAlign - 1) / kAlign * kAlign; }
+  Arena() = default;
+  Arena(const Arena&) = delete;
+  Arena& operator=(const Arena&) = delete;
+  ~Arena() { release(); }
+  void reserve(std::size_t bytes) {
+    release();
+    if (bytes) DBAG_CUDA(cudaMalloc(&base_, bytes));
+    cap_ = bytes;
+  }
+  void* take(std::size_t bytes) {
+    const std::size_t b = round(bytes);
+    if (used_ + b > cap_)
+      throw Error(DBAG_INTERNAL, "memory pool overflow: predicted " + std::to_string(cap_) + " bytes, need more");
+    void* p = base_ + used_;
+    used_ += b;
+    return p;
+  }
+  std::size_t capacity() const { return cap_; }
+  std::size_t used() const { return used_; }
+
+ private:
+  void release() {
+    if (base_) cudaFree(base_);
+    base_ = nullptr;
+    cap_ = used_ = 0;
+  }
+  char* base_ = nullptr;
+  std::size_t cap_ = 0, used_ = 0;
+};
+
 template <class T>
 class DevBuf {
  public:
+  using value_type = T;
   DevBuf() = default;
   DevBuf(const DevBuf&) = delete;
   DevBuf& operator=(const DevBuf&) = delete;
@@ -48,28 +89,54 @@ class DevBuf {
     release();
     n_ = n;
     if (n) DBAG_CUDA(cudaMalloc(&p_, n * sizeof(T)));
+    owned_ = true;
   }
-  void upload(const T* h, std::size_t n) {
-    alloc(std::max<std::size_t>(n, 1));
-    if (n) DBAG_CUDA(cudaMemcpy(p_, h, n * sizeof(T), cudaMemcpyHostToDevice));
+  void alloc(std::size_t n, Arena& a) {  // a slice of the rank's pool
+    release();
+    n_ = n;
+    p_ = static_cast<T*>(a.take(n * sizeof(T)));
   }
-  void upload(const std::vector<T>& v) { upload(v.data(), v.size()); }
+  void copy_in(const std::vector<T>& v) {
+    if (v.size() > n_) throw Error(DBAG_INTERNAL, "device buffer smaller than its upload");
+    if (!v.empty()) DBAG_CUDA(cudaMemcpy(p_, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
+  }
   T* get() const { return p_; }
   std::size_t size() const { return n_; }
   void swap(DevBuf& o) {
     std::swap(p_, o.p_);
     std::swap(n_, o.n_);
+    std::swap(owned_, o.owned_);
   }
 
  private:
   void release() {
-    if (p_) cudaFree(p_);
+    if (p_ && owned_) cudaFree(p_);
     p_ = nullptr;
     n_ = 0;
+    owned_ = false;
   }
   T* p_ = nullptr;
   std::size_t n_ = 0;
+  bool owned_ = false;
 };
+
+// Element counts of one rank's shard buffers (Rank::shard_buffers), from the
+// host-side partition plan and device layout alone.
+struct ShardSizes {
+  std::size_t N, slots, dpt_ptr, chunk_slot, cam_part_ptr, halo_slot, part, cam_ptr, cam_glob, n_loc, n_halo_loc,
+      halo, red, cm, pl, recs, n_long, xp_full, m;
+};
+
+inline void check_problem(const dbag_problem& p) {
+  if (p.num_cameras < 0 || p.num_points < 0 || p.num_observations < 0)
+    throw Error(DBAG_SHAPE, "negative problem dimensions");
+  for (std::int64_t e = 0; e < p.num_observations; ++e) {
+    if (p.camera_id[e] < 0 || p.camera_id[e] >= p.num_cameras)
+      throw Error(DBAG_INVALID_ARGUMENT, "edge references unknown camera " + std::to_string(p.camera_id[e]));
+    if (p.point_id[e] < 0 || p.point_id[e] >= p.num_points)
+      throw Error(DBAG_INVALID_ARGUMENT, "edge references unknown point " + std::to_string(p.point_id[e]));
+  }
+}
 
 inline int grid_for(std::int64_t n, int threads, int cap) {
   const std::int64_t b = (n + threads - 1) / threads;
@@ -129,17 +196,86 @@ class Rank {
   int last_dse_count() const { return dse_count_; }
   std::int64_t launches() const { return launches_; }
 
+  // ------------------------------------------------------- memory pool ----
+  static ShardSizes shard_sizes(const ShardPlan& pl, const DeviceLayout& d) {
+    ShardSizes z{};
+    z.N = static_cast<std::size_t>(pl.range.count);
+    z.m = static_cast<std::size_t>(pl.m);
+    z.slots = d.slot_dpt.size();
+    z.dpt_ptr = d.dpt_ptr.size();
+    z.chunk_slot = d.chunk_slot.size();
+    z.cam_part_ptr = d.cam_part_ptr.size();
+    z.halo_slot = d.halo_slot.size();
+    z.part = static_cast<std::size_t>(d.n_part) * 9;
+    z.cam_ptr = pl.cam_ptr.size();
+    z.cam_glob = pl.cams.to_global.size();
+    z.n_loc = static_cast<std::size_t>(pl.pts.size());
+    z.n_halo_loc = 0;
+    for (std::size_t lp = 0; lp < z.n_loc; ++lp) z.n_halo_loc += pl.halo_of_lpt[lp] >= 0;
+    z.halo = static_cast<std::size_t>(std::max<std::int64_t>(pl.n_shared, 1)) * 12;
+    z.red = std::max<std::size_t>(8 * dev::kRedBlocksMax, 2 * (z.m * 32 / 256 + 64));
+    z.cm = z.m * 9;
+    z.pl = z.n_loc * 3;
+    z.recs = static_cast<std::size_t>(std::max<std::size_t>(d.chunk_slot.size(), 1)) * dev::Rec<T>::kLen;
+    z.n_long = 0;
+    for (std::size_t t = 0; t + 1 < d.tile_chunk.size(); ++t) z.n_long += d.tile_chunk[t + 1] - d.tile_chunk[t] > 1;
+    z.xp_full = static_cast<std::size_t>(pl.n) * 3;
+    return z;
+  }
+
+  // Every pool-backed buffer of the rank with its element count; the one
+  // list both the prediction and the allocation walk.
+  template <class F>
+  static void shard_buffers(const ShardSizes& z, F&& f) {
+    for (auto pm : {&Rank::slot_cam_, &Rank::slot_dpt_, &Rank::slot_edge_, &Rank::cslot_dslot_})
+      f(pm, pm == &Rank::slot_dpt_ || pm == &Rank::slot_edge_ ? z.slots : z.N);
+    for (auto pm : {&Rank::slot_px_, &Rank::slot_py_, &Rank::slot_w_}) f(pm, z.N);
+    f(&Rank::dpt_ptr_, z.dpt_ptr);
+    f(&Rank::chunk_slot_, z.chunk_slot);
+    f(&Rank::cam_part_ptr_, z.cam_part_ptr);
+    f(&Rank::halo_slot_, z.halo_slot);
+    f(&Rank::halo_pos_, z.halo_slot);
+    f(&Rank::slot_chunk_, z.slots);
+    f(&Rank::cam_ptr_, z.cam_ptr);
+    f(&Rank::cam_glob_, z.cam_glob);
+    for (auto pm : {&Rank::dpt_glob_d_, &Rank::halo_of_}) f(pm, z.n_loc);
+    f(&Rank::owned_, z.n_loc);
+    for (auto pm : {&Rank::halo_dpt_, &Rank::halo_idx_}) f(pm, z.n_halo_loc);
+    f(&Rank::long_chunk_, z.n_long);
+    f(&Rank::part_, z.part);
+    f(&Rank::halo_buf_, z.halo);
+    f(&Rank::red_part_, z.red);
+    for (auto pm : {&Rank::xc_, &Rank::xct_, &Rank::dxc_, &Rank::v_, &Rank::g_, &Rank::r_, &Rank::z_, &Rank::p_,
+                    &Rank::q_, &Rank::ctmp_, &Rank::p2_})
+      f(pm, z.cm);
+    for (auto pm : {&Rank::xp_, &Rank::xpt_, &Rank::dxp_, &Rank::w_}) f(pm, z.pl);
+    for (auto pm : {&Rank::B_, &Rank::Bd_, &Rank::Binv_, &Rank::Bexp_}) f(pm, z.cm * 9);
+    for (auto pm : {&Rank::C_, &Rank::Cd_}) f(pm, z.pl * 3);
+    f(&Rank::Cinv_, z.pl * 3 + 16 / sizeof(S));  // slack for 16-byte-rounded reads
+    f(&Rank::Jb_, z.N * 28);
+    f(&Rank::E_, z.recs);
+    f(&Rank::xp_full_, z.xp_full);
+    f(&Rank::gsc_, 1);
+    f(&Rank::g_pq_cam_, z.m);
+    f(&Rank::g_bar_, 1);
+  }
+
+  // Device bytes upload() reserves for this shard (exact: upload checks it).
+  static std::size_t predict_bytes(const ShardSizes& z) {
+    std::size_t b = 0;
+    shard_buffers(z, [&](auto pm, std::size_t n) {
+      using Buf = std::remove_reference_t<decltype(std::declval<Rank&>().*pm)>;
+      b += Arena::round(std::max<std::size_t>(n, 1) * sizeof(typename Buf::value_type));
+    });
+    return b;
+  }
+  std::size_t pool_bytes() const { return pool_.capacity(); }
+  std::size_t pool_used() const { return pool_.used(); }
+
   // ------------------------------------------------------------ upload ----
   void upload(const dbag_problem& p, int jac_mode) {
     DBAG_CUDA(cudaSetDevice(device_));
-    if (p.num_cameras < 0 || p.num_points < 0 || p.num_observations < 0)
-      throw Error(DBAG_SHAPE, "negative problem dimensions");
-    for (std::int64_t e = 0; e < p.num_observations; ++e) {
-      if (p.camera_id[e] < 0 || p.camera_id[e] >= p.num_cameras)
-        throw Error(DBAG_INVALID_ARGUMENT, "edge references unknown camera " + std::to_string(p.camera_id[e]));
-      if (p.point_id[e] < 0 || p.point_id[e] >= p.num_points)
-        throw Error(DBAG_INVALID_ARGUMENT, "edge references unknown point " + std::to_string(p.point_id[e]));
-    }
+    check_problem(p);
     jac_mode_ = jac_mode;
     destroy_graph();
     plan_ = plan_shard(p.camera_id, p.point_id, p.num_observations, p.num_cameras, p.num_points, comm_->size(),
@@ -165,31 +301,16 @@ class Rank {
       s_w[s] = wt ? wt[base + e] : S(1);
       if (!(s_w[s] >= S(0))) throw Error(DBAG_INVALID_ARGUMENT, "edge weight must be >= 0");
     }
-    slot_cam_.upload(s_cam);
-    slot_dpt_.upload(lay_.slot_dpt);
-    slot_edge_.upload(lay_.slot_edge);
-    slot_px_.upload(s_px);
-    slot_py_.upload(s_py);
-    slot_w_.upload(s_w);
-    dpt_ptr_.upload(lay_.dpt_ptr);
     n_tiles_ = static_cast<int>(lay_.tile_pt.size()) - 1;
-    chunk_slot_.upload(lay_.chunk_slot);
-    cam_part_ptr_.upload(lay_.cam_part_ptr);
-    halo_slot_.upload(lay_.halo_slot);
-    slot_chunk_.upload(lay_.slot_chunk);
     n_chunks_ = static_cast<std::int32_t>(lay_.chunk_slot.size());
     n_chunk_part_ = static_cast<std::int32_t>(lay_.ucam_cam.size());
-    part_.alloc(std::max<std::size_t>(static_cast<std::size_t>(lay_.n_part) * 9, 1));
     // camera-major view (assembly of B, v)
     std::vector<std::int32_t> cptr32(plan_.cam_ptr.begin(), plan_.cam_ptr.end());
-    cam_ptr_.upload(cptr32);
-    cam_glob_.upload(plan_.cams.to_global);
     std::vector<std::int32_t> dslot_of_edge(static_cast<std::size_t>(N_));
     for (std::int64_t s = 0; s < N_; ++s) dslot_of_edge[static_cast<std::size_t>(lay_.slot_edge[static_cast<std::size_t>(s)])] = static_cast<std::int32_t>(s);
     std::vector<std::int32_t> cslot(static_cast<std::size_t>(N_));
     for (std::int64_t c = 0; c < N_; ++c)
       cslot[static_cast<std::size_t>(c)] = dslot_of_edge[static_cast<std::size_t>(plan_.cam_blk[static_cast<std::size_t>(c)])];
-    cslot_dslot_.upload(cslot);
     // device points
     dpt_glob_.resize(static_cast<std::size_t>(n_loc_));
     std::vector<std::int32_t> halo_of(static_cast<std::size_t>(n_loc_), -1);
@@ -206,24 +327,32 @@ class Rank {
       }
     }
     owned_h_ = owned;
-    dpt_glob_d_.upload(dpt_glob_);
-    halo_of_.upload(halo_of);
-    owned_.upload(owned);
     n_halo_loc_ = static_cast<std::int32_t>(hl.size());
-    halo_dpt_.upload(hl);
-    halo_idx_.upload(hi);
-    halo_buf_.alloc(static_cast<std::size_t>(std::max<std::int64_t>(H_, 1)) * 12);
-    // grid-reduction partials: enough for one warp per camera
-    red_part_.alloc(std::max<std::size_t>(8 * dev::kRedBlocksMax, 2 * (static_cast<std::size_t>(p.num_cameras) * 32 / 256 + 64)));
-    // state + system
-    const std::size_t cm = static_cast<std::size_t>(m_) * 9, pl = static_cast<std::size_t>(n_loc_) * 3;
-    for (DevBuf<S>* b : {&xc_, &xct_, &dxc_, &v_, &g_, &r_, &z_, &p_, &q_, &ctmp_}) b->alloc(std::max<std::size_t>(cm, 1));
-    for (DevBuf<S>* b : {&xp_, &xpt_, &dxp_, &w_}) b->alloc(std::max<std::size_t>(pl, 1));
-    for (DevBuf<S>* b : {&B_, &Bd_, &Binv_, &Bexp_}) b->alloc(std::max<std::size_t>(cm * 9, 1));
-    p2_.alloc(std::max<std::size_t>(cm, 1));
-    for (DevBuf<S>* b : {&C_, &Cd_}) b->alloc(std::max<std::size_t>(pl * 3, 1));
-    Cinv_.alloc(pl * 3 + 16 / sizeof(S));  // slack for the 16-byte-rounded TMA reads
-    Jb_.alloc(std::max<std::size_t>(static_cast<std::size_t>(N_) * 28, 1));
+    // the whole shard in one pool allocation, sized before any copy
+    const ShardSizes z = shard_sizes(plan_, lay_);
+    pool_.reserve(predict_bytes(z));
+    shard_buffers(z, [&](auto pm, std::size_t n) { (this->*pm).alloc(std::max<std::size_t>(n, 1), pool_); });
+    if (pool_.used() != pool_.capacity()) throw Error(DBAG_INTERNAL, "memory pool prediction mismatch");
+    slot_cam_.copy_in(s_cam);
+    slot_dpt_.copy_in(lay_.slot_dpt);
+    slot_edge_.copy_in(lay_.slot_edge);
+    slot_px_.copy_in(s_px);
+    slot_py_.copy_in(s_py);
+    slot_w_.copy_in(s_w);
+    dpt_ptr_.copy_in(lay_.dpt_ptr);
+    chunk_slot_.copy_in(lay_.chunk_slot);
+    cam_part_ptr_.copy_in(lay_.cam_part_ptr);
+    halo_slot_.copy_in(lay_.halo_slot);
+    slot_chunk_.copy_in(lay_.slot_chunk);
+    cam_ptr_.copy_in(cptr32);
+    cam_glob_.copy_in(plan_.cams.to_global);
+    cslot_dslot_.copy_in(cslot);
+    dpt_glob_d_.copy_in(dpt_glob_);
+    halo_of_.copy_in(halo_of);
+    owned_.copy_in(owned);
+    halo_dpt_.copy_in(hl);
+    halo_idx_.copy_in(hi);
+    DBAG_CUDA(cudaMemset(g_bar_.get(), 0, sizeof(unsigned long long)));
     build_records(s_cam);
     set_state(static_cast<const S*>(p.cameras), static_cast<const S*>(p.points));
     have_system_ = false;
@@ -481,11 +610,7 @@ class Rank {
   // call sequence stays aligned across ranks.
   PcgOut pcg_stream(double tol, int max_iters) {
     constexpr int kRunAhead = 8;
-    if (!gsc_.get()) {
-      gsc_.alloc(1);
-      DBAG_CUDA(cudaMallocHost(&gsc_h_, sizeof(dev::GScal<S>)));
-    }
-    if (g_pq_cam_.size() < static_cast<std::size_t>(std::max(m_, 1))) g_pq_cam_.alloc(std::max<std::size_t>(m_, 1));
+    if (!gsc_h_) DBAG_CUDA(cudaMallocHost(&gsc_h_, sizeof(dev::GScal<S>)));
     dev::GBufs<S> B = gbufs();
     B.c_total = ctmp_.get();
     const dev::RedWs ws = red();
@@ -608,11 +733,7 @@ class Rank {
 
   void build_graph() {
     destroy_graph();
-    if (!gsc_.get()) {
-      gsc_.alloc(1);
-      DBAG_CUDA(cudaMallocHost(&gsc_h_, sizeof(dev::GScal<S>)));
-    }
-    g_pq_cam_.alloc(std::max<std::size_t>(m_, 1));
+    if (!gsc_h_) DBAG_CUDA(cudaMallocHost(&gsc_h_, sizeof(dev::GScal<S>)));
     dev::GBufs<S> B = gbufs();
     dev::RedWs ws = red();
     dev::GScal<S>* sc = gsc_.get();
@@ -638,7 +759,6 @@ class Rank {
     const char* fse = std::getenv("DBAG_FS");
     g_fused_ = !(fse && std::string(fse) == "0") && cam_warp_blocks <= fs_per_sm * sms &&
                cam_warp_blocks <= dev::kRedBlocksMax;
-    if (!g_bar_.get()) g_bar_.alloc(1);
     DBAG_CUDA(cudaMemset(g_bar_.get(), 0, sizeof(unsigned long long)));
     unsigned long long* bar = g_bar_.get();
     void* a_fs[] = {&B, &ws, &sc, &hw, &bar};
@@ -1129,13 +1249,13 @@ class Rank {
           }
       }
     }
-    E_.upload(recs);
+    E_.copy_in(recs);
     n_long_ = static_cast<std::int32_t>(long_first.size());
-    long_chunk_.upload(long_first);
+    long_chunk_.copy_in(long_first);
     std::vector<std::int32_t> hpos(lay_.halo_slot.size());
     for (std::size_t i = 0; i < hpos.size(); ++i)
       hpos[i] = lay_.part_pos[static_cast<std::size_t>(n_chunk_part_) + i];
-    halo_pos_.upload(hpos);
+    halo_pos_.copy_in(hpos);
   }
 
   dev::DseArgs<S, T> dse_args(const S* x) {
@@ -1262,6 +1382,7 @@ class Rank {
   std::vector<std::int32_t> dpt_glob_;
   std::vector<std::uint8_t> owned_h_;
 
+  Arena pool_;  // declared first: destroyed after the buffers carved from it
   DevBuf<std::int32_t> slot_cam_, slot_dpt_, slot_edge_, dpt_ptr_, chunk_slot_, cam_part_ptr_, halo_slot_, slot_chunk_,
       long_chunk_, halo_pos_, cam_ptr_, cam_glob_, cslot_dslot_, dpt_glob_d_,
       halo_of_, halo_dpt_, halo_idx_;

@@ -344,6 +344,17 @@ def shared_points(problem: BAProblem, worker_count: int) -> np.ndarray:
     return ids[:cnt.value]
 
 
+def predict_memory(problem: BAProblem, worker_count: int = 1, rank: int = 0, coupling_fp32: bool = False) -> int:
+    """Device bytes rank `rank` of `worker_count` reserves in its one pool
+    allocation at upload (the paper's predicted-size memory pool, SURVEY.md
+    §8f f4). Host-only: runs the partition and the device layout, no GPU."""
+    s = problem.c_struct()
+    b = C.c_uint64()
+    _check(N.lib().dbag_predict_memory(C.byref(s), problem.precision, int(coupling_fp32), worker_count, rank,
+                                       C.byref(b)))
+    return b.value
+
+
 # ------------------------------------------------------------------ solver --
 
 DAMPING_IDENTITY, DAMPING_DIAG_SCALED = 0, 1
@@ -660,6 +671,12 @@ class RankContext:
         t = C.c_double()
         _check(N.lib().dbag_time_dse_pass(self.h, int(reps), C.byref(t)))
         return t.value
+
+    def memory_pool(self):
+        """(reserved, used) bytes of this context's device pool."""
+        r, u = C.c_uint64(), C.c_uint64()
+        _check(N.lib().dbag_memory_pool(self.h, C.byref(r), C.byref(u)))
+        return r.value, u.value
 
     def launch_count(self) -> int:
         n = C.c_int64()

@@ -36,6 +36,9 @@ int main(int argc, char** argv) {
     threw = true;
   }
   CHECK(threw);
+  // predicted-size pool: host-only, lean variant below FP64, shards below the whole
+  const std::uint64_t pool1 = dba::predict_memory(problem), pool_lean = dba::predict_memory(problem, 1, 0, true);
+  CHECK(pool1 > 800u * 27 * 8 && pool_lean < pool1 && dba::predict_memory(problem, 3, 1) < pool1);
   // BAL text round trip and the ParseError contract (tests/test_problem.cpp:35-80)
   std::ostringstream bal;
   dba::serialize_bal(problem, bal);

@@ -519,3 +519,32 @@ def test_host_driven_dpcg_loop(k, monkeypatch):
     p = ring(40, 400, 8, radius=1.0, noise=0.5, seed=2024, nobs=3197)
     cfg = dba.SolverConfig(max_iterations=4, workers=k, pcg_tol=1e-12, pcg_max_iters=2000)
     _compare_histories(dba.lm_solve(p, cfg), O.lm_solve(p, cfg), 1e-9)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("lean", [False, True])
+def test_memory_pool_matches_prediction(lean):
+    """Predicted-size pool: upload reserves exactly the
+    host-side prediction in one allocation and fills it; the device's free
+    memory drops by that much (up to the driver's 2 MiB granularity); the
+    solve afterwards allocates nothing more than the per-context scratch."""
+    import torch
+    p = ring(60, 3000, 6, noise=0.5, seed=7)
+    pred = dba.predict_memory(p, coupling_fp32=lean)
+    with dba.RankContext(0, 8, coupling_fp32=lean) as c:
+        torch.cuda.synchronize()
+        free0 = torch.cuda.mem_get_info(0)[0]
+        c.upload(p)
+        assert c.memory_pool() == (pred, pred)
+        free1 = torch.cuda.mem_get_info(0)[0]
+        assert pred <= free0 - free1 <= pred + 4 * 2**20
+        c.linearize()
+        c.damp_factor(1e-4, dba.DAMPING_DIAG_SCALED)
+        c.rhs()
+        c.pcg(1e-6, 100)
+        assert free1 - torch.cuda.mem_get_info(0)[0] <= 4 * 2**20
+        c.upload(p)  # re-upload replaces the pool
+        assert c.memory_pool() == (pred, pred)
+    for k in (2, 3):
+        preds = [dba.predict_memory(p, k, r, coupling_fp32=lean) for r in range(k)]
+        assert max(preds) < pred

@@ -1,0 +1,56 @@
+"""Predicted-size memory pool: the
+host-side prediction of a rank's device footprint (dbag_predict_memory). It
+needs no GPU; tests/test_gpu_parity.py::test_memory_pool_matches_prediction
+checks that upload reserves exactly this many bytes in one allocation."""
+import numpy as np
+import pytest
+
+import paper_2112_01349_b200 as dba
+
+ALIGN = 256
+
+
+@pytest.fixture(scope="module")
+def ladybug():
+    return dba.generate_synthetic(dba.SyntheticOptions(cameras=49, points=7776, num_observations=31843, seed=1))
+
+
+def _floor_bytes(p, k, rank, s, t):
+    """Lower bound from the dominant per-edge arrays alone: E records
+    (27 lanes of t bytes per slot), the assembly rows (28 s per edge), the
+    slot arrays (4 int32 + 3 scalars per edge)."""
+    n_k = len(dba.partition_edges(p, k)[rank].edge_ids)
+    return n_k * (27 * t + 28 * s + 16 + 3 * s)
+
+
+@pytest.mark.parametrize("k", [1, 2, 4])
+def test_prediction_bounds_and_split(ladybug, k):
+    for rank in range(k):
+        b = dba.predict_memory(ladybug, k, rank)
+        assert b % ALIGN == 0
+        lo = _floor_bytes(ladybug, k, rank, 8, 8)
+        assert lo < b < 2 * lo + 4 * 2**20
+    # the shards split the edge-proportional part: K ranks together hold
+    # about one problem plus the replicated camera space
+    tot = sum(dba.predict_memory(ladybug, k, r) for r in range(k))
+    one = dba.predict_memory(ladybug, 1, 0)
+    assert one <= tot < one * 1.05 + k * 2**20
+
+
+def test_precision_variants_order(ladybug):
+    b64 = dba.predict_memory(ladybug)
+    lean = dba.predict_memory(ladybug, coupling_fp32=True)
+    p32 = ladybug.astype(np.float32)
+    assert lean < b64
+    # E lanes dominate the saving: 27 x 4 bytes per slot, up to chunk padding
+    n = ladybug.num_observations
+    assert 27 * 4 * n <= b64 - lean < 27 * 4 * n * 1.6
+    assert dba.predict_memory(p32) < lean
+
+
+def test_prediction_is_deterministic_and_validates(ladybug):
+    assert dba.predict_memory(ladybug, 2, 1) == dba.predict_memory(ladybug, 2, 1)
+    with pytest.raises(dba.InvalidArgumentError):
+        dba.predict_memory(ladybug, 2, 2)  # rank out of range
+    with pytest.raises(dba.InvalidArgumentError):
+        dba.predict_memory(ladybug, 0, 0)
