@@ -280,6 +280,7 @@ def run_ours(args):
                 "d2h_bytes_per_step": state_bytes},
         "clocks": clk.summary(),
         "gpu_launches": int(launches),
+        "device_pool_bytes": int(ctx.memory_pool()[0]),
     }
     if world == 1 and rank == 0 and not args.no_secondary:
         line["secondary"] = secondary(args, flush)

@@ -222,7 +222,8 @@ __global__ void k_residuals(std::int64_t N, const std::int32_t* __restrict__ slo
 // Fused K1+K2(+K3)+K5-E: gather, jets (or closed form), residual, Jacobian,
 // E = w Jc^T Jp. Jb row: [r0 r1 | J0[12] | J1[12] | w pad].
 template <class S, int MODE, class T = S>
-__global__ void __launch_bounds__(128) k_linearize(std::int64_t N, const std::int32_t* __restrict__ slot_cam,
+__global__ void __launch_bounds__(128) k_linearize(std::int64_t s0, std::int64_t s1,
+                                                   const std::int32_t* __restrict__ slot_cam,
                                                    const std::int32_t* __restrict__ slot_pt,
                                                    const std::int32_t* __restrict__ slot_edge,
                                                    std::int64_t edge_base, const S* __restrict__ px,
@@ -232,8 +233,8 @@ __global__ void __launch_bounds__(128) k_linearize(std::int64_t N, const std::in
                                                    const std::int32_t* __restrict__ slot_chunk,
                                                    const std::int32_t* __restrict__ chunk_slot,
                                                    unsigned long long* bad_edge) {
-  const std::int64_t s = blockIdx.x * std::int64_t(blockDim.x) + threadIdx.x;
-  if (s >= N) return;
+  const std::int64_t s = s0 + blockIdx.x * std::int64_t(blockDim.x) + threadIdx.x;
+  if (s >= s1) return;
   const S* cam = xc + std::size_t(slot_cam[s]) * 9;
   const S* x = xp + std::size_t(slot_pt[s]) * 3;
   S c[9], X[3], r[2], J[2][12];
@@ -247,7 +248,7 @@ __global__ void __launch_bounds__(128) k_linearize(std::int64_t N, const std::in
     return;
   }
   const S wt = w[s];
-  S* row = Jb + std::size_t(s) * 28;
+  S* row = Jb + std::size_t(s - s0) * 28;  // Jb holds the batch [s0, s1)
   row[0] = r[0];
   row[1] = r[1];
 #pragma unroll
@@ -268,13 +269,14 @@ __global__ void __launch_bounds__(128) k_linearize(std::int64_t N, const std::in
 // C[p] += w Jp^T Jp, w[p] -= w Jp^T r over the point's slots in edge order
 // (dba/block_matrix.hpp:382-386). Thread per local point.
 template <class S>
-__global__ void k_assemble_points(std::int32_t n_loc, const std::int32_t* __restrict__ pt_ptr,
-                                  const S* __restrict__ Jb, S* __restrict__ C, S* __restrict__ wv) {
-  const std::int32_t p = blockIdx.x * blockDim.x + threadIdx.x;
-  if (p >= n_loc) return;
+__global__ void k_assemble_points(std::int32_t d0, std::int32_t d1, const std::int32_t* __restrict__ pt_ptr,
+                                  std::int64_t s0, const S* __restrict__ Jb, S* __restrict__ C,
+                                  S* __restrict__ wv) {
+  const std::int32_t p = d0 + static_cast<std::int32_t>(blockIdx.x * blockDim.x + threadIdx.x);
+  if (p >= d1) return;
   S c[3][3] = {}, g[3] = {};
   for (std::int32_t s = pt_ptr[p]; s < pt_ptr[p + 1]; ++s) {
-    const S* row = Jb + std::size_t(s) * 28;
+    const S* row = Jb + std::size_t(s - s0) * 28;
     const S r0 = row[0], r1 = row[1], wt = row[26];
     S jp0[3], jp1[3];
 #pragma unroll
@@ -298,20 +300,25 @@ __global__ void k_assemble_points(std::int32_t n_loc, const std::int32_t* __rest
 }
 
 // B[c] += w Jc^T Jc, v[c] -= w Jc^T r (dba/block_matrix.hpp:378-385), one CTA
-// per local camera over its camera-major slots.
+// per local camera over its camera-major slots of the Jb batch starting at
+// slot s0. With several batches (carry != nullptr) a CTA per camera the
+// batch touches (cam_list) adds its double sums to `carry` (54 per camera)
+// and k_carry_out writes B and v after the last batch.
 template <class S, int NT>
 __global__ void __launch_bounds__(NT) k_assemble_cameras(const std::int32_t* __restrict__ cam_ptr,
                                                          const std::int32_t* __restrict__ cam_glob,
                                                          const std::int32_t* __restrict__ cslot_pslot,
-                                                         const S* __restrict__ Jb, S* __restrict__ B,
-                                                         S* __restrict__ v) {
-  const std::int32_t lc = blockIdx.x;
+                                                         std::int64_t s0, const S* __restrict__ Jb,
+                                                         S* __restrict__ B, S* __restrict__ v,
+                                                         double* __restrict__ carry,
+                                                         const std::int32_t* __restrict__ cam_list) {
+  const std::int32_t lc = cam_list ? cam_list[blockIdx.x] : static_cast<std::int32_t>(blockIdx.x);
   double acc[54];  // 45 upper-triangular B entries + 9 v entries
 #pragma unroll
   for (int k = 0; k < 54; ++k) acc[k] = 0.0;
   for (std::int32_t cs = cam_ptr[lc] + threadIdx.x; cs < cam_ptr[lc + 1]; cs += NT) {
     const std::int32_t ps = cslot_pslot[cs];
-    const S* row = Jb + std::size_t(ps) * 28;
+    const S* row = Jb + std::size_t(ps - s0) * 28;
     S jc0[9], jc1[9];
 #pragma unroll
     for (int k = 0; k < 9; ++k) {
@@ -333,7 +340,12 @@ __global__ void __launch_bounds__(NT) k_assemble_cameras(const std::int32_t* __r
   double out[54];
 #pragma unroll
   for (int k = 0; k < 54; ++k) out[k] = block_reduce<SumOp>(acc[k], red);
-  if (threadIdx.x == 0) {
+  if (threadIdx.x == 0 && carry) {
+    double* cy = carry + std::size_t(lc) * 54;
+#pragma unroll
+    for (int k = 0; k < 54; ++k) cy[k] += out[k];
+  }
+  if (threadIdx.x == 0 && !carry) {
     S* b = B + std::size_t(cg) * 81;
 #pragma unroll
     for (int i = 0; i < 9; ++i)
@@ -346,6 +358,24 @@ __global__ void __launch_bounds__(NT) k_assemble_cameras(const std::int32_t* __r
 #pragma unroll
     for (int i = 0; i < 9; ++i) v[std::size_t(cg) * 9 + i] = S(out[45 + i]);
   }
+}
+
+// B and v of every local camera from the batch sums (multi-batch assembly).
+template <class S>
+__global__ void k_carry_out(std::int32_t m_loc, const std::int32_t* __restrict__ cam_glob,
+                            const double* __restrict__ carry, S* __restrict__ B, S* __restrict__ v) {
+  const std::int32_t lc = blockIdx.x * blockDim.x + threadIdx.x;
+  if (lc >= m_loc) return;
+  const double* cy = carry + std::size_t(lc) * 54;
+  S* b = B + std::size_t(cam_glob[lc]) * 81;
+  int q = 0;
+  for (int i = 0; i < 9; ++i)
+    for (int j = i; j < 9; ++j) {
+      b[i * 9 + j] = S(cy[q]);
+      b[j * 9 + i] = S(cy[q]);
+      ++q;
+    }
+  for (int i = 0; i < 9; ++i) v[std::size_t(cam_glob[lc]) * 9 + i] = S(cy[45 + i]);
 }
 
 // ------------------------------------------------------ damp + factor ----

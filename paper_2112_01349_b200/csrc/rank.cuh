@@ -124,7 +124,7 @@ class DevBuf {
 // host-side partition plan and device layout alone.
 struct ShardSizes {
   std::size_t N, slots, dpt_ptr, chunk_slot, cam_part_ptr, halo_slot, part, cam_ptr, cam_glob, n_loc, n_halo_loc,
-      halo, red, cm, pl, recs, n_long, xp_full, m;
+      halo, red, cm, pl, recs, n_long, xp_full, m, jb, carry, cam_list;
 };
 
 inline void check_problem(const dbag_problem& p) {
@@ -197,6 +197,28 @@ class Rank {
   std::int64_t launches() const { return launches_; }
 
   // ------------------------------------------------------- memory pool ----
+  // Jb, the per-edge [r, J, w] rows linearize hands to assembly, is live
+  // only inside linearize(): it holds one batch of whole device points of at
+  // most DBAG_JB_BATCH slots (default 2^23; a larger point takes a batch of
+  // its own) instead of all N rows, so city-scale shards do not keep
+  // 224 bytes per edge of scratch through the PCG.
+  static std::int64_t jb_batch_cap() {
+    const char* e = std::getenv("DBAG_JB_BATCH");
+    const long long v = e ? std::atoll(e) : 0;
+    return v > 0 ? v : (std::int64_t(1) << 23);
+  }
+  // Batch boundaries in device points (first 0, last n_loc).
+  static std::vector<std::int32_t> jb_batches(const std::vector<std::int32_t>& dpt_ptr) {
+    const std::int64_t cap = jb_batch_cap();
+    const std::int32_t np = static_cast<std::int32_t>(dpt_ptr.size()) - 1;
+    std::vector<std::int32_t> b{0};
+    for (std::int32_t d = 0; d < np; ++d)
+      if (d > b.back() && dpt_ptr[static_cast<std::size_t>(d) + 1] - dpt_ptr[static_cast<std::size_t>(b.back())] > cap)
+        b.push_back(d);
+    b.push_back(std::max(np, 0));
+    return b;
+  }
+
   static ShardSizes shard_sizes(const ShardPlan& pl, const DeviceLayout& d) {
     ShardSizes z{};
     z.N = static_cast<std::size_t>(pl.range.count);
@@ -220,6 +242,14 @@ class Rank {
     z.n_long = 0;
     for (std::size_t t = 0; t + 1 < d.tile_chunk.size(); ++t) z.n_long += d.tile_chunk[t + 1] - d.tile_chunk[t] > 1;
     z.xp_full = static_cast<std::size_t>(pl.n) * 3;
+    const std::vector<std::int32_t> jb = jb_batches(d.dpt_ptr);
+    const std::size_t nb = jb.size() - 1;
+    z.jb = 0;
+    for (std::size_t b = 0; b < nb; ++b)
+      z.jb = std::max<std::size_t>(z.jb, d.dpt_ptr.empty() ? 0 : d.dpt_ptr[jb[b + 1]] - d.dpt_ptr[jb[b]]);
+    z.cam_ptr = nb * pl.cam_ptr.size();
+    z.carry = nb > 1 ? (pl.cam_ptr.size() - 1) * 54 : 0;
+    z.cam_list = nb > 1 ? nb * (pl.cam_ptr.size() - 1) : 0;
     return z;
   }
 
@@ -252,7 +282,9 @@ class Rank {
     for (auto pm : {&Rank::B_, &Rank::Bd_, &Rank::Binv_, &Rank::Bexp_}) f(pm, z.cm * 9);
     for (auto pm : {&Rank::C_, &Rank::Cd_}) f(pm, z.pl * 3);
     f(&Rank::Cinv_, z.pl * 3 + 16 / sizeof(S));  // slack for 16-byte-rounded reads
-    f(&Rank::Jb_, z.N * 28);
+    f(&Rank::Jb_, z.jb * 28);
+    f(&Rank::carry_, z.carry);
+    f(&Rank::cam_list_, z.cam_list);
     f(&Rank::E_, z.recs);
     f(&Rank::xp_full_, z.xp_full);
     f(&Rank::gsc_, 1);
@@ -344,7 +376,40 @@ class Rank {
     cam_part_ptr_.copy_in(lay_.cam_part_ptr);
     halo_slot_.copy_in(lay_.halo_slot);
     slot_chunk_.copy_in(lay_.slot_chunk);
+    std::vector<std::int32_t> cam_list_h;
+    {  // camera-major slot lists per Jb batch, edge order inside each camera
+      jb_pt_ = jb_batches(lay_.dpt_ptr);
+      const std::size_t nb = jb_pt_.size() - 1, mc = cptr32.size();
+      jb_ncam_.clear();
+      if (nb > 1) cam_list_h.assign(nb * (mc - 1), 0);
+      if (nb > 1) {
+        std::vector<std::int32_t> bs(nb + 1);
+        for (std::size_t b = 0; b <= nb; ++b) bs[b] = lay_.dpt_ptr[static_cast<std::size_t>(jb_pt_[b])];
+        std::vector<std::int32_t> bptr(nb * mc + 1, 0), bslot(cslot.size());
+        auto batch_of = [&](std::int32_t ds) {
+          return static_cast<std::size_t>(std::upper_bound(bs.begin(), bs.end(), ds) - bs.begin()) - 1;
+        };
+        for (std::size_t lc = 0; lc + 1 < mc; ++lc)
+          for (std::int32_t cs = cptr32[lc]; cs < cptr32[lc + 1]; ++cs)
+            ++bptr[batch_of(cslot[static_cast<std::size_t>(cs)]) * mc + lc + 1];
+        for (std::size_t i = 1; i < bptr.size(); ++i) bptr[i] += bptr[i - 1];
+        std::vector<std::int32_t> fill(bptr.begin(), bptr.end() - 1);
+        for (std::size_t lc = 0; lc + 1 < mc; ++lc)
+          for (std::int32_t cs = cptr32[lc]; cs < cptr32[lc + 1]; ++cs) {
+            const std::int32_t ds = cslot[static_cast<std::size_t>(cs)];
+            bslot[static_cast<std::size_t>(fill[batch_of(ds) * mc + lc]++)] = ds;
+          }
+        bptr.pop_back();  // batch b's cam_ptr: bptr[b*mc .. b*mc + mc)
+        jb_ncam_.assign(nb, 0);  // the cameras batch b touches, at cam_list[b*(mc-1) ..)
+        for (std::size_t b = 0; b < nb; ++b)
+          for (std::size_t lc = 0; lc + 1 < mc; ++lc)
+            if (bptr[b * mc + lc + 1] > bptr[b * mc + lc]) cam_list_h[b * (mc - 1) + jb_ncam_[b]++] = static_cast<std::int32_t>(lc);
+        cptr32.swap(bptr);
+        cslot.swap(bslot);
+      }
+    }
     cam_ptr_.copy_in(cptr32);
+    cam_list_.copy_in(cam_list_h);
     cam_glob_.copy_in(plan_.cams.to_global);
     cslot_dslot_.copy_in(cslot);
     dpt_glob_d_.copy_in(dpt_glob_);
@@ -426,24 +491,33 @@ class Rank {
   void linearize() {
     DBAG_CUDA(cudaSetDevice(device_));
     DBAG_CUDA(cudaMemsetAsync(bad_.get(), 0xff, sizeof(unsigned long long), st_));
-    if (N_ > 0) {
-      const int blocks = static_cast<int>((N_ + 127) / 128);
-      auto kern = jac_mode_ == 1 ? dev::k_linearize<S, 1, T> : dev::k_linearize<S, 0, T>;
-      launch(kern, blocks, 128, N_, slot_cam_.get(), slot_dpt_.get(), slot_edge_.get(), plan_.range.start,
-             slot_px_.get(), slot_py_.get(), slot_w_.get(), xc_.get(), xp_.get(), Jb_.get(), E_.get(), slot_chunk_.get(),
-             chunk_slot_.get(), bad_.get());
+    DBAG_CUDA(cudaMemsetAsync(B_.get(), 0, B_.size() * sizeof(S), st_));
+    DBAG_CUDA(cudaMemsetAsync(v_.get(), 0, v_.size() * sizeof(S), st_));
+    if (jb_pt_.size() > 2) DBAG_CUDA(cudaMemsetAsync(carry_.get(), 0, carry_.size() * sizeof(double), st_));
+    auto kern = jac_mode_ == 1 ? dev::k_linearize<S, 1, T> : dev::k_linearize<S, 0, T>;
+    const int nb = static_cast<int>(jb_pt_.size()) - 1;
+    for (int b = 0; b < nb && N_ > 0; ++b) {  // one Jb batch of whole points at a time
+      const std::int32_t d0 = jb_pt_[static_cast<std::size_t>(b)], d1 = jb_pt_[static_cast<std::size_t>(b) + 1];
+      const std::int64_t s0 = lay_.dpt_ptr[static_cast<std::size_t>(d0)], s1 = lay_.dpt_ptr[static_cast<std::size_t>(d1)];
+      if (s1 > s0)
+        launch(kern, static_cast<int>((s1 - s0 + 127) / 128), 128, s0, s1, slot_cam_.get(), slot_dpt_.get(),
+               slot_edge_.get(), plan_.range.start, slot_px_.get(), slot_py_.get(), slot_w_.get(), xc_.get(), xp_.get(),
+               Jb_.get(), E_.get(), slot_chunk_.get(), chunk_slot_.get(), bad_.get());
+      if (d1 > d0)
+        launch(dev::k_assemble_points<S>, grid_for(d1 - d0, 128, 1 << 30), 128, d0, d1, dpt_ptr_.get(), s0, Jb_.get(),
+               C_.get(), w_.get());
+      const int ncam = nb > 1 ? jb_ncam_[static_cast<std::size_t>(b)] : m_loc_;
+      if (ncam > 0)
+        launch(dev::k_assemble_cameras<S, 256>, ncam, 256, cam_ptr_.get() + static_cast<std::size_t>(b) * (m_loc_ + 1),
+               cam_glob_.get(), cslot_dslot_.get(), s0, Jb_.get(), B_.get(), v_.get(), nb > 1 ? carry_.get() : nullptr,
+               nb > 1 ? cam_list_.get() + static_cast<std::size_t>(b) * m_loc_ : nullptr);
     }
+    if (nb > 1 && m_loc_ > 0)
+      launch(dev::k_carry_out<S>, grid_for(m_loc_, 128, 1 << 30), 128, m_loc_, cam_glob_.get(),
+             static_cast<const double*>(carry_.get()), B_.get(), v_.get());
     tally_.edges += static_cast<std::uint64_t>(N_);
     const std::int64_t bad = agree_min_index(bad_.get());
     if (bad >= 0) throw degenerate_depth(bad);
-    DBAG_CUDA(cudaMemsetAsync(B_.get(), 0, B_.size() * sizeof(S), st_));
-    DBAG_CUDA(cudaMemsetAsync(v_.get(), 0, v_.size() * sizeof(S), st_));
-    if (n_loc_ > 0)
-      launch(dev::k_assemble_points<S>, grid_for(n_loc_, 128, 1 << 30), 128, n_loc_, dpt_ptr_.get(), Jb_.get(),
-             C_.get(), w_.get());
-    if (m_loc_ > 0)
-      launch(dev::k_assemble_cameras<S, 256>, m_loc_, 256, cam_ptr_.get(), cam_glob_.get(), cslot_dslot_.get(),
-             Jb_.get(), B_.get(), v_.get());
     comm_->allreduce_sum(B_.get(), static_cast<std::int64_t>(m_) * 81, kT, st_);
     halo_exchange_Cw();
     comm_->allreduce_sum(v_.get(), static_cast<std::int64_t>(m_) * 9, kT, st_);
@@ -998,6 +1072,7 @@ class Rank {
   void get_jacobians(S* res, S* jac) {
     DBAG_CUDA(cudaSetDevice(device_));
     DBAG_CUDA(cudaStreamSynchronize(st_));
+    if (jb_pt_.size() > 2) throw Error(DBAG_INVALID_ARGUMENT, "Jacobian rows are kept for one Jb batch only");
     std::vector<S> jb(static_cast<std::size_t>(N_) * 28);
     DBAG_CUDA(cudaMemcpy(jb.data(), Jb_.get(), sizeof(S) * jb.size(), cudaMemcpyDeviceToHost));
     for (std::int64_t s = 0; s < N_; ++s) {
@@ -1402,6 +1477,10 @@ class Rank {
   cudaGraph_t g_graph_ = nullptr;
   cudaGraphExec_t g_exec_ = nullptr;
   DevBuf<S> Jb_, part_, halo_buf_;
+  DevBuf<double> carry_;               // k_assemble_cameras sums across Jb batches
+  std::vector<std::int32_t> jb_pt_;    // Jb batch boundaries (device points)
+  std::vector<std::int32_t> jb_ncam_;  // cameras each Jb batch touches
+  DevBuf<std::int32_t> cam_list_;      // ... their local ids, m_loc per batch
   DevBuf<T> E_;  // chunk records: E lanes (T) + RecMeta
   DevBuf<Scal> sc_;
   DevBuf<double> red_part_, dsc_, bounce_;

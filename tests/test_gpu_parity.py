@@ -548,3 +548,32 @@ def test_memory_pool_matches_prediction(lean):
     for k in (2, 3):
         preds = [dba.predict_memory(p, k, r, coupling_fp32=lean) for r in range(k)]
         assert max(preds) < pred
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("k", [1, 2])
+def test_batched_assembly_scratch(monkeypatch, k):
+    """Jb (the per-edge rows linearize hands to assembly) in batches of whole
+    points (DBAG_JB_BATCH slots): C, w and E are computed exactly as in one
+    batch; B and v add the batches' double-precision sums, so they agree to
+    rounding; the LM trajectory matches; the pool shrinks accordingly."""
+    p = ring(50, 2000, 6, noise=0.5, seed=11)
+    out = {}
+    for cap in (0, 700):
+        if cap:
+            monkeypatch.setenv("DBAG_JB_BATCH", str(cap))
+        else:
+            monkeypatch.delenv("DBAG_JB_BATCH", raising=False)
+        with dba.RankContext(0, 8) as c:
+            c.upload(p)
+            c.linearize()
+            out[cap] = [np.array(a, copy=True) for a in c.system()]
+            out[cap].append(c.memory_pool()[0])
+        out[cap].append(dba.lm_solve(p, dba.SolverConfig(max_iterations=4, pcg_tol=1e-10, pcg_max_iters=1000,
+                                                         workers=k)))
+    B0, C0, E0, v0, w0, pool0, st0 = out[0]
+    B1, C1, E1, v1, w1, pool1, st1 = out[700]
+    assert np.array_equal(C1, C0) and np.array_equal(w1, w0) and np.array_equal(E1, E0)
+    assert rel(B1, B0) < 1e-14 and rel(v1, v0) < 1e-14
+    assert pool0 - pool1 >= (p.num_observations - 700 - 200) * 28 * 8
+    _compare_histories(st1, st0, 1e-9, check_lambda=False)

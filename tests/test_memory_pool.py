@@ -54,3 +54,15 @@ def test_prediction_is_deterministic_and_validates(ladybug):
         dba.predict_memory(ladybug, 2, 2)  # rank out of range
     with pytest.raises(dba.InvalidArgumentError):
         dba.predict_memory(ladybug, 0, 0)
+
+
+def test_assembly_scratch_is_bounded(ladybug, monkeypatch):
+    """The Jb assembly rows (28 scalars per edge) are held for one batch of
+    whole points at a time: with DBAG_JB_BATCH slots the pool shrinks by
+    the rows of all but one batch, plus a 54-double carry per camera."""
+    full = dba.predict_memory(ladybug)
+    monkeypatch.setenv("DBAG_JB_BATCH", "4096")
+    small = dba.predict_memory(ladybug)
+    n = ladybug.num_observations
+    saved = full - small
+    assert (n - 4096 - 64) * 28 * 8 - 49 * 54 * 8 - 8 * 2**10 <= saved <= (n - 4096) * 28 * 8 + 4 * 2**10
