@@ -46,6 +46,7 @@ struct DseArgs {
   S* out_pt;
   const std::int32_t* long_chunk;  // first chunk of each long tile
   std::int32_t n_long;
+  std::int32_t pf_dist;  // > 0: chunk c prefetches record c + pf_dist into L2
 };
 
 // Shared work area of a chunk pass. a (3 x kTile), b (3 x kTile) and the
@@ -256,8 +257,18 @@ __device__ __forceinline__ void dse_chunk_at(const DseArgs<S, T>& A, DseWork<S>&
   }
 }
 
+__device__ __forceinline__ void l2_prefetch(const void* p, unsigned bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
 template <class S, int MODE, class G, class T>
 __device__ __forceinline__ void dse_chunk(const DseArgs<S, T>& A, DseWork<S>& sm, std::int32_t chunk, const G& gx) {
+  // One wave ahead: the record the CTA pf_dist chunks later will read is
+  // streamed into L2 now (E is constant through the PCG, so this may run
+  // before the producer wait), decoupling HBM traffic from the pass's
+  // per-chunk latency chain.
+  if (A.pf_dist > 0 && threadIdx.x == 0 && chunk + A.pf_dist < A.n_chunks)
+    l2_prefetch(A.rec + std::size_t(chunk + A.pf_dist) * Rec<T>::kLen, unsigned(Rec<T>::kLen * sizeof(T)));
   dse_chunk_at<S, MODE>(A, sm, A.rec + std::size_t(chunk) * Rec<T>::kLen, gx);
 }
 

@@ -1346,7 +1346,25 @@ class Rank {
     a.out_pt = dxp_.get();
     a.long_chunk = long_chunk_.get();
     a.n_long = n_long_;
+    a.pf_dist = pf_dist();
     return a;
+  }
+
+  // L2 prefetch distance of the chunk pass: one wave of resident CTAs
+  // (DBAG_PF overrides; 0 disables).
+  std::int32_t pf_dist() {
+    if (pf_dist_ < 0) {
+      const char* e = std::getenv("DBAG_PF");
+      if (e) {
+        pf_dist_ = std::max(0, std::atoi(e));
+      } else {
+        int per_sm = 0, sms = 0;
+        DBAG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dev::k_g_pass<S, T>, dev::kTile, 0));
+        DBAG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device_));
+        pf_dist_ = per_sm * sms;
+      }
+    }
+    return pf_dist_;
   }
 
   template <int MODE>
@@ -1479,6 +1497,7 @@ class Rank {
   DevBuf<S> Jb_, part_, halo_buf_;
   DevBuf<double> carry_;               // k_assemble_cameras sums across Jb batches
   std::vector<std::int32_t> jb_pt_;    // Jb batch boundaries (device points)
+  std::int32_t pf_dist_ = -1;
   std::vector<std::int32_t> jb_ncam_;  // cameras each Jb batch touches
   DevBuf<std::int32_t> cam_list_;      // ... their local ids, m_loc per batch
   DevBuf<T> E_;  // chunk records: E lanes (T) + RecMeta
