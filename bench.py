@@ -62,6 +62,30 @@ def dse_bytes(N, n, m, s):
     return N * (27 * s + 4) + 9 * n * s + 108 * m * s
 
 
+def lm_bytes(N, n, m, s, I, linearized=True):
+    """Algorithmic bytes of one LM iteration (SURVEY.md §8d B_LM) with I PCG
+    iterations and R = I // 50 residual refreshes; the leading 1 of B_PCG is
+    the reference's DSE on x0 = 0, kept in the count."""
+    b_lin = N * (3 * s + 8) + 3 * n * s + 9 * m * s + 27 * N * s + 90 * m * s + 12 * n * s
+    b_fact = 162 * m * s + 18 * n * s
+    b_rhs = N * (27 * s + 4) + 12 * n * s + 9 * m * s
+    b_pcg = (1 + I + I // 50) * dse_bytes(N, n, m, s) + I * 153 * m * s
+    b_back = N * (27 * s + 4) + 15 * n * s
+    b_cost = N * (3 * s + 8) + 6 * n * s + 18 * m * s
+    return (b_lin if linearized else 0) + b_fact + b_rhs + b_pcg + b_back + b_cost
+
+
+def lm_roofline(N, n, m, s, I, world, peak, ms_step, prof, steps):
+    """Whole-iteration roofline: B_LM / (K peak) against the
+    measured t_LM, and the DSE edge throughput N (1 + I + R) / t_PCG."""
+    b = lm_bytes(N, n, m, s, I)
+    t_roof_ms = b / (world * peak * 1e9) * 1e3
+    t_pcg_ms = prof["dse_ms"] / max(steps, 1)
+    return {"bytes_per_step": b, "roofline_ms": t_roof_ms, "measured_ms": ms_step, "frac": t_roof_ms / ms_step,
+            "pcg_ms_per_step": t_pcg_ms,
+            "dse_edges_per_s": N * (1 + I + I // 50) / (t_pcg_ms / 1e3) if t_pcg_ms > 0 else None}
+
+
 class ClockSampler:
     """nvidia-smi clocks + throttle reasons sampled during the timed region."""
 
@@ -281,6 +305,7 @@ def run_ours(args):
         "clocks": clk.summary(),
         "gpu_launches": int(launches),
         "device_pool_bytes": int(ctx.memory_pool()[0]),
+        "lm_roofline": lm_roofline(N, n, m, 8, pcg, world, peak, ms_step, prof, args.steps),
     }
     if world == 1 and rank == 0 and not args.no_secondary:
         line["secondary"] = secondary(args, flush)
