@@ -554,14 +554,35 @@ __global__ void __launch_bounds__(kRedThreads) k_g_fs(GBufs<S> B, RedWs ws, GSca
 constexpr int kFscThreads = 544;  // 17 warps: a 16-CTA cluster covers 272 cameras with one camera per warp
 constexpr int kFscWarps = kFscThreads / 32;
 
+// Cluster sums over distributed shared memory without remote reads: before
+// the cluster barrier each CTA pushes its value into slot [its rank] of the
+// inbox of every CTA that needs the sum (remote stores, issued in parallel
+// by the lanes of one warp); after it, a warp reduces its local inbox in a
+// fixed tree order, so every CTA gets the same bits and no CTA has to wait
+// for another to finish reading before it exits.
+__device__ __forceinline__ void cluster_push(const cooperative_groups::cluster_group& cluster, double* inbox,
+                                             int rank, double v, int lane, int to_lo, int to_hi) {
+  const int r = to_lo + lane;
+  if (r < to_hi) *cluster.map_shared_rank(inbox + rank, r) = v;
+}
+__device__ __forceinline__ double inbox_sum(const double* inbox, int lane, int ncta) {
+  double t = lane < ncta ? inbox[lane] : 0.0;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) t += __shfl_down_sync(0xffffffffu, t, o);
+  return t;  // lane 0
+}
+
 template <class S, int CPW>
 __global__ void __launch_bounds__(kFscThreads, 1) k_g_fsc(GBufs<S> B, GScal<S>* sc, cudaGraphConditionalHandle h_while) {
   namespace cg = cooperative_groups;
   cg::cluster_group cluster = cg::this_cluster();
   __shared__ double w_pq[kFscWarps], w_rho[kFscWarps], w_rn[kFscWarps];
-  __shared__ double cta_sum[3];  // this CTA's p'q, rho, |r|^2 (read by the cluster)
+  __shared__ double in_pq[32], in_rho[32], in_rn[32];  // cluster_push inboxes, one slot per CTA
   __shared__ double pq_all;
   pdl_allow_dependents();
+  // phase 0 of the cluster barrier: arrive now, wait before the first
+  // remote store (every CTA of the cluster has started by then)
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int row = lane < 9 ? lane : 0;
   const int rank = int(cluster.block_rank()), ncta = int(cluster.num_blocks());
@@ -617,6 +638,7 @@ __global__ void __launch_bounds__(kFscThreads, 1) k_g_fsc(GBufs<S> B, GScal<S>* 
       if (row == i) cr[j] = acc[i];
   }
   if (done != 0 || n < 0 || beta != beta) return;  // uniform over the cluster (n < 0, NaN beta: never)
+  asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
   DBAG_TL(n, 1, rank == 0 && threadIdx.x == 0);
   DBAG_TL(n, 2, rank == 0 && threadIdx.x == 0);
   const bool pcg = phase == 0;
@@ -642,20 +664,19 @@ __global__ void __launch_bounds__(kFscThreads, 1) k_g_fsc(GBufs<S> B, GScal<S>* 
   if (pcg) {
     if (lane == 0) w_pq[warp] = pq_w;
     __syncthreads();
-    if (threadIdx.x == 0) {
+    if (warp == 0) {
       double b = 0.0;
       for (int w = 0; w < kFscWarps; ++w) b += w_pq[w];
-      cta_sum[0] = b;
+      cluster_push(cluster, in_pq, rank, b, lane, 0, ncta);  // to every CTA
     }
     DBAG_TL(n, 3, rank == 0 && threadIdx.x == 0);
     cluster.sync();
     DBAG_TL(n, 4, rank == 0 && threadIdx.x == 0);
-    if (threadIdx.x == 0) {
-      double a = 0.0;
-      for (int r = 0; r < ncta; ++r) a += *cluster.map_shared_rank(&cta_sum[0], r);
-      pq_all = a;
+    if (warp == 0) {
+      const double t = inbox_sum(in_pq, lane, ncta);
+      if (lane == 0) pq_all = t;
     }
-    cluster.sync();  // every CTA has read every cta_sum[0]
+    __syncthreads();
     pq = pq_all;
     DBAG_TL(n, 5, rank == 0 && threadIdx.x == 0);
     if (!(pq > 0.0) || isinf(pq)) {  // p'q breakdown (uniform over the cluster)
@@ -707,22 +728,23 @@ __global__ void __launch_bounds__(kFscThreads, 1) k_g_fsc(GBufs<S> B, GScal<S>* 
     w_rn[warp] = rn_w;
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
+  if (warp == 0) {
     double a = 0.0, b = 0.0;
     for (int w = 0; w < kFscWarps; ++w) {
       a += w_rho[w];
       b += w_rn[w];
     }
-    cta_sum[1] = a;
-    cta_sum[2] = b;
+    cluster_push(cluster, in_rho, rank, a, lane, 0, 1);  // to CTA 0
+    cluster_push(cluster, in_rn, rank, b, lane, 0, 1);
   }
   cluster.sync();
+  if (rank != 0) return;
+  double rho = 0.0, rn = 0.0;
+  if (warp == 0) {
+    rho = inbox_sum(in_rho, lane, ncta);
+    rn = inbox_sum(in_rn, lane, ncta);
+  }
   if (rank == 0 && threadIdx.x == 0) {
-    double rho = 0.0, rn = 0.0;
-    for (int r = 0; r < ncta; ++r) {
-      rho += *cluster.map_shared_rank(&cta_sum[1], r);
-      rn += *cluster.map_shared_rank(&cta_sum[2], r);
-    }
     DBAG_TL(n, 6, true);
     sc->dse_count += 1;
     if (pcg) {
@@ -737,7 +759,6 @@ __global__ void __launch_bounds__(kFscThreads, 1) k_g_fsc(GBufs<S> B, GScal<S>* 
       finish_iteration(sc, rho, rn, h_while);
     }
   }
-  cluster.sync();  // CTA 0 has read every CTA's sums
 }
 
 }  // namespace dev
