@@ -49,20 +49,31 @@ struct DseArgs {
   std::int32_t pf_dist;  // > 0: chunk c prefetches record c + pf_dist into L2
 };
 
-// Shared work area of a chunk pass. a (3 x kTile), b (3 x kTile) and the
-// staged camera vectors xs live only through the point solves; y (9 x kTile)
-// only from then on, so y overlays them (a smaller footprint leaves L1 room
-// for the in-flight E lines of more resident CTAs).
+// Shared work area of a chunk pass: a (3 x kTile), b (3 x kTile) and the
+// staged camera vectors xs, then y (9 x kTile) in its own buffer (20 KB per
+// CTA in FP64): writing y needs no barrier after the b reads. Overlaying y
+// on a/b/xs (DBAG_Y_OVERLAY=1, 11 KB) costs that barrier and measured 3 %
+// slower per LM iteration (trafalgar and venice).
+#ifndef DBAG_Y_OVERLAY
+#define DBAG_Y_OVERLAY 0
+#endif
 template <class S>
 struct DseWork {
   S buf[kTile * 9];
+#if !DBAG_Y_OVERLAY
+  S ybuf[kTile * 9];
+#endif
   std::int32_t upart[kTile];
   std::uint8_t uslot[kTile];
   std::uint8_t ubeg[kTile + 8];
   __device__ __forceinline__ S (*a())[3] { return reinterpret_cast<S(*)[3]>(buf); }
   __device__ __forceinline__ S (*b())[3] { return reinterpret_cast<S(*)[3]>(buf + 3 * kTile); }
   __device__ __forceinline__ S* xs() { return buf + 6 * kTile; }
+#if DBAG_Y_OVERLAY
   __device__ __forceinline__ S (*y())[9] { return reinterpret_cast<S(*)[9]>(buf); }
+#else
+  __device__ __forceinline__ S (*y())[9] { return reinterpret_cast<S(*)[9]>(ybuf); }
+#endif
 };
 static_assert(6 * kTile + kXsCams * 9 <= 9 * kTile, "a, b and xs must fit under y");
 
@@ -248,12 +259,14 @@ __device__ __forceinline__ void dse_chunk_at(const DseArgs<S, T>& A, DseWork<S>&
   __syncthreads();
   if constexpr (MODE != 1) {
     const S b0 = sm.b()[pti][0], b1 = sm.b()[pti][1], b2 = sm.b()[pti][2];
+#if DBAG_Y_OVERLAY
     __syncthreads();  // y overlays b
+#endif
 #pragma unroll
     for (int i = 0; i < 9; ++i) sm.y()[tid][i] = (e[i * 3] * b0 + e[i * 3 + 1] * b1) + e[i * 3 + 2] * b2;
     __syncthreads();
     fold_cameras(A, nu, sm.ubeg, sm.uslot, sm.upart, YRows<S>{sm.y()});
-    __syncthreads();
+    // one chunk per CTA (k_g_pass, k_dse_chunk): no trailing barrier
   }
 }
 
