@@ -577,3 +577,28 @@ def test_batched_assembly_scratch(monkeypatch, k):
     assert rel(B1, B0) < 1e-14 and rel(v1, v0) < 1e-14
     assert pool0 - pool1 >= (p.num_observations - 700 - 200) * 28 * 8
     _compare_histories(st1, st0, 1e-9, check_lambda=False)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("variant", ["cluster", "grid-barrier", "fold+step kernels"])
+@pytest.mark.parametrize("k", [1, 2])
+def test_dpcg_pq_breakdown(variant, k, monkeypatch):
+    """p'q <= 0 stops DPCG with PcgBreakdownError (dba/solver.hpp:238-241),
+    uniformly over the graph's fold + step forms and the K > 1 loop: an
+    indefinite reduced system S = I - E C^-1 E^T (B = C = I, large E) and a
+    right-hand side along a negative direction of S."""
+    if variant != "cluster":
+        monkeypatch.setenv("DBAG_FSC", "0")
+    if variant == "fold+step kernels":
+        monkeypatch.setenv("DBAG_FS", "0")
+    p = ProblemFactory(123).random_problem(2, 3, 6)
+    m, n, N = p.num_cameras, p.num_points, p.num_observations
+    E = np.random.default_rng(5).uniform(-3, 3, (N, 27))
+    blocks = (np.tile(np.eye(9), (m, 1, 1)), np.tile(np.eye(3), (n, 1, 1)), E)
+    cams, pts, cid, pid, *_ = p.arrays()
+    Ed = dense_coupling(E.reshape(N, 9, 3), cid, pid, m, n)
+    S = np.eye(9 * m) - Ed @ Ed.T
+    w, V = np.linalg.eigh(S)
+    assert w[0] < 0
+    with pytest.raises(dba.PcgBreakdownError):
+        dba.group_operator(p, k, V[:, 0], mode=1, blocks=blocks, tol=1e-12, max_iters=100)
