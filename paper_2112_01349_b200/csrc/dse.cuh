@@ -167,7 +167,7 @@ struct YRows {  // y[slot][9] rows (DseWork)
 template <class S>
 __device__ __forceinline__ void stage_meta(const RecMeta& M, DseWork<S>& sm) {
   const int tid = threadIdx.x;
-  sm.upart[tid] = M.upart[tid];
+  if (tid < kPfParts || tid < M.nu) sm.upart[tid] = M.upart[tid];
   sm.uslot[tid] = M.uslot[tid];
   sm.ubeg[tid] = M.ubeg[tid];
   if (tid < 8) sm.ubeg[kTile + tid] = M.ubeg[kTile + tid];
@@ -281,7 +281,7 @@ __device__ __forceinline__ void dse_chunk(const DseArgs<S, T>& A, DseWork<S>& sm
   // before the producer wait), decoupling HBM traffic from the pass's
   // per-chunk latency chain.
   if (A.pf_dist > 0 && threadIdx.x == 0 && chunk + A.pf_dist < A.n_chunks)
-    l2_prefetch(A.rec + std::size_t(chunk + A.pf_dist) * Rec<T>::kLen, unsigned(Rec<T>::kLen * sizeof(T)));
+    l2_prefetch(A.rec + std::size_t(chunk + A.pf_dist) * Rec<T>::kLen, rec_hot_bytes<T>());
   dse_chunk_at<S, MODE>(A, sm, A.rec + std::size_t(chunk) * Rec<T>::kLen, gx);
 }
 

@@ -16,6 +16,8 @@
 // sums per-block partials in block order.
 #pragma once
 
+#include <cstddef>
+
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -36,16 +38,25 @@ constexpr int kXsCams = 32;  // distinct cameras of a chunk whose vectors are ga
 struct RecMeta {
   std::int32_t p0, np, nslots, nchunk;  // first device point, points, slots; nchunk > 1: long tile
   std::int32_t nu, ci, pad0, pad1;      // distinct cameras; chunk index inside its tile
-  std::int32_t cam[kTile];              // camera of each slot (padding: 0)
-  std::int32_t upart[kTile];            // camera-major partial position of each distinct camera
   std::int32_t ucam[kXsCams];           // camera id of distinct camera u < kXsCams
   std::uint8_t pt[kTile];               // slot -> point index in the tile
   std::uint8_t uslot[kTile];            // slots grouped by camera
   std::uint8_t ubeg[kTile + 8];         // camera u's slots: uslot[ubeg[u] .. ubeg[u+1])
   std::uint8_t pbeg[kTile + 8];         // point i's slots: [pbeg[i], pbeg[i+1])
   std::uint8_t su[kTile];               // slot -> its distinct camera u (inverse of uslot / ubeg)
+  std::int32_t upart[kTile];            // camera-major partial position of each distinct camera
+  std::int32_t cam[kTile];              // camera of each slot (padding: 0); read only when nu > kXsCams
 };
 static_assert(sizeof(RecMeta) % 16 == 0, "record metadata must keep 16-byte alignment");
+// Bytes of a record the pass reads for a chunk with at most kPfParts
+// distinct cameras: the E lanes and the metadata up to upart[kPfParts)
+// (cam[] and the rest of upart[] are read only by rarer chunks).
+constexpr int kPfParts = 16;
+template <class S>
+constexpr unsigned rec_hot_bytes() {
+  return unsigned(27 * kTile * sizeof(S) + offsetof(RecMeta, upart) + kPfParts * sizeof(std::int32_t));
+}
+static_assert(rec_hot_bytes<double>() % 16 == 0 && rec_hot_bytes<float>() % 16 == 0, "bulk prefetch size");
 
 // E chunk record: 27 lanes x kTile slots (lane-major) then RecMeta; one
 // record per 128-slot chunk of the device slot order.
