@@ -418,7 +418,7 @@ __device__ __forceinline__ void grid_barrier(unsigned long long* count) {
 // Same arithmetic (and association) as k_g_fold + k_g_step except the final
 // rho / |r|^2 block reductions (one camera per warp here).
 template <class S>
-__global__ void __launch_bounds__(kRedThreads) k_g_fs(GBufs<S> B, RedWs ws, GScal<S>* sc,
+__global__ void __maxnreg__(128) k_g_fs(GBufs<S> B, RedWs ws, GScal<S>* sc,  // 80 registers spilled 48 B
                                                       cudaGraphConditionalHandle h_while, unsigned long long* bar) {
   __shared__ double red[32];
   __shared__ double pq_all;
