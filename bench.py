@@ -6,14 +6,21 @@ A step is one LM iteration of the reference's inner loop
 assemble (+ all-reduce), damp + factor, rhs, DPCG to pcg_tol / pcg_max_iters,
 back-substitution, trial cost and model terms. Every step starts from the
 same state x0 at lambda0 and the accept is not committed, so each step does
-identical work (SURVEY.md §8d timing note).
+identical work (SURVEY.md §8d timing note). The headline workload is
+Venice-1778 (BASELINE.json configs[2], the configuration the metric is quoted
+"at 1/2/4/8 B200" on); a real 10-iteration solve's IterationRecord
+wall-second deltas are reported beside it (BASELINE.md §3 t_LM).
 
   python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--workload NAME]
 
-N > 1 runs under torchrun, one process per GPU, NCCL between ranks.
-`--impl reference` times the CPU restatement of the reference (oracle/, the
+N > 1: one process per GPU, NCCL between ranks. Under torchrun (the driver)
+the ranks come from the environment; a bare `python bench.py --gpus N`
+re-launches itself under torch.distributed.run with N processes.
+`--impl reference` times the CPU restatement of the reference (oracle/; the
 reference itself cannot be compiled here: Eigen/doctest/CLI11 are absent) on
-the host cores, on the same workload.
+the host's physical cores, K rank threads as dba/comms.hpp:214-234, on the
+same workload. That process imports only oracle/ (its own generator, config
+and ctypes structs), never the product package.
 """
 import argparse
 import json
@@ -36,8 +43,9 @@ WORKLOADS = {  # (cameras, points, observations) — BASELINE.json configs
     "final-13682": (13682, 4456117, 28987644),
     "city-50k": (50000, 20000000, 150000000),
 }
-DEFAULT_WORKLOAD = "trafalgar-257"  # configs[1]: the 1-B200 configuration
-SECONDARY_WORKLOAD = "venice-1778"  # configs[2]: larger than L2, HBM-bound
+DEFAULT_WORKLOAD = "venice-1778"  # configs[2]: the metric's "1/2/4/8 B200" configuration; fits one GPU
+SECONDARY_WORKLOAD = "trafalgar-257"  # configs[1]: the FP32/FP64 1-B200 configuration
+PCG_SAMPLE = 20  # PCG iterations per bounded CPU-reference sample step
 
 
 def load_peaks():
@@ -48,12 +56,45 @@ def load_peaks():
         return 6650.0, "fallback"
 
 
-def make_problem(name, dtype=np.float64):
-    import paper_2112_01349_b200 as dba
+def synth_kwargs(name):
+    """The BASELINE.md §3 instance: ring recipe, seed 1, count-exact, +-0.5 px noise."""
     m, n, N = WORKLOADS[name]
-    p = dba.generate_synthetic(dba.SyntheticOptions(cameras=m, points=n, num_observations=N, seed=1,
-                                                    pixel_noise=0.5))
+    return dict(cameras=m, points=n, num_observations=N, seed=1, pixel_noise=0.5)
+
+
+def make_problem(name, dtype=np.float64):
+    """The product's generator (windowed search; bit-identical to the oracle's
+    exhaustive restatement of dba/synthetic.hpp, tests/test_generator.py)."""
+    import paper_2112_01349_b200 as dba
+    p = dba.generate_synthetic(dba.SyntheticOptions(**synth_kwargs(name)))
     return p if dtype == np.float64 else p.astype(dtype)
+
+
+def make_oracle_problem(name, dtype=np.float64):
+    """The same instance from the oracle's own generator (no product import)."""
+    from oracle import oracle as O
+    p = O.generate_synthetic(O.SynthOptions(**synth_kwargs(name)))
+    return p if dtype == np.float64 else p.astype(dtype)
+
+
+def host_info():
+    """nproc / lscpu of this host: logical CPUs, physical cores, model."""
+    info = {"nproc": os.cpu_count() or 1}
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        kv = {}
+        for line in out.splitlines():
+            if ":" in line:
+                k, v = line.split(":", 1)
+                kv[k.strip()] = v.strip()
+        info["model"] = kv.get("Model name")
+        info["threads_per_core"] = int(kv.get("Thread(s) per core", "1"))
+        info["physical_cores"] = int(kv.get("Core(s) per socket", "0")) * int(kv.get("Socket(s)", "1"))
+    except Exception:
+        pass
+    if not info.get("physical_cores"):
+        info["physical_cores"] = info["nproc"]
+    return info
 
 
 def dse_bytes(N, n, m, s):
@@ -139,36 +180,99 @@ def dist_env():
 
 
 def cpu_threads():
-    # The reference's threading model: K worker threads, one rank each
-    # (dba/comms.hpp:214-234). Its all-reduce reads K x len per rank
-    # (dba/comms.hpp:76-81), so more than 16 ranks slows it down.
-    return max(1, min(os.cpu_count() or 1, 16))
+    """K for the CPU reference: the host's physical core count (BASELINE.md
+    §3), one rank thread each, as the reference's run_on_workers."""
+    return max(1, host_info()["physical_cores"])
+
+
+def scaled_lm_seconds(phases, dse_sample, dse_full):
+    """One LM iteration's seconds from a bounded sample: every phase as
+    measured (oracle.PHASES), the DPCG loop (phase 4) scaled from the
+    sample's loop DSE count to the full iteration's (every loop DSE is the
+    same work: one E^T x / C^-1 / E b round with its two all-reduces,
+    dba/solver.hpp:149-181; the first DSE, on x0, is in the setup phase)."""
+    ph = np.asarray(phases, dtype=float)
+    return float(ph.sum() - ph[4] + ph[4] * (dse_full - 1) / max(int(dse_sample) - 1, 1))
+
+
+def cpu_reference_steps(p, k, n_steps, dse_full=None, calibrate=True):
+    """Times the oracle's LM step on k rank threads. With calibrate, first one
+    FULL LM iteration (unscaled, gives the full DSE count); then n_steps
+    bounded samples (DPCG capped at PCG_SAMPLE iterations) scaled to the full
+    iteration. Returns (per-step seconds, info)."""
+    from oracle import oracle as O
+    cfg = O.OracleConfig(workers=k)
+    info = {"threads": k, "pcg_sample": PCG_SAMPLE}
+    if calibrate:
+        ph, its, dse = O.lm_probe_phases(p, cfg, 1)
+        dse_full = int(dse[0])
+        info.update(full_iteration_s=float(ph[0].sum()), full_pcg_iterations=int(its[0]),
+                    full_phases_s=dict(zip(O.PHASES, map(float, ph[0]))))
+    info["dse_per_full_iteration"] = int(dse_full)
+    ph, its, dse = O.lm_probe_phases(p, cfg, n_steps, pcg_sample=PCG_SAMPLE)
+    secs = [scaled_lm_seconds(ph[i], dse[i], dse_full) for i in range(n_steps)]
+    info["sample_phases_s"] = dict(zip(O.PHASES, map(float, ph.mean(0))))
+    info["sample_dse_calls"] = int(dse[-1])
+    return secs, info
 
 
 def run_reference(args):
+    """The reference arm: the CPU restatement (oracle/) of the reference's
+    solver on this host's physical cores. Imports oracle/ only."""
     world, rank, _ = dist_env()
     if rank != 0:
         return
-    from oracle import oracle as O
-    import paper_2112_01349_b200 as dba
     m, n, N = WORKLOADS[args.workload]
-    p = make_problem(args.workload)
+    t_gen = time.perf_counter()
+    p = make_oracle_problem(args.workload)
+    t_gen = time.perf_counter() - t_gen
+    host = host_info()
     k = cpu_threads()
-    cfg = dba.SolverConfig(workers=k)
-    secs, its = O.lm_probe_steps(p, cfg, args.warmup + args.steps)
-    timed = secs[args.warmup:]
+    # warm-up: the first step is one FULL LM iteration (calibration: the full
+    # DSE count and an unscaled t_LM); the rest are bounded samples.
+    secs, info = cpu_reference_steps(p, k, args.warmup - 1 + args.steps if args.warmup >= 1 else args.steps)
+    timed = secs[-args.steps:]
     t = float(np.mean(timed))
     value = N / t
-    sample = f"{args.workload} full LM iteration from x0 (oracle restatement, {k} rank threads)"
+    # K = 1 (BASELINE.md §3): one bounded sample, scaled the same way
+    secs1, info1 = cpu_reference_steps(p, 1, 1, dse_full=info["dse_per_full_iteration"], calibrate=False)
+    sample = (f"{args.workload}: each step one LM iteration from x0 (oracle restatement, {k} rank threads), "
+              f"DPCG capped at {PCG_SAMPLE} iterations and its time scaled to the full iteration's "
+              f"{info['dse_per_full_iteration']} DSEs; warm-up step 1 ran the full iteration unscaled "
+              f"({info['full_iteration_s']:.2f} s, {info['full_pcg_iterations']} PCG iterations)")
     print(json.dumps({
         "impl": "reference", "metric": "edges_per_sec_per_lm_iteration", "value": value, "unit": "edges/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": args.workload, "cameras": m, "points": n, "observations": N,
-                   "pcg_iterations_per_step": int(its[-1]), "solver": "SolverConfig defaults"},
-        "cpu_baseline": {"value": value, "unit": "edges/s", "cores": k, "kind": "port", "sample": sample},
+        "config": workload_config(args.workload, info["full_pcg_iterations"]),
+        "cpu_baseline": {"value": value, "unit": "edges/s", "cores": k, "kind": "port", "sample": sample,
+                         "host": host, "jacobian": "autodiff", "detail": info,
+                         "k1": {"value": N / secs1[0], "unit": "edges/s", "cores": 1, "seconds": secs1[0],
+                                "sample": f"one bounded sample at K = 1 (DPCG capped at {PCG_SAMPLE}, scaled)",
+                                "detail": info1}},
         "e2e": {"value": value, "unit": "edges/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "instance_generation_s": t_gen,
+        "repo_libs_loaded": repo_libs_loaded(),
     }), flush=True)
+
+
+def repo_libs_loaded():
+    """In-tree shared objects mapped into this process (the reference arm
+    must show oracle/ only)."""
+    try:
+        with open("/proc/self/maps") as f:
+            return sorted({os.path.relpath(l.split()[-1], ROOT) for l in f
+                           if l.rstrip().endswith(".so") and l.split()[-1].startswith(ROOT)})
+    except Exception:
+        return None
+
+
+def workload_config(name, pcg):
+    m, n, N = WORKLOADS[name]
+    return {"workload": name, "cameras": m, "points": n, "observations": N, "pcg_iterations_per_step": int(pcg),
+            "solver": "SolverConfig defaults (diag_scaled, lambda0 1e-4, pcg_tol 1e-6, pcg_max_iters 500)",
+            "step": "one LM iteration from x0 (linearize+assemble, damp+factor, rhs, DPCG, backsub, trial cost)",
+            "instance": "dba/synthetic.hpp ring, seed 1, count-exact, +-0.5 px noise (BASELINE.md §3)"}
 
 
 def flush_l2(buf):
@@ -221,21 +325,46 @@ def dse_roofline(ctx, prof, b_dse, peak, steps, total_ms, world):
                     "traffic = ncu dram bytes of one standalone launch (profiles/ncu_traffic.json)"}
 
 
+def solve_t_lm(p, world, rank, uid, device, iters=10):
+    """BASELINE.md §3 t_LM: a real lm_solve (SolverConfig defaults,
+    max_iterations 10), per-iteration seconds = consecutive
+    IterationRecord.wall_seconds deltas (rejects, which do not relinearize,
+    included). Iteration 1's figure also holds the initial cost."""
+    import paper_2112_01349_b200 as dba
+    cfg = dba.SolverConfig(workers=world, max_iterations=iters)
+    if world == 1:
+        st = dba.lm_solve(p, cfg, devices=[device])
+    else:
+        st = dba.lm_solve_rank(p, cfg, rank, world, uid, device)
+    wall = [r.wall_seconds for r in st.history]
+    dt = [wall[0]] + [b - a for a, b in zip(wall, wall[1:])]
+    N = p.num_observations
+    return {"iterations": len(dt), "t_lm_s": dt, "mean_t_lm_s": float(np.mean(dt)),
+            "edges_per_s": N / float(np.mean(dt)), "pcg_iterations": [r.pcg_iterations for r in st.history],
+            "accepted": [r.accepted for r in st.history], "cost": [r.cost for r in st.history],
+            "termination": st.termination, "note": "host wall clock of the one-shot dbag_lm_solve (upload excluded)"}
+
+
 def run_ours(args):
     import torch
     import paper_2112_01349_b200 as dba
     world, rank, local = dist_env()
     dist = None
+    ndev = max(dba.device_count(), 1)
+    device = local % ndev
+    uid = None
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("gloo")
         uid = [dba.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
-        ctx = dba.RankContext(local, 8, nccl=(rank, world, uid[0]))
+        uid = uid[0]
+        ctx = dba.RankContext(device, 8, nccl=(rank, world, uid))
+        print(f"[bench] rank {rank}/{world}: NCCL communicator up on cuda:{device}", file=sys.stderr, flush=True)
     else:
-        ctx = dba.RankContext(0, 8)
-    torch.cuda.set_device(local)
-    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=f"cuda:{local}")
+        ctx = dba.RankContext(device, 8)
+    torch.cuda.set_device(device)
+    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=f"cuda:{device}")
     m, n, N = WORKLOADS[args.workload]
     p = make_problem(args.workload)
     ctx.upload(p)
@@ -247,7 +376,7 @@ def run_ours(args):
     ctx.synchronize()
     l0 = ctx.launch_count()
     ctx.profile(True)
-    with ClockSampler(local) as clk:
+    with ClockSampler(device) as clk:
         ms, pcg = time_steps(ctx, cfg, args.steps, flush)
     prof = ctx.profile()
     ctx.profile(False)
@@ -285,36 +414,31 @@ def run_ours(args):
     b_dse = dse_bytes(N // world, n, m, 8)
     roof = dse_roofline(ctx, prof, b_dse, peak, args.steps, total_ms, world)
     roof["peak_kind"] = peak_kind
-    try:
-        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
-            roof["traffic"] = json.load(f).get(args.workload, {}).get("dram_bytes_per_launch")
-    except Exception:
-        pass
+    roof["traffic"], roof["traffic_source"] = ncu_traffic(args.workload)
+    ctx.close()
     line = {
         "metric": "edges_per_sec_per_lm_iteration", "value": value, "unit": "edges/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": args.workload, "cameras": m, "points": n, "observations": N,
-                   "pcg_iterations_per_step": pcg, "parallelism": f"edge-partitioned x{world}",
-                   "solver": "SolverConfig defaults (diag_scaled, lambda0 1e-4, pcg_tol 1e-6, pcg_max_iters 500)",
-                   "l2": "flushed (512 MiB write) between timed steps",
-                   "step": "one LM iteration from x0 (linearize+assemble, factor, rhs, DPCG, backsub, trial cost)"},
+        "config": dict(workload_config(args.workload, pcg), parallelism=f"edge-partitioned x{world}",
+                       l2="flushed (512 MiB write) between timed steps; the E stream (1.2 GB) exceeds L2 anyway"),
         "roofline": roof,
         "e2e": {"value": N / e2e_s, "unit": "edges/s", "h2d_bytes_per_step": state_bytes,
                 "d2h_bytes_per_step": state_bytes},
         "clocks": clk.summary(),
         "gpu_launches": int(launches),
-        "device_pool_bytes": int(ctx.memory_pool()[0]),
         "lm_roofline": lm_roofline(N, n, m, 8, pcg, world, peak, ms_step, prof, args.steps),
     }
+    if not args.no_solve:
+        line["solve"] = solve_t_lm(p, world, rank, uid, device)
     if world == 1 and rank == 0 and not args.no_secondary:
-        line["secondary"] = secondary(args, flush)
-        line["fp32"] = secondary(args, flush, args.workload, np.float32)
-        # memory-lean variant on the HBM-bound size
-        line["secondary_coupling_fp32"] = secondary(args, flush, SECONDARY_WORKLOAD, coupling_fp32=True)
+        line["secondary"] = secondary(flush, SECONDARY_WORKLOAD)
+        line["secondary_fp32"] = secondary(flush, SECONDARY_WORKLOAD, np.float32)
+        line["fp32"] = secondary(flush, args.workload, np.float32)
+        # memory-lean variant
+        line["coupling_fp32"] = secondary(flush, args.workload, coupling_fp32=True)
     if world == 1 and rank == 0 and not args.no_cpu:
-        line["cpu_baseline"] = cpu_baseline(args, p)
-    ctx.close()
+        line["cpu_baseline"] = cpu_baseline(args, p, pcg)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if dist:
@@ -322,10 +446,20 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
-def secondary(args, flush, name=SECONDARY_WORKLOAD, dtype=np.float64, coupling_fp32=False):
-    """The same step on another configuration: the Venice-shaped problem
-    (inputs larger than L2), or the headline workload in FP32 (BASELINE.json
-    configs[1] is quoted FP32/FP64)."""
+def ncu_traffic(name, dtype="f64"):
+    """dram__bytes_read + write per launch of the dominant kernel from the
+    committed `ncu --set full` capture (the recipe's source for `traffic`)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            e = json.load(f).get(name if dtype == "f64" else f"{name}/{dtype}", {})
+        return e.get("dram_bytes_per_launch"), e.get("source")
+    except Exception:
+        return None, None
+
+
+def secondary(flush, name, dtype=np.float64, coupling_fp32=False):
+    """The same step on another configuration / precision: Trafalgar-257
+    (BASELINE.json configs[1], FP32/FP64), FP32, or the memory-lean variant."""
     import paper_2112_01349_b200 as dba
     m, n, N = WORKLOADS[name]
     s = np.dtype(dtype).itemsize
@@ -333,10 +467,10 @@ def secondary(args, flush, name=SECONDARY_WORKLOAD, dtype=np.float64, coupling_f
     with dba.RankContext(0, s, coupling_fp32=coupling_fp32) as ctx:
         ctx.upload(p)
         cfg = dba.SolverConfig()
-        for _ in range(2):
+        for _ in range(3):
             ctx.probe_step(cfg.lambda0, cfg)
         ctx.profile(True)
-        ms, pcg = time_steps(ctx, cfg, 3, flush)
+        ms, pcg = time_steps(ctx, cfg, 5, flush)
         prof = ctx.profile()
         t = sum(ms) / len(ms)
         peak, _ = load_peaks()
@@ -344,27 +478,53 @@ def secondary(args, flush, name=SECONDARY_WORKLOAD, dtype=np.float64, coupling_f
         if coupling_fp32:  # E lanes at 4 bytes, everything else FP64
             b_dse = N * (27 * 4 + 4) + 9 * n * 8 + 108 * m * 8
         roof = dse_roofline(ctx, prof, b_dse, peak, len(ms), sum(ms), 1)
-    try:
-        if s == 8 and not coupling_fp32:  # the committed captures are FP64 with FP64 E
-            with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
-                roof["traffic"] = json.load(f).get(name, {}).get("dram_bytes_per_launch")
-    except Exception:
-        pass
+    tag = "f64" if s == 8 and not coupling_fp32 else ("f64e32" if coupling_fp32 else "f32")
+    roof["traffic"], roof["traffic_source"] = ncu_traffic(name, tag)
     return {"workload": name, "dtype": ("f64 (E blocks stored f32)" if coupling_fp32 else "f64") if s == 8 else "f32",
             "ms_per_step": t, "value": N / (t / 1e3),
             "unit": "edges/s", "pcg_iterations_per_step": pcg, "roofline": roof}
 
 
-def cpu_baseline(args, p):
-    """The CPU restatement on this host: one LM-iteration step (bounded sample)."""
-    from oracle import oracle as O
-    import paper_2112_01349_b200 as dba
+def cpu_baseline(args, p, pcg):
+    """The CPU restatement on this host's physical cores: one bounded sample
+    of the step (DPCG capped at PCG_SAMPLE iterations, scaled to the GPU
+    step's 1 + I + I//50 DSEs; the same iteration count both sides)."""
     k = cpu_threads()
-    secs, its = O.lm_probe_steps(p, dba.SolverConfig(workers=k), 1)
+    dse_full = 1 + pcg + pcg // 50
+    secs, info = cpu_reference_steps(p, k, 1, dse_full=dse_full, calibrate=False)
     N = WORKLOADS[args.workload][2]
-    return {"value": N / float(secs[0]), "unit": "edges/s", "cores": k, "kind": "port",
-            "sample": f"1 LM-iteration step of {args.workload} ({int(its[0])} PCG iterations), {k} rank threads",
-            "seconds": float(secs[0])}
+    return {"value": N / secs[0], "unit": "edges/s", "cores": k, "kind": "port", "host": host_info(),
+            "sample": f"1 LM-iteration step of {args.workload}, {k} rank threads, DPCG capped at {PCG_SAMPLE} "
+                      f"iterations and scaled to {dse_full} DSEs", "seconds": secs[0], "detail": info}
+
+
+def dry_run(args):
+    """Launcher check without a GPU: every rank joins a gloo group and rank 0
+    reports how many ranks reached it."""
+    world, rank, _ = dist_env()
+    n = 1
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        dist.init_process_group("gloo")
+        t = torch.ones(1)
+        dist.all_reduce(t)
+        n = int(t.item())
+        dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "n_gpus": args.gpus, "world_size": world, "ranks_reached": n}), flush=True)
+
+
+def relaunch(args):
+    """`python bench.py --gpus N` without torchrun: re-run this script under
+    torch.distributed.run with N processes (one per GPU), as the driver does."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 def main():
@@ -376,7 +536,13 @@ def main():
     ap.add_argument("--workload", default=DEFAULT_WORKLOAD, choices=sorted(WORKLOADS))
     ap.add_argument("--no-secondary", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-solve", action="store_true")
+    ap.add_argument("--dry-run", action="store_true", help="launcher check only (no GPU work)")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch(args))
+    if args.dry_run:
+        return dry_run(args)
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -40,6 +40,8 @@
 #include <limits>
 #include <memory>
 #include <mutex>
+#include <numeric>
+#include <random>
 #include <stdexcept>
 #include <string>
 #include <thread>
@@ -1003,7 +1005,8 @@ struct PcgResult {
 template <class S>
 PcgResult dpcg(std::vector<S>& x, const BlockDiag<S, 9>& Bd, const Factored<S, 9>& Binv, const EdgeBlocks<S>& E,
                const Factored<S, 3>& Cinv, const std::vector<S>& rhs, Group& g, int rank, double tol,
-               int max_iters, Counters* cnt, int* dse_calls = nullptr) {
+               int max_iters, Counters* cnt, int* dse_calls = nullptr, double* setup_seconds = nullptr) {
+  const auto t_entry = std::chrono::steady_clock::now();
   const std::size_t dim = rhs.size();
   const double rhs_norm = std::sqrt(dot_d(rhs.data(), rhs.data(), dim));
   if (rhs_norm == 0.0) {
@@ -1021,6 +1024,8 @@ PcgResult dpcg(std::vector<S>& x, const BlockDiag<S, 9>& Bd, const Factored<S, 9
   double rho_prev = 0;
   int n = 0;
   double r_norm = std::sqrt(dot_d(r.data(), r.data(), dim));
+  // (bench instrumentation only: the setup before the loop, for sampling)
+  if (setup_seconds) *setup_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_entry).count();
   while (r_norm > tol * rhs_norm && n < max_iters) {
     z = r;
     Binv.solve_in_place(z.data());
@@ -1233,6 +1238,199 @@ State<S> lm_solve(const Problem<S>& pb, const Config& cfg) {
   std::vector<State<S>> states(static_cast<std::size_t>(cfg.workers));
   run_on_workers(g, [&](int r) { states[std::size_t(r)] = lm_solve_rank(pb, cfg, parts[std::size_t(r)], g, r); });
   return std::move(states[0]);
+}
+
+// ------------------------------------------------------------ synthetic ----
+// dba/synthetic.hpp:19-146, restated with the count-exact extension of
+// SURVEY.md §8d (Q_p = floor(N/n) + [p < N mod n]) and the U(-a, a) pixel
+// noise of tests/acceptance.cpp:88-99 (second mt19937_64(seed) stream, edge
+// order). The nearest-camera search is the reference's EXHAUSTIVE O(n m)
+// scan (dba/synthetic.hpp:118-131), run in parallel over points (each point's
+// choice is independent); the product's windowed search is checked against
+// this one. The point draw order is fixed to x -> y -> z (the reference leaves
+// it to the compiler, dba/synthetic.hpp:108-109).
+struct SynthOptions {
+  std::int32_t cameras = 20000, points = 80000, obs_per_point = 1000, exhaustive_search = 1;
+  std::uint64_t seed = 1;
+  double circle_radius = 8.0, base_focal = 1000.0, pose_noise = 0.01, intrinsic_noise = 0.5, point_noise = 0.1;
+  std::int64_t num_observations = 0;
+  double pixel_noise = 0.0;
+};
+
+class UniformDraw {  // dba/synthetic.hpp:40-50
+ public:
+  explicit UniformDraw(std::uint64_t seed) : e_(seed) {}
+  double unit() { return double(e_() >> 11) * 0x1.0p-53; }
+  double range(double lo, double hi) { return lo + (hi - lo) * unit(); }
+
+ private:
+  std::mt19937_64 e_;
+};
+
+inline std::int32_t synth_q(const SynthOptions& o, std::int32_t p) {
+  if (o.num_observations <= 0) return o.obs_per_point;
+  return std::int32_t(o.num_observations / o.points + (p < o.num_observations % o.points ? 1 : 0));
+}
+
+inline std::int64_t synth_count(const SynthOptions& o) {
+  if (o.cameras < 1 || o.points < 1 || (o.num_observations <= 0 && o.obs_per_point < 1))
+    throw OracleError(kInvalidArgument, "synthetic counts must be positive");
+  if (o.num_observations > 0 && o.num_observations < o.points)
+    throw OracleError(kInvalidArgument, "count-exact mode needs at least one observation per point");
+  const std::int64_t qmax = o.num_observations > 0 ? (o.num_observations + o.points - 1) / o.points : o.obs_per_point;
+  if (qmax > o.cameras)
+    throw OracleError(kInvalidArgument, "obs-per-point " + std::to_string(qmax) + " exceeds camera count " +
+                                            std::to_string(o.cameras));
+  return o.num_observations > 0 ? o.num_observations : std::int64_t(o.points) * o.obs_per_point;
+}
+
+// Eigen::AngleAxisd(const Matrix3d&) goes through Quaternion(Matrix3d)
+// (Eigen/src/Geometry/Quaternion.h, quaternionbase_assign_impl) and then
+// AngleAxis(Quaternion) (AngleAxis.h): restated here.
+inline void matrix_to_angle_axis(const double R[3][3], double out[3]) {
+  double q[4];  // x y z w
+  const double tr = (R[0][0] + R[1][1]) + R[2][2];
+  if (tr > 0) {
+    double t = std::sqrt(tr + 1.0);
+    q[3] = 0.5 * t;
+    t = 0.5 / t;
+    q[0] = (R[2][1] - R[1][2]) * t;
+    q[1] = (R[0][2] - R[2][0]) * t;
+    q[2] = (R[1][0] - R[0][1]) * t;
+  } else {
+    int i = 0;
+    if (R[1][1] > R[0][0]) i = 1;
+    if (R[2][2] > R[i][i]) i = 2;
+    const int j = (i + 1) % 3, k = (j + 1) % 3;
+    double t = std::sqrt(R[i][i] - R[j][j] - R[k][k] + 1.0);
+    q[i] = 0.5 * t;
+    t = 0.5 / t;
+    q[3] = (R[k][j] - R[j][k]) * t;
+    q[j] = (R[j][i] + R[i][j]) * t;
+    q[k] = (R[k][i] + R[i][k]) * t;
+  }
+  double nrm = std::sqrt((q[0] * q[0] + q[1] * q[1]) + q[2] * q[2]);
+  if (nrm == 0.0) {
+    out[0] = out[1] = out[2] = 0.0;
+    return;
+  }
+  const double angle = 2.0 * std::atan2(nrm, std::abs(q[3]));
+  if (q[3] < 0) nrm = -nrm;
+  for (int a = 0; a < 3; ++a) out[a] = angle * (q[a] / nrm);
+}
+
+struct Synthetic {
+  std::vector<double> cams, pts, px, py;
+  std::vector<std::int32_t> cam_id, pt_id;
+};
+
+inline Synthetic generate_synthetic(const SynthOptions& o, int threads) {
+  const std::int64_t N = synth_count(o);
+  const std::int32_t m = o.cameras, n = o.points;
+  UniformDraw rng(o.seed);
+  Synthetic out;
+  out.cams.resize(std::size_t(m) * 9);
+  out.pts.resize(std::size_t(n) * 3);
+  std::vector<double> centers(std::size_t(m) * 3);
+  constexpr double kPi = 3.14159265358979323846;  // EIGEN_PI
+  for (std::int32_t i = 0; i < m; ++i) {
+    const double ang = 2.0 * kPi * double(i) / double(m);
+    const double c[3] = {o.circle_radius * std::cos(ang), o.circle_radius * std::sin(ang), 0.0};
+    for (int a = 0; a < 3; ++a) centers[std::size_t(i) * 3 + a] = c[a];
+    // look_at_origin (dba/synthetic.hpp:52-64): rows right, cz x right, cz
+    auto normalize = [](double v[3]) {
+      const double n2 = (v[0] * v[0] + v[1] * v[1]) + v[2] * v[2];
+      if (n2 > 0) {
+        const double nn = std::sqrt(n2);
+        for (int a = 0; a < 3; ++a) v[a] /= nn;
+      }
+    };
+    double cz[3] = {c[0], c[1], c[2]};
+    normalize(cz);
+    double right[3] = {0.0 * cz[2] - 1.0 * cz[1], 1.0 * cz[0] - 0.0 * cz[2], 0.0 * cz[1] - 0.0 * cz[0]};
+    normalize(right);
+    const double up[3] = {cz[1] * right[2] - cz[2] * right[1], cz[2] * right[0] - cz[0] * right[2],
+                          cz[0] * right[1] - cz[1] * right[0]};
+    const double R[3][3] = {{right[0], right[1], right[2]}, {up[0], up[1], up[2]}, {cz[0], cz[1], cz[2]}};
+    double* cam = &out.cams[std::size_t(i) * 9];
+    matrix_to_angle_axis(R, cam);
+    for (int r = 0; r < 3; ++r) cam[3 + r] = -((R[r][0] * c[0] + R[r][1] * c[1]) + R[r][2] * c[2]);
+    for (int j = 0; j < 3; ++j) cam[j] += rng.range(0.0, o.pose_noise);
+    for (int j = 0; j < 3; ++j) cam[3 + j] += rng.range(0.0, o.pose_noise);
+    cam[6] = o.base_focal + rng.range(0.0, o.intrinsic_noise);
+    cam[7] = rng.range(0.0, o.intrinsic_noise);
+    cam[8] = rng.range(0.0, o.intrinsic_noise);
+  }
+  std::vector<double> truth(std::size_t(n) * 3);
+  for (std::int32_t i = 0; i < n; ++i) {
+    double* t = &truth[std::size_t(i) * 3];
+    t[0] = rng.range(-0.1, 0.1);
+    t[1] = rng.range(-0.1, 0.1);
+    t[2] = rng.range(-0.03, 0.03);
+    double* s = &out.pts[std::size_t(i) * 3];
+    s[0] = t[0] + rng.range(-o.point_noise, o.point_noise);
+    s[1] = t[1] + rng.range(-o.point_noise, o.point_noise);
+    s[2] = t[2];
+  }
+  // edge offsets of each point (point-major)
+  std::vector<std::int64_t> off(std::size_t(n) + 1, 0);
+  for (std::int32_t p = 0; p < n; ++p) off[std::size_t(p) + 1] = off[std::size_t(p)] + synth_q(o, p);
+  out.cam_id.resize(std::size_t(N));
+  out.pt_id.resize(std::size_t(N));
+  out.px.resize(std::size_t(N));
+  out.py.resize(std::size_t(N));
+  std::atomic<std::int64_t> bad{std::numeric_limits<std::int64_t>::max()};
+  auto work = [&](std::int32_t p0, std::int32_t p1) {
+    std::vector<std::int32_t> order(static_cast<std::size_t>(m));
+    std::vector<double> d2(static_cast<std::size_t>(m));
+    for (std::int32_t p = p0; p < p1; ++p) {
+      const double* X = &truth[std::size_t(p) * 3];
+      const std::int32_t q = synth_q(o, p);
+      std::iota(order.begin(), order.end(), 0);
+      for (std::int32_t c = 0; c < m; ++c) {  // (centers[c] - X).squaredNorm()
+        const double dx = centers[std::size_t(c) * 3] - X[0], dy = centers[std::size_t(c) * 3 + 1] - X[1],
+                     dz = centers[std::size_t(c) * 3 + 2] - X[2];
+        d2[std::size_t(c)] = (dx * dx + dy * dy) + dz * dz;
+      }
+      std::nth_element(order.begin(), order.begin() + (q - 1), order.end(), [&](std::int32_t a, std::int32_t b) {
+        return d2[std::size_t(a)] != d2[std::size_t(b)] ? d2[std::size_t(a)] < d2[std::size_t(b)] : a < b;
+      });
+      std::sort(order.begin(), order.begin() + q);
+      for (std::int32_t k = 0; k < q; ++k) {
+        const std::int64_t e = off[std::size_t(p)] + k;
+        const std::int32_t c = order[std::size_t(k)];
+        double r[2] = {0.0, 0.0};
+        if (!residual(&out.cams[std::size_t(c) * 9], X, 0.0, 0.0, r)) {
+          std::int64_t cur = bad.load();
+          while (e < cur && !bad.compare_exchange_weak(cur, e)) {
+          }
+        }
+        out.cam_id[std::size_t(e)] = c;
+        out.pt_id[std::size_t(e)] = p;
+        out.px[std::size_t(e)] = r[0];
+        out.py[std::size_t(e)] = r[1];
+      }
+    }
+  };
+  const int T = std::max(1, std::min<int>(threads, n));
+  std::vector<std::thread> th;
+  for (int t = 0; t < T; ++t) {
+    const std::int32_t a = std::int32_t(std::int64_t(n) * t / T), b = std::int32_t(std::int64_t(n) * (t + 1) / T);
+    th.emplace_back(work, a, b);
+  }
+  for (auto& t : th) t.join();
+  if (bad.load() != std::numeric_limits<std::int64_t>::max()) throw DegenerateDepth(bad.load());
+  if (o.pixel_noise > 0) {
+    std::mt19937_64 noise(o.seed);
+    const double amp = 2.0 * o.pixel_noise;
+    for (std::int64_t i = 0; i < N; ++i) {
+      const double u = double(noise() >> 11) * 0x1.0p-53;
+      const double v = double(noise() >> 11) * 0x1.0p-53;
+      out.px[std::size_t(i)] += (u - 0.5) * amp;
+      out.py[std::size_t(i)] += (v - 0.5) * amp;
+    }
+  }
+  return out;
 }
 
 }  // namespace orc

@@ -494,10 +494,15 @@ int orc_lm_solve(int prec, const orc_problem* p, const orc_config* c, orc_result
 // times, one LM iteration of lm_solve_rank (dba/solver.hpp:330-425) from x0
 // at lambda0 — linearize + assemble + all-reduce B, C, v, w, damp, factor,
 // rhs, dpcg, back-substitution, trial cost, model terms — with
-// K = config->workers threads. seconds[i] is the wall time of step i (max
-// over ranks); pcg_iters the PCG count of the step.
-int orc_lm_probe_steps(int prec, const orc_problem* p, const orc_config* c, int steps, double* seconds,
-                       int* pcg_iters) {
+// K = config->workers threads. phases[step * 7 + i] (max over ranks) holds
+// the seconds of: 0 linearize + assemble + all-reduces, 1 damp + factor,
+// 2 rhs, 3 dpcg setup (norms, r = g - S x0), 4 the dpcg loop,
+// 5 back-substitution + trial state, 6 trial cost + model terms.
+// pcg_sample > 0 caps the DPCG at that many iterations (a bounded sample of
+// the step: the bench scales phase 4 by the full step's loop DSE count over
+// dse_calls[step] - 1); pcg_iters / dse_calls report what ran.
+int orc_lm_probe_phases(int prec, const orc_problem* p, const orc_config* c, int steps, int pcg_sample,
+                        double* phases, int* pcg_iters, int* dse_calls) {
   auto run = [&](auto tag) {
     using S = decltype(tag);
     return guarded([&] {
@@ -505,8 +510,9 @@ int orc_lm_probe_steps(int prec, const orc_problem* p, const orc_config* c, int 
       const auto cfg = to_cfg(c);
       const auto parts = orc::partition_edges(pb, cfg.workers);
       orc::Group g(cfg.workers);
-      std::vector<double> secs(std::size_t(steps) * cfg.workers, 0.0);
-      std::vector<int> its(std::size_t(steps), 0);
+      const int K = cfg.workers;
+      std::vector<double> ph(std::size_t(steps) * K * 7, 0.0);
+      std::vector<int> its(std::size_t(steps), 0), dses(std::size_t(steps), 0);
       orc::run_on_workers(g, [&](int r) {
         const auto& part = parts[std::size_t(r)];
         orc::Evaluator<S> ev(pb, part, cfg.jacobian);
@@ -518,27 +524,43 @@ int orc_lm_probe_steps(int prec, const orc_problem* p, const orc_config* c, int 
         const std::size_t cdim = std::size_t(pb.m) * 9, pdim = std::size_t(pb.n) * 3;
         std::vector<S> gvec(cdim), dxc, dxp(pdim), txc(cdim), txp(pdim), ptmp, ctmp(cdim);
         const double lambda = cfg.lambda0;
+        const int cap = pcg_sample > 0 ? std::min(pcg_sample, cfg.pcg_max_iters) : cfg.pcg_max_iters;
+        using clk = std::chrono::steady_clock;
         for (int s = 0; s < steps; ++s) {
-          const auto t0 = std::chrono::steady_clock::now();
+          double* P = &ph[(std::size_t(s) * K + r) * 7];
+          auto t = clk::now();
+          auto lap = [&](int i) {
+            const auto now = clk::now();
+            P[i] += std::chrono::duration<double>(now - t).count();
+            t = now;
+          };
           const auto& bt = ev.linearize(pb.cams.data(), pb.pts.data(), nullptr);
           orc::assemble(bt, ev, h);
           g.allreduce_sum(r, h.B.a.data(), h.B.a.size());
           g.allreduce_sum(r, h.C.a.data(), h.C.a.size());
           g.allreduce_sum(r, h.v.data(), h.v.size());
           g.allreduce_sum(r, h.w.data(), h.w.size());
-          int pcg = 0;
+          lap(0);
+          int pcg = 0, dse = 0;
           try {
             h.B.damp_into(static_cast<S>(lambda), cfg.damping, Bd);
             h.C.damp_into(static_cast<S>(lambda), cfg.damping, Cd);
             Cf.factor(Cd);
             Bf.factor(Bd);
+            lap(1);
             ptmp = h.w;
             Cf.solve_in_place(ptmp.data());
+            ctmp.assign(cdim, S(0));
             h.E.apply(ptmp.data(), ctmp.data(), nullptr);
             g.allreduce_sum(r, ctmp.data(), ctmp.size());
             for (std::size_t i = 0; i < cdim; ++i) gvec[i] = h.v[i] - ctmp[i];
+            lap(2);
             dxc.assign(cdim, S(0));
-            pcg = orc::dpcg(dxc, Bd, Bf, h.E, Cf, gvec, g, r, cfg.pcg_tol, cfg.pcg_max_iters, nullptr).iterations;
+            double setup = 0;
+            pcg = orc::dpcg(dxc, Bd, Bf, h.E, Cf, gvec, g, r, cfg.pcg_tol, cap, nullptr, &dse, &setup).iterations;
+            lap(4);
+            P[3] += setup;
+            P[4] -= setup;
             ptmp.assign(pdim, S(0));
             h.E.apply_t(dxc.data(), ptmp.data(), nullptr);
             g.allreduce_sum(r, ptmp.data(), ptmp.size());
@@ -546,6 +568,7 @@ int orc_lm_probe_steps(int prec, const orc_problem* p, const orc_config* c, int 
             Cf.solve_in_place(dxp.data());
             for (std::size_t i = 0; i < cdim; ++i) txc[i] = pb.cams[i] + dxc[i];
             for (std::size_t i = 0; i < pdim; ++i) txp[i] = pb.pts[i] + dxp[i];
+            lap(5);
             orc::distributed_cost(ev, txc.data(), txp.data(), g, r, nullptr);
             double step_inf = 0, damp = 0;
             for (std::size_t i = 0; i < cdim; ++i) step_inf = std::max(step_inf, std::abs(double(dxc[i])));
@@ -557,23 +580,72 @@ int orc_lm_probe_steps(int prec, const orc_problem* p, const orc_config* c, int 
             volatile double model = damp + orc::dot_d(dxc.data(), h.v.data(), cdim) +
                                     orc::dot_d(dxp.data(), h.w.data(), pdim) + step_inf;
             (void)model;
+            lap(6);
           } catch (const orc::SingularBlock&) {
           } catch (const orc::PcgBreakdown&) {
           }
-          secs[std::size_t(s) * cfg.workers + r] =
-              std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
-          if (r == 0) its[std::size_t(s)] = pcg;
+          if (r == 0) {
+            its[std::size_t(s)] = pcg;
+            dses[std::size_t(s)] = dse;
+          }
         }
       });
       for (int s = 0; s < steps; ++s) {
-        double mx = 0;
-        for (int r = 0; r < cfg.workers; ++r) mx = std::max(mx, secs[std::size_t(s) * cfg.workers + r]);
-        seconds[s] = mx;
+        for (int i = 0; i < 7; ++i) {
+          double mx = 0;
+          for (int r = 0; r < K; ++r) mx = std::max(mx, ph[(std::size_t(s) * K + r) * 7 + i]);
+          phases[std::size_t(s) * 7 + i] = mx;
+        }
         if (pcg_iters) pcg_iters[s] = its[std::size_t(s)];
+        if (dse_calls) dse_calls[s] = dses[std::size_t(s)];
       }
     });
   };
   return prec == 8 ? run(double{}) : run(float{});
+}
+
+// generate_synthetic (dba/synthetic.hpp:70-146) + the count-exact / pixel
+// noise extension, with the reference's exhaustive nearest-camera scan run
+// on `threads` host threads. Options struct layout = dbag_synthetic_options.
+typedef struct orc_synth {
+  std::int32_t cameras, points, obs_per_point, exhaustive_search;
+  std::uint64_t seed;
+  double circle_radius, base_focal, pose_noise, intrinsic_noise, point_noise;
+  std::int64_t num_observations;
+  double pixel_noise;
+} orc_synth;
+
+static orc::SynthOptions to_synth(const orc_synth* s) {
+  orc::SynthOptions o;
+  o.cameras = s->cameras;
+  o.points = s->points;
+  o.obs_per_point = s->obs_per_point;
+  o.seed = s->seed;
+  o.circle_radius = s->circle_radius;
+  o.base_focal = s->base_focal;
+  o.pose_noise = s->pose_noise;
+  o.intrinsic_noise = s->intrinsic_noise;
+  o.point_noise = s->point_noise;
+  o.num_observations = s->num_observations;
+  o.pixel_noise = s->pixel_noise;
+  return o;
+}
+
+int orc_synthetic_count(const orc_synth* s, std::int64_t* n_obs) {
+  return guarded([&] { *n_obs = orc::synth_count(to_synth(s)); });
+}
+
+int orc_generate_synthetic(const orc_synth* s, int threads, double* cams, double* pts, std::int32_t* cam_id,
+                           std::int32_t* pt_id, double* px, double* py) {
+  return guarded([&] {
+    const orc::Synthetic g = orc::generate_synthetic(to_synth(s), threads);
+    std::copy(g.cams.begin(), g.cams.end(), cams);
+    std::copy(g.pts.begin(), g.pts.end(), pts);
+    std::copy(g.cam_id.begin(), g.cam_id.end(), cam_id);
+    std::copy(g.pt_id.begin(), g.pt_id.end(), pt_id);
+    std::copy(g.px.begin(), g.px.end(), px);
+    std::copy(g.py.begin(), g.py.end(), py);
+  });
 }
 
 }  // extern "C"

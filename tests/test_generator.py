@@ -73,3 +73,20 @@ def test_pixel_noise_stream():
     dx, dy = b[4] - a[4], b[5] - a[5]
     assert np.all(np.abs(dx) <= 0.5) and np.all(np.abs(dy) <= 0.5)
     assert dx.std() > 0.2 and dy.std() > 0.2
+
+
+@pytest.mark.parametrize("shape", [(49, 7776, 31843), (257, 65132, 225911), (1778, 993923, 5001946)],
+                         ids=["ladybug-49", "trafalgar-257", "venice-1778"])
+def test_product_generator_equals_oracle_restatement(shape):
+    """The product's windowed count-exact generator (csrc/synthetic.cpp) is
+    bit-identical, on every output array, to the oracle's independent
+    restatement of dba/synthetic.hpp:70-146 with the reference's exhaustive
+    O(n m) nearest-camera scan, at the BASELINE.json shapes (BASELINE.md §3
+    instance: seed 1, +-0.5 px noise). The reference arm of bench.py builds
+    its instance with the oracle's generator, so both arms see the same input."""
+    m, n, N = shape
+    kw = dict(cameras=m, points=n, num_observations=N, seed=1, pixel_noise=0.5)
+    a = dba.generate_synthetic(dba.SyntheticOptions(**kw)).arrays()
+    b = O.generate_synthetic(O.SynthOptions(**kw)).arrays()
+    for x, y in zip(a, b):
+        assert x.dtype == y.dtype and np.array_equal(x, y)
