@@ -185,14 +185,18 @@ def cpu_threads():
     return max(1, host_info()["physical_cores"])
 
 
+PCG_HEAD = 5  # DPCG iterations the oracle counts into its "dpcg head" phase
+
+
 def scaled_lm_seconds(phases, dse_sample, dse_full):
     """One LM iteration's seconds from a bounded sample: every phase as
-    measured (oracle.PHASES), the DPCG loop (phase 4) scaled from the
-    sample's loop DSE count to the full iteration's (every loop DSE is the
-    same work: one E^T x / C^-1 / E b round with its two all-reduces,
-    dba/solver.hpp:149-181; the first DSE, on x0, is in the setup phase)."""
+    measured (oracle.PHASES), the steady DPCG loop (phase 4: after the DSE on
+    x0 and the first PCG_HEAD iterations) scaled from the sample's DSE count
+    to the full iteration's — every loop DSE is the same work: one
+    E^T x / C^-1 / E b round with its two all-reduces, dba/solver.hpp:149-181."""
     ph = np.asarray(phases, dtype=float)
-    return float(ph.sum() - ph[4] + ph[4] * (dse_full - 1) / max(int(dse_sample) - 1, 1))
+    head = 1 + PCG_HEAD
+    return float(ph.sum() - ph[4] + ph[4] * (dse_full - head) / max(int(dse_sample) - head, 1))
 
 
 def cpu_reference_steps(p, k, n_steps, dse_full=None, calibrate=True):

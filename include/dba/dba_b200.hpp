@@ -16,6 +16,7 @@
 #pragma once
 
 #include <array>
+#include <chrono>
 #include <cmath>
 #include <cstdint>
 #include <istream>
@@ -208,6 +209,7 @@ struct SolverConfig {
   MseConvention mse = MseConvention::half_per_observation;
   JacobianMode jacobian = JacobianMode::autodiff;
   bool check_rank_identity = false;
+  std::chrono::milliseconds collective_timeout{60000};  // dba/solver.hpp:54
   std::vector<int> devices{0};  // B200 placement: rank r -> devices[r % size]
   bool coupling_fp32 = false;     // B200 extension (row f4): E blocks stored in FP32 under an FP64 solve
 
@@ -226,6 +228,7 @@ struct SolverConfig {
     c.mse_half = mse == MseConvention::half_per_observation ? 1 : 0;
     c.jacobian = jacobian == JacobianMode::analytic ? 1 : 0;
     c.check_rank_identity = check_rank_identity ? 1 : 0;
+    c.collective_timeout_ms = static_cast<int64_t>(collective_timeout.count());
     c.coupling_fp32 = coupling_fp32 ? 1 : 0;
     return c;
   }

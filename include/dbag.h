@@ -66,6 +66,7 @@ typedef struct dbag_config {
   int32_t mse_half;            /* 1 half_per_observation (default), 0 per_observation */
   int32_t jacobian;            /* 0 autodiff (default), 1 analytic */
   int32_t check_rank_identity; /* rank-divergence probe, dba/solver.hpp:479-501 */
+  int64_t collective_timeout_ms; /* SolverConfig::collective_timeout (dba/solver.hpp:54), default 60000; <= 0 = default */
 } dbag_config;
 
 /* SolverState + IterationRecord history (dba/solver.hpp:57-85). The caller
@@ -185,6 +186,9 @@ int dbag_create_ex(int device, int precision, int coupling_fp32, dbag_ctx** out)
 /* Context for rank `rank` of an NCCL communicator (multi-process). */
 int dbag_create_nccl(int device, int rank, int nranks, const unsigned char* nccl_id128, int precision,
                      dbag_ctx** out);
+/* Same, with the memory-lean variant (coupling_fp32 needs precision 8). */
+int dbag_create_nccl_ex(int device, int rank, int nranks, const unsigned char* nccl_id128, int precision,
+                        int coupling_fp32, dbag_ctx** out);
 int dbag_destroy(dbag_ctx* ctx);
 
 /* EdgeEvaluator ctor + PartitionedHessian ctor (dba/edge_eval.hpp:79-97,
@@ -210,7 +214,10 @@ int dbag_rhs(dbag_ctx* ctx);
 int dbag_pcg(dbag_ctx* ctx, double tol, int max_iters, int* iterations, int* converged);
 /* dx_p = C^-1 (w - allreduce(E_k^T dx_c)); trial = x + dx (dba/solver.hpp:371-379). */
 int dbag_backsub_trial(dbag_ctx* ctx);
-/* step_inf, damping term, dx_c.v + dx_p.w (dba/solver.hpp:383-410). */
+/* step_inf, damping term, dx_c.v + dx_p.w (dba/solver.hpp:383-410) of the
+ * last backsub_trial. lambda / policy must be the preceding damp_factor's
+ * (the reference's trial damps and scores with one pair); otherwise
+ * DBAG_INVALID_ARGUMENT. */
 int dbag_model_terms(dbag_ctx* ctx, double lambda, int policy, double* step_inf, double* damping_term, double* gv);
 /* x <- trial (dba/solver.hpp:433-437). */
 int dbag_accept(dbag_ctx* ctx);
@@ -268,6 +275,22 @@ int dbag_group_operator(int precision, const dbag_problem* p, int k, int device,
 /* WorkerGroup::allreduce_sum over K in-process ranks on `device`:
  * data is K x len fp64 (rank-major), reduced in place. */
 int dbag_group_allreduce(int k, int device, int64_t len, double* data);
+
+/* ---- WorkerGroup handle: dba::WorkerGroup (dba/comms.hpp:35-234) ---------
+ * K in-process ranks on devices[rank % n_devices]; each rank's calls come
+ * from that rank's own host thread (run_on_workers). Collectives validate
+ * call sequence, kind, element type and length, and a missing rank trips
+ * the timeout with a message naming the absent ranks (DBAG_COLLECTIVE);
+ * abort() makes every pending and later collective fail. Up to 256 ranks.
+ * allreduce_sum reduces a HOST buffer in place (staged through the rank's
+ * device, summed in ascending rank order: bit-identical on every rank). */
+typedef struct dbag_group dbag_group;
+int dbag_group_create(int k, const int* devices, int n_devices, int64_t timeout_ms, dbag_group** out);
+int dbag_group_destroy(dbag_group* g);
+int dbag_group_barrier(dbag_group* g, int rank);                                   /* comms.hpp:56-63 */
+int dbag_group_allreduce_sum(dbag_group* g, int rank, void* data, int64_t len, int precision); /* :67-91 */
+int dbag_group_abort(dbag_group* g, const char* why);                              /* :96-105 */
+int dbag_group_sequence(dbag_group* g, int rank, uint64_t* out);                   /* :52-53 */
 
 #ifdef __cplusplus
 }

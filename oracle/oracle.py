@@ -84,8 +84,8 @@ def lib():
             "orc_assemble": (C.c_int, [C.c_int, P(Problem), C.c_int, C.c_int, C.c_int, vp, vp, vp, vp, vp]),
             "orc_damp": (C.c_int, [C.c_int, C.c_int64, vp, C.c_double, C.c_int, vp]),
             "orc_factor_solve": (C.c_int, [C.c_int, C.c_int64, vp, vp]),
-            "orc_dse": (C.c_int, [P(Problem), C.c_int, C.c_double, C.c_int, vp, vp, P(C.c_int)]),
-            "orc_dpcg": (C.c_int, [P(Problem), C.c_int, C.c_double, C.c_int, vp, C.c_double, C.c_int, vp,
+            "orc_dse": (C.c_int, [C.c_int, P(Problem), C.c_int, C.c_double, C.c_int, vp, vp, P(C.c_int)]),
+            "orc_dpcg": (C.c_int, [C.c_int, P(Problem), C.c_int, C.c_double, C.c_int, vp, C.c_double, C.c_int, vp,
                                    P(C.c_int), P(C.c_int), P(C.c_int)]),
             "orc_blocks_solve": (C.c_int, [P(Problem), C.c_int, vp, vp, vp, C.c_int, vp, C.c_double, C.c_int, vp,
                                            P(C.c_int), P(C.c_int)]),
@@ -312,20 +312,23 @@ def factor_solve(blocks, x):
 
 
 def dse(problem, k, lam, policy, x):
+    """dse on the problem's own damped system at the problem's precision."""
     s = _ps(problem)
-    out = np.zeros(9 * problem.num_cameras)
+    d = np.dtype(problem.dtype)
+    out = np.zeros(9 * problem.num_cameras, d)
     ident = C.c_int()
-    xx = _d(x)
-    check(lib().orc_dse(C.byref(s), k, lam, policy, xx.ctypes.data, out.ctypes.data, C.byref(ident)))
+    xx = _d(x, d)
+    check(lib().orc_dse(_prec(problem), C.byref(s), k, lam, policy, xx.ctypes.data, out.ctypes.data, C.byref(ident)))
     return out, bool(ident.value)
 
 
 def dpcg(problem, k, lam, policy, rhs, tol, max_iters):
     s = _ps(problem)
-    x = np.zeros(9 * problem.num_cameras)
+    d = np.dtype(problem.dtype)
+    x = np.zeros(9 * problem.num_cameras, d)
     it, conv, ident = C.c_int(), C.c_int(), C.c_int()
-    rr = _d(rhs)
-    check(lib().orc_dpcg(C.byref(s), k, lam, policy, rr.ctypes.data, tol, max_iters, x.ctypes.data,
+    rr = _d(rhs, d)
+    check(lib().orc_dpcg(_prec(problem), C.byref(s), k, lam, policy, rr.ctypes.data, tol, max_iters, x.ctypes.data,
                          C.byref(it), C.byref(conv), C.byref(ident)))
     return x, it.value, bool(conv.value), bool(ident.value)
 

@@ -385,46 +385,57 @@ int orc_factor_solve(int bs, std::int64_t nb, const double* blocks, double* x) {
 // DSE (dba/solver.hpp:149-181) on the partitioned, damped system of the
 // problem's own linearization (tests/test_solver.cpp:46-68). out = rank 0's
 // result; *rank_identical = all ranks bitwise equal.
-int orc_dse(const orc_problem* p, int k, double lambda, int policy, const double* x, double* out, int* rank_identical) {
-  return guarded([&] {
-    const auto pb = load<double>(p);
-    std::vector<std::vector<double>> outs(static_cast<std::size_t>(k));
-    with_system<double>(pb, k, lambda, policy, [&](int r, orc::Group& g, orc::Hessian<double>& h,
-                                                  orc::BlockDiag<double, 9>& Bd, orc::Factored<double, 9>&,
-                                                  orc::Factored<double, 3>& Cf) {
-      outs[std::size_t(r)].resize(std::size_t(pb.m) * 9);
-      orc::DseWs<double> ws;
-      orc::dse(x, Bd, h.E, Cf, g, r, outs[std::size_t(r)].data(), ws, nullptr);
+int orc_dse(int prec, const orc_problem* p, int k, double lambda, int policy, const void* xv, void* outv,
+            int* rank_identical) {
+  auto run = [&](auto tag) {
+    using S = decltype(tag);
+    return guarded([&] {
+      const auto pb = load<S>(p);
+      const S* x = static_cast<const S*>(xv);
+      std::vector<std::vector<S>> outs(static_cast<std::size_t>(k));
+      with_system<S>(pb, k, lambda, policy, [&](int r, orc::Group& g, orc::Hessian<S>& h, orc::BlockDiag<S, 9>& Bd,
+                                                orc::Factored<S, 9>&, orc::Factored<S, 3>& Cf) {
+        outs[std::size_t(r)].resize(std::size_t(pb.m) * 9);
+        orc::DseWs<S> ws;
+        orc::dse(x, Bd, h.E, Cf, g, r, outs[std::size_t(r)].data(), ws, nullptr);
+      });
+      *rank_identical = 1;
+      for (int r = 1; r < k; ++r)
+        if (std::memcmp(outs[std::size_t(r)].data(), outs[0].data(), outs[0].size() * sizeof(S)) != 0)
+          *rank_identical = 0;
+      std::copy(outs[0].begin(), outs[0].end(), static_cast<S*>(outv));
     });
-    *rank_identical = 1;
-    for (int r = 1; r < k; ++r)
-      if (std::memcmp(outs[std::size_t(r)].data(), outs[0].data(), outs[0].size() * 8) != 0) *rank_identical = 0;
-    std::copy(outs[0].begin(), outs[0].end(), out);
-  });
+  };
+  return prec == 8 ? run(double{}) : run(float{});
 }
 
 // DPCG (dba/solver.hpp:202-257) on the same system.
-int orc_dpcg(const orc_problem* p, int k, double lambda, int policy, const double* rhs, double tol, int max_iters,
-             double* x_out, int* iterations, int* converged, int* rank_identical) {
-  return guarded([&] {
-    const auto pb = load<double>(p);
-    std::vector<std::vector<double>> xs(static_cast<std::size_t>(k));
-    std::vector<orc::PcgResult> res(static_cast<std::size_t>(k));
-    const std::vector<double> g(rhs, rhs + std::size_t(pb.m) * 9);
-    with_system<double>(pb, k, lambda, policy, [&](int r, orc::Group& grp, orc::Hessian<double>& h,
-                                                  orc::BlockDiag<double, 9>& Bd, orc::Factored<double, 9>& Bf,
-                                                  orc::Factored<double, 3>& Cf) {
-      auto& x = xs[std::size_t(r)];
-      x.assign(std::size_t(pb.m) * 9, 0.0);
-      res[std::size_t(r)] = orc::dpcg(x, Bd, Bf, h.E, Cf, g, grp, r, tol, max_iters, nullptr);
+int orc_dpcg(int prec, const orc_problem* p, int k, double lambda, int policy, const void* rhsv, double tol,
+             int max_iters, void* x_out, int* iterations, int* converged, int* rank_identical) {
+  auto run = [&](auto tag) {
+    using S = decltype(tag);
+    return guarded([&] {
+      const auto pb = load<S>(p);
+      std::vector<std::vector<S>> xs(static_cast<std::size_t>(k));
+      std::vector<orc::PcgResult> res(static_cast<std::size_t>(k));
+      const S* rhs = static_cast<const S*>(rhsv);
+      const std::vector<S> g(rhs, rhs + std::size_t(pb.m) * 9);
+      with_system<S>(pb, k, lambda, policy, [&](int r, orc::Group& grp, orc::Hessian<S>& h,
+                                                orc::BlockDiag<S, 9>& Bd, orc::Factored<S, 9>& Bf,
+                                                orc::Factored<S, 3>& Cf) {
+        auto& x = xs[std::size_t(r)];
+        x.assign(std::size_t(pb.m) * 9, S(0));
+        res[std::size_t(r)] = orc::dpcg(x, Bd, Bf, h.E, Cf, g, grp, r, tol, max_iters, nullptr);
+      });
+      *rank_identical = 1;
+      for (int r = 1; r < k; ++r)
+        if (std::memcmp(xs[std::size_t(r)].data(), xs[0].data(), xs[0].size() * sizeof(S)) != 0) *rank_identical = 0;
+      std::copy(xs[0].begin(), xs[0].end(), static_cast<S*>(x_out));
+      *iterations = res[0].iterations;
+      *converged = res[0].converged ? 1 : 0;
     });
-    *rank_identical = 1;
-    for (int r = 1; r < k; ++r)
-      if (std::memcmp(xs[std::size_t(r)].data(), xs[0].data(), xs[0].size() * 8) != 0) *rank_identical = 0;
-    std::copy(xs[0].begin(), xs[0].end(), x_out);
-    *iterations = res[0].iterations;
-    *converged = res[0].converged ? 1 : 0;
-  });
+  };
+  return prec == 8 ? run(double{}) : run(float{});
 }
 
 // DSE / DPCG on caller-fabricated blocks (tests/test_solver.cpp:75-105,
@@ -496,11 +507,12 @@ int orc_lm_solve(int prec, const orc_problem* p, const orc_config* c, orc_result
 // rhs, dpcg, back-substitution, trial cost, model terms — with
 // K = config->workers threads. phases[step * 7 + i] (max over ranks) holds
 // the seconds of: 0 linearize + assemble + all-reduces, 1 damp + factor,
-// 2 rhs, 3 dpcg setup (norms, r = g - S x0), 4 the dpcg loop,
-// 5 back-substitution + trial state, 6 trial cost + model terms.
-// pcg_sample > 0 caps the DPCG at that many iterations (a bounded sample of
-// the step: the bench scales phase 4 by the full step's loop DSE count over
-// dse_calls[step] - 1); pcg_iters / dse_calls report what ran.
+// 2 rhs, 3 dpcg head (norms, r = g - S x0 and the first kHead = 5 loop
+// iterations), 4 the rest of the dpcg loop, 5 back-substitution + trial
+// state, 6 trial cost + model terms. pcg_sample > 0 caps the DPCG at that
+// many iterations (a bounded sample of the step: the bench scales phase 4 by
+// the full step's remaining DSE count over dse_calls[step] - 1 - kHead);
+// pcg_iters / dse_calls report what ran.
 int orc_lm_probe_phases(int prec, const orc_problem* p, const orc_config* c, int steps, int pcg_sample,
                         double* phases, int* pcg_iters, int* dse_calls) {
   auto run = [&](auto tag) {
@@ -557,7 +569,9 @@ int orc_lm_probe_phases(int prec, const orc_problem* p, const orc_config* c, int
             lap(2);
             dxc.assign(cdim, S(0));
             double setup = 0;
-            pcg = orc::dpcg(dxc, Bd, Bf, h.E, Cf, gvec, g, r, cfg.pcg_tol, cap, nullptr, &dse, &setup).iterations;
+            constexpr int kHead = 5;
+            pcg = orc::dpcg(dxc, Bd, Bf, h.E, Cf, gvec, g, r, cfg.pcg_tol, cap, nullptr, &dse, &setup, kHead)
+                      .iterations;
             lap(4);
             P[3] += setup;
             P[4] -= setup;

@@ -25,7 +25,8 @@ class Problem(C.Structure):
 class Config(C.Structure):
     _fields_ = [("workers", i32), ("max_iterations", i32), ("pcg_tol", f64), ("pcg_max_iters", i32),
                 ("coupling_fp32", i32), ("lambda0", f64), ("lambda_max", f64), ("rel_tol", f64), ("step_tol", f64),
-                ("damping", i32), ("mse_half", i32), ("jacobian", i32), ("check_rank_identity", i32)]
+                ("damping", i32), ("mse_half", i32), ("jacobian", i32), ("check_rank_identity", i32),
+                ("collective_timeout_ms", i64)]
 
 
 class Result(C.Structure):
@@ -65,6 +66,13 @@ _SIGS = {
     "dbag_create": (C.c_int, [C.c_int, C.c_int, _P(vp)]),
     "dbag_create_ex": (C.c_int, [C.c_int, C.c_int, C.c_int, _P(vp)]),
     "dbag_create_nccl": (C.c_int, [C.c_int, C.c_int, C.c_int, vp, C.c_int, _P(vp)]),
+    "dbag_create_nccl_ex": (C.c_int, [C.c_int, C.c_int, C.c_int, vp, C.c_int, C.c_int, _P(vp)]),
+    "dbag_group_create": (C.c_int, [C.c_int, _P(C.c_int), C.c_int, i64, _P(vp)]),
+    "dbag_group_destroy": (C.c_int, [vp]),
+    "dbag_group_barrier": (C.c_int, [vp, C.c_int]),
+    "dbag_group_allreduce_sum": (C.c_int, [vp, C.c_int, vp, i64, C.c_int]),
+    "dbag_group_abort": (C.c_int, [vp, C.c_char_p]),
+    "dbag_group_sequence": (C.c_int, [vp, C.c_int, _P(u64)]),
     "dbag_destroy": (C.c_int, [vp]),
     "dbag_upload_problem": (C.c_int, [vp, _P(Problem), C.c_int]),
     "dbag_set_state": (C.c_int, [vp, vp, vp]),

@@ -8,6 +8,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cstdlib>
 #include <cstring>
 #include <exception>
@@ -83,6 +84,10 @@ void with_rank(dbag_ctx* c, Fn&& fn) {
   else fn(*c->r32);
 }
 
+std::chrono::milliseconds timeout_of(const dbag_config& c) {
+  return std::chrono::milliseconds(c.collective_timeout_ms > 0 ? c.collective_timeout_ms : 60000);
+}
+
 void fill_result(const Outcome& o, int K, dbag_result* out) {
   out->iterations = o.iteration;
   out->termination = o.termination;
@@ -106,16 +111,6 @@ void fill_result(const Outcome& o, int K, dbag_result* out) {
       if (out->rec_worker_block_ops) out->rec_worker_block_ops[at] = r.worker_block_ops[static_cast<std::size_t>(k)];
     }
   }
-}
-
-// Writes this rank's owned points (and, on rank 0, the cameras) of the
-// current state into full-size host vectors.
-template <class R, class S = typename R::Scalar>
-void export_state(R& rk, S* xc, S* xp) {
-  const ShardPlan& pl = rk.plan();
-  std::vector<S> cams(static_cast<std::size_t>(pl.m) * 9);
-  rk.get_state(cams.data(), xp, /*owned_only=*/true);
-  if (xc && pl.rank == 0) std::copy(cams.begin(), cams.end(), xc);
 }
 
 // Runs body(rank) on one host thread per rank (run_on_workers,
@@ -150,14 +145,14 @@ void lm_group(const dbag_problem* p, const dbag_config* c, const int* devices, i
   std::vector<int> devs(devices, devices + std::max(n_devices, 0));
   if (devs.empty()) devs.push_back(0);
   split_edges(p->num_observations, K);  // validates K like partition_edges
-  Group g(K, devs);
-  if (out->x_p) std::memcpy(out->x_p, p->points, sizeof(S) * 3 * static_cast<std::size_t>(p->num_points));
+  Group g(K, devs, timeout_of(*c));
   run_ranks(g, [&](int r) {
     GroupComm comm(&g, r);
     Rank<S, T> rk(g.device_of(r), &comm);
     rk.upload(*p, c->jacobian);
     const Outcome o = lm_solve_rank(rk, *c, p->num_observations);
-    export_state(rk, static_cast<S*>(out->x_c), static_cast<S*>(out->x_p));
+    // rank 0's state (dba/solver.hpp:533), x_p assembled over the group
+    rk.gather_state(r == 0 ? static_cast<S*>(out->x_c) : nullptr, r == 0 ? static_cast<S*>(out->x_p) : nullptr);
     if (r == 0) fill_result(o, K, out);
   });
 }
@@ -171,8 +166,10 @@ void lm_nccl(const dbag_problem* p, const dbag_config* c, int rank, int nranks, 
   Rank<S, T> rk(device, &comm);
   rk.upload(*p, c->jacobian);
   const Outcome o = lm_solve_rank(rk, *c, p->num_observations);
-  if (out->x_p) std::memcpy(out->x_p, p->points, sizeof(S) * 3 * static_cast<std::size_t>(p->num_points));
-  export_state(rk, static_cast<S*>(out->x_c), static_cast<S*>(out->x_p));
+  // Every rank returns the full, rank-identical state (dba/solver.hpp:533):
+  // cameras are replicated; x_p is assembled over the communicator from
+  // each point's owner (Rank::gather_state).
+  rk.gather_state(static_cast<S*>(out->x_c), static_cast<S*>(out->x_p));
   fill_result(o, nranks, out);
 }
 
@@ -236,6 +233,7 @@ void dbag_default_config(dbag_config* c) {  // dba/solver.hpp:39-55
   c->mse_half = 1;
   c->jacobian = 0;
   c->check_rank_identity = 0;
+  c->collective_timeout_ms = 60000;
 }
 
 int dbag_device_count(int* out) {
@@ -420,17 +418,25 @@ int dbag_create_ex(int device, int precision, int coupling_fp32, dbag_ctx** out)
 
 int dbag_create(int device, int precision, dbag_ctx** out) { return dbag_create_ex(device, precision, 0, out); }
 
-int dbag_create_nccl(int device, int rank, int nranks, const unsigned char* id, int precision, dbag_ctx** out) {
+int dbag_create_nccl_ex(int device, int rank, int nranks, const unsigned char* id, int precision, int coupling_fp32,
+                        dbag_ctx** out) {
   return guarded([&] {
     check_precision(precision);
+    if (coupling_fp32 && precision != 8)
+      throw Error(DBAG_INVALID_ARGUMENT, "coupling_fp32 needs precision 8 (FP64 arithmetic, FP32 E blocks)");
     DBAG_CUDA(cudaSetDevice(device));
     auto ctx = std::make_unique<dbag_ctx>();
     ctx->precision = precision;
     ctx->comm = std::make_unique<NcclComm>(rank, nranks, id);
-    if (precision == 8) ctx->r64 = std::make_unique<Rank<double>>(device, ctx->comm.get());
+    if (precision == 8 && coupling_fp32) ctx->r64l = std::make_unique<Rank<double, float>>(device, ctx->comm.get());
+    else if (precision == 8) ctx->r64 = std::make_unique<Rank<double>>(device, ctx->comm.get());
     else ctx->r32 = std::make_unique<Rank<float>>(device, ctx->comm.get());
     *out = ctx.release();
   });
+}
+
+int dbag_create_nccl(int device, int rank, int nranks, const unsigned char* id, int precision, dbag_ctx** out) {
+  return dbag_create_nccl_ex(device, rank, nranks, id, precision, 0, out);
 }
 
 int dbag_destroy(dbag_ctx* ctx) {
@@ -511,9 +517,17 @@ int dbag_backsub_trial(dbag_ctx* ctx) {
 }
 
 int dbag_model_terms(dbag_ctx* ctx, double lambda, int policy, double* step_inf, double* damping_term, double* gv) {
-  (void)lambda;
-  (void)policy;  // fixed by the preceding damp_factor, as in the reference trial
-  return guarded([&] { with_rank(ctx, [&](auto& rk) { rk.model_terms(step_inf, damping_term, gv); }); });
+  // The reference's trial evaluates the damping term with the lambda and
+  // policy it damped with (dba/solver.hpp:350-353, 389-408): the device sums
+  // were formed with the preceding damp_factor's pair, so another pair is an
+  // error rather than a silently different model.
+  return guarded([&] {
+    with_rank(ctx, [&](auto& rk) {
+      if (lambda != rk.damping_lambda() || policy != rk.damping_policy())
+        throw Error(DBAG_INVALID_ARGUMENT, "model_terms: lambda/policy differ from the preceding damp_factor's");
+      rk.model_terms(step_inf, damping_term, gv);
+    });
+  });
 }
 
 int dbag_accept(dbag_ctx* ctx) {
@@ -678,6 +692,81 @@ int dbag_group_allreduce(int k, int device, int64_t len, double* data) {
       cudaStreamDestroy(s);
       cudaFree(d);
     });
+  });
+}
+
+// ---- WorkerGroup handle (dba/comms.hpp:35-234) -----------------------------
+struct dbag_group {
+  std::unique_ptr<Group> g;
+  std::vector<cudaStream_t> streams;
+};
+
+int dbag_group_create(int k, const int* devices, int n_devices, int64_t timeout_ms, dbag_group** out) {
+  return guarded([&] {
+    std::vector<int> devs(devices, devices + std::max(n_devices, 0));
+    if (devs.empty()) devs.push_back(0);
+    auto h = std::make_unique<dbag_group>();
+    h->g = std::make_unique<Group>(k, devs, std::chrono::milliseconds(timeout_ms > 0 ? timeout_ms : 60000));
+    h->streams.resize(static_cast<std::size_t>(k));
+    for (int r = 0; r < k; ++r) {
+      DBAG_CUDA(cudaSetDevice(h->g->device_of(r)));
+      DBAG_CUDA(cudaStreamCreateWithFlags(&h->streams[static_cast<std::size_t>(r)], cudaStreamNonBlocking));
+    }
+    *out = h.release();
+  });
+}
+
+int dbag_group_destroy(dbag_group* h) {
+  return guarded([&] {
+    if (!h) return;
+    for (std::size_t r = 0; r < h->streams.size(); ++r) {
+      cudaSetDevice(h->g->device_of(static_cast<int>(r)));
+      cudaStreamDestroy(h->streams[r]);
+    }
+    delete h;
+  });
+}
+
+static void check_group_rank(dbag_group* h, int rank) {
+  if (!h || rank < 0 || rank >= h->g->size()) throw Error(DBAG_INVALID_ARGUMENT, "bad group handle or rank");
+}
+
+int dbag_group_barrier(dbag_group* h, int rank) {
+  return guarded([&] {
+    check_group_rank(h, rank);
+    h->g->barrier(rank);
+  });
+}
+
+int dbag_group_allreduce_sum(dbag_group* h, int rank, void* data, int64_t len, int precision) {
+  return guarded([&] {
+    check_group_rank(h, rank);
+    check_precision(precision);
+    if (len < 0 || (len > 0 && !data)) throw Error(DBAG_INVALID_ARGUMENT, "bad all-reduce buffer");
+    DBAG_CUDA(cudaSetDevice(h->g->device_of(rank)));
+    cudaStream_t s = h->streams[static_cast<std::size_t>(rank)];
+    const std::size_t bytes = static_cast<std::size_t>(len) * static_cast<std::size_t>(precision);
+    void* d = nullptr;
+    DBAG_CUDA(cudaMalloc(&d, std::max<std::size_t>(bytes, 8)));
+    std::unique_ptr<void, void (*)(void*)> keep(d, [](void* q) { cudaFree(q); });
+    DBAG_CUDA(cudaMemcpyAsync(d, data, bytes, cudaMemcpyHostToDevice, s));
+    h->g->allreduce(rank, d, len, precision == 8 ? DType::f64 : DType::f32, false, s);
+    DBAG_CUDA(cudaMemcpyAsync(data, d, bytes, cudaMemcpyDeviceToHost, s));
+    DBAG_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+int dbag_group_abort(dbag_group* h, const char* why) {
+  return guarded([&] {
+    if (!h) throw Error(DBAG_INVALID_ARGUMENT, "null group handle");
+    h->g->abort(why ? why : "aborted by caller");
+  });
+}
+
+int dbag_group_sequence(dbag_group* h, int rank, uint64_t* out) {
+  return guarded([&] {
+    check_group_rank(h, rank);
+    *out = h->g->sequence(rank);
   });
 }
 

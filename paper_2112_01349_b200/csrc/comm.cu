@@ -6,8 +6,8 @@
 namespace dbag {
 namespace {
 
-constexpr int kMaxGroup = 16;
-struct SlotPtrs {
+constexpr int kMaxGroup = Group::kMaxRanks;
+struct SlotPtrs {  // 2 KB: inside the 4 KB kernel-parameter limit
   const void* p[kMaxGroup];
 };
 
@@ -40,7 +40,8 @@ ncclDataType_t nccl_type(DType t) { return t == DType::f64 ? ncclDouble : ncclFl
 Group::Group(int k, std::vector<int> devices, std::chrono::milliseconds timeout)
     : k_(k), devices_(std::move(devices)), timeout_(timeout) {
   if (k < 1) throw Error(DBAG_INVALID_ARGUMENT, "worker group needs at least one rank");
-  if (k > kMaxGroup) throw Error(DBAG_INVALID_ARGUMENT, "in-process group supports at most 16 ranks");
+  if (k > kMaxGroup)
+    throw Error(DBAG_INVALID_ARGUMENT, "in-process group supports at most " + std::to_string(kMaxGroup) + " ranks");
   if (devices_.empty()) devices_.push_back(0);
   std::vector<int> dev(static_cast<std::size_t>(k));
   for (int r = 0; r < k; ++r) dev[static_cast<std::size_t>(r)] = devices_[static_cast<std::size_t>(r) % devices_.size()];
@@ -138,7 +139,9 @@ void Group::validate(int rank, std::int64_t count, int kind) {
     const Slot& s = slots_[static_cast<std::size_t>(r)];
     std::string problem;
     if (s.seq != seq) problem = "is at call sequence " + std::to_string(s.seq) + ", this rank at " + std::to_string(seq);
-    else if (s.kind != kind) problem = "entered a different collective kind or element type";
+    else if ((s.kind == kBarrier) != (kind == kBarrier) || ((s.kind ^ kind) & 1))
+      problem = "entered a different collective kind";
+    else if (s.kind != kind) problem = "passed a different element type";
     else if (s.count != count)
       problem = "passed length " + std::to_string(s.count) + ", this rank passed " + std::to_string(count);
     if (!problem.empty()) {
@@ -148,6 +151,22 @@ void Group::validate(int rank, std::int64_t count, int kind) {
       throw Error(DBAG_COLLECTIVE, why_);
     }
   }
+}
+
+void Group::barrier(int rank) {
+  {
+    std::lock_guard<std::mutex> lk(mu_);
+    if (aborted_) throw Error(DBAG_COLLECTIVE, "collective aborted: " + why_);
+    slots_[static_cast<std::size_t>(rank)] = Slot{nullptr, 0, kBarrier, ++seq_[static_cast<std::size_t>(rank)]};
+  }
+  rendezvous(rank);
+  validate(rank, 0, kBarrier);
+  rendezvous(rank);  // slots stay valid until every rank validated
+}
+
+std::uint64_t Group::sequence(int rank) const {
+  std::lock_guard<std::mutex> lk(mu_);
+  return seq_[static_cast<std::size_t>(rank)];
 }
 
 void* Group::scratch(int rank, std::size_t bytes) {

@@ -56,12 +56,19 @@ class SelfComm final : public Comm {
 // Shared state of an in-process group of K ranks.
 class Group {
  public:
-  Group(int k, std::vector<int> devices, std::chrono::milliseconds timeout = std::chrono::milliseconds(600000));
+  // Up to kMaxRanks ranks (the slot pointers travel as one kernel argument);
+  // timeout = SolverConfig::collective_timeout (dba/solver.hpp:54, 60 s).
+  static constexpr int kMaxRanks = 256;
+  Group(int k, std::vector<int> devices, std::chrono::milliseconds timeout = std::chrono::milliseconds(60000));
   ~Group();
   int size() const { return k_; }
   int device_of(int rank) const { return devices_[static_cast<std::size_t>(rank)]; }
 
   void allreduce(int rank, void* data, std::int64_t count, DType t, bool is_max, cudaStream_t s);
+  // WorkerGroup::barrier (dba/comms.hpp:56-63): validated rendezvous.
+  void barrier(int rank);
+  // WorkerGroup::sequence (dba/comms.hpp:52-53): collectives entered by rank.
+  std::uint64_t sequence(int rank) const;
   void abort(const std::string& why);
   bool aborted() const;
 
@@ -69,9 +76,10 @@ class Group {
   struct Slot {
     void* ptr = nullptr;
     std::int64_t count = 0;
-    int kind = 0;  // dtype * 2 + is_max
+    int kind = 0;  // kBarrier, or all-reduce: dtype * 2 + is_max
     std::uint64_t seq = 0;
   };
+  static constexpr int kBarrier = 8;
   void rendezvous(int rank);
   void validate(int rank, std::int64_t count, int kind);
   void* scratch(int rank, std::size_t bytes);
@@ -91,7 +99,6 @@ class Group {
   std::vector<cudaEvent_t> ready_, done_;
   std::vector<void*> scratch_;
   std::vector<std::size_t> scratch_bytes_;
-  std::vector<void**> dev_slots_;  // per rank: device array of K pointers
 };
 
 class GroupComm final : public Comm {

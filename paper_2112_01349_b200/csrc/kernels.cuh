@@ -615,6 +615,17 @@ __global__ void k_point_rows(std::int32_t n, const std::int32_t* __restrict__ id
   }
 }
 
+// glob[idx[d]] = dev[d] for the points this rank owns (gather_state).
+template <class S>
+__global__ void k_owned_rows(std::int32_t n, const std::int32_t* __restrict__ idx,
+                             const std::uint8_t* __restrict__ owned, const S* __restrict__ src, S* __restrict__ dst) {
+  const std::int32_t d = blockIdx.x * blockDim.x + threadIdx.x;
+  if (d >= n || !owned[d]) return;
+  const std::size_t g = std::size_t(idx[d]) * 3, l = std::size_t(d) * 3;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) dst[g + k] = src[l + k];
+}
+
 // rows[idx[i]] = 0 for W-wide rows.
 template <class S, int W>
 __global__ void k_zero_rows(std::int32_t n, const std::int32_t* __restrict__ idx, S* __restrict__ rows) {

@@ -124,7 +124,7 @@ class DevBuf {
 // host-side partition plan and device layout alone.
 struct ShardSizes {
   std::size_t N, slots, dpt_ptr, chunk_slot, cam_part_ptr, halo_slot, part, cam_ptr, cam_glob, n_loc, n_halo_loc,
-      halo, red, cm, pl, recs, n_long, xp_full, m, jb, carry, cam_list;
+      halo, red, cm, pl, recs, n_long, xp_full, m, jb, carry, cam_list, bounce;
 };
 
 inline void check_problem(const dbag_problem& p) {
@@ -250,6 +250,7 @@ class Rank {
     z.cam_ptr = nb * pl.cam_ptr.size();
     z.carry = nb > 1 ? (pl.cam_ptr.size() - 1) * 54 : 0;
     z.cam_list = nb > 1 ? nb * (pl.cam_ptr.size() - 1) : 0;
+    z.bounce = pl.ranks > 1 ? 4 * static_cast<std::size_t>(pl.ranks) : 0;  // tallies (2K) and identity probe (4K)
     return z;
   }
 
@@ -290,6 +291,7 @@ class Rank {
     f(&Rank::gsc_, 1);
     f(&Rank::g_pq_cam_, z.m);
     f(&Rank::g_bar_, 1);
+    f(&Rank::bounce_, z.bounce);
   }
 
   // Device bytes upload() reserves for this shard (exact: upload checks it).
@@ -1007,6 +1009,29 @@ class Rank {
     gv_ = hbuf_[2] + hbuf_[6];
   }
 
+  double damping_lambda() const { return lambda_; }
+  int damping_policy() const { return policy_; }
+
+  // The full state on every rank (lm_solve returns rank 0's, and every
+  // rank's is identical, dba/solver.hpp:282-285, 533): x_c is replicated;
+  // x_p is zero-filled in global order, each rank scatters the points it
+  // owns, and a sum-all-reduce over the communicator assembles it (every
+  // entry gets exactly one nonzero contribution, so the sum is exact).
+  void gather_state(S* xc, S* xp) {
+    DBAG_CUDA(cudaSetDevice(device_));
+    if (xc)
+      DBAG_CUDA(cudaMemcpyAsync(xc, xc_.get(), sizeof(S) * 9 * static_cast<std::size_t>(m_), cudaMemcpyDeviceToHost, st_));
+    const std::size_t full = static_cast<std::size_t>(n_glob_) * 3;
+    DBAG_CUDA(cudaMemsetAsync(xp_full_.get(), 0, sizeof(S) * std::max<std::size_t>(full, 1), st_));
+    if (n_loc_ > 0)
+      launch(dev::k_owned_rows<S>, grid_for(n_loc_, 256, 1 << 30), 256, n_loc_,
+             static_cast<const std::int32_t*>(dpt_glob_d_.get()), static_cast<const std::uint8_t*>(owned_.get()),
+             static_cast<const S*>(xp_.get()), xp_full_.get());
+    comm_->allreduce_sum(xp_full_.get(), static_cast<std::int64_t>(full), kT, st_);
+    if (xp) DBAG_CUDA(cudaMemcpyAsync(xp, xp_full_.get(), sizeof(S) * full, cudaMemcpyDeviceToHost, st_));
+    DBAG_CUDA(cudaStreamSynchronize(st_));
+  }
+
   void model_terms(double* step_inf, double* damp, double* gv) const {
     *step_inf = step_inf_;
     *damp = damp_term_;
@@ -1044,11 +1069,12 @@ class Rank {
     *ip = hbuf_[0];
   }
 
-  // Sum-all-reduce of a small host vector through a device bounce buffer.
+  // Sum-all-reduce of a small host vector (at most 4K doubles: the per-rank
+  // tallies and the rank-identity probe) through the pool's bounce buffer.
   void allreduce_host(double* v, int n) {
     DBAG_CUDA(cudaSetDevice(device_));
     if (comm_->size() == 1) return;
-    if (!bounce_.get() || bounce_.size() < static_cast<std::size_t>(n)) bounce_.alloc(static_cast<std::size_t>(n));
+    if (bounce_.size() < static_cast<std::size_t>(n)) throw Error(DBAG_INTERNAL, "host all-reduce exceeds the bounce buffer");
     DBAG_CUDA(cudaMemcpyAsync(bounce_.get(), v, sizeof(double) * n, cudaMemcpyHostToDevice, st_));
     comm_->allreduce_sum(bounce_.get(), n, DType::f64, st_);
     DBAG_CUDA(cudaMemcpyAsync(v, bounce_.get(), sizeof(double) * n, cudaMemcpyDeviceToHost, st_));

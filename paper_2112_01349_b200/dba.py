@@ -377,6 +377,7 @@ class SolverConfig:
     mse: int = MSE_HALF_PER_OBSERVATION
     jacobian: int = JACOBIAN_AUTODIFF
     check_rank_identity: bool = False
+    collective_timeout: float = 60000.0  # milliseconds (std::chrono::milliseconds, dba/solver.hpp:54)
     # B200 extension: FP64 solve with the coupling blocks E
     # stored in FP32 (half the DSE stream; not the reference's numerics)
     coupling_fp32: bool = False
@@ -388,6 +389,7 @@ class SolverConfig:
         c.rel_tol, c.step_tol, c.damping = self.rel_tol, self.step_tol, self.damping
         c.mse_half, c.jacobian, c.check_rank_identity = self.mse, self.jacobian, int(self.check_rank_identity)
         c.coupling_fp32 = int(self.coupling_fp32)
+        c.collective_timeout_ms = int(self.collective_timeout)
         return c
 
 
@@ -564,8 +566,8 @@ class RankContext:
             _check(N.lib().dbag_create_ex(device, precision, int(coupling_fp32), C.byref(h)))
         else:
             rank, nranks, uid = nccl
-            _check(N.lib().dbag_create_nccl(device, rank, nranks, C.create_string_buffer(bytes(uid), 128), precision,
-                                            C.byref(h)))
+            _check(N.lib().dbag_create_nccl_ex(device, rank, nranks, C.create_string_buffer(bytes(uid), 128),
+                                               precision, int(coupling_fp32), C.byref(h)))
         self.h = h
         self.m = self.n = self.nobs = 0
 
@@ -622,6 +624,7 @@ class RankContext:
         _check(N.lib().dbag_linearize(self.h, C.byref(bad)))
 
     def damp_factor(self, lam: float, policy: int = DAMPING_DIAG_SCALED):
+        self._damping = (float(lam), int(policy))
         _check(N.lib().dbag_damp_factor(self.h, lam, policy, None, None))
 
     def rhs(self):
@@ -635,9 +638,13 @@ class RankContext:
     def backsub_trial(self):
         _check(N.lib().dbag_backsub_trial(self.h))
 
-    def model_terms(self):
+    def model_terms(self, lam: Optional[float] = None, policy: Optional[int] = None):
+        """(step_inf, damping term, dx.v + dx.w) of the last trial; lam/policy
+        default to the preceding damp_factor's (others raise)."""
+        d_lam, d_pol = getattr(self, "_damping", (0.0, DAMPING_DIAG_SCALED))
         a, b, c = C.c_double(), C.c_double(), C.c_double()
-        _check(N.lib().dbag_model_terms(self.h, 0.0, 0, C.byref(a), C.byref(b), C.byref(c)))
+        _check(N.lib().dbag_model_terms(self.h, d_lam if lam is None else lam, d_pol if policy is None else policy,
+                                        C.byref(a), C.byref(b), C.byref(c)))
         return a.value, b.value, c.value
 
     def accept(self):
@@ -755,6 +762,82 @@ def group_allreduce(data: np.ndarray, device: int = 0) -> np.ndarray:
     a = np.ascontiguousarray(data, np.float64).copy()
     _check(N.lib().dbag_group_allreduce(a.shape[0], device, a.shape[1], a.ctypes.data))
     return a
+
+
+class WorkerGroup:
+    """dba::WorkerGroup (dba/comms.hpp:35-234) over K in-process ranks on
+    GPUs: every rank calls from its own thread (run_on_workers). Collectives
+    validate sequence / kind / type / length; a missing rank trips the
+    timeout (CollectiveError naming the absent ranks); abort() fails every
+    pending and later collective. allreduce_sum reduces in ascending rank
+    order on the device: bit-identical on every rank."""
+
+    def __init__(self, workers: int, timeout_ms: float = 60000.0, devices: Sequence[int] = (0,)):
+        devs = (C.c_int * len(devices))(*devices)
+        h = C.c_void_p()
+        _check(N.lib().dbag_group_create(int(workers), devs, len(devices), int(timeout_ms), C.byref(h)))
+        self.h, self.k = h, int(workers)
+
+    def workers(self) -> int:
+        return self.k
+
+    def close(self):
+        if self.h:
+            N.lib().dbag_group_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def barrier(self, rank: int):
+        _check(N.lib().dbag_group_barrier(self.h, int(rank)))
+
+    def allreduce_sum(self, rank: int, data: np.ndarray):
+        """In place on a contiguous float32/float64 array."""
+        if data.dtype not in (np.float32, np.float64) or not data.flags.c_contiguous:
+            raise InvalidArgumentError("allreduce_sum needs a contiguous float32/float64 array")
+        _check(N.lib().dbag_group_allreduce_sum(self.h, int(rank), data.ctypes.data, data.size, data.itemsize))
+        return data
+
+    def abort(self, reason: str = "aborted"):
+        _check(N.lib().dbag_group_abort(self.h, reason.encode()))
+
+    def sequence(self, rank: int) -> int:
+        v = C.c_uint64()
+        _check(N.lib().dbag_group_sequence(self.h, int(rank), C.byref(v)))
+        return v.value
+
+
+def run_on_workers(group: WorkerGroup, body):
+    """dba::run_on_workers (dba/comms.hpp:214-234): body(rank) on one thread
+    per rank; the first failure aborts the group and is re-raised after all
+    threads joined."""
+    import threading
+    first = []
+    lock = threading.Lock()
+
+    def run(r):
+        try:
+            body(r)
+        except BaseException as e:  # noqa: BLE001 - re-raised below
+            with lock:
+                if not first:
+                    first.append(e)
+            try:
+                group.abort(f"rank {r} failed: {e}")
+            except Error:
+                pass
+
+    th = [threading.Thread(target=run, args=(r,)) for r in range(group.workers())]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    if first:
+        raise first[0]
 
 
 def device_count() -> int:

@@ -1,0 +1,200 @@
+"""dba::WorkerGroup semantics on the B200 group backend (Group in comm.cu,
+through the dbag_group_* C ABI): the reference's tests/test_comms.cpp cases,
+with Python threads as the rank threads (run_on_workers)."""
+import threading
+
+import numpy as np
+import pytest
+
+import paper_2112_01349_b200 as dba
+from paper_2112_01349_b200.dba import CollectiveError, WorkerGroup, run_on_workers
+
+pytestmark = pytest.mark.gpu
+
+
+def test_two_rank_allreduce_sums_elementwise():
+    """tests/test_comms.cpp:12-20."""
+    g = WorkerGroup(2)
+    data = [np.array([1.0, 2.0]), np.array([3.0, 4.0])]
+    run_on_workers(g, lambda r: g.allreduce_sum(r, data[r]))
+    assert data[0].tolist() == [4, 6] and data[1].tolist() == [4, 6]
+
+
+def test_single_rank_allreduce_is_identity():
+    """tests/test_comms.cpp:22-30."""
+    g = WorkerGroup(1)
+    d = np.array([1.5, -2.25, 0.0])
+    e = d.copy()
+    run_on_workers(g, lambda r: g.allreduce_sum(r, d))
+    assert np.array_equal(d, e)
+
+
+def test_allreduce_bitwise_sequential_and_rank_identical():
+    """tests/test_comms.cpp:32-58: ascending-rank fixed association."""
+    k, n = 4, 257
+    rng = np.random.default_rng(2024)
+    locals_ = [rng.uniform(-1e6, 1e6, n) for _ in range(k)]
+    expected = locals_[0].copy()
+    for r in range(1, k):
+        expected += locals_[r]
+
+    def run():
+        g = WorkerGroup(k)
+        data = [v.copy() for v in locals_]
+        run_on_workers(g, lambda r: g.allreduce_sum(r, data[r]))
+        return data
+
+    once, twice = run(), run()
+    for r in range(k):
+        assert np.array_equal(once[r], expected) and np.array_equal(twice[r], once[r])
+
+
+def test_barrier_releases_everyone_and_sequences_align():
+    """tests/test_comms.cpp:60-76."""
+    k = 3
+    g = WorkerGroup(k)
+    inside = [0]
+    lock = threading.Lock()
+    saw_all = [True]
+
+    def body(r):
+        import time
+        for rnd in range(5):
+            if r == rnd % k:
+                time.sleep(0.002)
+            with lock:
+                inside[0] += 1
+            g.barrier(r)
+            if inside[0] < k * (rnd + 1):
+                saw_all[0] = False
+            g.barrier(r)
+
+    run_on_workers(g, body)
+    assert saw_all[0]
+    assert all(g.sequence(r) == 10 for r in range(k))
+
+
+def test_barrier_stress_no_lost_wakeups():
+    """tests/test_comms.cpp:78-89 (2,000 rounds instead of 10,000: each
+    round is a ctypes call from a Python thread)."""
+    k, rounds = 4, 2000
+    g = WorkerGroup(k)
+    counts = [0] * k
+
+    def body(r):
+        for _ in range(rounds):
+            g.barrier(r)
+            counts[r] += 1
+
+    run_on_workers(g, body)
+    assert counts == [rounds] * k
+
+
+def test_length_mismatch_is_fatal():
+    """tests/test_comms.cpp:91-100."""
+    g = WorkerGroup(2)
+    a, b = np.ones(5), np.ones(7)
+    with pytest.raises(CollectiveError, match="length"):
+        run_on_workers(g, lambda r: g.allreduce_sum(r, a if r == 0 else b))
+
+
+def test_mismatched_kinds_are_fatal_not_deadlock():
+    """tests/test_comms.cpp:102-114."""
+    g = WorkerGroup(2)
+    v = np.ones(3)
+    with pytest.raises(CollectiveError, match="kind"):
+        run_on_workers(g, lambda r: g.allreduce_sum(r, v.copy()) if r == 0 else g.barrier(r))
+
+
+def test_mismatched_element_types_are_fatal():
+    """dba/comms.hpp:183-184: a different element type is a mismatch."""
+    g = WorkerGroup(2)
+    with pytest.raises(CollectiveError, match="element type"):
+        run_on_workers(g, lambda r: g.allreduce_sum(r, np.ones(3, np.float32 if r else np.float64)))
+
+
+def test_missing_rank_trips_timeout_with_diagnostic():
+    """tests/test_comms.cpp:116-129: 50 ms timeout, message names rank 2."""
+    g = WorkerGroup(3, timeout_ms=50)
+    with pytest.raises(CollectiveError) as ei:
+        run_on_workers(g, lambda r: g.barrier(r) if r != 2 else None)
+    assert "timeout" in str(ei.value) and "2" in str(ei.value)
+
+
+def test_failing_rank_aborts_group():
+    """tests/test_comms.cpp:131-143: the failure propagates instead of a hang."""
+    g = WorkerGroup(2, timeout_ms=5000)
+
+    def body(r):
+        if r == 1:
+            raise RuntimeError("boom")
+        g.barrier(r)
+
+    with pytest.raises(RuntimeError, match="boom"):
+        run_on_workers(g, body)
+
+
+def test_float_buffers_and_scalars():
+    """tests/test_comms.cpp:145-160."""
+    g = WorkerGroup(2)
+    data = [np.array([1.0, 2.0], np.float32), np.array([0.5, -1.0], np.float32)]
+    run_on_workers(g, lambda r: g.allreduce_sum(r, data[r]))
+    assert data[0].tolist() == [1.5, 1.0]
+    g2 = WorkerGroup(3)
+    res = [np.array([v]) for v in (1.0, 10.0, 100.0)]
+    run_on_workers(g2, lambda r: g2.allreduce_sum(r, res[r]))
+    assert all(x[0] == 111.0 for x in res)
+
+
+def test_more_than_sixteen_ranks():
+    """The reference's WorkerGroup takes any K; the group backend carries up
+    to 256 (the 16-rank cap)."""
+    p = dba.generate_synthetic(dba.SyntheticOptions(cameras=24, points=120, obs_per_point=6, seed=3,
+                                                    pixel_noise=0.5))
+    st = dba.lm_solve(p, dba.SolverConfig(workers=20, max_iterations=2))
+    from oracle import oracle as O
+    o = O.lm_solve(p, dba.SolverConfig(workers=20, max_iterations=2))
+    assert [r.accepted for r in st.history] == [r.accepted for r in o.history]
+    for a, b in zip(st.history, o.history):
+        assert abs(a.cost - b.cost) <= 1e-9 * b.cost
+
+
+def test_lm_state_assembled_over_the_group():
+    """lm_solve returns rank 0's full state (dba/solver.hpp:533); with K ranks
+    x_p is assembled on the device over the group (Rank::gather_state, the
+    same code the NCCL path runs): equal to the oracle's at K = 1 and 3."""
+    from oracle import oracle as O
+    p = dba.generate_synthetic(dba.SyntheticOptions(cameras=16, points=90, obs_per_point=5, seed=5,
+                                                    pixel_noise=0.5))
+    for k in (1, 3):
+        cfg = dba.SolverConfig(workers=k, max_iterations=3, pcg_tol=1e-12)
+        g, o = dba.lm_solve(p, cfg), O.lm_solve(p, cfg)
+        assert np.max(np.abs(g.x_c - o.x_c)) <= 1e-8 * np.max(np.abs(o.x_c))
+        assert np.max(np.abs(g.x_p - o.x_p)) <= 1e-8 * np.max(np.abs(o.x_p))
+
+
+def test_nccl_single_rank_returns_full_state():
+    """dbag_lm_solve_rank (one process per GPU over NCCL) at nranks = 1:
+    the full state comes back (ranks got partial x_p)."""
+    p = dba.generate_synthetic(dba.SyntheticOptions(cameras=16, points=90, obs_per_point=5, seed=5,
+                                                    pixel_noise=0.5))
+    cfg = dba.SolverConfig(max_iterations=3)
+    a = dba.lm_solve_rank(p, cfg, 0, 1, dba.nccl_unique_id(), 0)
+    b = dba.lm_solve(p, cfg)
+    assert np.array_equal(a.x_c, b.x_c) and np.array_equal(a.x_p, b.x_p)
+
+
+def test_model_terms_reject_a_different_lambda():
+    """dbag_model_terms: the damping term is scored with the damp_factor's
+    lambda/policy (dba/solver.hpp:389-408); another pair raises."""
+    p = dba.generate_synthetic(dba.SyntheticOptions(cameras=12, points=60, obs_per_point=4, seed=2))
+    with dba.RankContext(0, 8) as ctx:
+        ctx.upload(p)
+        ctx.linearize()
+        ctx.damp_factor(1e-3, dba.dba.DAMPING_DIAG_SCALED)
+        ctx.rhs()
+        ctx.pcg(1e-6, 100)
+        ctx.backsub_trial()
+        assert ctx.model_terms()[1] > 0
+        with pytest.raises(dba.dba.InvalidArgumentError):
+            ctx.model_terms(lam=1e-2)

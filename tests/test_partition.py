@@ -79,3 +79,35 @@ def test_halo_plan_point_major():
                 owners.setdefault(q, set()).add(r)
         expect = sorted(q for q, s in owners.items() if len(s) > 1)
         assert list(sh) == expect
+
+
+@pytest.mark.parametrize("shape,split", [
+    ((1778, 993923, 5001946), [625244] * 2 + [625243] * 6),
+    ((13682, 4456117, 28987644), [3623456] * 4 + [3623455] * 4),
+], ids=["venice-1778", "final-13682"])
+def test_k8_integer_exact_at_baseline_shapes(shape, split):
+    """K = 8 on the BASELINE.json instances: the split
+    (dba/partition.hpp:76-103: first N mod K ranks +1), every LocalIndexMap
+    and build_groups array equal to the oracle's, integer for integer, and
+    the halo plan (points touched by more than one rank) equal to an
+    independent numpy count and at most K - 1 points (point-major edges)."""
+    m, n, N = shape
+    p = dba.generate_synthetic(dba.SyntheticOptions(cameras=m, points=n, num_observations=N, seed=1, pixel_noise=0.5))
+    k = 8
+    parts = dba.partition_edges(p, k)
+    assert [len(g.edge_ids) for g in parts] == split
+    for r in range(k):
+        o = O.partition(p, k, r)
+        g = parts[r]
+        assert g.edge_ids[0] == o["start"] and len(g.edge_ids) == o["count"]
+        for a, b in ((g.camera_map.to_global, o["cam_g"]), (g.point_map.to_global, o["pt_g"]),
+                     (g.cam_ptr, o["cam_ptr"]), (g.cam_blocks, o["cam_blk"]), (g.pt_ptr, o["pt_ptr"]),
+                     (g.pt_blocks, o["pt_blk"])):
+            assert a.dtype.kind == b.dtype.kind and np.array_equal(a, b)
+    pid = p.arrays()[3]
+    bounds = np.cumsum([0] + split)
+    first = pid[bounds[:-1]]
+    last = pid[bounds[1:] - 1]
+    expect = sorted({int(a) for a, b in zip(last[:-1], first[1:]) if a == b})
+    shared = dba.shared_points(p, k)
+    assert list(shared) == expect and len(shared) <= k - 1
