@@ -103,6 +103,15 @@ def dse_bytes(N, n, m, s):
     return N * (27 * s + 4) + 9 * n * s + 108 * m * s
 
 
+def dse_layout_bytes(N, n, m, s, t=None):
+    """Compulsory bytes of one DSE pass over THIS layout: the factored
+    coupling records (18 lanes of G = sqrt(w) Jc per edge, kernels.cuh
+    kLanesFact, t bytes each) plus one camera index per edge, C^-1 per point,
+    B, x, out and R per camera. The reference layout (dse_bytes) stores 27."""
+    t = s if t is None else t
+    return N * (18 * t + 4) + 9 * n * s + 117 * m * s
+
+
 def lm_bytes(N, n, m, s, I, linearized=True):
     """Algorithmic bytes of one LM iteration (SURVEY.md §8d B_LM) with I PCG
     iterations and R = I // 50 residual refreshes; the leading 1 of B_PCG is
@@ -301,7 +310,122 @@ def time_steps(ctx, cfg, steps, flush):
     return ms, pcg
 
 
-def dse_roofline(ctx, prof, b_dse, peak, steps, total_ms, world):
+def dse_roofline(ctx, prof, b_dse, peak, steps, total_ms, world, b_layout=None):
+    """Roofline of the dominant kernel, the DSE pass (B_DSE bytes
+    per pass). The time per pass is measured live over the timed steps: CUDA
+    events on the context's stream around every DPCG (one graph launch at
+    K = 1) divided by its DSE count — so it also holds the camera fold + PCG
+    step that follow each pass inside the graph (a few %): `frac` is a lower
+    bound for the pass alone. For reference, the pass launched alone back to
+    back on the finished solve's state is `standalone_launch_ms`."""
+    dse_per_step = prof["dse_launches"] / max(steps, 1)
+    per = prof["dse_ms"] / max(prof["dse_launches"], 1)
+    kernel = ("k_g_pass (+ its camera fold / PCG step), in-graph, CUDA events over the timed steps" if world == 1
+              else "k_g_pass (+ halo / camera all-reduce, fold, step) of the K > 1 DPCG, CUDA events")
+    standalone = None
+    if world == 1:
+        try:
+            standalone = ctx.time_dse_pass(20)
+        except Exception:  # DBAG_PCG selected a non-graph DPCG
+            kernel = "DPCG (DBAG_PCG=%s), device time per DSE" % os.environ.get("DBAG_PCG")
+    achieved = b_dse / (per / 1e3) / 1e9
+    lay = {} if b_layout is None else {
+        "layout_bytes_per_launch": b_layout, "layout_achieved": b_layout / (per / 1e3) / 1e9,
+        "layout_frac": b_layout / (per / 1e3) / 1e9 / peak}
+    out = {"bound": "hbm", "kernel": kernel, "achieved": achieved, "peak": peak, "unit": "GB/s",
+           "frac": achieved / peak, "traffic": None, "bytes_per_launch": b_dse, "avg_launch_ms": per, **lay,
+           "launches_per_step": dse_per_step, "standalone_launch_ms": standalone,
+           "standalone_frac": (b_dse / (standalone / 1e3) / 1e9 / peak) if standalone else None,
+           "share_of_step": per * dse_per_step / max(total_ms / max(steps, 1), 1e-9),
+           "note": "achieved = algorithmic DSE bytes per pass (SURVEY 8d: 27 scalars of E per edge, the "
+                   "reference's layout) / device ms per pass; layout_* = the same against the compulsory bytes "
+                   "of the factored records this build streams (18 scalars per edge); traffic = ncu DRAM bytes "
+                   "of one launch (profiles/ncu_traffic.json)"}
+    return out
+
+
+def run_reference(args):
+    """The reference arm: the CPU restatement (oracle/) of the reference's
+    solver on this host's physical cores. Imports oracle/ only."""
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    m, n, N = WORKLOADS[args.workload]
+    t_gen = time.perf_counter()
+    p = make_oracle_problem(args.workload)
+    t_gen = time.perf_counter() - t_gen
+    host = host_info()
+    k = cpu_threads()
+    # warm-up: the first step is one FULL LM iteration (calibration: the full
+    # DSE count and an unscaled t_LM); the rest are bounded samples.
+    secs, info = cpu_reference_steps(p, k, args.warmup - 1 + args.steps if args.warmup >= 1 else args.steps)
+    timed = secs[-args.steps:]
+    t = float(np.mean(timed))
+    value = N / t
+    # K = 1 (BASELINE.md §3): one bounded sample, scaled the same way
+    secs1, info1 = cpu_reference_steps(p, 1, 1, dse_full=info["dse_per_full_iteration"], calibrate=False)
+    sample = (f"{args.workload}: each step one LM iteration from x0 (oracle restatement, {k} rank threads), "
+              f"DPCG capped at {PCG_SAMPLE} iterations and its time scaled to the full iteration's "
+              f"{info['dse_per_full_iteration']} DSEs; warm-up step 1 ran the full iteration unscaled "
+              f"({info['full_iteration_s']:.2f} s, {info['full_pcg_iterations']} PCG iterations)")
+    print(json.dumps({
+        "impl": "reference", "metric": "edges_per_sec_per_lm_iteration", "value": value, "unit": "edges/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": workload_config(args.workload, info["full_pcg_iterations"]),
+        "cpu_baseline": {"value": value, "unit": "edges/s", "cores": k, "kind": "port", "sample": sample,
+                         "host": host, "jacobian": "autodiff", "detail": info,
+                         "k1": {"value": N / secs1[0], "unit": "edges/s", "cores": 1, "seconds": secs1[0],
+                                "sample": f"one bounded sample at K = 1 (DPCG capped at {PCG_SAMPLE}, scaled)",
+                                "detail": info1}},
+        "e2e": {"value": value, "unit": "edges/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "instance_generation_s": t_gen,
+        "repo_libs_loaded": repo_libs_loaded(),
+    }), flush=True)
+
+
+def repo_libs_loaded():
+    """In-tree shared objects mapped into this process (the reference arm
+    must show oracle/ only)."""
+    try:
+        with open("/proc/self/maps") as f:
+            return sorted({os.path.relpath(l.split()[-1], ROOT) for l in f
+                           if l.rstrip().endswith(".so") and l.split()[-1].startswith(ROOT)})
+    except Exception:
+        return None
+
+
+def workload_config(name, pcg):
+    m, n, N = WORKLOADS[name]
+    return {"workload": name, "cameras": m, "points": n, "observations": N, "pcg_iterations_per_step": int(pcg),
+            "solver": "SolverConfig defaults (diag_scaled, lambda0 1e-4, pcg_tol 1e-6, pcg_max_iters 500)",
+            "step": "one LM iteration from x0 (linearize+assemble, damp+factor, rhs, DPCG, backsub, trial cost)",
+            "instance": "dba/synthetic.hpp ring, seed 1, count-exact, +-0.5 px noise (BASELINE.md §3)"}
+
+
+def flush_l2(buf):
+    import torch
+    buf.zero_()
+    torch.cuda.synchronize()
+
+
+def time_steps(ctx, cfg, steps, flush):
+    """Per-step device time (CUDA events on the context's stream), L2 flushed
+    between steps outside the timed window."""
+    ms = []
+    pcg = 0
+    for _ in range(steps):
+        if flush is not None:
+            flush_l2(flush)
+        ctx.synchronize()
+        ctx.mark(0)
+        _, pcg, _ = ctx.probe_step(cfg.lambda0, cfg)
+        ctx.mark(1)
+        ms.append(ctx.elapsed_ms())
+    return ms, pcg
+
+
+def dse_roofline(ctx, prof, b_dse, peak, steps, total_ms, world, b_layout=None):
     """Roofline of the dominant kernel, the DSE pass (B_DSE bytes
     per pass). Single rank: the graph DPCG's k_g_pass, timed live with CUDA
     events on the context's stream, launched alone back to back on the state
@@ -319,14 +443,17 @@ def dse_roofline(ctx, prof, b_dse, peak, steps, total_ms, world):
         except Exception:  # DBAG_PCG selected a non-graph DPCG
             kernel = "DPCG (DBAG_PCG=%s), device time per DSE" % os.environ.get("DBAG_PCG")
     achieved = b_dse / (per / 1e3) / 1e9
+    lay = {} if b_layout is None else {
+        "layout_bytes_per_launch": b_layout, "layout_achieved": b_layout / (per / 1e3) / 1e9,
+        "layout_frac": b_layout / (per / 1e3) / 1e9 / peak}
     return {"bound": "hbm", "kernel": kernel, "achieved": achieved, "peak": peak, "unit": "GB/s",
-            "frac": achieved / peak, "traffic": None, "bytes_per_launch": b_dse, "avg_launch_ms": per,
+            "frac": achieved / peak, "traffic": None, "bytes_per_launch": b_dse, "avg_launch_ms": per, **lay,
             "launches_per_step": dse_per_step, "in_graph_ms_per_dse": loop_ms_per_dse,
             "share_of_step": per * dse_per_step / max(total_ms / max(steps, 1), 1e-9),
-            "note": "achieved = algorithmic DSE bytes per pass (SURVEY 8d) / device ms per launch; "
-                    "the pass re-reads E from HBM each PCG iteration (ncu, warm caches: L2 hit rate ~20 %) "
-                    "and is latency-bound at trafalgar-257's 1780 chunk CTAs (2.4 waves); "
-                    "traffic = ncu dram bytes of one standalone launch (profiles/ncu_traffic.json)"}
+            "note": "achieved = algorithmic DSE bytes per pass (SURVEY 8d: 27 scalars of E per edge, the "
+                    "reference's layout) / device ms per launch; layout_* = the same against the compulsory bytes "
+                    "of the factored records this build streams (18 scalars per edge); traffic = ncu DRAM bytes "
+                    "of one launch (profiles/ncu_traffic.json)"}
 
 
 def solve_t_lm(p, world, rank, uid, device, iters=10):
@@ -416,7 +543,7 @@ def run_ours(args):
 
     peak, peak_kind = load_peaks()
     b_dse = dse_bytes(N // world, n, m, 8)
-    roof = dse_roofline(ctx, prof, b_dse, peak, args.steps, total_ms, world)
+    roof = dse_roofline(ctx, prof, b_dse, peak, args.steps, total_ms, world, dse_layout_bytes(N // world, n, m, 8))
     roof["peak_kind"] = peak_kind
     roof["traffic"], roof["traffic_source"] = ncu_traffic(args.workload)
     ctx.close()
@@ -479,9 +606,11 @@ def secondary(flush, name, dtype=np.float64, coupling_fp32=False):
         t = sum(ms) / len(ms)
         peak, _ = load_peaks()
         b_dse = dse_bytes(N, n, m, s)
+        b_lay = dse_layout_bytes(N, n, m, s)
         if coupling_fp32:  # E lanes at 4 bytes, everything else FP64
             b_dse = N * (27 * 4 + 4) + 9 * n * 8 + 108 * m * 8
-        roof = dse_roofline(ctx, prof, b_dse, peak, len(ms), sum(ms), 1)
+            b_lay = dse_layout_bytes(N, n, m, 8, 4)
+        roof = dse_roofline(ctx, prof, b_dse, peak, len(ms), sum(ms), 1, b_lay)
     tag = "f64" if s == 8 and not coupling_fp32 else ("f64e32" if coupling_fp32 else "f32")
     roof["traffic"], roof["traffic_source"] = ncu_traffic(name, tag)
     return {"workload": name, "dtype": ("f64 (E blocks stored f32)" if coupling_fp32 else "f64") if s == 8 else "f32",

@@ -47,6 +47,7 @@ struct DseArgs {
   const std::int32_t* long_chunk;  // first chunk of each long tile
   std::int32_t n_long;
   std::int32_t pf_dist;  // > 0: chunk c prefetches record c + pf_dist into L2
+  const S* Rm;           // per-camera R (9m, row-major): factored records only
 };
 
 // Shared work area of a chunk pass: a (3 x kTile), b (3 x kTile) and the
@@ -63,6 +64,7 @@ struct DseWork {
 #if !DBAG_Y_OVERLAY
   S ybuf[kTile * 9];
 #endif
+  S rs[kXsCams * 9];  // R of the chunk's distinct cameras (factored records)
   std::int32_t upart[kTile];
   std::uint8_t uslot[kTile];
   std::uint8_t ubeg[kTile + 8];
@@ -77,9 +79,9 @@ struct DseWork {
 };
 static_assert(6 * kTile + kXsCams * 9 <= 9 * kTile, "a, b and xs must fit under y");
 
-template <class T>
+template <class T, int L>
 __device__ __forceinline__ const RecMeta& rec_meta(const T* R) {
-  return *reinterpret_cast<const RecMeta*>(R + Rec<T>::kE);
+  return *reinterpret_cast<const RecMeta*>(R + Rec<T, L>::kE);
 }
 
 // Point finish: halo deposit or b = C^-1 a (MODE 0), dx_p = C^-1 (w - a)
@@ -191,16 +193,19 @@ struct GatherX {
   __device__ __forceinline__ S combine(const Raw& r) const { return r.v; }
 };
 // One 128-slot chunk whose record is at R (global or shared memory);
-// normal tiles only (long tiles return).
-template <class S, int MODE, class G, class T>
+// normal tiles only (long tiles return). L = record lanes (kLanesFact:
+// G = sqrt(w) Jc with the cameras' R staged in shared memory; kLanesDense:
+// the 9x3 blocks).
+template <class S, int MODE, int L, class G, class T>
 __device__ __forceinline__ void dse_chunk_at(const DseArgs<S, T>& A, DseWork<S>& sm, const T* R, G gx) {
+  constexpr bool kFact = L == kLanesFact;
   const int tid = threadIdx.x;
-  const RecMeta& M = rec_meta(R);
+  const RecMeta& M = rec_meta<T, L>(R);
   // Load order (measured): header and metadata first; then the loads that
-  // depend on them and sit on the tile's critical path (C factors, then the
-  // camera gathers after the producer wait); the 27-lane E stream, needed
-  // only from the a-phase on, is issued behind the gathers so it does not
-  // queue ahead of them.
+  // depend on them and sit on the tile's critical path (C factors, the
+  // cameras' R — constant, so before the producer wait — then the camera
+  // gathers after it); the E-lane stream, needed only from the a-phase on,
+  // is issued behind the gathers so it does not queue ahead of them.
   const int4 hdr = *reinterpret_cast<const int4*>(&M.p0);  // p0, np, nslots, nchunk
   const int su = M.su[tid];
   const int pti = M.pt[tid];
@@ -209,10 +214,18 @@ __device__ __forceinline__ void dse_chunk_at(const DseArgs<S, T>& A, DseWork<S>&
   if (MODE != 1) stage_meta(M, sm);
   if (hdr.w > 1) return;  // long tile: dse_long
   const std::int32_t p0 = hdr.x, np = hdr.y;
-  S L[9], wv[3];
-  if (tid < np) load_point<S, MODE>(A, p0 + tid, L, wv);
-  if (!gx.ready()) return;
+  S L9[9], wv[3];
+  if (tid < np) load_point<S, MODE>(A, p0 + tid, L9, wv);
   const bool staged = nu <= kXsCams;
+  S rraw[3];
+  if (kFact && staged) {
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      const int t = tid + kTile * j;
+      if (t < nu * 9) rraw[j] = __ldg(A.Rm + std::size_t(M.ucam[t / 9]) * 9 + (t - (t / 9) * 9));
+    }
+  }
+  if (!gx.ready()) return;
   typename G::Raw graw[3];  // the chunk's camera vectors, once per (camera, row)
   if (MODE != 2 && staged) {
 #pragma unroll
@@ -221,26 +234,28 @@ __device__ __forceinline__ void dse_chunk_at(const DseArgs<S, T>& A, DseWork<S>&
       if (t < nu * 9) graw[j] = gx.raw(M.ucam[t / 9], t - (t / 9) * 9);
     }
   }
-  S e[27];
+  S e[L];
 #pragma unroll
-  for (int k = 0; k < 27; ++k) e[k] = S(R[k * kTile + tid]);  // padding slots hold zeros
+  for (int k = 0; k < L; ++k) e[k] = S(R[k * kTile + tid]);  // padding slots hold zeros
+  if (staged && (kFact || MODE != 2)) {
+#pragma unroll
+    for (int j = 0; j < 3; ++j)
+      if (tid + kTile * j < nu * 9) {
+        if (MODE != 2) sm.xs()[tid + kTile * j] = gx.combine(graw[j]);
+        if (kFact) sm.rs[tid + kTile * j] = rraw[j];
+      }
+    __syncthreads();
+  }
+  // this slot's camera R: staged, or straight from global for > kXsCams cameras
+  const std::int32_t cam = staged ? 0 : M.cam[tid];
+  const S* Rc = kFact ? (staged ? sm.rs + su * 9 : A.Rm + std::size_t(cam) * 9) : nullptr;
   if (MODE != 2) {
-    if (staged) {
-#pragma unroll
-      for (int j = 0; j < 3; ++j)
-        if (tid + kTile * j < nu * 9) sm.xs()[tid + kTile * j] = gx.combine(graw[j]);
-      __syncthreads();
-    }
     S a[3] = {S(0), S(0), S(0)};
     if (tid < hdr.z) {
-      const std::int32_t cam = staged ? 0 : M.cam[tid];
+      S xv[9];
 #pragma unroll
-      for (int i = 0; i < 9; ++i) {
-        const S xv = staged ? sm.xs()[su * 9 + i] : gx(cam, i);
-        a[0] += e[i * 3 + 0] * xv;
-        a[1] += e[i * 3 + 1] * xv;
-        a[2] += e[i * 3 + 2] * xv;
-      }
+      for (int i = 0; i < 9; ++i) xv[i] = staged ? sm.xs()[su * 9 + i] : gx(cam, i);
+      coupling_t<S, L>(e, Rc, xv, a);
     }
 #pragma unroll
     for (int j = 0; j < 3; ++j) sm.a()[tid][j] = a[j];
@@ -252,7 +267,7 @@ __device__ __forceinline__ void dse_chunk_at(const DseArgs<S, T>& A, DseWork<S>&
       for (int q = pb0; q < pb1; ++q)
 #pragma unroll
         for (int j = 0; j < 3; ++j) tt[j] += sm.a()[q][j];
-    finish_point<S, MODE>(A, p0 + tid, L, wv, tt, b);
+    finish_point<S, MODE>(A, p0 + tid, L9, wv, tt, b);
 #pragma unroll
     for (int j = 0; j < 3; ++j) sm.b()[tid][j] = b[j];
   }
@@ -262,8 +277,10 @@ __device__ __forceinline__ void dse_chunk_at(const DseArgs<S, T>& A, DseWork<S>&
 #if DBAG_Y_OVERLAY
     __syncthreads();  // y overlays b
 #endif
+    S y[9];
+    coupling_b<S, L>(e, Rc, b0, b1, b2, y);
 #pragma unroll
-    for (int i = 0; i < 9; ++i) sm.y()[tid][i] = (e[i * 3] * b0 + e[i * 3 + 1] * b1) + e[i * 3 + 2] * b2;
+    for (int i = 0; i < 9; ++i) sm.y()[tid][i] = y[i];
     __syncthreads();
     fold_cameras(A, nu, sm.ubeg, sm.uslot, sm.upart, YRows<S>{sm.y()});
     // one chunk per CTA (k_g_pass, k_dse_chunk): no trailing barrier
@@ -274,15 +291,15 @@ __device__ __forceinline__ void l2_prefetch(const void* p, unsigned bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
 
-template <class S, int MODE, class G, class T>
+template <class S, int MODE, int L, class G, class T>
 __device__ __forceinline__ void dse_chunk(const DseArgs<S, T>& A, DseWork<S>& sm, std::int32_t chunk, const G& gx) {
   // One wave ahead: the record the CTA pf_dist chunks later will read is
   // streamed into L2 now (E is constant through the PCG, so this may run
   // before the producer wait), decoupling HBM traffic from the pass's
   // per-chunk latency chain.
   if (A.pf_dist > 0 && threadIdx.x == 0 && chunk + A.pf_dist < A.n_chunks)
-    l2_prefetch(A.rec + std::size_t(chunk + A.pf_dist) * Rec<T>::kLen, rec_hot_bytes<T>());
-  dse_chunk_at<S, MODE>(A, sm, A.rec + std::size_t(chunk) * Rec<T>::kLen, gx);
+    l2_prefetch(A.rec + std::size_t(chunk + A.pf_dist) * Rec<T, L>::kLen, rec_hot_bytes<T, L>());
+  dse_chunk_at<S, MODE, L>(A, sm, A.rec + std::size_t(chunk) * Rec<T, L>::kLen, gx);
 }
 
 // Resident CTAs per SM the chunk pass is compiled for (register budget):
@@ -298,34 +315,36 @@ constexpr int pass_min_blocks() {
   return sizeof(T) == 4 ? DBAG_PASS_MINB_F32E : DBAG_PASS_MINB_F64E;
 }
 
-template <class S, int MODE, class T = S>
+template <class S, int MODE, class T = S, int L = kLanesFact>
 __global__ void __launch_bounds__(kTile, pass_min_blocks<T>()) k_dse_chunk(DseArgs<S, T> A) {
   __shared__ DseWork<S> sm;
-  dse_chunk<S, MODE>(A, sm, blockIdx.x, GatherX<S>{A.x});
+  dse_chunk<S, MODE, L>(A, sm, blockIdx.x, GatherX<S>{A.x});
 }
 
 // One CTA per long tile (a single point observed more than 128 times).
-template <class S, int MODE, class G, class T>
+template <class S, int MODE, int L, class G, class T>
 __device__ __forceinline__ void dse_long(const DseArgs<S, T>& A, DseWork<S>& sm, std::int32_t li, G gx) {
+  constexpr bool kFact = L == kLanesFact;
   if (!gx.ready()) return;
   const int tid = threadIdx.x;
   const std::int32_t c0 = A.long_chunk[li];
-  const RecMeta& M0 = rec_meta(A.rec + std::size_t(c0) * Rec<T>::kLen);
+  const RecMeta& M0 = rec_meta<T, L>(A.rec + std::size_t(c0) * Rec<T, L>::kLen);
   const std::int32_t p = M0.p0, nchunk = M0.nchunk;
   S a[3] = {S(0), S(0), S(0)};
   if (MODE != 2) {
     for (std::int32_t c = c0; c < c0 + nchunk; ++c) {
-      const T* R = A.rec + std::size_t(c) * Rec<T>::kLen;
-      const RecMeta& M = rec_meta(R);
+      const T* R = A.rec + std::size_t(c) * Rec<T, L>::kLen;
+      const RecMeta& M = rec_meta<T, L>(R);
       if (tid < M.nslots) {
         const std::int32_t cam = M.cam[tid];
+        S e[L], xv[9], as[3];
 #pragma unroll
-        for (int i = 0; i < 9; ++i) {
-          const S xv = gx(cam, i);
-          a[0] += S(R[(i * 3 + 0) * kTile + tid]) * xv;
-          a[1] += S(R[(i * 3 + 1) * kTile + tid]) * xv;
-          a[2] += S(R[(i * 3 + 2) * kTile + tid]) * xv;
-        }
+        for (int k = 0; k < L; ++k) e[k] = S(R[k * kTile + tid]);
+#pragma unroll
+        for (int i = 0; i < 9; ++i) xv[i] = gx(cam, i);
+        coupling_t<S, L>(e, kFact ? A.Rm + std::size_t(cam) * 9 : nullptr, xv, as);
+#pragma unroll
+        for (int j = 0; j < 3; ++j) a[j] += as[j];
       }
     }
   }
@@ -338,9 +357,9 @@ __device__ __forceinline__ void dse_long(const DseArgs<S, T>& A, DseWork<S>& sm,
       for (int k = 0; k < kTile; ++k)
 #pragma unroll
         for (int j = 0; j < 3; ++j) tt[j] += sm.a()[k][j];
-    S L[9], wv[3];
-    load_point<S, MODE>(A, p, L, wv);
-    finish_point<S, MODE>(A, p, L, wv, tt, b);
+    S L9[9], wv[3];
+    load_point<S, MODE>(A, p, L9, wv);
+    finish_point<S, MODE>(A, p, L9, wv, tt, b);
 #pragma unroll
     for (int j = 0; j < 3; ++j) sm.b()[0][j] = b[j];
   }
@@ -348,14 +367,16 @@ __device__ __forceinline__ void dse_long(const DseArgs<S, T>& A, DseWork<S>& sm,
     __syncthreads();
     const S b0 = sm.b()[0][0], b1 = sm.b()[0][1], b2 = sm.b()[0][2];  // y overlays b below
     for (std::int32_t c = c0; c < c0 + nchunk; ++c) {
-      const T* R = A.rec + std::size_t(c) * Rec<T>::kLen;
-      const RecMeta& M = rec_meta(R);
+      const T* R = A.rec + std::size_t(c) * Rec<T, L>::kLen;
+      const RecMeta& M = rec_meta<T, L>(R);
       __syncthreads();
       stage_meta(M, sm);
+      S e[L], y[9];
 #pragma unroll
-      for (int i = 0; i < 9; ++i)
-        sm.y()[tid][i] = (S(R[(i * 3) * kTile + tid]) * b0 + S(R[(i * 3 + 1) * kTile + tid]) * b1) +
-                       S(R[(i * 3 + 2) * kTile + tid]) * b2;
+      for (int k = 0; k < L; ++k) e[k] = S(R[k * kTile + tid]);
+      coupling_b<S, L>(e, kFact ? A.Rm + std::size_t(M.cam[tid]) * 9 : nullptr, b0, b1, b2, y);
+#pragma unroll
+      for (int i = 0; i < 9; ++i) sm.y()[tid][i] = y[i];
       __syncthreads();
       fold_cameras(A, M.nu, sm.ubeg, sm.uslot, sm.upart, YRows<S>{sm.y()});
     }
@@ -363,10 +384,10 @@ __device__ __forceinline__ void dse_long(const DseArgs<S, T>& A, DseWork<S>& sm,
   __syncthreads();
 }
 
-template <class S, int MODE, class T = S>
+template <class S, int MODE, class T = S, int L = kLanesFact>
 __global__ void __launch_bounds__(kTile) k_dse_long(DseArgs<S, T> A) {
   __shared__ DseWork<S> sm;
-  dse_long<S, MODE>(A, sm, blockIdx.x, GatherX<S>{A.x});
+  dse_long<S, MODE, L>(A, sm, blockIdx.x, GatherX<S>{A.x});
 }
 
 }  // namespace dev

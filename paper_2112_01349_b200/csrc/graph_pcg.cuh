@@ -263,7 +263,7 @@ __device__ __forceinline__ void camera_fold(const GBufs<S>& B, std::int32_t cam,
 
 // The body's DSE pass: CTAs [0, n_long) take the long tiles, the rest one
 // chunk each (GatherGraph).
-template <class S, class T = S>
+template <class S, class T = S, int L = kLanesFact>
 __global__ void __launch_bounds__(kTile, pass_min_blocks<T>()) k_g_pass(DseArgs<S, T> A, GBufs<S> B, const GScal<S>* sc) {
   __shared__ DseWork<S> sm;
   pdl_allow_dependents();
@@ -276,9 +276,9 @@ __global__ void __launch_bounds__(kTile, pass_min_blocks<T>()) k_g_pass(DseArgs<
   }
 #endif
   if (blk < A.n_long)
-    dse_long<S, 0>(A, sm, blk, gx);
+    dse_long<S, 0, L>(A, sm, blk, gx);
   else
-    dse_chunk<S, 0>(A, sm, blk - A.n_long, gx);
+    dse_chunk<S, 0, L>(A, sm, blk - A.n_long, gx);
 }
 
 // Finish of an iteration: rho_prev, rho, |r|^2, n + 1, beta, loop decision.

@@ -48,32 +48,51 @@ struct RecMeta {
   std::int32_t cam[kTile];              // camera of each slot (padding: 0); read only when nu > kXsCams
 };
 static_assert(sizeof(RecMeta) % 16 == 0, "record metadata must keep 16-byte alignment");
+// Coupling-block storage per slot, the L lanes of a chunk record:
+//   kLanesFact = 18  factored (the product path): G = sqrt(w) Jc, the
+//       edge's 2x9 camera Jacobian scaled by sqrt(w), lanes r * 9 + k. The
+//       reference's block E = w Jc^T Jp (dba/block_matrix.hpp:380-381) is
+//       E = G^T Gt R with Gt = G[:, 3:6] (dr/dt = dr/dP) and R = dP/dX the
+//       camera's rotation matrix (one per camera, Rank::Rm_), since
+//       Jp = dr/dP R. E^T x = R^T Gt^T (G x), E b = G^T Gt (R b): 18 scalars
+//       per edge instead of 27 (1/3 fewer bytes on the DSE stream), fewer
+//       registers, every product the reference forms (rounding-level
+//       reassociation only). This is the implicit-Schur storage of the
+//       Jacobian blocks (cf. Ceres' ImplicitSchurComplement), here with Jp
+//       folded into the camera's R.
+//   kLanesDense = 27  the 9x3 block itself, row-major (i * 3 + j): used for
+//       caller-fabricated blocks (Rank::set_system, any 9x3 E).
+constexpr int kLanesFact = 18;
+constexpr int kLanesDense = 27;
+
 // Bytes of a record the pass reads for a chunk with at most kPfParts
 // distinct cameras: the E lanes and the metadata up to upart[kPfParts)
 // (cam[] and the rest of upart[] are read only by rarer chunks).
 constexpr int kPfParts = 16;
-template <class S>
+template <class S, int L = kLanesFact>
 constexpr unsigned rec_hot_bytes() {
-  return unsigned(27 * kTile * sizeof(S) + offsetof(RecMeta, upart) + kPfParts * sizeof(std::int32_t));
+  return unsigned(L * kTile * sizeof(S) + offsetof(RecMeta, upart) + kPfParts * sizeof(std::int32_t));
 }
 static_assert(rec_hot_bytes<double>() % 16 == 0 && rec_hot_bytes<float>() % 16 == 0, "bulk prefetch size");
+static_assert(rec_hot_bytes<double, kLanesDense>() % 16 == 0 && rec_hot_bytes<float, kLanesDense>() % 16 == 0,
+              "bulk prefetch size");
 
-// E chunk record: 27 lanes x kTile slots (lane-major) then RecMeta; one
+// E chunk record: L lanes x kTile slots (lane-major) then RecMeta; one
 // record per 128-slot chunk of the device slot order.
-template <class S>
+template <class S, int L = kLanesFact>
 struct Rec {
-  static constexpr int kE = 27 * kTile;
+  static constexpr int kE = L * kTile;
   static constexpr int kMeta = int(sizeof(RecMeta) / sizeof(S));
   static constexpr int kLen = kE + kMeta;
   static constexpr int kBytes = kLen * int(sizeof(S));
 };
 
-// Offset of E(k, slot s) inside the record array.
-template <class S>
-__device__ __forceinline__ std::size_t rec_at(const std::int32_t* slot_chunk, const std::int32_t* chunk_slot,
-                                              std::int64_t s) {
+// Offset of lane 0 of slot s inside the record array.
+template <class S, int L = kLanesFact>
+__host__ __device__ __forceinline__ std::size_t rec_at(const std::int32_t* slot_chunk, const std::int32_t* chunk_slot,
+                                                       std::int64_t s) {
   const std::int32_t c = slot_chunk[s];
-  return std::size_t(c) * Rec<S>::kLen + std::size_t(s - chunk_slot[c]);
+  return std::size_t(c) * Rec<S, L>::kLen + std::size_t(s - chunk_slot[c]);
 }
 
 template <int BS>
@@ -232,7 +251,7 @@ __global__ void k_residuals(std::int64_t N, const std::int32_t* __restrict__ slo
 // ---------------------------------------------------------- linearize ----
 // Fused K1+K2(+K3)+K5-E: gather, jets (or closed form), residual, Jacobian,
 // E = w Jc^T Jp. Jb row: [r0 r1 | J0[12] | J1[12] | w pad].
-template <class S, int MODE, class T = S>
+template <class S, int MODE, class T = S, int L = kLanesFact>
 __global__ void __launch_bounds__(128) k_linearize(std::int64_t s0, std::int64_t s1,
                                                    const std::int32_t* __restrict__ slot_cam,
                                                    const std::int32_t* __restrict__ slot_pt,
@@ -269,12 +288,84 @@ __global__ void __launch_bounds__(128) k_linearize(std::int64_t s0, std::int64_t
   }
   row[26] = wt;
   row[27] = S(0);
-  const std::size_t base = rec_at<T>(slot_chunk, chunk_slot, s);
+  const std::size_t base = rec_at<T, L>(slot_chunk, chunk_slot, s);
+  if constexpr (L == kLanesFact) {  // G = sqrt(w) Jc (exact copy for unit weights)
+    const S sw = wt == S(1) ? S(1) : sqrt(wt);
 #pragma unroll
-  for (int i = 0; i < 9; ++i)
+    for (int r = 0; r < 2; ++r)
 #pragma unroll
-    for (int j = 0; j < 3; ++j)
-      E[base + std::size_t(i * 3 + j) * kTile] = T(fm(wt, fa(fm(J[0][i], J[0][9 + j]), fm(J[1][i], J[1][9 + j]))));
+      for (int k = 0; k < 9; ++k) E[base + std::size_t(r * 9 + k) * kTile] = T(fm(sw, J[r][k]));
+  } else {
+#pragma unroll
+    for (int i = 0; i < 9; ++i)
+#pragma unroll
+      for (int j = 0; j < 3; ++j)
+        E[base + std::size_t(i * 3 + j) * kTile] = T(fm(wt, fa(fm(J[0][i], J[0][9 + j]), fm(J[1][i], J[1][9 + j]))));
+  }
+}
+
+// R(aa) = c I + s1 [aa]x + c2 aa aa^T per camera (row-major, 9m), with the
+// model's coefficients (dba/problem.hpp:89-118, Taylor branch included):
+// dP/dX of the Snavely model, the factor that turns the stored dr/dt into
+// Jp = dr/dP R (factored coupling records).
+template <class S>
+__global__ void k_cam_rotations(std::int32_t m, const S* __restrict__ xc, S* __restrict__ Rm) {
+  const std::int32_t c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= m) return;
+  const S a0 = xc[std::size_t(c) * 9], a1 = xc[std::size_t(c) * 9 + 1], a2 = xc[std::size_t(c) * 9 + 2];
+  const S t = fa(fa(fm(a0, a0), fm(a1, a1)), fm(a2, a2));
+  S cs, s1, c2;
+  rot_coeffs(t, cs, s1, c2);
+  const S a[3] = {a0, a1, a2};
+  const S k[3][3] = {{S(0), -a2, a1}, {a2, S(0), -a0}, {-a1, a0, S(0)}};
+  S* o = Rm + std::size_t(c) * 9;
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) o[i * 3 + j] = fa(fa(i == j ? cs : S(0), fm(s1, k[i][j])), fm(c2, fm(a[i], a[j])));
+}
+
+// E^T x (a 3-vector) and E b (a 9-vector) of one slot for either record
+// layout: e = the slot's L lanes, Rc = its camera's R (factored only).
+template <class S, int L>
+__device__ __forceinline__ void coupling_t(const S* e, const S* Rc, const S* xv, S* a) {
+  if constexpr (L == kLanesFact) {
+    S u0 = S(0), u1 = S(0);
+#pragma unroll
+    for (int k = 0; k < 9; ++k) {
+      u0 += e[k] * xv[k];
+      u1 += e[9 + k] * xv[k];
+    }
+    S h[3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) h[i] = e[3 + i] * u0 + e[12 + i] * u1;
+#pragma unroll
+    for (int j = 0; j < 3; ++j) a[j] = (Rc[j] * h[0] + Rc[3 + j] * h[1]) + Rc[6 + j] * h[2];
+  } else {
+#pragma unroll
+    for (int j = 0; j < 3; ++j) a[j] = S(0);
+#pragma unroll
+    for (int i = 0; i < 9; ++i) {
+      a[0] += e[i * 3 + 0] * xv[i];
+      a[1] += e[i * 3 + 1] * xv[i];
+      a[2] += e[i * 3 + 2] * xv[i];
+    }
+  }
+}
+template <class S, int L>
+__device__ __forceinline__ void coupling_b(const S* e, const S* Rc, S b0, S b1, S b2, S* y) {
+  if constexpr (L == kLanesFact) {
+    S g[3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) g[i] = (Rc[i * 3] * b0 + Rc[i * 3 + 1] * b1) + Rc[i * 3 + 2] * b2;
+    const S v0 = (e[3] * g[0] + e[4] * g[1]) + e[5] * g[2];
+    const S v1 = (e[12] * g[0] + e[13] * g[1]) + e[14] * g[2];
+#pragma unroll
+    for (int k = 0; k < 9; ++k) y[k] = e[k] * v0 + e[9 + k] * v1;
+  } else {
+#pragma unroll
+    for (int i = 0; i < 9; ++i) y[i] = (e[i * 3] * b0 + e[i * 3 + 1] * b1) + e[i * 3 + 2] * b2;
+  }
 }
 
 // C[p] += w Jp^T Jp, w[p] -= w Jp^T r over the point's slots in edge order
@@ -577,12 +668,13 @@ struct PcgScal {
 // ----------------------------------------------------- DSE camera side ----
 // Halo slots after the all-reduce of their points' a_p: b_p = C_p^-1 a_p,
 // y_s = E_s b_p into the slot's own partial.
-template <class S, class T = S>
+template <class S, class T = S, int L = kLanesFact>
 __global__ void k_halo_fix(std::int32_t n, const std::int32_t* __restrict__ halo_slot,
                            const std::int32_t* __restrict__ slot_dpt, const std::int32_t* __restrict__ halo_of,
                            const S* __restrict__ halo_buf, const S* __restrict__ Cinv, const T* __restrict__ E,
                            const std::int32_t* __restrict__ slot_chunk, const std::int32_t* __restrict__ chunk_slot,
-                           const std::int32_t* __restrict__ halo_pos, S* __restrict__ part) {
+                           const std::int32_t* __restrict__ halo_pos, S* __restrict__ part,
+                           const std::int32_t* __restrict__ slot_cam, const S* __restrict__ Rm) {
   const std::int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const std::int32_t s = halo_slot[i];
@@ -591,11 +683,13 @@ __global__ void k_halo_fix(std::int32_t n, const std::int32_t* __restrict__ halo
 #pragma unroll
   for (int j = 0; j < 3; ++j) b[j] = halo_buf[std::size_t(halo_of[p]) * 3 + j];
   llt_solve<S, 3>(Cinv + std::size_t(p) * 9, b);
-  const T* e = E + rec_at<T>(slot_chunk, chunk_slot, s);
+  const T* ep = E + rec_at<T, L>(slot_chunk, chunk_slot, s);
+  S e[L], y[9];
 #pragma unroll
-  for (int r = 0; r < 9; ++r)
-    part[std::size_t(halo_pos[i]) * 9 + r] =
-        (S(e[(r * 3) * kTile]) * b[0] + S(e[(r * 3 + 1) * kTile]) * b[1]) + S(e[(r * 3 + 2) * kTile]) * b[2];
+  for (int k = 0; k < L; ++k) e[k] = S(ep[std::size_t(k) * kTile]);
+  coupling_b<S, L>(e, L == kLanesFact ? Rm + std::size_t(slot_cam[s]) * 9 : nullptr, b[0], b[1], b[2], y);
+#pragma unroll
+  for (int r = 0; r < 9; ++r) part[std::size_t(halo_pos[i]) * 9 + r] = y[r];
 }
 
 // Point rows between global order and device-point order:

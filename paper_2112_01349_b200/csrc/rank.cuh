@@ -238,7 +238,7 @@ class Rank {
     z.red = std::max<std::size_t>(8 * dev::kRedBlocksMax, 2 * (z.m * 32 / 256 + 64));
     z.cm = z.m * 9;
     z.pl = z.n_loc * 3;
-    z.recs = static_cast<std::size_t>(std::max<std::size_t>(d.chunk_slot.size(), 1)) * dev::Rec<T>::kLen;
+    z.recs = static_cast<std::size_t>(std::max<std::size_t>(d.chunk_slot.size(), 1)) * dev::Rec<T, dev::kLanesFact>::kLen;
     z.n_long = 0;
     for (std::size_t t = 0; t + 1 < d.tile_chunk.size(); ++t) z.n_long += d.tile_chunk[t + 1] - d.tile_chunk[t] > 1;
     z.xp_full = static_cast<std::size_t>(pl.n) * 3;
@@ -277,7 +277,7 @@ class Rank {
     f(&Rank::halo_buf_, z.halo);
     f(&Rank::red_part_, z.red);
     for (auto pm : {&Rank::xc_, &Rank::xct_, &Rank::dxc_, &Rank::v_, &Rank::g_, &Rank::r_, &Rank::z_, &Rank::p_,
-                    &Rank::q_, &Rank::ctmp_, &Rank::p2_})
+                    &Rank::q_, &Rank::ctmp_, &Rank::p2_, &Rank::Rm_})
       f(pm, z.cm);
     for (auto pm : {&Rank::xp_, &Rank::xpt_, &Rank::dxp_, &Rank::w_}) f(pm, z.pl);
     for (auto pm : {&Rank::B_, &Rank::Bd_, &Rank::Binv_, &Rank::Bexp_}) f(pm, z.cm * 9);
@@ -362,6 +362,13 @@ class Rank {
     }
     owned_h_ = owned;
     n_halo_loc_ = static_cast<std::int32_t>(hl.size());
+    {  // points no edge observes: no rank holds them; they keep their x0
+      std::vector<std::uint8_t> seen(static_cast<std::size_t>(p.num_points), 0);
+      for (std::int64_t e = 0; e < p.num_observations; ++e) seen[static_cast<std::size_t>(p.point_id[e])] = 1;
+      orphans_.clear();
+      for (std::int32_t q = 0; q < p.num_points; ++q)
+        if (!seen[static_cast<std::size_t>(q)]) orphans_.push_back(q);
+    }
     // the whole shard in one pool allocation, sized before any copy
     const ShardSizes z = shard_sizes(plan_, lay_);
     pool_.reserve(predict_bytes(z));
@@ -420,7 +427,8 @@ class Rank {
     halo_dpt_.copy_in(hl);
     halo_idx_.copy_in(hi);
     DBAG_CUDA(cudaMemset(g_bar_.get(), 0, sizeof(unsigned long long)));
-    build_records(s_cam);
+    fact_ = true;
+    E_.copy_in(build_records<dev::kLanesFact>(s_cam));
     set_state(static_cast<const S*>(p.cameras), static_cast<const S*>(p.points));
     have_system_ = false;
   }
@@ -431,6 +439,9 @@ class Rank {
   // order there.
   void set_state(const S* xc, const S* xp) {
     DBAG_CUDA(cudaSetDevice(device_));
+    orphan_x_.resize(orphans_.size() * 3);
+    for (std::size_t i = 0; i < orphans_.size(); ++i)
+      for (int k = 0; k < 3; ++k) orphan_x_[i * 3 + k] = xp[static_cast<std::size_t>(orphans_[i]) * 3 + k];
     DBAG_CUDA(cudaMemcpyAsync(xc_.get(), xc, sizeof(S) * 9 * static_cast<std::size_t>(m_), cudaMemcpyHostToDevice, st_));
     const std::size_t full = static_cast<std::size_t>(n_glob_) * 3;
     if (xp_full_.size() < std::max<std::size_t>(full, 1)) xp_full_.alloc(std::max<std::size_t>(full, 1));
@@ -496,7 +507,10 @@ class Rank {
     DBAG_CUDA(cudaMemsetAsync(B_.get(), 0, B_.size() * sizeof(S), st_));
     DBAG_CUDA(cudaMemsetAsync(v_.get(), 0, v_.size() * sizeof(S), st_));
     if (jb_pt_.size() > 2) DBAG_CUDA(cudaMemsetAsync(carry_.get(), 0, carry_.size() * sizeof(double), st_));
-    auto kern = jac_mode_ == 1 ? dev::k_linearize<S, 1, T> : dev::k_linearize<S, 0, T>;
+    use_factored();
+    if (m_ > 0)  // the cameras' R at the linearization point (factored records)
+      launch(dev::k_cam_rotations<S>, grid_for(m_, 128, 1 << 30), 128, m_, static_cast<const S*>(xc_.get()), Rm_.get());
+    auto kern = jac_mode_ == 1 ? dev::k_linearize<S, 1, T, dev::kLanesFact> : dev::k_linearize<S, 0, T, dev::kLanesFact>;
     const int nb = static_cast<int>(jb_pt_.size()) - 1;
     for (int b = 0; b < nb && N_ > 0; ++b) {  // one Jb batch of whole points at a time
       const std::int32_t d0 = jb_pt_[static_cast<std::size_t>(b)], d1 = jb_pt_[static_cast<std::size_t>(b) + 1];
@@ -708,13 +722,11 @@ class Rank {
     for (;;) {
       for (int u = 0; u < kRunAhead; ++u, ++passes) {
         if (H_ > 0) DBAG_CUDA(cudaMemsetAsync(halo_buf_.get(), 0, sizeof(S) * 3 * static_cast<std::size_t>(H_), st_));
-        launch(dev::k_g_pass<S, T>, n_long_ + n_chunks_, dev::kTile, A, B, csc);
+        if (fact_) launch(dev::k_g_pass<S, T, dev::kLanesFact>, n_long_ + n_chunks_, dev::kTile, A, B, csc);
+        else launch(dev::k_g_pass<S, T, dev::kLanesDense>, n_long_ + n_chunks_, dev::kTile, A, B, csc);
         if (H_ > 0) {
           comm_->allreduce_sum(halo_buf_.get(), 3 * H_, kT, st_);
-          if (nh > 0)
-            launch(dev::k_halo_fix<S, T>, grid_for(nh, 128, 1 << 30), 128, nh, halo_slot_.get(), slot_dpt_.get(),
-                   halo_of_.get(), static_cast<const S*>(halo_buf_.get()), static_cast<const S*>(Cinv_.get()),
-                   static_cast<const T*>(E_.get()), slot_chunk_.get(), chunk_slot_.get(), halo_pos_.get(), part_.get());
+          if (nh > 0) halo_fix(nh);
         }
         cam_reduce<0>(nullptr, ctmp_.get());
         comm_->allreduce_sum(ctmp_.get(), static_cast<std::int64_t>(m_) * 9, kT, st_);
@@ -865,7 +877,8 @@ class Rank {
     g_unroll_ = DBAG_GRAPH_UNROLL;
     if (const char* ue = std::getenv("DBAG_UNROLL")) g_unroll_ = std::max(1, std::atoi(ue));
     for (int u = 0; u < g_unroll_; ++u) {
-      void* pass = reinterpret_cast<void*>(dev::k_g_pass<S, T>);
+      void* pass = fact_ ? reinterpret_cast<void*>(dev::k_g_pass<S, T, dev::kLanesFact>)
+                         : reinterpret_cast<void*>(dev::k_g_pass<S, T, dev::kLanesDense>);
       const int pgrid = n_long_ + n_chunks_;
       const int psmem = 0;
       cur = u ? add_kernel_pdl(body, cur, pass, pgrid, dev::kTile, a_pass, psmem)
@@ -890,10 +903,11 @@ class Rank {
                            a_step);
     }
     DBAG_CUDA(cudaGraphInstantiate(&g_exec_, g_graph_, 0));
+    g_fact_ = fact_;
   }
 
   PcgOut pcg_graph(double tol, int max_iters) {
-    if (!g_exec_) build_graph();
+    if (!g_exec_ || g_fact_ != fact_) build_graph();
     dev::GScal<S> init{};
     init.tol = tol;
     init.max_iters = max_iters;
@@ -963,7 +977,10 @@ class Rank {
     cudaEvent_t e0, e1;
     DBAG_CUDA(cudaEventCreate(&e0));
     DBAG_CUDA(cudaEventCreate(&e1));
-    auto one = [&] { launch(dev::k_g_pass<S, T>, grid, dev::kTile, A, B, sc); };
+    auto one = [&] {
+      if (fact_) launch(dev::k_g_pass<S, T, dev::kLanesFact>, grid, dev::kTile, A, B, sc);
+      else launch(dev::k_g_pass<S, T, dev::kLanesDense>, grid, dev::kTile, A, B, sc);
+    };
     one();  // warm-up
     DBAG_CUDA(cudaEventRecord(e0, st_));
     for (int r = 0; r < reps; ++r) one();
@@ -1030,6 +1047,9 @@ class Rank {
     comm_->allreduce_sum(xp_full_.get(), static_cast<std::int64_t>(full), kT, st_);
     if (xp) DBAG_CUDA(cudaMemcpyAsync(xp, xp_full_.get(), sizeof(S) * full, cudaMemcpyDeviceToHost, st_));
     DBAG_CUDA(cudaStreamSynchronize(st_));
+    if (xp)  // unobserved points: unchanged since set_state (the reference never moves them)
+      for (std::size_t i = 0; i < orphans_.size(); ++i)
+        for (int k = 0; k < 3; ++k) xp[static_cast<std::size_t>(orphans_[i]) * 3 + k] = orphan_x_[i * 3 + k];
   }
 
   void model_terms(double* step_inf, double* damp, double* gv) const {
@@ -1129,12 +1149,35 @@ class Rank {
       if (w) std::copy(ww.begin() + d * 3, ww.begin() + d * 3 + 3, w + g * 3);
     }
     if (E) {
-      std::vector<T> e(E_.size());
-      DBAG_CUDA(cudaMemcpy(e.data(), E_.get(), sizeof(T) * e.size(), cudaMemcpyDeviceToHost));
-      for (std::int64_t s = 0; s < N_; ++s) {
-        const std::int64_t ed = lay_.slot_edge[static_cast<std::size_t>(s)];
-        const std::size_t at = rec_offset(s);
-        for (int k = 0; k < 27; ++k) E[ed * 27 + k] = S(e[at + static_cast<std::size_t>(k) * dev::kTile]);
+      std::vector<std::int32_t> scam(static_cast<std::size_t>(N_));
+      if (N_ > 0)
+        DBAG_CUDA(cudaMemcpy(scam.data(), slot_cam_.get(), sizeof(std::int32_t) * scam.size(), cudaMemcpyDeviceToHost));
+      if (fact_) {  // E = G^T Gt R (kernels.cuh kLanesFact)
+        std::vector<T> e(E_.size());
+        std::vector<S> R(static_cast<std::size_t>(m_) * 9);
+        DBAG_CUDA(cudaMemcpy(e.data(), E_.get(), sizeof(T) * e.size(), cudaMemcpyDeviceToHost));
+        DBAG_CUDA(cudaMemcpy(R.data(), Rm_.get(), sizeof(S) * R.size(), cudaMemcpyDeviceToHost));
+        for (std::int64_t s = 0; s < N_; ++s) {
+          const std::int64_t ed = lay_.slot_edge[static_cast<std::size_t>(s)];
+          const std::size_t at = rec_offset<dev::kLanesFact>(s);
+          double g[18];
+          for (int k = 0; k < 18; ++k) g[k] = double(e[at + static_cast<std::size_t>(k) * dev::kTile]);
+          const S* Rc = R.data() + static_cast<std::size_t>(scam[static_cast<std::size_t>(s)]) * 9;
+          double jp[2][3];
+          for (int r = 0; r < 2; ++r)
+            for (int j = 0; j < 3; ++j)
+              jp[r][j] = g[r * 9 + 3] * double(Rc[j]) + g[r * 9 + 4] * double(Rc[3 + j]) + g[r * 9 + 5] * double(Rc[6 + j]);
+          for (int i = 0; i < 9; ++i)
+            for (int j = 0; j < 3; ++j) E[ed * 27 + i * 3 + j] = S(g[i] * jp[0][j] + g[9 + i] * jp[1][j]);
+        }
+      } else {
+        std::vector<T> e(Edense_.size());
+        DBAG_CUDA(cudaMemcpy(e.data(), Edense_.get(), sizeof(T) * e.size(), cudaMemcpyDeviceToHost));
+        for (std::int64_t s = 0; s < N_; ++s) {
+          const std::int64_t ed = lay_.slot_edge[static_cast<std::size_t>(s)];
+          const std::size_t at = rec_offset<dev::kLanesDense>(s);
+          for (int k = 0; k < 27; ++k) E[ed * 27 + k] = S(e[at + static_cast<std::size_t>(k) * dev::kTile]);
+        }
       }
     }
   }
@@ -1158,22 +1201,27 @@ class Rank {
       DBAG_CUDA(cudaMemcpy(C_.get(), c.data(), sizeof(S) * c.size(), cudaMemcpyHostToDevice));
       DBAG_CUDA(cudaMemcpy(w_.get(), ww.data(), sizeof(S) * ww.size(), cudaMemcpyHostToDevice));
     }
-    if (E_table) {
-      std::vector<T> e(E_.size());
-      DBAG_CUDA(cudaMemcpy(e.data(), E_.get(), sizeof(T) * e.size(), cudaMemcpyDeviceToHost));
+    if (E_table) {  // arbitrary 9x3 blocks: the dense record layout from here on
+      std::vector<std::int32_t> scam(static_cast<std::size_t>(N_));
+      if (N_ > 0)
+        DBAG_CUDA(cudaMemcpy(scam.data(), slot_cam_.get(), sizeof(std::int32_t) * scam.size(), cudaMemcpyDeviceToHost));
+      std::vector<T> e = build_records<dev::kLanesDense>(scam);
       for (std::int64_t s = 0; s < N_; ++s) {
         const std::int64_t ed = plan_.range.start + lay_.slot_edge[static_cast<std::size_t>(s)];
-        const std::size_t at = rec_offset(s);
+        const std::size_t at = rec_offset<dev::kLanesDense>(s);
         for (int k = 0; k < 27; ++k) e[at + static_cast<std::size_t>(k) * dev::kTile] = T(E_table[ed * 27 + k]);
       }
-      DBAG_CUDA(cudaMemcpy(E_.get(), e.data(), sizeof(T) * e.size(), cudaMemcpyHostToDevice));
+      if (Edense_.size() != e.size()) Edense_.alloc(e.size());
+      Edense_.copy_in(e);
+      fact_ = false;
     }
     have_system_ = true;
   }
 
+  template <int L>
   std::size_t rec_offset(std::int64_t s) const {
     const std::int32_t c = lay_.slot_chunk[static_cast<std::size_t>(s)];
-    return static_cast<std::size_t>(c) * dev::Rec<T>::kLen +
+    return static_cast<std::size_t>(c) * dev::Rec<T, L>::kLen +
            static_cast<std::size_t>(s - lay_.chunk_slot[static_cast<std::size_t>(c)]);
   }
 
@@ -1287,10 +1335,7 @@ class Rank {
     const std::int32_t nh = static_cast<std::int32_t>(lay_.halo_slot.size());
     if (MODE == 0 && H_ > 0) {
       comm_->allreduce_sum(halo_buf_.get(), 3 * H_, kT, st_);
-      if (nh > 0)
-        launch(dev::k_halo_fix<S, T>, grid_for(nh, 128, 1 << 30), 128, nh, halo_slot_.get(), slot_dpt_.get(),
-               halo_of_.get(), static_cast<const S*>(halo_buf_.get()), static_cast<const S*>(Cinv_.get()),
-               static_cast<const T*>(E_.get()), slot_chunk_.get(), chunk_slot_.get(), halo_pos_.get(), part_.get());
+      if (nh > 0) halo_fix(nh);
     } else if (MODE == 2 && nh > 0) {
       // rhs: C and w are complete on every rank, so the chunk partials
       // already hold the halo slots' E_s C^-1 w; the halo slots' own
@@ -1301,11 +1346,13 @@ class Rank {
     }
   }
 
-  // E chunk records: zero E lanes plus each chunk's static metadata
-  // (kernels.cuh RecMeta); the E lanes are (re)written by k_linearize.
-  void build_records(const std::vector<std::int32_t>& s_cam) {
+  // E chunk records of L lanes (kernels.cuh kLanesFact / kLanesDense): zero
+  // lanes plus each chunk's static metadata (RecMeta); the lanes are
+  // (re)written by k_linearize (factored) or set_system (dense).
+  template <int L>
+  std::vector<T> build_records(const std::vector<std::int32_t>& s_cam) {
     const std::size_t nc = static_cast<std::size_t>(std::max(n_chunks_, 1));
-    std::vector<T> recs(nc * dev::Rec<T>::kLen, T(0));
+    std::vector<T> recs(nc * dev::Rec<T, L>::kLen, T(0));
     std::vector<std::int32_t> long_first;
     const std::size_t nt = lay_.tile_pt.size() - 1;
     for (std::size_t t = 0; t < nt; ++t) {
@@ -1314,8 +1361,8 @@ class Rank {
       const std::int32_t ch0 = lay_.tile_chunk[t], ch1 = lay_.tile_chunk[t + 1];
       if (ch1 - ch0 > 1) long_first.push_back(ch0);
       for (std::int32_t c = ch0; c < ch1; ++c) {
-        auto* M = reinterpret_cast<dev::RecMeta*>(recs.data() + static_cast<std::size_t>(c) * dev::Rec<T>::kLen +
-                                                  dev::Rec<T>::kE);
+        auto* M = reinterpret_cast<dev::RecMeta*>(recs.data() + static_cast<std::size_t>(c) * dev::Rec<T, L>::kLen +
+                                                  dev::Rec<T, L>::kE);
         const std::int32_t c0 = lay_.chunk_slot[static_cast<std::size_t>(c)];
         const std::int32_t c1 = (c + 1 < ch1) ? lay_.chunk_slot[static_cast<std::size_t>(c) + 1]
                                               : lay_.dpt_ptr[static_cast<std::size_t>(p1)];
@@ -1350,19 +1397,36 @@ class Rank {
           }
       }
     }
-    E_.copy_in(recs);
     n_long_ = static_cast<std::int32_t>(long_first.size());
     long_chunk_.copy_in(long_first);
     std::vector<std::int32_t> hpos(lay_.halo_slot.size());
     for (std::size_t i = 0; i < hpos.size(); ++i)
       hpos[i] = lay_.part_pos[static_cast<std::size_t>(n_chunk_part_) + i];
     halo_pos_.copy_in(hpos);
+    return recs;
+  }
+
+  // Back to the factored records (linearize writes them); the graph is
+  // rebuilt for the record layout on its next use.
+  void use_factored() { fact_ = true; }
+
+  void halo_fix(std::int32_t nh) {
+    if (fact_)
+      launch(dev::k_halo_fix<S, T, dev::kLanesFact>, grid_for(nh, 128, 1 << 30), 128, nh, halo_slot_.get(),
+             slot_dpt_.get(), halo_of_.get(), static_cast<const S*>(halo_buf_.get()), static_cast<const S*>(Cinv_.get()),
+             static_cast<const T*>(E_.get()), slot_chunk_.get(), chunk_slot_.get(), halo_pos_.get(), part_.get(),
+             static_cast<const std::int32_t*>(slot_cam_.get()), static_cast<const S*>(Rm_.get()));
+    else
+      launch(dev::k_halo_fix<S, T, dev::kLanesDense>, grid_for(nh, 128, 1 << 30), 128, nh, halo_slot_.get(),
+             slot_dpt_.get(), halo_of_.get(), static_cast<const S*>(halo_buf_.get()), static_cast<const S*>(Cinv_.get()),
+             static_cast<const T*>(Edense_.get()), slot_chunk_.get(), chunk_slot_.get(), halo_pos_.get(), part_.get(),
+             static_cast<const std::int32_t*>(slot_cam_.get()), static_cast<const S*>(Rm_.get()));
   }
 
   dev::DseArgs<S, T> dse_args(const S* x) {
     dev::DseArgs<S, T> a;
     a.n_chunks = n_chunks_;
-    a.rec = E_.get();
+    a.rec = fact_ ? E_.get() : Edense_.get();
     a.x = x;
     a.Cinv = Cinv_.get();
     a.w = w_.get();
@@ -1373,6 +1437,7 @@ class Rank {
     a.long_chunk = long_chunk_.get();
     a.n_long = n_long_;
     a.pf_dist = pf_dist();
+    a.Rm = Rm_.get();
     return a;
   }
 
@@ -1385,7 +1450,8 @@ class Rank {
         pf_dist_ = std::max(0, std::atoi(e));
       } else {
         int per_sm = 0, sms = 0;
-        DBAG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dev::k_g_pass<S, T>, dev::kTile, 0));
+        DBAG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dev::k_g_pass<S, T, dev::kLanesFact>,
+                                                                 dev::kTile, 0));
         DBAG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device_));
         pf_dist_ = per_sm * sms;
       }
@@ -1397,8 +1463,13 @@ class Rank {
   void stream_pass(const S* x) {
     if (n_chunks_ == 0) return;
     const dev::DseArgs<S, T> a = dse_args(x);
-    launch(dev::k_dse_chunk<S, MODE, T>, n_chunks_, dev::kTile, a);
-    if (n_long_ > 0) launch(dev::k_dse_long<S, MODE, T>, n_long_, dev::kTile, a);
+    if (fact_) {
+      launch(dev::k_dse_chunk<S, MODE, T, dev::kLanesFact>, n_chunks_, dev::kTile, a);
+      if (n_long_ > 0) launch(dev::k_dse_long<S, MODE, T, dev::kLanesFact>, n_long_, dev::kTile, a);
+    } else {
+      launch(dev::k_dse_chunk<S, MODE, T, dev::kLanesDense>, n_chunks_, dev::kTile, a);
+      if (n_long_ > 0) launch(dev::k_dse_long<S, MODE, T, dev::kLanesDense>, n_long_, dev::kTile, a);
+    }
   }
 
   template <int EPI>
@@ -1500,6 +1571,8 @@ class Rank {
   double prof_point_ms_ = 0, prof_cam_ms_ = 0;
   std::vector<std::int32_t> dpt_glob_;
   std::vector<std::uint8_t> owned_h_;
+  std::vector<std::int32_t> orphans_;  // global ids of points no edge observes
+  std::vector<S> orphan_x_;            // their state (set_state)
 
   Arena pool_;  // declared first: destroyed after the buffers carved from it
   DevBuf<std::int32_t> slot_cam_, slot_dpt_, slot_edge_, dpt_ptr_, chunk_slot_, cam_part_ptr_, halo_slot_, slot_chunk_,
@@ -1526,7 +1599,10 @@ class Rank {
   std::int32_t pf_dist_ = -1;
   std::vector<std::int32_t> jb_ncam_;  // cameras each Jb batch touches
   DevBuf<std::int32_t> cam_list_;      // ... their local ids, m_loc per batch
-  DevBuf<T> E_;  // chunk records: E lanes (T) + RecMeta
+  DevBuf<T> E_;       // chunk records: factored lanes G = sqrt(w) Jc (T) + RecMeta (pool)
+  DevBuf<T> Edense_;  // 9x3-block records for caller-fabricated E (set_system; outside the pool)
+  DevBuf<S> Rm_;      // per-camera R at the linearization point (factored records)
+  bool fact_ = true, g_fact_ = true;
   DevBuf<Scal> sc_;
   DevBuf<double> red_part_, dsc_, bounce_;
   DevBuf<unsigned> red_cnt_;

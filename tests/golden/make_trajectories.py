@@ -23,10 +23,10 @@ from oracle import oracle as O  # noqa: E402
 
 SHAPES = {"ladybug-49": (49, 7776, 31843), "trafalgar-257": (257, 65132, 225911)}
 RUNS = {  # name -> (shape, dtype, K values)
-    "ladybug-49/f64": ("ladybug-49", np.float64, (1, 2, 4, 8)),
-    "ladybug-49/f32": ("ladybug-49", np.float32, (1, 2, 4, 8)),
-    "trafalgar-257/f64": ("trafalgar-257", np.float64, (1, 2, 4, 8)),
-    "trafalgar-257/f32": ("trafalgar-257", np.float32, (1, 2, 4, 8)),
+    "ladybug-49/f64": ("ladybug-49", np.float64, (1, 2, 3, 4, 5, 6, 7, 8)),
+    "ladybug-49/f32": ("ladybug-49", np.float32, (1, 2, 3, 4, 5, 6, 7, 8)),
+    "trafalgar-257/f64": ("trafalgar-257", np.float64, (1, 2, 3, 4, 5, 6, 7, 8)),
+    "trafalgar-257/f32": ("trafalgar-257", np.float32, (1, 2, 3, 4, 5, 6, 7, 8)),
 }
 OUT = os.path.join(os.path.dirname(os.path.abspath(__file__)), "trajectories.json")
 

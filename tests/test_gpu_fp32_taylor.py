@@ -41,8 +41,8 @@ def test_fp32_linearize_matches_fp32_oracle(mode):
     assert res.dtype == np.float32 and r0.dtype == np.float32
     px, py = p.arrays()[4:6]
     for e in range(res.shape[1]):
-        # r = projection - pixel cancels: float ulps scale with |pixel| (~500)
-        scale = max(1.0, float(np.hypot(px[e], py[e])))
+        # r = projection - pixel cancels: float ulps scale with |projection|
+        scale = max(1.0, float(np.hypot(px[e], py[e])), float(np.linalg.norm(r0[:, e])))
         assert np.linalg.norm(res[:, e] - r0[:, e]) <= F32_LIN * scale
         assert np.linalg.norm(jac[:, :, e] - j0[:, :, e]) <= F32_LIN * max(1.0, np.linalg.norm(j0[:, :, e]))
 

@@ -15,12 +15,15 @@ def ladybug():
     return dba.generate_synthetic(dba.SyntheticOptions(cameras=49, points=7776, num_observations=31843, seed=1))
 
 
+LANES = 18  # factored coupling records: G = sqrt(w) Jc per slot (kernels.cuh kLanesFact)
+
+
 def _floor_bytes(p, k, rank, s, t):
     """Lower bound from the dominant per-edge arrays alone: E records
-    (27 lanes of t bytes per slot), the assembly rows (28 s per edge), the
+    (18 lanes of t bytes per slot), the assembly rows (28 s per edge), the
     slot arrays (4 int32 + 3 scalars per edge)."""
     n_k = len(dba.partition_edges(p, k)[rank].edge_ids)
-    return n_k * (27 * t + 28 * s + 16 + 3 * s)
+    return n_k * (LANES * t + 28 * s + 16 + 3 * s)
 
 
 @pytest.mark.parametrize("k", [1, 2, 4])
@@ -42,9 +45,9 @@ def test_precision_variants_order(ladybug):
     lean = dba.predict_memory(ladybug, coupling_fp32=True)
     p32 = ladybug.astype(np.float32)
     assert lean < b64
-    # E lanes dominate the saving: 27 x 4 bytes per slot, up to chunk padding
+    # E lanes dominate the saving: 18 x 4 bytes per slot, up to chunk padding
     n = ladybug.num_observations
-    assert 27 * 4 * n <= b64 - lean < 27 * 4 * n * 1.6
+    assert LANES * 4 * n <= b64 - lean < LANES * 4 * n * 1.6
     assert dba.predict_memory(p32) < lean
 
 
