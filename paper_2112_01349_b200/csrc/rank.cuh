@@ -33,6 +33,7 @@
 #include "common.hpp"
 #include "dse.cuh"
 #include "graph_pcg.cuh"
+#include "stream.cuh"
 #include "kernels.cuh"
 #include "partition.hpp"
 
@@ -124,7 +125,7 @@ class DevBuf {
 // host-side partition plan and device layout alone.
 struct ShardSizes {
   std::size_t N, slots, dpt_ptr, chunk_slot, cam_part_ptr, halo_slot, part, cam_ptr, cam_glob, n_loc, n_halo_loc,
-      halo, red, cm, pl, recs, n_long, xp_full, m, jb, carry, cam_list, bounce;
+      halo, red, cm, pl, recs, n_long, ctab, xp_full, m, jb, carry, cam_list, bounce;
 };
 
 inline void check_problem(const dbag_problem& p) {
@@ -240,7 +241,11 @@ class Rank {
     z.pl = z.n_loc * 3;
     z.recs = static_cast<std::size_t>(std::max<std::size_t>(d.chunk_slot.size(), 1)) * dev::Rec<T, dev::kLanesFact>::kLen;
     z.n_long = 0;
-    for (std::size_t t = 0; t + 1 < d.tile_chunk.size(); ++t) z.n_long += d.tile_chunk[t + 1] - d.tile_chunk[t] > 1;
+    z.ctab = 0;
+    for (std::size_t t = 0; t + 1 < d.tile_chunk.size(); ++t) {
+      z.n_long += d.tile_chunk[t + 1] - d.tile_chunk[t] > 1;
+      z.ctab += 4 * (d.tile_chunk[t + 1] - d.tile_chunk[t] == 1);
+    }
     z.xp_full = static_cast<std::size_t>(pl.n) * 3;
     const std::vector<std::int32_t> jb = jb_batches(d.dpt_ptr);
     const std::size_t nb = jb.size() - 1;
@@ -273,6 +278,7 @@ class Rank {
     f(&Rank::owned_, z.n_loc);
     for (auto pm : {&Rank::halo_dpt_, &Rank::halo_idx_}) f(pm, z.n_halo_loc);
     f(&Rank::long_chunk_, z.n_long);
+    f(&Rank::ctab_, z.ctab);
     f(&Rank::part_, z.part);
     f(&Rank::halo_buf_, z.halo);
     f(&Rank::red_part_, z.red);
@@ -722,8 +728,7 @@ class Rank {
     for (;;) {
       for (int u = 0; u < kRunAhead; ++u, ++passes) {
         if (H_ > 0) DBAG_CUDA(cudaMemsetAsync(halo_buf_.get(), 0, sizeof(S) * 3 * static_cast<std::size_t>(H_), st_));
-        if (fact_) launch(dev::k_g_pass<S, T, dev::kLanesFact>, n_long_ + n_chunks_, dev::kTile, A, B, csc);
-        else launch(dev::k_g_pass<S, T, dev::kLanesDense>, n_long_ + n_chunks_, dev::kTile, A, B, csc);
+        launch_pass(A, B, csc);
         if (H_ > 0) {
           comm_->allreduce_sum(halo_buf_.get(), 3 * H_, kT, st_);
           if (nh > 0) halo_fix(nh);
@@ -876,13 +881,25 @@ class Rank {
     cudaGraphNode_t cur = nullptr;
     g_unroll_ = DBAG_GRAPH_UNROLL;
     if (const char* ue = std::getenv("DBAG_UNROLL")) g_unroll_ = std::max(1, std::atoi(ue));
+    const bool streamed = use_stream();
+    const dev::ChunkTab* tab = reinterpret_cast<const dev::ChunkTab*>(ctab_.get());
+    std::int32_t nn = n_norm_;
+    void* a_stream[] = {&A, &B, &csc, &tab, &nn};
     for (int u = 0; u < g_unroll_; ++u) {
       void* pass = fact_ ? reinterpret_cast<void*>(dev::k_g_pass<S, T, dev::kLanesFact>)
                          : reinterpret_cast<void*>(dev::k_g_pass<S, T, dev::kLanesDense>);
-      const int pgrid = n_long_ + n_chunks_;
-      const int psmem = 0;
-      cur = u ? add_kernel_pdl(body, cur, pass, pgrid, dev::kTile, a_pass, psmem)
-              : add_kernel(body, nullptr, pass, pgrid, dev::kTile, a_pass, psmem);
+      int pgrid = n_long_ + n_chunks_, pblock = dev::kTile, psmem = 0;
+      void** pargs = a_pass;
+      if (streamed) {
+        const StreamCfg& c = stream_cfg();
+        pass = c.fn;
+        pgrid = c.grid;
+        pblock = dev::kStreamThreads;
+        psmem = c.smem;
+        pargs = a_stream;
+      }
+      cur = u ? add_kernel_pdl(body, cur, pass, pgrid, pblock, pargs, psmem)
+              : add_kernel(body, nullptr, pass, pgrid, pblock, pargs, psmem);
       if (g_cluster_ > 0) {
         cur = add_kernel_pdl(body, cur, fsc_fn, g_cluster_, dev::kFscThreads, a_fsc);
         cudaLaunchAttributeValue cv{};
@@ -969,7 +986,6 @@ class Rank {
     const dev::DseArgs<S, T> A = dse_args(nullptr);
     const dev::GBufs<S> B = gbufs();
     const dev::GScal<S>* sc = gsc_.get();
-    const int grid = n_long_ + n_chunks_;
     dev::GScal<S> live = *gsc_h_;  // the finished solve's scalars, reopened
     live.done = 0;
     *gsc_h_ = live;
@@ -977,10 +993,7 @@ class Rank {
     cudaEvent_t e0, e1;
     DBAG_CUDA(cudaEventCreate(&e0));
     DBAG_CUDA(cudaEventCreate(&e1));
-    auto one = [&] {
-      if (fact_) launch(dev::k_g_pass<S, T, dev::kLanesFact>, grid, dev::kTile, A, B, sc);
-      else launch(dev::k_g_pass<S, T, dev::kLanesDense>, grid, dev::kTile, A, B, sc);
-    };
+    auto one = [&] { launch_pass(A, B, sc); };
     one();  // warm-up
     DBAG_CUDA(cudaEventRecord(e0, st_));
     for (int r = 0; r < reps; ++r) one();
@@ -1399,6 +1412,21 @@ class Rank {
     }
     n_long_ = static_cast<std::int32_t>(long_first.size());
     long_chunk_.copy_in(long_first);
+    {  // staged-chunk table of the streaming pass (stream.cuh ChunkTab)
+      std::vector<std::int32_t> tab;
+      for (std::size_t t = 0; t < nt; ++t) {
+        if (lay_.tile_chunk[t + 1] - lay_.tile_chunk[t] != 1) continue;
+        const std::int32_t p0 = lay_.tile_pt[t], np = lay_.tile_pt[t + 1] - p0;
+        const std::size_t b0 = static_cast<std::size_t>(p0) * 9 * sizeof(S);
+        const std::size_t nb = (b0 & 15) + static_cast<std::size_t>(std::min(np, dev::kCStage)) * 9 * sizeof(S);
+        tab.push_back(lay_.tile_chunk[t]);
+        tab.push_back(static_cast<std::int32_t>(b0 >> 4));
+        tab.push_back(static_cast<std::int32_t>((nb + 15) / 16 * 16));
+        tab.push_back(0);
+      }
+      n_norm_ = static_cast<std::int32_t>(tab.size() / 4);
+      ctab_.copy_in(tab);
+    }
     std::vector<std::int32_t> hpos(lay_.halo_slot.size());
     for (std::size_t i = 0; i < hpos.size(); ++i)
       hpos[i] = lay_.part_pos[static_cast<std::size_t>(n_chunk_part_) + i];
@@ -1421,6 +1449,58 @@ class Rank {
              slot_dpt_.get(), halo_of_.get(), static_cast<const S*>(halo_buf_.get()), static_cast<const S*>(Cinv_.get()),
              static_cast<const T*>(Edense_.get()), slot_chunk_.get(), chunk_slot_.get(), halo_pos_.get(), part_.get(),
              static_cast<const std::int32_t*>(slot_cam_.get()), static_cast<const S*>(Rm_.get()));
+  }
+
+  // ---- the persistent TMA-fed pass (stream.cuh) ----------------------------
+  // Opt-in (DBAG_STREAM=1): measured 5 % (venice FP64) to 30 % (FP32,
+  // trafalgar) slower than the one-CTA-per-chunk k_g_pass;
+  // DBAG_NST sets its stage-ring depth (2, 3 or 4; 2 measured best).
+  struct StreamCfg {
+    void* fn = nullptr;
+    int smem = 0, grid = 0;
+    bool fact = false;
+  };
+  static bool use_stream() {
+    const char* e = std::getenv("DBAG_STREAM");
+    return e && std::string(e) == "1";
+  }
+  template <int L>
+  static void* stream_fn(int nst) {
+    if (nst == 2) return reinterpret_cast<void*>(dev::k_g_stream<S, T, L, 2>);
+    if (nst == 4) return reinterpret_cast<void*>(dev::k_g_stream<S, T, L, 4>);
+    return reinterpret_cast<void*>(dev::k_g_stream<S, T, L, 3>);
+  }
+  const StreamCfg& stream_cfg() {
+    if (scfg_.fn && scfg_.fact == fact_) return scfg_;
+    int nst = 2;
+    if (const char* e = std::getenv("DBAG_NST")) nst = std::min(4, std::max(2, std::atoi(e)));
+    StreamCfg c;
+    c.fact = fact_;
+    c.fn = fact_ ? stream_fn<dev::kLanesFact>(nst) : stream_fn<dev::kLanesDense>(nst);
+    c.smem = fact_ ? dev::StreamLayout<S, T, dev::kLanesFact>::bytes(nst)
+                   : dev::StreamLayout<S, T, dev::kLanesDense>::bytes(nst);
+    DBAG_CUDA(cudaFuncSetAttribute(c.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, c.smem));
+    int per_sm = 0, sms = 0;
+    DBAG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, c.fn, dev::kStreamThreads, c.smem));
+    DBAG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device_));
+    c.grid = std::max(1, std::min(std::max(per_sm, 1) * sms, std::max(n_norm_, n_long_)));
+    scfg_ = c;
+    return scfg_;
+  }
+  // One DSE pass of the graph body outside a graph (run-ahead loop, timing).
+  void launch_pass(const dev::DseArgs<S, T>& A, const dev::GBufs<S>& B, const dev::GScal<S>* sc) {
+    if (!use_stream()) {
+      if (fact_) launch(dev::k_g_pass<S, T, dev::kLanesFact>, n_long_ + n_chunks_, dev::kTile, A, B, sc);
+      else launch(dev::k_g_pass<S, T, dev::kLanesDense>, n_long_ + n_chunks_, dev::kTile, A, B, sc);
+      return;
+    }
+    const StreamCfg& c = stream_cfg();
+    const dev::ChunkTab* tab = reinterpret_cast<const dev::ChunkTab*>(ctab_.get());
+    std::int32_t nn = n_norm_;
+    void* args[] = {const_cast<dev::DseArgs<S, T>*>(&A), const_cast<dev::GBufs<S>*>(&B), &sc, &tab, &nn};
+    DBAG_CUDA(cudaLaunchKernel(c.fn, dim3(static_cast<unsigned>(c.grid)), dim3(dev::kStreamThreads), args,
+                               static_cast<std::size_t>(c.smem), st_));
+    ++launches_;
   }
 
   dev::DseArgs<S, T> dse_args(const S* x) {
@@ -1554,6 +1634,7 @@ class Rank {
   std::int64_t N_ = 0, H_ = 0;
   int n_tiles_ = 0;
   std::int32_t n_long_ = 0;
+  std::int32_t n_norm_ = 0;  // single-chunk tiles: the streaming pass's staged chunks
   std::int32_t n_chunks_ = 0;
   bool have_system_ = false;
   double lambda_ = 0;
@@ -1576,7 +1657,7 @@ class Rank {
 
   Arena pool_;  // declared first: destroyed after the buffers carved from it
   DevBuf<std::int32_t> slot_cam_, slot_dpt_, slot_edge_, dpt_ptr_, chunk_slot_, cam_part_ptr_, halo_slot_, slot_chunk_,
-      long_chunk_, halo_pos_, cam_ptr_, cam_glob_, cslot_dslot_, dpt_glob_d_,
+      long_chunk_, ctab_, halo_pos_, cam_ptr_, cam_glob_, cslot_dslot_, dpt_glob_d_,
       halo_of_, halo_dpt_, halo_idx_;
   DevBuf<std::uint8_t> owned_;
   DevBuf<S> slot_px_, slot_py_, slot_w_;
@@ -1597,6 +1678,7 @@ class Rank {
   DevBuf<double> carry_;               // k_assemble_cameras sums across Jb batches
   std::vector<std::int32_t> jb_pt_;    // Jb batch boundaries (device points)
   std::int32_t pf_dist_ = -1;
+  StreamCfg scfg_;
   std::vector<std::int32_t> jb_ncam_;  // cameras each Jb batch touches
   DevBuf<std::int32_t> cam_list_;      // ... their local ids, m_loc per batch
   DevBuf<T> E_;       // chunk records: factored lanes G = sqrt(w) Jc (T) + RecMeta (pool)

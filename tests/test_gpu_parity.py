@@ -602,3 +602,21 @@ def test_dpcg_pq_breakdown(variant, k, monkeypatch):
     assert w[0] < 0
     with pytest.raises(dba.PcgBreakdownError):
         dba.group_operator(p, k, V[:, 0], mode=1, blocks=blocks, tol=1e-12, max_iters=100)
+
+
+@pytest.mark.parametrize("shape", ["chunks", "long-tiles"])
+@pytest.mark.parametrize("k", [1, 2])
+def test_streaming_pass_variant(shape, k, monkeypatch):
+    """The opt-in persistent TMA-fed DSE pass (stream.cuh, DBAG_STREAM=1:
+    cp.async.bulk record + C-factor stages, mbarrier ring, gather warps) gives
+    the oracle's trajectory in the graph DPCG (K = 1) and in the run-ahead
+    loop of K = 2 ranks (halo points), with ordinary chunks and with long
+    tiles (points observed by more than 128 cameras)."""
+    monkeypatch.setenv("DBAG_STREAM", "1")
+    monkeypatch.setenv("DBAG_NST", "2")
+    if shape == "chunks":
+        p = ring(60, 800, 6, radius=1.0, noise=0.5, seed=4, nobs=800 * 6 + 13)
+    else:
+        p = ring(220, 30, 150, seed=7, radius=1.0, noise=0.5, nobs=30 * 150 + 17)
+    cfg = dba.SolverConfig(max_iterations=4, workers=k, pcg_tol=1e-12, pcg_max_iters=2000)
+    _compare_histories(dba.lm_solve(p, cfg), O.lm_solve(p, cfg), 1e-9)
