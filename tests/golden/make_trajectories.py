@@ -21,12 +21,15 @@ ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)
 sys.path.insert(0, ROOT)
 from oracle import oracle as O  # noqa: E402
 
-SHAPES = {"ladybug-49": (49, 7776, 31843), "trafalgar-257": (257, 65132, 225911)}
+SHAPES = {"ladybug-49": (49, 7776, 31843), "trafalgar-257": (257, 65132, 225911),
+          "venice-1778": (1778, 993923, 5001946)}
+ITERS = {"venice-1778/f64": 2}  # 4-6 CPU minutes per run on 8-16 threads: the first two iterations
 RUNS = {  # name -> (shape, dtype, K values)
     "ladybug-49/f64": ("ladybug-49", np.float64, (1, 2, 3, 4, 5, 6, 7, 8)),
     "ladybug-49/f32": ("ladybug-49", np.float32, (1, 2, 3, 4, 5, 6, 7, 8)),
     "trafalgar-257/f64": ("trafalgar-257", np.float64, (1, 2, 3, 4, 5, 6, 7, 8)),
     "trafalgar-257/f32": ("trafalgar-257", np.float32, (1, 2, 3, 4, 5, 6, 7, 8)),
+    "venice-1778/f64": ("venice-1778", np.float64, (4, 8, 16)),
 }
 OUT = os.path.join(os.path.dirname(os.path.abspath(__file__)), "trajectories.json")
 
@@ -38,10 +41,11 @@ def main(names):
         m, n, N = SHAPES[shape]
         p = O.generate_synthetic(O.SynthOptions(cameras=m, points=n, num_observations=N, seed=1, pixel_noise=0.5))
         p = p.astype(dtype)
-        entry = {"shape": [m, n, N], "dtype": np.dtype(dtype).name, "max_iterations": 10, "runs": {}}
+        iters = ITERS.get(name, 10)
+        entry = {"shape": [m, n, N], "dtype": np.dtype(dtype).name, "max_iterations": iters, "runs": {}}
         for k in ks:
             t = time.time()
-            st = O.lm_solve(p, O.OracleConfig(workers=k, max_iterations=10))
+            st = O.lm_solve(p, O.OracleConfig(workers=k, max_iterations=iters))
             entry["runs"][str(k)] = {
                 "cost": [r.cost for r in st.history], "lambda": [r.lambda_ for r in st.history],
                 "accepted": [r.accepted for r in st.history], "pcg": [r.pcg_iterations for r in st.history],
