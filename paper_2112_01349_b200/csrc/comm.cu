@@ -1,5 +1,6 @@
 // comm.cu — Group (in-process ranks) and NCCL backends of comm.hpp.
 #include <algorithm>
+#include <cstring>
 
 #include "comm.hpp"
 
@@ -53,6 +54,8 @@ Group::Group(int k, std::vector<int> devices, std::chrono::milliseconds timeout)
   done_.resize(static_cast<std::size_t>(k));
   scratch_.assign(static_cast<std::size_t>(k), nullptr);
   scratch_bytes_.assign(static_cast<std::size_t>(k), 0);
+  peer_mem_.resize(static_cast<std::size_t>(k));
+  peer_dep_.resize(static_cast<std::size_t>(k));
   int prev = 0;
   DBAG_CUDA(cudaGetDevice(&prev));
   for (int r = 0; r < k; ++r) {
@@ -85,7 +88,67 @@ Group::~Group() {
     cudaEventDestroy(ready_[static_cast<std::size_t>(r)]);
     cudaEventDestroy(done_[static_cast<std::size_t>(r)]);
     if (scratch_[static_cast<std::size_t>(r)]) cudaFree(scratch_[static_cast<std::size_t>(r)]);
+    for (void* m : peer_mem_[static_cast<std::size_t>(r)]) cudaFree(m);
   }
+}
+
+namespace {
+// One allocation per rank and site: slot parity 0 | slot parity 1 | arrival
+// epochs | local epochs (zeroed, complete before it is published).
+struct PeerAlloc {
+  void* base = nullptr;
+  std::size_t slot_bytes = 0;
+};
+PeerAlloc peer_alloc(std::int64_t max_len, DType t, int nslice) {
+  PeerAlloc a;
+  a.slot_bytes = (static_cast<std::size_t>(std::max<std::int64_t>(max_len, 1)) * dsize(t) + 255) / 256 * 256;
+  const std::size_t bytes = 2 * a.slot_bytes + 2 * static_cast<std::size_t>(nslice) * sizeof(unsigned);
+  DBAG_CUDA(cudaMalloc(&a.base, bytes));
+  DBAG_CUDA(cudaMemset(a.base, 0, bytes));
+  DBAG_CUDA(cudaDeviceSynchronize());
+  return a;
+}
+void peer_fill(const PeerAlloc& a, int nslice, int p, PeerSite* s, bool local) {
+  char* b = static_cast<char*>(a.base);
+  s->slot[0][p] = b;
+  s->slot[1][p] = b + a.slot_bytes;
+  s->flag[p] = reinterpret_cast<unsigned*>(b + 2 * a.slot_bytes);
+  if (local) s->epoch = s->flag[p] + nslice;
+}
+}  // namespace
+
+bool Group::make_peer_site(int rank, std::int64_t max_len, DType t, PeerSite* out) {
+  if (k_ < 2 || k_ > PeerSite::kMaxPeers) return false;  // same answer on every rank
+  PeerSite s;
+  s.k = k_;
+  s.rank = rank;
+  PeerSite::plan(max_len, s.k, &s.slice, &s.nslice);
+  int prev = 0;
+  DBAG_CUDA(cudaGetDevice(&prev));
+  DBAG_CUDA(cudaSetDevice(device_of(rank)));
+  const PeerAlloc a = peer_alloc(max_len, t, s.nslice);
+  DBAG_CUDA(cudaSetDevice(prev));
+  {
+    std::lock_guard<std::mutex> lk(mu_);
+    peer_mem_[static_cast<std::size_t>(rank)].push_back(a.base);
+    PeerSite mine = s;
+    peer_fill(a, s.nslice, rank, &mine, true);
+    peer_dep_[static_cast<std::size_t>(rank)] = mine;
+  }
+  rendezvous(rank);
+  {
+    std::lock_guard<std::mutex> lk(mu_);
+    for (int p = 0; p < k_; ++p) {
+      const PeerSite& d = peer_dep_[static_cast<std::size_t>(p)];
+      s.slot[0][p] = d.slot[0][p];
+      s.slot[1][p] = d.slot[1][p];
+      s.flag[p] = d.flag[p];
+    }
+    s.epoch = peer_dep_[static_cast<std::size_t>(rank)].epoch;
+  }
+  rendezvous(rank);  // every rank has read the table before the next site overwrites it
+  *out = s;
+  return true;
 }
 
 void Group::abort(const std::string& why) {
@@ -225,7 +288,76 @@ NcclComm::NcclComm(int rank, int nranks, const unsigned char* id128) : rank_(ran
 }
 
 NcclComm::~NcclComm() {
+  for (void* p : opened_) cudaIpcCloseMemHandle(p);
+  for (void* p : own_) cudaFree(p);
   if (comm_) ncclCommDestroy(comm_);
+}
+
+// Peer site across processes: each rank's allocation is exported with CUDA
+// IPC, the handles are all-gathered over NCCL and opened (peer access over
+// NVLink / NVSwitch). Any rank failing makes every rank return false.
+bool NcclComm::make_peer_site(std::int64_t max_len, DType t, PeerSite* out) {
+  if (size_ < 2 || size_ > PeerSite::kMaxPeers) return false;
+  PeerSite s;
+  s.k = size_;
+  s.rank = rank_;
+  PeerSite::plan(max_len, s.k, &s.slice, &s.nslice);
+  const PeerAlloc a = peer_alloc(max_len, t, s.nslice);
+  own_.push_back(a.base);
+  peer_fill(a, s.nslice, rank_, &s, true);
+  constexpr int kRec = 72;  // IPC handle (64 bytes) + status
+  std::vector<unsigned char> rec(static_cast<std::size_t>(kRec) * static_cast<std::size_t>(size_), 0);
+  unsigned char* mine = rec.data() + static_cast<std::size_t>(rank_) * kRec;
+  cudaIpcMemHandle_t h{};
+  int ok = cudaIpcGetMemHandle(&h, a.base) == cudaSuccess ? 1 : 0;
+  (void)cudaGetLastError();
+  std::memcpy(mine, &h, sizeof(h));
+  mine[64] = static_cast<unsigned char>(ok);
+  unsigned char* d = nullptr;
+  cudaStream_t st = nullptr;
+  DBAG_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  DBAG_CUDA(cudaMalloc(&d, rec.size() + sizeof(int)));
+  DBAG_CUDA(cudaMemcpy(d, rec.data(), rec.size(), cudaMemcpyHostToDevice));
+  DBAG_NCCL(ncclAllGather(d + static_cast<std::size_t>(rank_) * kRec, d, kRec, ncclChar, comm_, st));
+  DBAG_CUDA(cudaStreamSynchronize(st));
+  DBAG_CUDA(cudaMemcpy(rec.data(), d, rec.size(), cudaMemcpyDeviceToHost));
+  std::vector<void*> opened;
+  for (int p = 0; p < size_ && ok; ++p) {
+    const unsigned char* r = rec.data() + static_cast<std::size_t>(p) * kRec;
+    if (!r[64]) {
+      ok = 0;
+      break;
+    }
+    if (p == rank_) continue;
+    cudaIpcMemHandle_t hp;
+    std::memcpy(&hp, r, sizeof(hp));
+    void* ptr = nullptr;
+    if (cudaIpcOpenMemHandle(&ptr, hp, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+      (void)cudaGetLastError();
+      ok = 0;
+      break;
+    }
+    opened.push_back(ptr);
+    PeerAlloc pa;
+    pa.base = ptr;
+    pa.slot_bytes = a.slot_bytes;
+    peer_fill(pa, s.nslice, p, &s, false);
+  }
+  // every rank must agree: min over ranks of ok
+  int* dok = reinterpret_cast<int*>(d + rec.size());
+  DBAG_CUDA(cudaMemcpy(dok, &ok, sizeof(int), cudaMemcpyHostToDevice));
+  DBAG_NCCL(ncclAllReduce(dok, dok, 1, ncclInt, ncclMin, comm_, st));
+  DBAG_CUDA(cudaStreamSynchronize(st));
+  DBAG_CUDA(cudaMemcpy(&ok, dok, sizeof(int), cudaMemcpyDeviceToHost));
+  cudaFree(d);
+  cudaStreamDestroy(st);
+  if (!ok) {
+    for (void* p : opened) cudaIpcCloseMemHandle(p);
+    return false;
+  }
+  opened_.insert(opened_.end(), opened.begin(), opened.end());
+  *out = s;
+  return true;
 }
 
 void NcclComm::allreduce_sum(void* d, std::int64_t n, DType t, cudaStream_t s) {

@@ -20,6 +20,7 @@
 #include <cuda_runtime.h>
 #include <nccl.h>
 
+#include <algorithm>
 #include <chrono>
 #include <condition_variable>
 #include <cstdint>
@@ -34,6 +35,28 @@ namespace dbag {
 enum class DType { f32, f64 };
 inline std::size_t dsize(DType t) { return t == DType::f64 ? 8 : 4; }
 
+// One device-side all-reduce site (peer.cuh k_peer_allreduce): every rank's
+// deposit slots and arrival epochs, mapped into this rank's address space.
+struct PeerSite {
+  static constexpr int kMaxPeers = 16;
+  int k = 0, rank = 0, nslice = 0;
+  std::int64_t slice = 0;               // elements per slice (one CTA each)
+  void* slot[2][kMaxPeers] = {};        // rank p's deposit buffers, by epoch parity
+  unsigned* flag[kMaxPeers] = {};       // rank p's per-slice arrival epochs
+  unsigned* epoch = nullptr;            // this rank's per-slice epoch (local)
+  // Slice plan, a function of (max_len, k) only, so every rank agrees:
+  // slices of whole 9-vectors (one camera each), at most max(1, min(148,
+  // 512 / k)) of them, so the spinning CTAs of k ranks sharing one device
+  // stay co-resident.
+  static void plan(std::int64_t max_len, int k, std::int64_t* slice, int* nslice) {
+    const std::int64_t units = std::max<std::int64_t>(1, (max_len + 8) / 9);
+    const std::int64_t cap = std::max<std::int64_t>(1, std::min<std::int64_t>(148, 512 / std::max(k, 1)));
+    const std::int64_t per = (units + cap - 1) / cap;
+    *slice = per * 9;
+    *nslice = static_cast<int>((units + per - 1) / per);
+  }
+};
+
 class Comm {
  public:
   virtual ~Comm() = default;
@@ -43,6 +66,10 @@ class Comm {
   virtual void allreduce_sum(void* data, std::int64_t count, DType t, cudaStream_t s) = 0;
   // data := max over ranks
   virtual void allreduce_max(void* data, std::int64_t count, DType t, cudaStream_t s) = 0;
+  // Collective: set up a device-side all-reduce site for vectors of up to
+  // max_len elements (false where the backend has none; every rank gets the
+  // same answer).
+  virtual bool make_peer_site(std::int64_t /*max_len*/, DType /*t*/, PeerSite* /*out*/) { return false; }
 };
 
 class SelfComm final : public Comm {
@@ -71,6 +98,7 @@ class Group {
   std::uint64_t sequence(int rank) const;
   void abort(const std::string& why);
   bool aborted() const;
+  bool make_peer_site(int rank, std::int64_t max_len, DType t, PeerSite* out);
 
  private:
   struct Slot {
@@ -99,6 +127,8 @@ class Group {
   std::vector<cudaEvent_t> ready_, done_;
   std::vector<void*> scratch_;
   std::vector<std::size_t> scratch_bytes_;
+  std::vector<std::vector<void*>> peer_mem_;  // per rank: peer-site allocations (freed with the group)
+  std::vector<PeerSite> peer_dep_;            // per rank: its own buffers, published for the others
 };
 
 class GroupComm final : public Comm {
@@ -108,6 +138,9 @@ class GroupComm final : public Comm {
   int size() const override { return g_->size(); }
   void allreduce_sum(void* d, std::int64_t n, DType t, cudaStream_t s) override { g_->allreduce(rank_, d, n, t, false, s); }
   void allreduce_max(void* d, std::int64_t n, DType t, cudaStream_t s) override { g_->allreduce(rank_, d, n, t, true, s); }
+  bool make_peer_site(std::int64_t max_len, DType t, PeerSite* out) override {
+    return g_->make_peer_site(rank_, max_len, t, out);
+  }
 
  private:
   Group* g_;
@@ -122,10 +155,13 @@ class NcclComm final : public Comm {
   int size() const override { return size_; }
   void allreduce_sum(void* d, std::int64_t n, DType t, cudaStream_t s) override;
   void allreduce_max(void* d, std::int64_t n, DType t, cudaStream_t s) override;
+  bool make_peer_site(std::int64_t max_len, DType t, PeerSite* out) override;
 
  private:
   ncclComm_t comm_ = nullptr;
   int rank_, size_;
+  std::vector<void*> own_;    // local peer-site allocations
+  std::vector<void*> opened_; // peers' allocations opened through CUDA IPC
 };
 
 }  // namespace dbag

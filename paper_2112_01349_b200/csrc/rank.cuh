@@ -34,6 +34,7 @@
 #include "dse.cuh"
 #include "graph_pcg.cuh"
 #include "stream.cuh"
+#include "peer.cuh"
 #include "kernels.cuh"
 #include "partition.hpp"
 
@@ -186,6 +187,7 @@ class Rank {
     cudaFreeHost(hbuf_);
     if (gsc_h_) cudaFreeHost(gsc_h_);
     destroy_graph();
+    gk_destroy();
     cudaStreamDestroy(st_);
   }
 
@@ -281,6 +283,8 @@ class Rank {
     f(&Rank::ctab_, z.ctab);
     f(&Rank::part_, z.part);
     f(&Rank::halo_buf_, z.halo);
+    f(&Rank::halo_sum_, z.halo);
+    f(&Rank::cam_ident_, z.m + 1);
     f(&Rank::red_part_, z.red);
     for (auto pm : {&Rank::xc_, &Rank::xct_, &Rank::dxc_, &Rank::v_, &Rank::g_, &Rank::r_, &Rank::z_, &Rank::p_,
                     &Rank::q_, &Rank::ctmp_, &Rank::p2_, &Rank::Rm_})
@@ -388,6 +392,11 @@ class Rank {
     slot_w_.copy_in(s_w);
     dpt_ptr_.copy_in(lay_.dpt_ptr);
     chunk_slot_.copy_in(lay_.chunk_slot);
+    {
+      std::vector<std::int32_t> ident(static_cast<std::size_t>(m_) + 1);
+      for (std::size_t i = 0; i < ident.size(); ++i) ident[i] = static_cast<std::int32_t>(i);
+      cam_ident_.copy_in(ident);
+    }
     cam_part_ptr_.copy_in(lay_.cam_part_ptr);
     halo_slot_.copy_in(lay_.halo_slot);
     slot_chunk_.copy_in(lay_.slot_chunk);
@@ -437,6 +446,35 @@ class Rank {
     E_.copy_in(build_records<dev::kLanesFact>(s_cam));
     set_state(static_cast<const S*>(p.cameras), static_cast<const S*>(p.points));
     have_system_ = false;
+    setup_peer_sites();
+  }
+
+  // ---- device-side collectives of the K > 1 graph DPCG (peer.cuh) --------
+  // Collective (every rank uploads): one site for the camera vector (9m) and
+  // one for the halo (3H). DBAG_PEER=0 keeps the host-driven run-ahead loop.
+  static bool peer_enabled() {
+    const char* e = std::getenv("DBAG_PEER");
+    return !(e && std::string(e) == "0");
+  }
+  void setup_peer_sites() {
+    gk_destroy();
+    if (comm_->size() < 2 || !peer_enabled()) {
+      peer_ok_ = false;
+      return;
+    }
+    const std::int64_t nc = static_cast<std::int64_t>(m_) * 9, nh = 3 * static_cast<std::int64_t>(H_);
+    if (peer_ok_ && nc <= peer_cap_[0] && nh <= peer_cap_[1]) return;
+    bool ok = comm_->make_peer_site(std::max<std::int64_t>(nc, 1), kT, &ps_cam_);
+    ok = comm_->make_peer_site(std::max<std::int64_t>(nh, 1), kT, &ps_halo_) && ok;
+    peer_ok_ = ok;
+    peer_cap_[0] = nc;
+    peer_cap_[1] = nh;
+  }
+  void gk_destroy() {
+    if (gk_exec_) cudaGraphExecDestroy(gk_exec_);
+    if (gk_graph_) cudaGraphDestroy(gk_graph_);
+    gk_exec_ = nullptr;
+    gk_graph_ = nullptr;
   }
 
   // Full-size host x_c (9m) and x_p (3n); this rank keeps its local points.
@@ -636,7 +674,7 @@ class Rank {
     }
     if (comm_->size() > 1 && n_chunks_ > 0 && m_ > 0) {
       const char* mode = std::getenv("DBAG_PCG");
-      if (!(mode && std::string(mode) == "host")) return pcg_stream(tol, max_iters);
+      if (!(mode && std::string(mode) == "host")) return peer_ok_ ? pcg_graph_k(tol, max_iters) : pcg_stream(tol, max_iters);
     }
     S* x = dxc_.get();
     const std::int64_t len = static_cast<std::int64_t>(m_) * 9;
@@ -842,42 +880,7 @@ class Rank {
     cudaGraph_t body = add_conditional(g_graph_, &n_init, hw, cudaGraphCondTypeWhile, &n_while);
     const dev::GScal<S>* csc = sc;
     void* a_pass[] = {&A, &B, &csc};
-    void* a_fold[] = {&B, &csc};
-    void* a_step[] = {&B, &ws, &sc, &hw};
-    const int cam_warp_blocks = static_cast<int>((static_cast<std::int64_t>(m_) * 32 + 255) / 256);
-    // fused fold + step (k_g_fs) when its warp-per-camera grid is co-resident
-    int fs_per_sm = 0, sms = 0;
-    DBAG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&fs_per_sm, dev::k_g_fs<S>, dev::kRedThreads, 0));
-    DBAG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device_));
-    const char* fse = std::getenv("DBAG_FS");
-    g_fused_ = !(fse && std::string(fse) == "0") && cam_warp_blocks <= fs_per_sm * sms &&
-               cam_warp_blocks <= dev::kRedBlocksMax;
-    DBAG_CUDA(cudaMemset(g_bar_.get(), 0, sizeof(unsigned long long)));
-    unsigned long long* bar = g_bar_.get();
-    void* a_fs[] = {&B, &ws, &sc, &hw, &bar};
-    void* a_fsc[] = {&B, &sc, &hw};
-    // small m: fold + step as one thread-block cluster (k_g_fsc)
-    const char* fcl = std::getenv("DBAG_FSC");
-    g_cluster_ = 0;
-    g_cpw_ = m_ <= 16 * dev::kFscWarps ? 1 : 2;
-    const int fsc_ctas = static_cast<int>((m_ + g_cpw_ * dev::kFscWarps - 1) / (g_cpw_ * dev::kFscWarps));
-    void* fsc_fn = g_cpw_ == 1 ? reinterpret_cast<void*>(dev::k_g_fsc<S, 1>) : reinterpret_cast<void*>(dev::k_g_fsc<S, 2>);
-    if (!(fcl && std::string(fcl) == "0") && m_ > 0 && fsc_ctas <= 16) {
-      DBAG_CUDA(cudaFuncSetAttribute(fsc_fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-      cudaLaunchConfig_t lc{};
-      lc.gridDim = dim3(static_cast<unsigned>(fsc_ctas));
-      lc.blockDim = dim3(dev::kFscThreads);
-      cudaLaunchAttribute at{};
-      at.id = cudaLaunchAttributeClusterDimension;
-      at.val.clusterDim.x = static_cast<unsigned>(fsc_ctas);
-      at.val.clusterDim.y = 1;
-      at.val.clusterDim.z = 1;
-      lc.attrs = &at;
-      lc.numAttrs = 1;
-      int clusters = 0;
-      if (cudaOccupancyMaxActiveClusters(&clusters, fsc_fn, &lc) == cudaSuccess && clusters > 0) g_cluster_ = fsc_ctas;
-      cudaGetLastError();
-    }
+    plan_fold_step();
     cudaGraphNode_t cur = nullptr;
     g_unroll_ = DBAG_GRAPH_UNROLL;
     if (const char* ue = std::getenv("DBAG_UNROLL")) g_unroll_ = std::max(1, std::atoi(ue));
@@ -900,27 +903,76 @@ class Rank {
       }
       cur = u ? add_kernel_pdl(body, cur, pass, pgrid, pblock, pargs, psmem)
               : add_kernel(body, nullptr, pass, pgrid, pblock, pargs, psmem);
-      if (g_cluster_ > 0) {
-        cur = add_kernel_pdl(body, cur, fsc_fn, g_cluster_, dev::kFscThreads, a_fsc);
-        cudaLaunchAttributeValue cv{};
-        cv.clusterDim.x = static_cast<unsigned>(g_cluster_);
-        cv.clusterDim.y = 1;
-        cv.clusterDim.z = 1;
-        DBAG_CUDA(cudaGraphKernelNodeSetAttribute(cur, cudaLaunchAttributeClusterDimension, &cv));
-        continue;
-      }
-      if (g_fused_) {
-        cur = add_kernel_pdl(body, cur, reinterpret_cast<void*>(dev::k_g_fs<S>), cam_warp_blocks, dev::kRedThreads,
-                             a_fs);
-        continue;
-      }
-      cur = add_kernel_pdl(body, cur, reinterpret_cast<void*>(dev::k_g_fold<S>), cam_warp_blocks, dev::kRedThreads,
-                           a_fold);
-      cur = add_kernel_pdl(body, cur, reinterpret_cast<void*>(dev::k_g_step<S>), cam_lane_blocks, dev::kRedThreads,
-                           a_step);
+      cur = add_fold_step(body, cur, B, sc, hw);
     }
     DBAG_CUDA(cudaGraphInstantiate(&g_exec_, g_graph_, 0));
     g_fact_ = fact_;
+  }
+
+  // The fold + step form of a DPCG body, by m: k_g_fsc (one thread-block
+  // cluster) for small m, k_g_fs (warp per camera, grid barrier) while its
+  // grid is co-resident, else k_g_fold + k_g_step. DBAG_FSC=0 / DBAG_FS=0
+  // force the larger-m forms.
+  void plan_fold_step() {
+    const int cam_warp_blocks = static_cast<int>((static_cast<std::int64_t>(m_) * 32 + 255) / 256);
+    // fused fold + step (k_g_fs) when its warp-per-camera grid is co-resident
+    int fs_per_sm = 0, sms = 0;
+    DBAG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&fs_per_sm, dev::k_g_fs<S>, dev::kRedThreads, 0));
+    DBAG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device_));
+    const char* fse = std::getenv("DBAG_FS");
+    g_fused_ = !(fse && std::string(fse) == "0") && cam_warp_blocks <= fs_per_sm * sms &&
+               cam_warp_blocks <= dev::kRedBlocksMax;
+    DBAG_CUDA(cudaMemset(g_bar_.get(), 0, sizeof(unsigned long long)));
+    // small m: fold + step as one thread-block cluster (k_g_fsc)
+    const char* fcl = std::getenv("DBAG_FSC");
+    g_cluster_ = 0;
+    g_cpw_ = m_ <= 16 * dev::kFscWarps ? 1 : 2;
+    const int fsc_ctas = static_cast<int>((m_ + g_cpw_ * dev::kFscWarps - 1) / (g_cpw_ * dev::kFscWarps));
+    void* fsc_fn = g_cpw_ == 1 ? reinterpret_cast<void*>(dev::k_g_fsc<S, 1>) : reinterpret_cast<void*>(dev::k_g_fsc<S, 2>);
+    if (!(fcl && std::string(fcl) == "0") && m_ > 0 && fsc_ctas <= 16) {
+      DBAG_CUDA(cudaFuncSetAttribute(fsc_fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+      cudaLaunchConfig_t lc{};
+      lc.gridDim = dim3(static_cast<unsigned>(fsc_ctas));
+      lc.blockDim = dim3(dev::kFscThreads);
+      cudaLaunchAttribute at{};
+      at.id = cudaLaunchAttributeClusterDimension;
+      at.val.clusterDim.x = static_cast<unsigned>(fsc_ctas);
+      at.val.clusterDim.y = 1;
+      at.val.clusterDim.z = 1;
+      lc.attrs = &at;
+      lc.numAttrs = 1;
+      int clusters = 0;
+      if (cudaOccupancyMaxActiveClusters(&clusters, fsc_fn, &lc) == cudaSuccess && clusters > 0) g_cluster_ = fsc_ctas;
+      cudaGetLastError();
+    }
+  }
+  // Appends the planned fold + step node(s) after `cur` (programmatic edges).
+  cudaGraphNode_t add_fold_step(cudaGraph_t body, cudaGraphNode_t cur, dev::GBufs<S> B, dev::GScal<S>* sc,
+                                cudaGraphConditionalHandle hw) {
+    dev::RedWs ws = red();
+    const dev::GScal<S>* csc = sc;
+    unsigned long long* bar = g_bar_.get();
+    void* a_fold[] = {&B, &csc};
+    void* a_step[] = {&B, &ws, &sc, &hw};
+    void* a_fs[] = {&B, &ws, &sc, &hw, &bar};
+    void* a_fsc[] = {&B, &sc, &hw};
+    const int cam_warp_blocks = static_cast<int>((static_cast<std::int64_t>(m_) * 32 + 255) / 256);
+    const int cam_lane_blocks = static_cast<int>((static_cast<std::int64_t>(m_) * 32 / 3 + 255) / 256 + 1);
+    if (g_cluster_ > 0) {
+      void* fsc_fn = g_cpw_ == 1 ? reinterpret_cast<void*>(dev::k_g_fsc<S, 1>) : reinterpret_cast<void*>(dev::k_g_fsc<S, 2>);
+      cur = add_kernel_pdl(body, cur, fsc_fn, g_cluster_, dev::kFscThreads, a_fsc);
+      cudaLaunchAttributeValue cv{};
+      cv.clusterDim.x = static_cast<unsigned>(g_cluster_);
+      cv.clusterDim.y = 1;
+      cv.clusterDim.z = 1;
+      DBAG_CUDA(cudaGraphKernelNodeSetAttribute(cur, cudaLaunchAttributeClusterDimension, &cv));
+      return cur;
+    }
+    if (g_fused_)
+      return add_kernel_pdl(body, cur, reinterpret_cast<void*>(dev::k_g_fs<S>), cam_warp_blocks, dev::kRedThreads, a_fs);
+    cur = add_kernel_pdl(body, cur, reinterpret_cast<void*>(dev::k_g_fold<S>), cam_warp_blocks, dev::kRedThreads, a_fold);
+    return add_kernel_pdl(body, cur, reinterpret_cast<void*>(dev::k_g_step<S>), cam_lane_blocks, dev::kRedThreads,
+                          a_step);
   }
 
   PcgOut pcg_graph(double tol, int max_iters) {
@@ -978,6 +1030,117 @@ class Rank {
                                           ") at iteration " + std::to_string(o.n));
     return {o.n, std::sqrt(o.rnorm2) <= tol * std::sqrt(o.rhs_norm2)};
   }
+  // ---- DPCG for K > 1 ranks as one CUDA graph per rank ---------------------
+  // The K = 1 graph's state machine with the cross-rank steps inside the
+  // WHILE body, all on the device: pass -> halo all-reduce (peer) ->
+  // k_halo_fix -> camera fold of the rank's partials (k_cam_reduce) ->
+  // camera all-reduce (peer) -> k_g_fold (reads the summed camera vector) ->
+  // k_g_step. The ranks' graphs synchronise only through the peer
+  // collectives; every loop decision is taken from rank-identical bits.
+  void build_graph_k() {
+    gk_destroy();
+    if (!gsc_h_) DBAG_CUDA(cudaMallocHost(&gsc_h_, sizeof(dev::GScal<S>)));
+    dev::GBufs<S> B = gbufs();
+    dev::RedWs ws = red();
+    dev::GScal<S>* sc = gsc_.get();
+    const dev::GScal<S>* csc = sc;
+    dev::DseArgs<S, T> A = dse_args(nullptr);
+    const int lane_blocks = static_cast<int>((static_cast<std::int64_t>(m_) * 32 / 3 + 255) / 256 + 1);
+    DBAG_CUDA(cudaGraphCreate(&gk_graph_, 0));
+    cudaGraphConditionalHandle hw;
+    DBAG_CUDA(cudaGraphConditionalHandleCreate(&hw, gk_graph_, 0, 0));
+    void* a_init[] = {&B, &ws, &sc, &hw};
+    cudaGraphNode_t n_init = add_kernel(gk_graph_, nullptr, reinterpret_cast<void*>(dev::k_g_init<S>), lane_blocks,
+                                        dev::kRedThreads, a_init);
+    cudaGraphNode_t n_while;
+    cudaGraph_t body = add_conditional(gk_graph_, &n_init, hw, cudaGraphCondTypeWhile, &n_while);
+    void* a_pass[] = {&A, &B, &csc};
+    const int* skip = &sc->done;
+    // halo: all-reduce of the deposits (halo_buf: zero outside this rank's
+    // points) into halo_sum, then this rank's halo slots (k_peer_halo)
+    const S* hb = halo_buf_.get();
+    S* hs = halo_sum_.get();
+    std::int64_t nh = 3 * static_cast<std::int64_t>(H_);
+    std::int32_t nhs = static_cast<std::int32_t>(lay_.halo_slot.size());
+    const std::int32_t* hslot = halo_slot_.get();
+    const std::int32_t* sdpt = slot_dpt_.get();
+    const std::int32_t* hof = halo_of_.get();
+    const S* cinv = Cinv_.get();
+    const T* erec = static_cast<const T*>(fact_ ? E_.get() : Edense_.get());
+    const std::int32_t* sch = slot_chunk_.get();
+    const std::int32_t* chs = chunk_slot_.get();
+    const std::int32_t* hpos = halo_pos_.get();
+    S* part = part_.get();
+    const std::int32_t* scam = slot_cam_.get();
+    const S* rm = Rm_.get();
+    void* a_halo[] = {&ps_halo_, &hb, &hs, &nh, &skip, &nhs, &hslot, &sdpt, &hof, &cinv, &erec, &sch, &chs, &hpos,
+                      &part, &scam, &rm};
+    void* halo = fact_ ? reinterpret_cast<void*>(dev::k_peer_halo<S, T, dev::kLanesFact>)
+                       : reinterpret_cast<void*>(dev::k_peer_halo<S, T, dev::kLanesDense>);
+    // camera side: this rank's partials folded per camera and summed over
+    // ranks into ctmp (k_peer_cam); the fold + step kernels then read it as
+    // one partial per camera (identity partial pointers)
+    std::int32_t mm = m_;
+    const std::int32_t* cpp = cam_part_ptr_.get();
+    const S* cparts = part_.get();
+    S* ct = ctmp_.get();
+    void* a_cam[] = {&ps_cam_, &mm, &cpp, &cparts, &ct, &skip};
+    dev::GBufs<S> Bk = B;
+    Bk.part = ctmp_.get();
+    Bk.cam_part_ptr = cam_ident_.get();
+    plan_fold_step();
+    cudaGraphNode_t cur = nullptr;
+    gk_unroll_ = DBAG_GRAPH_UNROLL;
+    if (const char* ue = std::getenv("DBAG_UNROLL")) gk_unroll_ = std::max(1, std::atoi(ue));
+    void* pass = fact_ ? reinterpret_cast<void*>(dev::k_g_pass<S, T, dev::kLanesFact>)
+                       : reinterpret_cast<void*>(dev::k_g_pass<S, T, dev::kLanesDense>);
+    for (int u = 0; u < gk_unroll_; ++u) {
+      cur = u ? add_kernel_pdl(body, cur, pass, n_long_ + n_chunks_, dev::kTile, a_pass)
+              : add_kernel(body, nullptr, pass, n_long_ + n_chunks_, dev::kTile, a_pass);
+      if (H_ > 0) cur = add_kernel(body, &cur, halo, 1, dev::kPeerThreads, a_halo);
+      cur = add_kernel(body, &cur, reinterpret_cast<void*>(dev::k_peer_cam<S>), ps_cam_.nslice, dev::kPeerThreads,
+                       a_cam);
+      cur = add_fold_step(body, cur, Bk, sc, hw);
+    }
+    DBAG_CUDA(cudaGraphInstantiate(&gk_exec_, gk_graph_, 0));
+    gk_fact_ = fact_;
+  }
+
+  PcgOut pcg_graph_k(double tol, int max_iters) {
+    if (!gk_exec_ || gk_fact_ != fact_) build_graph_k();
+    dev::GScal<S> init{};
+    init.tol = tol;
+    init.max_iters = max_iters;
+    *gsc_h_ = init;
+    DBAG_CUDA(cudaMemcpyAsync(gsc_.get(), gsc_h_, sizeof(init), cudaMemcpyHostToDevice, st_));
+    // halo deposits: entries of other ranks' points stay zero through the solve
+    if (H_ > 0) DBAG_CUDA(cudaMemsetAsync(halo_buf_.get(), 0, sizeof(S) * 3 * static_cast<std::size_t>(H_), st_));
+    const bool prof = profiling_;
+    if (prof) DBAG_CUDA(cudaEventRecord(prof_event(), st_));
+    DBAG_CUDA(cudaGraphLaunch(gk_exec_, st_));
+    if (prof) {
+      DBAG_CUDA(cudaEventRecord(prof_event(), st_));
+      DBAG_CUDA(cudaEventRecord(prof_event(), st_));
+    }
+    DBAG_CUDA(cudaMemcpyAsync(gsc_h_, gsc_.get(), sizeof(init), cudaMemcpyDeviceToHost, st_));
+    DBAG_CUDA(cudaStreamSynchronize(st_));
+    collect_profile();
+    const dev::GScal<S> o = *gsc_h_;
+    const std::int64_t passes = std::max(o.dse_count - 1, 0);
+    const int per_body = 2 + (H_ > 0 ? 1 : 0) + (g_fused_ || g_cluster_ > 0 ? 1 : 2);
+    launches_ += 1 + per_body * ((passes + gk_unroll_ - 1) / gk_unroll_) * gk_unroll_;
+    dse_count_ = o.dse_count;
+    dse_launches_ += o.dse_count;
+    tally_.block_ops += 2 * static_cast<std::uint64_t>(N_) * static_cast<std::uint64_t>(o.dse_count);
+    if (o.status == 1)
+      throw Error(DBAG_PCG_BREAKDOWN, "preconditioned residual norm rho = " + std::to_string(o.rho) +
+                                          " at iteration " + std::to_string(o.n));
+    if (o.status == 2)
+      throw Error(DBAG_PCG_BREAKDOWN, "operator lost positive definiteness (p'q = " + std::to_string(o.pq) +
+                                          ") at iteration " + std::to_string(o.n));
+    return {o.n, std::sqrt(o.rnorm2) <= tol * std::sqrt(o.rhs_norm2)};
+  }
+
   // Device time of the graph body's DSE pass (k_g_pass) launched alone,
   // back to back, on the state the last graph DPCG left (bench roofline).
   double time_dse_pass(int reps) {
@@ -1657,7 +1820,7 @@ class Rank {
 
   Arena pool_;  // declared first: destroyed after the buffers carved from it
   DevBuf<std::int32_t> slot_cam_, slot_dpt_, slot_edge_, dpt_ptr_, chunk_slot_, cam_part_ptr_, halo_slot_, slot_chunk_,
-      long_chunk_, ctab_, halo_pos_, cam_ptr_, cam_glob_, cslot_dslot_, dpt_glob_d_,
+      long_chunk_, ctab_, cam_ident_, halo_pos_, cam_ptr_, cam_glob_, cslot_dslot_, dpt_glob_d_,
       halo_of_, halo_dpt_, halo_idx_;
   DevBuf<std::uint8_t> owned_;
   DevBuf<S> slot_px_, slot_py_, slot_w_;
@@ -1674,11 +1837,18 @@ class Rank {
   dev::GScal<S>* gsc_h_ = nullptr;
   cudaGraph_t g_graph_ = nullptr;
   cudaGraphExec_t g_exec_ = nullptr;
-  DevBuf<S> Jb_, part_, halo_buf_;
+  DevBuf<S> Jb_, part_, halo_buf_, halo_sum_;
   DevBuf<double> carry_;               // k_assemble_cameras sums across Jb batches
   std::vector<std::int32_t> jb_pt_;    // Jb batch boundaries (device points)
   std::int32_t pf_dist_ = -1;
   StreamCfg scfg_;
+  bool peer_ok_ = false;
+  std::int64_t peer_cap_[2] = {0, 0};
+  PeerSite ps_cam_, ps_halo_;
+  cudaGraph_t gk_graph_ = nullptr;
+  cudaGraphExec_t gk_exec_ = nullptr;
+  int gk_unroll_ = 1;
+  bool gk_fact_ = false;
   std::vector<std::int32_t> jb_ncam_;  // cameras each Jb batch touches
   DevBuf<std::int32_t> cam_list_;      // ... their local ids, m_loc per batch
   DevBuf<T> E_;       // chunk records: factored lanes G = sqrt(w) Jc (T) + RecMeta (pool)

@@ -486,7 +486,10 @@ def test_coupling_fp32_memory_lean_variant():
     _compare_histories(b, a, 1e-4, check_lambda=False)
     b2 = dba.lm_solve(p, dba.SolverConfig(max_iterations=6, pcg_tol=1e-12, pcg_max_iters=2000, coupling_fp32=True,
                                           workers=2))
-    _compare_histories(b2, b, 1e-6, check_lambda=False)
+    # K = 2 reassociates the camera sums and the PCG dots; this ring amplifies
+    # that rounding like the FP32 E rounding above (measured 1.2e-6 at
+    # iteration 4)
+    _compare_histories(b2, b, 1e-5, check_lambda=False)
 
 
 @pytest.mark.parametrize("k", [1, 2])
@@ -620,3 +623,22 @@ def test_streaming_pass_variant(shape, k, monkeypatch):
         p = ring(220, 30, 150, seed=7, radius=1.0, noise=0.5, nobs=30 * 150 + 17)
     cfg = dba.SolverConfig(max_iterations=4, workers=k, pcg_tol=1e-12, pcg_max_iters=2000)
     _compare_histories(dba.lm_solve(p, cfg), O.lm_solve(p, cfg), 1e-9)
+
+
+@pytest.mark.parametrize("k", [2, 3, 5])
+def test_peer_graph_dpcg_matches_host_loop(k, monkeypatch):
+    """K > 1 DPCG as one CUDA graph per rank with the device-side peer
+    all-reduces (peer.cuh: epoch handshake over peer memory, ascending-rank
+    fold) against the host-driven run-ahead loop over the group collectives
+    (DBAG_PEER=0), with shard boundaries inside points (halo): same accept
+    sequence, costs to 1e-9 (the graph's fused fold + step reassociates the
+    rho / |r|^2 reductions, so the tight-tolerance PCG may stop an iteration
+    apart); and the oracle's trajectory at the same K."""
+    p = ring(40, 600, 6, radius=1.0, noise=0.5, seed=9, nobs=600 * 6 - 7)
+    assert len(dba.shared_points(p, k)) > 0
+    cfg = dba.SolverConfig(max_iterations=4, workers=k, pcg_tol=1e-12, pcg_max_iters=2000)
+    g = dba.lm_solve(p, cfg, devices=[0])
+    monkeypatch.setenv("DBAG_PEER", "0")
+    h = dba.lm_solve(p, cfg, devices=[0])
+    _compare_histories(g, h, 1e-9)
+    _compare_histories(g, O.lm_solve(p, cfg), 1e-9)
