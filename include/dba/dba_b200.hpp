@@ -20,6 +20,7 @@
 #include <cmath>
 #include <cstdint>
 #include <istream>
+#include <limits>
 #include <iterator>
 #include <ostream>
 #include <stdexcept>
@@ -169,6 +170,65 @@ class BAProblem {
     w_.push_back(o.weight);
     return static_cast<std::int32_t>(cam_id_.size()) - 1;
   }
+  // Node / edge views (dba/problem.hpp:219-227): states are stored flat
+  // (pack_cameras / pack_points layout), so these return copies.
+  CameraState<Scalar> camera(std::int32_t i) const {
+    const Scalar* q = cams_.data() + static_cast<std::size_t>(i) * kCameraParams;
+    CameraState<Scalar> c;
+    c.rotation = {q[0], q[1], q[2]};
+    c.translation = {q[3], q[4], q[5]};
+    c.focal = q[6];
+    c.k1 = q[7];
+    c.k2 = q[8];
+    return c;
+  }
+  PointState<Scalar> point(std::int32_t i) const {
+    const Scalar* q = pts_.data() + static_cast<std::size_t>(i) * kPointParams;
+    PointState<Scalar> p;
+    p.position = {q[0], q[1], q[2]};
+    return p;
+  }
+  Observation<Scalar> observation(std::int64_t e) const {
+    const std::size_t k = static_cast<std::size_t>(e);
+    Observation<Scalar> o;
+    o.camera_id = cam_id_[k];
+    o.point_id = pt_id_[k];
+    o.pixel = {px_[k], py_[k]};
+    o.weight = w_[k];
+    return o;
+  }
+  std::vector<CameraState<Scalar>> cameras() const {
+    std::vector<CameraState<Scalar>> v;
+    for (std::int32_t i = 0; i < num_cameras(); ++i) v.push_back(camera(i));
+    return v;
+  }
+  std::vector<PointState<Scalar>> points() const {
+    std::vector<PointState<Scalar>> v;
+    for (std::int32_t i = 0; i < num_points(); ++i) v.push_back(point(i));
+    return v;
+  }
+  std::vector<Observation<Scalar>> observations() const {
+    std::vector<Observation<Scalar>> v;
+    for (std::int64_t e = 0; e < num_observations(); ++e) v.push_back(observation(e));
+    return v;
+  }
+  // BAProblem::validate (dba/problem.hpp:231-255): warnings, not errors.
+  std::vector<std::string> validate() const {
+    std::vector<std::string> w;
+    std::vector<bool> cu(static_cast<std::size_t>(num_cameras())), pu(static_cast<std::size_t>(num_points()));
+    for (std::size_t e = 0; e < cam_id_.size(); ++e) {
+      cu[static_cast<std::size_t>(cam_id_[e])] = true;
+      pu[static_cast<std::size_t>(pt_id_[e])] = true;
+    }
+    for (std::int32_t i = 0; i < num_cameras(); ++i)
+      if (!cu[static_cast<std::size_t>(i)]) w.push_back("camera " + std::to_string(i) + " is not referenced by any observation");
+    for (std::int32_t i = 0; i < num_points(); ++i)
+      if (!pu[static_cast<std::size_t>(i)]) w.push_back("point " + std::to_string(i) + " is not referenced by any observation");
+    for (std::int32_t i = 0; i < num_cameras(); ++i)
+      if (!(cams_[static_cast<std::size_t>(i) * kCameraParams + 6] > Scalar(0)))
+        w.push_back("camera " + std::to_string(i) + " has non-positive focal length");
+    return w;
+  }
   std::int32_t num_cameras() const { return static_cast<std::int32_t>(cams_.size() / kCameraParams); }
   std::int32_t num_points() const { return static_cast<std::int32_t>(pts_.size() / kPointParams); }
   std::int64_t num_observations() const { return static_cast<std::int64_t>(cam_id_.size()); }
@@ -251,18 +311,51 @@ struct SolverState {
   double cost = 0;
   TerminationReason termination = TerminationReason::max_iterations;
   std::vector<IterationRecord> history;
+  // Most recent trial, feeding the convergence decision (dba/solver.hpp:80-84).
+  bool last_accepted = false;
+  double last_cost_change = std::numeric_limits<double>::infinity();
+  double last_step_inf = std::numeric_limits<double>::infinity();
+  double previous_cost = std::numeric_limits<double>::infinity();
 };
 
-// dba::lm_solve on B200: config.workers ranks, rank 0's state.
+namespace detail {
+// dbag_result -> SolverState (parameters already written through r.x_c / x_p).
 template <typename Scalar>
-SolverState<Scalar> lm_solve(const BAProblem<Scalar>& problem, const SolverConfig& config) {
-  static_assert(sizeof(Scalar) == 4 || sizeof(Scalar) == 8, "Scalar must be float or double");
-  const dbag_problem p = problem.c_view();
-  const dbag_config c = config.c_view();
-  const int cap = config.max_iterations, k = config.workers;
+void fill_state(const dbag_result& r, int cap, int k, const std::vector<std::int32_t>& it,
+                const std::vector<double>& cost, const std::vector<double>& mse, const std::vector<double>& lam,
+                const std::vector<std::int32_t>& pcg, const std::vector<std::int32_t>& acc,
+                const std::vector<double>& wall, const std::vector<std::uint64_t>& we,
+                const std::vector<std::uint64_t>& wb, SolverState<Scalar>& st) {
+  st.lambda = r.lambda;
+  st.nu = r.nu;
+  st.iteration = r.iterations;
+  st.cost = r.cost;
+  st.termination = static_cast<TerminationReason>(r.termination);
+  st.last_accepted = r.last_accepted != 0;
+  st.last_cost_change = r.last_cost_change;
+  st.last_step_inf = r.last_step_inf;
+  st.previous_cost = r.previous_cost;
+  for (int i = 0; i < std::min(cap, r.iterations); ++i) {
+    IterationRecord rec;
+    rec.iteration = it[static_cast<std::size_t>(i)];
+    rec.cost = cost[static_cast<std::size_t>(i)];
+    rec.mse = mse[static_cast<std::size_t>(i)];
+    rec.lambda = lam[static_cast<std::size_t>(i)];
+    rec.pcg_iterations = pcg[static_cast<std::size_t>(i)];
+    rec.accepted = acc[static_cast<std::size_t>(i)] != 0;
+    rec.wall_seconds = wall[static_cast<std::size_t>(i)];
+    rec.worker_edges.assign(we.begin() + i * k, we.begin() + (i + 1) * k);
+    rec.worker_block_ops.assign(wb.begin() + i * k, wb.begin() + (i + 1) * k);
+    st.history.push_back(rec);
+  }
+}
+
+// Runs fn(dbag_result&) with record buffers sized for cap iterations x k ranks.
+template <typename Scalar, class Fn>
+SolverState<Scalar> solve_into(std::size_t ncam, std::size_t npt, int cap, int k, Fn&& fn) {
   SolverState<Scalar> st;
-  st.x_c.resize(problem.packed_cameras().size());
-  st.x_p.resize(problem.packed_points().size());
+  st.x_c.resize(ncam);
+  st.x_p.resize(npt);
   std::vector<std::int32_t> it(cap), pcg(cap), acc(cap);
   std::vector<double> cost(cap), mse(cap), lam(cap), wall(cap);
   std::vector<std::uint64_t> we(static_cast<std::size_t>(cap) * k), wb(static_cast<std::size_t>(cap) * k);
@@ -279,32 +372,30 @@ SolverState<Scalar> lm_solve(const BAProblem<Scalar>& problem, const SolverConfi
   r.rec_worker_block_ops = wb.data();
   r.x_c = st.x_c.data();
   r.x_p = st.x_p.data();
-  detail::check(dbag_lm_solve(static_cast<int>(sizeof(Scalar)), &p, &c, config.devices.data(),
-                              static_cast<int>(config.devices.size()), &r));
-  st.lambda = r.lambda;
-  st.nu = r.nu;
-  st.iteration = r.iterations;
-  st.cost = r.cost;
-  st.termination = static_cast<TerminationReason>(r.termination);
-  for (int i = 0; i < std::min(cap, r.iterations); ++i) {
-    IterationRecord rec;
-    rec.iteration = it[static_cast<std::size_t>(i)];
-    rec.cost = cost[static_cast<std::size_t>(i)];
-    rec.mse = mse[static_cast<std::size_t>(i)];
-    rec.lambda = lam[static_cast<std::size_t>(i)];
-    rec.pcg_iterations = pcg[static_cast<std::size_t>(i)];
-    rec.accepted = acc[static_cast<std::size_t>(i)] != 0;
-    rec.wall_seconds = wall[static_cast<std::size_t>(i)];
-    rec.worker_edges.assign(we.begin() + i * k, we.begin() + (i + 1) * k);
-    rec.worker_block_ops.assign(wb.begin() + i * k, wb.begin() + (i + 1) * k);
-    st.history.push_back(rec);
-  }
+  fn(r);
+  fill_state(r, cap, k, it, cost, mse, lam, pcg, acc, wall, we, wb, st);
   return st;
+}
+}  // namespace detail
+
+// dba::lm_solve on B200: config.workers ranks, rank 0's state.
+template <typename Scalar>
+SolverState<Scalar> lm_solve(const BAProblem<Scalar>& problem, const SolverConfig& config) {
+  static_assert(sizeof(Scalar) == 4 || sizeof(Scalar) == 8, "Scalar must be float or double");
+  const dbag_problem p = problem.c_view();
+  const dbag_config c = config.c_view();
+  return detail::solve_into<Scalar>(problem.packed_cameras().size(), problem.packed_points().size(),
+                                    config.max_iterations, config.workers, [&](dbag_result& r) {
+                                      detail::check(dbag_lm_solve(static_cast<int>(sizeof(Scalar)), &p, &c,
+                                                                  config.devices.data(),
+                                                                  static_cast<int>(config.devices.size()), &r));
+                                    });
 }
 
 // ---- partitioning (dba/partition.hpp) ----------------------------------------
 struct EdgePartition {
   int worker_rank = 0;
+  int worker_count = 1;  // B200 facade: K of the split this partition belongs to
   std::vector<std::int32_t> edge_ids;
   std::vector<std::int32_t> camera_to_global, point_to_global;  // LocalIndexMap::to_global
 };
@@ -326,6 +417,7 @@ std::vector<EdgePartition> partition_edges(const BAProblem<Scalar>& problem, int
                                  cblk.data(), pptr.data(), pblk.data()));
     EdgePartition e;
     e.worker_rank = r;
+    e.worker_count = worker_count;
     for (std::int64_t i = 0; i < count; ++i) e.edge_ids.push_back(static_cast<std::int32_t>(start + i));
     e.camera_to_global.assign(cg.begin(), cg.begin() + nc);
     e.point_to_global.assign(pg.begin(), pg.begin() + np);
@@ -480,3 +572,7 @@ void serialize_bal(const BAProblem<Scalar>& problem, std::ostream& out) {
 }
 
 }  // namespace dba
+
+// the operator level (WorkerGroup, BlockDiagonal, EdgeBlockMatrix, dse, dpcg,
+// EdgeEvaluator, assemble_local, lm_solve_rank, ...)
+#include "dba_b200_ops.hpp"

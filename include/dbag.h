@@ -86,6 +86,9 @@ typedef struct dbag_result {
   uint64_t* rec_worker_block_ops; /* capacity x workers */
   void* x_c;                      /* 9m Scalar (out, may be NULL) */
   void* x_p;                      /* 3n Scalar (out, may be NULL) */
+  /* SolverState's most recent trial (dba/solver.hpp:80-84) */
+  int32_t last_accepted;
+  double last_cost_change, last_step_inf, previous_cost;
 } dbag_result;
 
 /* SyntheticOptions (dba/synthetic.hpp:19-30) plus the count-exact extension of
@@ -190,6 +193,12 @@ int dbag_create_nccl(int device, int rank, int nranks, const unsigned char* nccl
 int dbag_create_nccl_ex(int device, int rank, int nranks, const unsigned char* nccl_id128, int precision,
                         int coupling_fp32, dbag_ctx** out);
 int dbag_destroy(dbag_ctx* ctx);
+/* Context holding shard `rank` of `nranks` (partition_edges) with LOCAL
+ * collectives: the per-partition operators of EdgeEvaluator::linearize / cost
+ * and assemble_local (dba/edge_eval.hpp:79-122, 289-309; dba/block_matrix.hpp:
+ * 335-388): cost and the assembled B, C, v, w are this partition's own
+ * contribution, not all-reduced. */
+int dbag_create_shard(int device, int precision, int coupling_fp32, int rank, int nranks, dbag_ctx** out);
 
 /* EdgeEvaluator ctor + PartitionedHessian ctor (dba/edge_eval.hpp:79-97,
  * dba/block_matrix.hpp:185-204, 344-352): partitions the full problem, keeps
@@ -291,6 +300,25 @@ int dbag_group_barrier(dbag_group* g, int rank);                                
 int dbag_group_allreduce_sum(dbag_group* g, int rank, void* data, int64_t len, int precision); /* :67-91 */
 int dbag_group_abort(dbag_group* g, const char* why);                              /* :96-105 */
 int dbag_group_sequence(dbag_group* g, int rank, uint64_t* out);                   /* :52-53 */
+/* Rank `rank` of the group as an operator context (dba/solver.hpp:149-257,
+ * 295-299 called inside run_on_workers): every collective of the context's
+ * operators (cost, linearize, damp_factor, dse, dpcg, ...) goes through the
+ * group. Call from that rank's own thread; the group outlives the context. */
+int dbag_create_group_rank(dbag_group* g, int rank, int precision, int coupling_fp32, dbag_ctx** out);
+/* lm_solve_rank (dba/solver.hpp:295-518) on an uploaded context: collective
+ * over the context's ranks; out->x_c / x_p receive the full, rank-identical
+ * state. */
+int dbag_lm_solve_ctx(dbag_ctx* ctx, const dbag_config* c, dbag_result* out);
+
+/* ---- FactoredBlockDiagonal (dba/block_matrix.hpp:118-167) on the device --- */
+/* LLT of nblocks BS x BS row-major blocks (bs = 3 or 9): `factor` receives the
+ * device format (lower factor, reciprocal pivots above the diagonal, bs*bs
+ * per block); *bad_block = the lowest non-positive-definite block or -1
+ * (DBAG_SINGULAR_BLOCK is returned then). */
+int dbag_block_factor(int device, int precision, int bs, int64_t nblocks, const void* blocks, void* factor,
+                      int64_t* bad_block);
+/* x := D^-1 x blockwise from dbag_block_factor's factor. */
+int dbag_block_solve(int device, int precision, int bs, int64_t nblocks, const void* factor, void* x);
 
 #ifdef __cplusplus
 }

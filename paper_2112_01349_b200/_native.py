@@ -35,7 +35,8 @@ class Result(C.Structure):
                 ("rec_cost", C.POINTER(f64)), ("rec_mse", C.POINTER(f64)), ("rec_lambda", C.POINTER(f64)),
                 ("rec_pcg", C.POINTER(i32)), ("rec_accepted", C.POINTER(i32)), ("rec_wall", C.POINTER(f64)),
                 ("rec_worker_edges", C.POINTER(u64)), ("rec_worker_block_ops", C.POINTER(u64)),
-                ("x_c", vp), ("x_p", vp)]
+                ("x_c", vp), ("x_p", vp), ("last_accepted", i32), ("last_cost_change", f64),
+                ("last_step_inf", f64), ("previous_cost", f64)]
 
 
 class SynthOptions(C.Structure):
@@ -74,6 +75,11 @@ _SIGS = {
     "dbag_group_abort": (C.c_int, [vp, C.c_char_p]),
     "dbag_group_sequence": (C.c_int, [vp, C.c_int, _P(u64)]),
     "dbag_destroy": (C.c_int, [vp]),
+    "dbag_create_shard": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _P(vp)]),
+    "dbag_create_group_rank": (C.c_int, [vp, C.c_int, C.c_int, C.c_int, _P(vp)]),
+    "dbag_lm_solve_ctx": (C.c_int, [vp, _P(Config), _P(Result)]),
+    "dbag_block_factor": (C.c_int, [C.c_int, C.c_int, C.c_int, i64, vp, vp, _P(i64)]),
+    "dbag_block_solve": (C.c_int, [C.c_int, C.c_int, C.c_int, i64, vp, vp]),
     "dbag_upload_problem": (C.c_int, [vp, _P(Problem), C.c_int]),
     "dbag_set_state": (C.c_int, [vp, vp, vp]),
     "dbag_get_state": (C.c_int, [vp, vp, vp]),

@@ -95,6 +95,10 @@ void fill_result(const Outcome& o, int K, dbag_result* out) {
   out->lambda = o.lambda;
   out->nu = o.nu;
   out->workers = K;
+  out->last_accepted = o.last_accepted ? 1 : 0;
+  out->last_cost_change = o.last_cost_change;
+  out->last_step_inf = o.last_step_inf;
+  out->previous_cost = o.previous_cost;
   const int n = std::min<int>(out->capacity, static_cast<int>(o.history.size()));
   for (int i = 0; i < n; ++i) {
     const Record& r = o.history[static_cast<std::size_t>(i)];
@@ -417,6 +421,30 @@ int dbag_create_ex(int device, int precision, int coupling_fp32, dbag_ctx** out)
 }
 
 int dbag_create(int device, int precision, dbag_ctx** out) { return dbag_create_ex(device, precision, 0, out); }
+
+namespace {
+// A context over `comm` (owned by the context) on `device`.
+void make_ctx(int device, int precision, int coupling_fp32, std::unique_ptr<Comm> comm, dbag_ctx** out) {
+  check_precision(precision);
+  if (coupling_fp32 && precision != 8)
+    throw Error(DBAG_INVALID_ARGUMENT, "coupling_fp32 needs precision 8 (FP64 arithmetic, FP32 E blocks)");
+  DBAG_CUDA(cudaSetDevice(device));
+  auto ctx = std::make_unique<dbag_ctx>();
+  ctx->precision = precision;
+  ctx->comm = std::move(comm);
+  if (precision == 8 && coupling_fp32) ctx->r64l = std::make_unique<Rank<double, float>>(device, ctx->comm.get());
+  else if (precision == 8) ctx->r64 = std::make_unique<Rank<double>>(device, ctx->comm.get());
+  else ctx->r32 = std::make_unique<Rank<float>>(device, ctx->comm.get());
+  *out = ctx.release();
+}
+}  // namespace
+
+int dbag_create_shard(int device, int precision, int coupling_fp32, int rank, int nranks, dbag_ctx** out) {
+  return guarded([&] {
+    if (nranks < 1 || rank < 0 || rank >= nranks) throw Error(DBAG_INVALID_ARGUMENT, "bad shard rank / count");
+    make_ctx(device, precision, coupling_fp32, std::make_unique<LocalComm>(rank, nranks), out);
+  });
+}
 
 int dbag_create_nccl_ex(int device, int rank, int nranks, const unsigned char* id, int precision, int coupling_fp32,
                         dbag_ctx** out) {
@@ -767,6 +795,113 @@ int dbag_group_sequence(dbag_group* h, int rank, uint64_t* out) {
   return guarded([&] {
     check_group_rank(h, rank);
     *out = h->g->sequence(rank);
+  });
+}
+
+int dbag_create_group_rank(dbag_group* h, int rank, int precision, int coupling_fp32, dbag_ctx** out) {
+  return guarded([&] {
+    check_group_rank(h, rank);
+    make_ctx(h->g->device_of(rank), precision, coupling_fp32, std::make_unique<GroupComm>(h->g.get(), rank), out);
+  });
+}
+
+int dbag_lm_solve_ctx(dbag_ctx* ctx, const dbag_config* c, dbag_result* out) {
+  return guarded([&] {
+    with_rank(ctx, [&](auto& rk) {
+      using R = std::remove_reference_t<decltype(rk)>;
+      using S = typename R::Scalar;
+      if (c->workers != ctx->comm->size())
+        throw Error(DBAG_INVALID_ARGUMENT, "config.workers must equal the context's rank count");
+      const Outcome o = lm_solve_rank(rk, *c, ctx->num_obs);
+      rk.gather_state(static_cast<S*>(out->x_c), static_cast<S*>(out->x_p));
+      fill_result(o, ctx->comm->size(), out);
+    });
+    ctx->cost_valid = false;
+  });
+}
+
+}  // extern "C"
+
+namespace {
+template <class S, int BS>
+void block_factor(std::int64_t nb, const void* blocks, void* factor, std::int64_t* bad) {
+  S *a = nullptr, *ad = nullptr, *f = nullptr;
+  unsigned long long* dbad = nullptr;
+  const std::size_t bytes = static_cast<std::size_t>(std::max<std::int64_t>(nb, 1)) * BS * BS * sizeof(S);
+  DBAG_CUDA(cudaMalloc(&a, bytes));
+  std::unique_ptr<void, void (*)(void*)> k1(a, [](void* q) { cudaFree(q); });
+  DBAG_CUDA(cudaMalloc(&ad, bytes));
+  std::unique_ptr<void, void (*)(void*)> k2(ad, [](void* q) { cudaFree(q); });
+  DBAG_CUDA(cudaMalloc(&f, bytes));
+  std::unique_ptr<void, void (*)(void*)> k3(f, [](void* q) { cudaFree(q); });
+  DBAG_CUDA(cudaMalloc(&dbad, sizeof(unsigned long long)));
+  std::unique_ptr<void, void (*)(void*)> k4(dbad, [](void* q) { cudaFree(q); });
+  DBAG_CUDA(cudaMemset(dbad, 0xff, sizeof(unsigned long long)));
+  if (nb > 0) {
+    DBAG_CUDA(cudaMemcpy(a, blocks, static_cast<std::size_t>(nb) * BS * BS * sizeof(S), cudaMemcpyHostToDevice));
+    dev::k_damp_factor<S, BS><<<grid_for(nb, 64, 1 << 30), 64>>>(nb, a, S(0), 0, ad, f,
+                                                                 static_cast<const std::int32_t*>(nullptr), dbad);
+    DBAG_LAUNCH_CHECK();
+    DBAG_CUDA(cudaMemcpy(factor, f, static_cast<std::size_t>(nb) * BS * BS * sizeof(S), cudaMemcpyDeviceToHost));
+  }
+  unsigned long long raw = ~0ull;
+  DBAG_CUDA(cudaMemcpy(&raw, dbad, sizeof(raw), cudaMemcpyDeviceToHost));
+  *bad = raw == ~0ull ? -1 : static_cast<std::int64_t>(raw);
+}
+template <class S, int BS>
+void block_solve(std::int64_t nb, const void* factor, void* x) {
+  if (nb <= 0) return;
+  S *f = nullptr, *v = nullptr;
+  DBAG_CUDA(cudaMalloc(&f, static_cast<std::size_t>(nb) * BS * BS * sizeof(S)));
+  std::unique_ptr<void, void (*)(void*)> k1(f, [](void* q) { cudaFree(q); });
+  DBAG_CUDA(cudaMalloc(&v, static_cast<std::size_t>(nb) * BS * sizeof(S)));
+  std::unique_ptr<void, void (*)(void*)> k2(v, [](void* q) { cudaFree(q); });
+  DBAG_CUDA(cudaMemcpy(f, factor, static_cast<std::size_t>(nb) * BS * BS * sizeof(S), cudaMemcpyHostToDevice));
+  DBAG_CUDA(cudaMemcpy(v, x, static_cast<std::size_t>(nb) * BS * sizeof(S), cudaMemcpyHostToDevice));
+  dev::k_block_solve<S, BS><<<grid_for(nb, 64, 1 << 30), 64>>>(nb, f, v);
+  DBAG_LAUNCH_CHECK();
+  DBAG_CUDA(cudaMemcpy(x, v, static_cast<std::size_t>(nb) * BS * sizeof(S), cudaMemcpyDeviceToHost));
+}
+void check_bs(int bs) {
+  if (bs != 3 && bs != 9) throw Error(DBAG_INVALID_ARGUMENT, "block size must be 3 or 9");
+}
+}  // namespace
+
+extern "C" {
+
+int dbag_block_factor(int device, int precision, int bs, int64_t nblocks, const void* blocks, void* factor,
+                      int64_t* bad_block) {
+  return guarded([&] {
+    check_precision(precision);
+    check_bs(bs);
+    DBAG_CUDA(cudaSetDevice(device));
+    std::int64_t bad = -1;
+    if (precision == 8) {
+      if (bs == 3) block_factor<double, 3>(nblocks, blocks, factor, &bad);
+      else block_factor<double, 9>(nblocks, blocks, factor, &bad);
+    } else {
+      if (bs == 3) block_factor<float, 3>(nblocks, blocks, factor, &bad);
+      else block_factor<float, 9>(nblocks, blocks, factor, &bad);
+    }
+    if (bad_block) *bad_block = bad;
+    if (bad >= 0)  // SingularBlockError(i, BS) (dba/block_matrix.hpp:128-129)
+      throw Error(DBAG_SINGULAR_BLOCK, "block " + std::to_string(bad) + " of size " + std::to_string(bs) +
+                                           " is not positive definite", bad, bs);
+  });
+}
+
+int dbag_block_solve(int device, int precision, int bs, int64_t nblocks, const void* factor, void* x) {
+  return guarded([&] {
+    check_precision(precision);
+    check_bs(bs);
+    DBAG_CUDA(cudaSetDevice(device));
+    if (precision == 8) {
+      if (bs == 3) block_solve<double, 3>(nblocks, factor, x);
+      else block_solve<double, 9>(nblocks, factor, x);
+    } else {
+      if (bs == 3) block_solve<float, 3>(nblocks, factor, x);
+      else block_solve<float, 9>(nblocks, factor, x);
+    }
   });
 }
 

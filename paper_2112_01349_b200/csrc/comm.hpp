@@ -80,6 +80,20 @@ class SelfComm final : public Comm {
   void allreduce_max(void*, std::int64_t, DType, cudaStream_t) override {}
 };
 
+// Shard `rank` of `size` evaluated on its own: collectives are the identity
+// (EdgeEvaluator / assemble_local semantics, one partition's contribution).
+class LocalComm final : public Comm {
+ public:
+  LocalComm(int rank, int size) : rank_(rank), size_(size) {}
+  int rank() const override { return rank_; }
+  int size() const override { return size_; }
+  void allreduce_sum(void*, std::int64_t, DType, cudaStream_t) override {}
+  void allreduce_max(void*, std::int64_t, DType, cudaStream_t) override {}
+
+ private:
+  int rank_, size_;
+};
+
 // Shared state of an in-process group of K ranks.
 class Group {
  public:

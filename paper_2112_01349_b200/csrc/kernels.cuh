@@ -579,6 +579,20 @@ __device__ __forceinline__ void llt_solve(const S* __restrict__ L, S* x) {
   }
 }
 
+// x := D^-1 x per block from the stored factor (FactoredBlockDiagonal::
+// solve_in_place, dba/block_matrix.hpp:140-152). Thread per block.
+template <class S, int BS>
+__global__ void k_block_solve(std::int64_t nb, const S* __restrict__ L, S* __restrict__ x) {
+  const std::int64_t i = blockIdx.x * std::int64_t(blockDim.x) + threadIdx.x;
+  if (i >= nb) return;
+  S v[BS];
+#pragma unroll
+  for (int r = 0; r < BS; ++r) v[r] = x[std::size_t(i) * BS + r];
+  llt_solve<S, BS>(L + std::size_t(i) * BS * BS, v);
+#pragma unroll
+  for (int r = 0; r < BS; ++r) x[std::size_t(i) * BS + r] = v[r];
+}
+
 // Explicit inverse of SPD blocks from their stored factor (L with 1/L_kk in
 // the upper triangle): A^-1 = L^-T L^-1. Used for the block-Jacobi
 // preconditioner z = B^-1 r (dba/solver.hpp:224-225) as a 9x9 GEMV.
