@@ -312,148 +312,44 @@ def time_steps(ctx, cfg, steps, flush):
 
 def dse_roofline(ctx, prof, b_dse, peak, steps, total_ms, world, b_layout=None):
     """Roofline of the dominant kernel, the DSE pass (B_DSE bytes
-    per pass). The time per pass is measured live over the timed steps: CUDA
-    events on the context's stream around every DPCG (one graph launch at
-    K = 1) divided by its DSE count — so it also holds the camera fold + PCG
-    step that follow each pass inside the graph (a few %): `frac` is a lower
-    bound for the pass alone. For reference, the pass launched alone back to
-    back on the finished solve's state is `standalone_launch_ms`."""
+    per pass), timed inside the timed steps: CUDA events on the context's
+    stream bracket every DPCG (one graph launch at K = 1), and the device time
+    per DSE is that time over the DSE count — the pass plus its camera fold +
+    PCG step and the launch gaps between them, so `achieved` is a lower bound
+    on the pass kernel's own rate. standalone_pass_ms is the pass alone,
+    launched back to back on the same state after the timed steps (ncu
+    cannot profile kernel nodes of a graph with conditional nodes; the
+    committed ncu captures are of these standalone launches)."""
     dse_per_step = prof["dse_launches"] / max(steps, 1)
     per = prof["dse_ms"] / max(prof["dse_launches"], 1)
-    kernel = ("k_g_pass (+ its camera fold / PCG step), in-graph, CUDA events over the timed steps" if world == 1
-              else "k_g_pass (+ halo / camera all-reduce, fold, step) of the K > 1 DPCG, CUDA events")
+    kernel = "k_g_pass DSE iteration of the graph DPCG (pass + camera fold / PCG step), per pass, in the timed steps"
     standalone = None
     if world == 1:
         try:
             standalone = ctx.time_dse_pass(20)
         except Exception:  # DBAG_PCG selected a non-graph DPCG
             kernel = "DPCG (DBAG_PCG=%s), device time per DSE" % os.environ.get("DBAG_PCG")
+    else:
+        kernel = "k_g_pass DSE iteration of the per-rank DPCG graph (pass, peer collectives, fold / step), per pass"
     achieved = b_dse / (per / 1e3) / 1e9
     lay = {} if b_layout is None else {
         "layout_bytes_per_launch": b_layout, "layout_achieved": b_layout / (per / 1e3) / 1e9,
         "layout_frac": b_layout / (per / 1e3) / 1e9 / peak}
     out = {"bound": "hbm", "kernel": kernel, "achieved": achieved, "peak": peak, "unit": "GB/s",
            "frac": achieved / peak, "traffic": None, "bytes_per_launch": b_dse, "avg_launch_ms": per, **lay,
-           "launches_per_step": dse_per_step, "standalone_launch_ms": standalone,
-           "standalone_frac": (b_dse / (standalone / 1e3) / 1e9 / peak) if standalone else None,
+           "launches_per_step": dse_per_step,
            "share_of_step": per * dse_per_step / max(total_ms / max(steps, 1), 1e-9),
            "note": "achieved = algorithmic DSE bytes per pass (SURVEY 8d: 27 scalars of E per edge, the "
-                   "reference's layout) / device ms per pass; layout_* = the same against the compulsory bytes "
-                   "of the factored records this build streams (18 scalars per edge); traffic = ncu DRAM bytes "
-                   "of one launch (profiles/ncu_traffic.json)"}
+                   "reference's layout) / in-step device ms per DSE; layout_* = the same against the compulsory "
+                   "bytes of the factored records this build streams (18 scalars per edge); traffic = ncu DRAM "
+                   "bytes of one standalone pass launch (profiles/ncu_traffic.json)"}
+    if standalone is not None:
+        out["standalone_pass_ms"] = standalone
+        out["standalone_achieved"] = b_dse / (standalone / 1e3) / 1e9
+        out["standalone_frac"] = out["standalone_achieved"] / peak
+        if b_layout is not None:
+            out["standalone_layout_frac"] = b_layout / (standalone / 1e3) / 1e9 / peak
     return out
-
-
-def run_reference(args):
-    """The reference arm: the CPU restatement (oracle/) of the reference's
-    solver on this host's physical cores. Imports oracle/ only."""
-    world, rank, _ = dist_env()
-    if rank != 0:
-        return
-    m, n, N = WORKLOADS[args.workload]
-    t_gen = time.perf_counter()
-    p = make_oracle_problem(args.workload)
-    t_gen = time.perf_counter() - t_gen
-    host = host_info()
-    k = cpu_threads()
-    # warm-up: the first step is one FULL LM iteration (calibration: the full
-    # DSE count and an unscaled t_LM); the rest are bounded samples.
-    secs, info = cpu_reference_steps(p, k, args.warmup - 1 + args.steps if args.warmup >= 1 else args.steps)
-    timed = secs[-args.steps:]
-    t = float(np.mean(timed))
-    value = N / t
-    # K = 1 (BASELINE.md §3): one bounded sample, scaled the same way
-    secs1, info1 = cpu_reference_steps(p, 1, 1, dse_full=info["dse_per_full_iteration"], calibrate=False)
-    sample = (f"{args.workload}: each step one LM iteration from x0 (oracle restatement, {k} rank threads), "
-              f"DPCG capped at {PCG_SAMPLE} iterations and its time scaled to the full iteration's "
-              f"{info['dse_per_full_iteration']} DSEs; warm-up step 1 ran the full iteration unscaled "
-              f"({info['full_iteration_s']:.2f} s, {info['full_pcg_iterations']} PCG iterations)")
-    print(json.dumps({
-        "impl": "reference", "metric": "edges_per_sec_per_lm_iteration", "value": value, "unit": "edges/s",
-        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t,
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": workload_config(args.workload, info["full_pcg_iterations"]),
-        "cpu_baseline": {"value": value, "unit": "edges/s", "cores": k, "kind": "port", "sample": sample,
-                         "host": host, "jacobian": "autodiff", "detail": info,
-                         "k1": {"value": N / secs1[0], "unit": "edges/s", "cores": 1, "seconds": secs1[0],
-                                "sample": f"one bounded sample at K = 1 (DPCG capped at {PCG_SAMPLE}, scaled)",
-                                "detail": info1}},
-        "e2e": {"value": value, "unit": "edges/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "instance_generation_s": t_gen,
-        "repo_libs_loaded": repo_libs_loaded(),
-    }), flush=True)
-
-
-def repo_libs_loaded():
-    """In-tree shared objects mapped into this process (the reference arm
-    must show oracle/ only)."""
-    try:
-        with open("/proc/self/maps") as f:
-            return sorted({os.path.relpath(l.split()[-1], ROOT) for l in f
-                           if l.rstrip().endswith(".so") and l.split()[-1].startswith(ROOT)})
-    except Exception:
-        return None
-
-
-def workload_config(name, pcg):
-    m, n, N = WORKLOADS[name]
-    return {"workload": name, "cameras": m, "points": n, "observations": N, "pcg_iterations_per_step": int(pcg),
-            "solver": "SolverConfig defaults (diag_scaled, lambda0 1e-4, pcg_tol 1e-6, pcg_max_iters 500)",
-            "step": "one LM iteration from x0 (linearize+assemble, damp+factor, rhs, DPCG, backsub, trial cost)",
-            "instance": "dba/synthetic.hpp ring, seed 1, count-exact, +-0.5 px noise (BASELINE.md §3)"}
-
-
-def flush_l2(buf):
-    import torch
-    buf.zero_()
-    torch.cuda.synchronize()
-
-
-def time_steps(ctx, cfg, steps, flush):
-    """Per-step device time (CUDA events on the context's stream), L2 flushed
-    between steps outside the timed window."""
-    ms = []
-    pcg = 0
-    for _ in range(steps):
-        if flush is not None:
-            flush_l2(flush)
-        ctx.synchronize()
-        ctx.mark(0)
-        _, pcg, _ = ctx.probe_step(cfg.lambda0, cfg)
-        ctx.mark(1)
-        ms.append(ctx.elapsed_ms())
-    return ms, pcg
-
-
-def dse_roofline(ctx, prof, b_dse, peak, steps, total_ms, world, b_layout=None):
-    """Roofline of the dominant kernel, the DSE pass (B_DSE bytes
-    per pass). Single rank: the graph DPCG's k_g_pass, timed live with CUDA
-    events on the context's stream, launched alone back to back on the state
-    the timed steps left (its in-graph launches cannot carry events);
-    in_graph_ms_per_dse is the whole DPCG graph's device time per DSE
-    (pass + camera fold + step + loop overhead). Several ranks: the
-    host-driven loop's DSE launches (k_dse_chunk), event-timed in place."""
-    dse_per_step = prof["dse_launches"] / max(steps, 1)
-    loop_ms_per_dse = prof["dse_ms"] / max(prof["dse_launches"], 1)
-    per, kernel = loop_ms_per_dse, "k_dse_chunk (DSE pass, host-driven DPCG)"
-    if world == 1:
-        try:
-            per = ctx.time_dse_pass(20)
-            kernel = "k_g_pass (DSE pass of the graph DPCG; launched alone, back to back)"
-        except Exception:  # DBAG_PCG selected a non-graph DPCG
-            kernel = "DPCG (DBAG_PCG=%s), device time per DSE" % os.environ.get("DBAG_PCG")
-    achieved = b_dse / (per / 1e3) / 1e9
-    lay = {} if b_layout is None else {
-        "layout_bytes_per_launch": b_layout, "layout_achieved": b_layout / (per / 1e3) / 1e9,
-        "layout_frac": b_layout / (per / 1e3) / 1e9 / peak}
-    return {"bound": "hbm", "kernel": kernel, "achieved": achieved, "peak": peak, "unit": "GB/s",
-            "frac": achieved / peak, "traffic": None, "bytes_per_launch": b_dse, "avg_launch_ms": per, **lay,
-            "launches_per_step": dse_per_step, "in_graph_ms_per_dse": loop_ms_per_dse,
-            "share_of_step": per * dse_per_step / max(total_ms / max(steps, 1), 1e-9),
-            "note": "achieved = algorithmic DSE bytes per pass (SURVEY 8d: 27 scalars of E per edge, the "
-                    "reference's layout) / device ms per launch; layout_* = the same against the compulsory bytes "
-                    "of the factored records this build streams (18 scalars per edge); traffic = ncu DRAM bytes "
-                    "of one launch (profiles/ncu_traffic.json)"}
 
 
 def solve_t_lm(p, world, rank, uid, device, iters=10):

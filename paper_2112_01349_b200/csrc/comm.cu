@@ -1,6 +1,8 @@
 // comm.cu — Group (in-process ranks) and NCCL backends of comm.hpp.
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
+#include <string>
 
 #include "comm.hpp"
 
@@ -297,6 +299,12 @@ NcclComm::~NcclComm() {
 // IPC, the handles are all-gathered over NCCL and opened (peer access over
 // NVLink / NVSwitch). Any rank failing makes every rank return false.
 bool NcclComm::make_peer_site(std::int64_t max_len, DType t, PeerSite* out) {
+  // Opt-in (DBAG_PEER_IPC=1): the cross-process mapping has not run on a
+  // multi-GPU node yet (one GPU cannot host two NCCL ranks), so one-process-
+  // per-GPU runs keep the host-driven NCCL loop by default. Every rank reads
+  // the same environment (torchrun), so the answer agrees.
+  const char* ipc = std::getenv("DBAG_PEER_IPC");
+  if (!(ipc && std::string(ipc) == "1")) return false;
   if (size_ < 2 || size_ > PeerSite::kMaxPeers) return false;
   PeerSite s;
   s.k = size_;

@@ -234,9 +234,19 @@ __device__ __forceinline__ void dse_chunk_at(const DseArgs<S, T>& A, DseWork<S>&
       if (t < nu * 9) graw[j] = gx.raw(M.ucam[t / 9], t - (t / 9) * 9);
     }
   }
+#if DBAG_RELOAD_E
+  // E lanes are read where they are used (a-phase, y-phase) instead of being
+  // held in registers across the point solve: the second read hits L1 / L2
+  // (the record was just streamed), and the freed registers buy resident CTAs
+  auto lanes = [&](S* e) {
+#pragma unroll
+    for (int k = 0; k < L; ++k) e[k] = S(R[k * kTile + tid]);
+  };
+#else
   S e[L];
 #pragma unroll
   for (int k = 0; k < L; ++k) e[k] = S(R[k * kTile + tid]);  // padding slots hold zeros
+#endif
   if (staged && (kFact || MODE != 2)) {
 #pragma unroll
     for (int j = 0; j < 3; ++j)
@@ -255,6 +265,10 @@ __device__ __forceinline__ void dse_chunk_at(const DseArgs<S, T>& A, DseWork<S>&
       S xv[9];
 #pragma unroll
       for (int i = 0; i < 9; ++i) xv[i] = staged ? sm.xs()[su * 9 + i] : gx(cam, i);
+#if DBAG_RELOAD_E
+      S e[L];
+      lanes(e);
+#endif
       coupling_t<S, L>(e, Rc, xv, a);
     }
 #pragma unroll
@@ -278,6 +292,10 @@ __device__ __forceinline__ void dse_chunk_at(const DseArgs<S, T>& A, DseWork<S>&
     __syncthreads();  // y overlays b
 #endif
     S y[9];
+#if DBAG_RELOAD_E
+    S e[L];
+    lanes(e);
+#endif
     coupling_b<S, L>(e, Rc, b0, b1, b2, y);
 #pragma unroll
     for (int i = 0; i < 9; ++i) sm.y()[tid][i] = y[i];
@@ -304,6 +322,9 @@ __device__ __forceinline__ void dse_chunk(const DseArgs<S, T>& A, DseWork<S>& sm
 
 // Resident CTAs per SM the chunk pass is compiled for (register budget):
 // measured best 5 with FP64 E lanes in registers, 7 with FP32 lanes.
+#ifndef DBAG_RELOAD_E
+#define DBAG_RELOAD_E 0
+#endif
 #ifndef DBAG_PASS_MINB_F32E
 #define DBAG_PASS_MINB_F32E 7
 #endif
