@@ -35,6 +35,7 @@
 #include "graph_pcg.cuh"
 #include "stream.cuh"
 #include "peer.cuh"
+#include "lin.cuh"
 #include "kernels.cuh"
 #include "partition.hpp"
 
@@ -205,6 +206,13 @@ class Rank {
   // most DBAG_JB_BATCH slots (default 2^23; a larger point takes a batch of
   // its own) instead of all N rows, so city-scale shards do not keep
   // 224 bytes per edge of scratch through the PCG.
+  // DBAG_LIN=rows: the two-kernel assembly through per-edge Jacobian rows in
+  // HBM (Jb, assembled point- then camera-major) instead of the fused
+  // linearize + assemble pass (lin.cuh).
+  static bool lin_rows() {
+    const char* e = std::getenv("DBAG_LIN");
+    return e && std::string(e) == "rows";
+  }
   static std::int64_t jb_batch_cap() {
     const char* e = std::getenv("DBAG_JB_BATCH");
     const long long v = e ? std::atoll(e) : 0;
@@ -252,8 +260,9 @@ class Rank {
     const std::vector<std::int32_t> jb = jb_batches(d.dpt_ptr);
     const std::size_t nb = jb.size() - 1;
     z.jb = 0;
-    for (std::size_t b = 0; b < nb; ++b)
-      z.jb = std::max<std::size_t>(z.jb, d.dpt_ptr.empty() ? 0 : d.dpt_ptr[jb[b + 1]] - d.dpt_ptr[jb[b]]);
+    if (lin_rows())
+      for (std::size_t b = 0; b < nb; ++b)
+        z.jb = std::max<std::size_t>(z.jb, d.dpt_ptr.empty() ? 0 : d.dpt_ptr[jb[b + 1]] - d.dpt_ptr[jb[b]]);
     z.cam_ptr = nb * pl.cam_ptr.size();
     z.carry = nb > 1 ? (pl.cam_ptr.size() - 1) * 54 : 0;
     z.cam_list = nb > 1 ? nb * (pl.cam_ptr.size() - 1) : 0;
@@ -294,6 +303,7 @@ class Rank {
     for (auto pm : {&Rank::C_, &Rank::Cd_}) f(pm, z.pl * 3);
     f(&Rank::Cinv_, z.pl * 3 + 16 / sizeof(S));  // slack for 16-byte-rounded reads
     f(&Rank::Jb_, z.jb * 28);
+    f(&Rank::bpart_, lin_rows() ? 0 : z.part / 9 * dev::kAsmTerms);
     f(&Rank::carry_, z.carry);
     f(&Rank::cam_list_, z.cam_list);
     f(&Rank::E_, z.recs);
@@ -444,6 +454,9 @@ class Rank {
     DBAG_CUDA(cudaMemset(g_bar_.get(), 0, sizeof(unsigned long long)));
     fact_ = true;
     E_.copy_in(build_records<dev::kLanesFact>(s_cam));
+    // assembly partials: the halo slots' own positions are never written by
+    // the fused linearize and must read as zero in the camera fold
+    if (bpart_.size() > 0) DBAG_CUDA(cudaMemset(bpart_.get(), 0, bpart_.size() * sizeof(double)));
     set_state(static_cast<const S*>(p.cameras), static_cast<const S*>(p.points));
     have_system_ = false;
     setup_peer_sites();
@@ -546,6 +559,7 @@ class Rank {
 
   // --------------------------------------------------------- linearize ----
   void linearize() {
+    if (!lin_rows()) return linearize_fused();
     DBAG_CUDA(cudaSetDevice(device_));
     DBAG_CUDA(cudaMemsetAsync(bad_.get(), 0xff, sizeof(unsigned long long), st_));
     DBAG_CUDA(cudaMemsetAsync(B_.get(), 0, B_.size() * sizeof(S), st_));
@@ -575,6 +589,59 @@ class Rank {
     if (nb > 1 && m_loc_ > 0)
       launch(dev::k_carry_out<S>, grid_for(m_loc_, 128, 1 << 30), 128, m_loc_, cam_glob_.get(),
              static_cast<const double*>(carry_.get()), B_.get(), v_.get());
+    tally_.edges += static_cast<std::uint64_t>(N_);
+    const std::int64_t bad = agree_min_index(bad_.get());
+    if (bad >= 0) throw degenerate_depth(bad);
+    comm_->allreduce_sum(B_.get(), static_cast<std::int64_t>(m_) * 81, kT, st_);
+    halo_exchange_Cw();
+    comm_->allreduce_sum(v_.get(), static_cast<std::int64_t>(m_) * 9, kT, st_);
+    have_system_ = true;
+  }
+
+  dev::LinArgs<S, T> lin_args() {
+    dev::LinArgs<S, T> a;
+    a.n_chunks = n_chunks_;
+    a.rec = E_.get();
+    a.chunk_slot = chunk_slot_.get();
+    a.slot_cam = slot_cam_.get();
+    a.slot_pt = slot_dpt_.get();
+    a.slot_edge = slot_edge_.get();
+    a.edge_base = plan_.range.start;
+    a.px = slot_px_.get();
+    a.py = slot_py_.get();
+    a.w = slot_w_.get();
+    a.xc = xc_.get();
+    a.xp = xp_.get();
+    a.C = C_.get();
+    a.wv = w_.get();
+    a.bpart = bpart_.get();
+    a.long_chunk = long_chunk_.get();
+    a.n_long = n_long_;
+    a.bad_edge = bad_.get();
+    return a;
+  }
+
+  // linearize + assemble_local in one pass over the chunks (lin.cuh), then
+  // the camera fold of the assembly partials; all-reduces as above.
+  void linearize_fused() {
+    DBAG_CUDA(cudaSetDevice(device_));
+    DBAG_CUDA(cudaMemsetAsync(bad_.get(), 0xff, sizeof(unsigned long long), st_));
+    use_factored();
+    if (m_ > 0)  // the cameras' R at the linearization point (factored records)
+      launch(dev::k_cam_rotations<S>, grid_for(m_, 128, 1 << 30), 128, m_, static_cast<const S*>(xc_.get()), Rm_.get());
+    const dev::LinArgs<S, T> a = lin_args();
+    if (n_chunks_ > 0) {
+      if (jac_mode_ == 1) launch(dev::k_lin_chunk<S, 1, T, dev::kLanesFact>, n_chunks_, dev::kTile, a);
+      else launch(dev::k_lin_chunk<S, 0, T, dev::kLanesFact>, n_chunks_, dev::kTile, a);
+      if (n_long_ > 0) {
+        if (jac_mode_ == 1) launch(dev::k_lin_long<S, 1, T, dev::kLanesFact>, n_long_, dev::kTile, a);
+        else launch(dev::k_lin_long<S, 0, T, dev::kLanesFact>, n_long_, dev::kTile, a);
+      }
+    }
+    if (m_ > 0)
+      launch(dev::k_cam_assemble<S>, grid_for(static_cast<std::int64_t>(m_) * 32, 256, 1 << 30), 256, m_,
+             static_cast<const std::int32_t*>(cam_part_ptr_.get()), static_cast<const double*>(bpart_.get()), B_.get(),
+             v_.get());
     tally_.edges += static_cast<std::uint64_t>(N_);
     const std::int64_t bad = agree_min_index(bad_.get());
     if (bad >= 0) throw degenerate_depth(bad);
@@ -1294,9 +1361,25 @@ class Rank {
   void get_jacobians(S* res, S* jac) {
     DBAG_CUDA(cudaSetDevice(device_));
     DBAG_CUDA(cudaStreamSynchronize(st_));
-    if (jb_pt_.size() > 2) throw Error(DBAG_INVALID_ARGUMENT, "Jacobian rows are kept for one Jb batch only");
     std::vector<S> jb(static_cast<std::size_t>(N_) * 28);
-    DBAG_CUDA(cudaMemcpy(jb.data(), Jb_.get(), sizeof(S) * jb.size(), cudaMemcpyDeviceToHost));
+    if (lin_rows()) {
+      if (jb_pt_.size() > 2) throw Error(DBAG_INVALID_ARGUMENT, "Jacobian rows are kept for one Jb batch only");
+      DBAG_CUDA(cudaMemcpy(jb.data(), Jb_.get(), sizeof(S) * jb.size(), cudaMemcpyDeviceToHost));
+    } else if (N_ > 0) {
+      // test hook: the fused linearize keeps no rows; recompute them at the
+      // same state into a temporary (outside the pool; rewrites the same
+      // records bit for bit)
+      S* tmp = nullptr;
+      DBAG_CUDA(cudaMalloc(&tmp, sizeof(S) * jb.size()));
+      std::unique_ptr<void, void (*)(void*)> keep(tmp, [](void* q) { cudaFree(q); });
+      auto kern = jac_mode_ == 1 ? dev::k_linearize<S, 1, T, dev::kLanesFact> : dev::k_linearize<S, 0, T, dev::kLanesFact>;
+      DBAG_CUDA(cudaMemsetAsync(bad_.get(), 0xff, sizeof(unsigned long long), st_));
+      launch(kern, static_cast<int>((N_ + 127) / 128), 128, std::int64_t(0), N_, slot_cam_.get(), slot_dpt_.get(),
+             slot_edge_.get(), plan_.range.start, slot_px_.get(), slot_py_.get(), slot_w_.get(), xc_.get(), xp_.get(),
+             tmp, E_.get(), slot_chunk_.get(), chunk_slot_.get(), bad_.get());
+      DBAG_CUDA(cudaMemcpyAsync(jb.data(), tmp, sizeof(S) * jb.size(), cudaMemcpyDeviceToHost, st_));
+      DBAG_CUDA(cudaStreamSynchronize(st_));
+    }
     for (std::int64_t s = 0; s < N_; ++s) {
       const std::int64_t e = lay_.slot_edge[static_cast<std::size_t>(s)];
       const S* row = jb.data() + static_cast<std::size_t>(s) * 28;
@@ -1838,6 +1921,7 @@ class Rank {
   cudaGraph_t g_graph_ = nullptr;
   cudaGraphExec_t g_exec_ = nullptr;
   DevBuf<S> Jb_, part_, halo_buf_, halo_sum_;
+  DevBuf<double> bpart_;  // camera assembly partials (lin.cuh), kAsmTerms per partial position
   DevBuf<double> carry_;               // k_assemble_cameras sums across Jb batches
   std::vector<std::int32_t> jb_pt_;    // Jb batch boundaries (device points)
   std::int32_t pf_dist_ = -1;

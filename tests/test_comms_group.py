@@ -154,9 +154,12 @@ def test_more_than_sixteen_ranks():
     st = dba.lm_solve(p, dba.SolverConfig(workers=20, max_iterations=2))
     from oracle import oracle as O
     o = O.lm_solve(p, dba.SolverConfig(workers=20, max_iterations=2))
+    # this radius-8 ring at pcg_tol 1e-6: the reference itself moves ~1e-9
+    # across K (reassociation); the bar is twice that spread or 1e-9
+    o1 = O.lm_solve(p, dba.SolverConfig(workers=1, max_iterations=2))
     assert [r.accepted for r in st.history] == [r.accepted for r in o.history]
-    for a, b in zip(st.history, o.history):
-        assert abs(a.cost - b.cost) <= 1e-9 * b.cost
+    for a, b, c in zip(st.history, o.history, o1.history):
+        assert abs(a.cost - b.cost) <= max(1e-9 * b.cost, 2 * abs(b.cost - c.cost))
 
 
 def test_lm_state_assembled_over_the_group():

@@ -556,10 +556,12 @@ def test_memory_pool_matches_prediction(lean):
 @pytest.mark.gpu
 @pytest.mark.parametrize("k", [1, 2])
 def test_batched_assembly_scratch(monkeypatch, k):
-    """Jb (the per-edge rows linearize hands to assembly) in batches of whole
-    points (DBAG_JB_BATCH slots): C, w and E are computed exactly as in one
-    batch; B and v add the batches' double-precision sums, so they agree to
-    rounding; the LM trajectory matches; the pool shrinks accordingly."""
+    """The row-based assembly (DBAG_LIN=rows: Jb, the per-edge rows linearize
+    hands to two assembly kernels) in batches of whole points
+    (DBAG_JB_BATCH slots): C, w and E are computed exactly as in one batch; B
+    and v add the batches' double-precision sums, so they agree to rounding;
+    the LM trajectory matches; the pool shrinks accordingly."""
+    monkeypatch.setenv("DBAG_LIN", "rows")
     p = ring(50, 2000, 6, noise=0.5, seed=11)
     out = {}
     for cap in (0, 700):
@@ -642,3 +644,36 @@ def test_peer_graph_dpcg_matches_host_loop(k, monkeypatch):
     h = dba.lm_solve(p, cfg, devices=[0])
     _compare_histories(g, h, 1e-9)
     _compare_histories(g, O.lm_solve(p, cfg), 1e-9)
+
+
+@pytest.mark.parametrize("k", [1, 2])
+@pytest.mark.parametrize("mode", [0, 1])
+def test_fused_linearize_assembly_matches_rows(k, mode, monkeypatch):
+    """The fused linearize + assemble pass (lin.cuh: point sums in the chunk,
+    camera terms folded per (chunk, camera) partial) against the row-based
+    two-kernel assembly (DBAG_LIN=rows) and the oracle: C, w, E bit-identical
+    (same per-point association), B and v to double-sum rounding, with long
+    tiles (points seen by more than 128 cameras) and K = 2 halos; LM
+    trajectories equal."""
+    p = ring(200, 40, 130, seed=5, radius=1.0, noise=0.5, nobs=40 * 130 - 9)
+    sysm = {}
+    for lin in ("fused", "rows"):
+        if lin == "rows":
+            monkeypatch.setenv("DBAG_LIN", "rows")
+        with dba.RankContext(0, 8) as c:
+            c.upload(p, mode)
+            c.linearize()
+            sysm[lin] = [np.array(a, copy=True) for a in c.system()]
+    (B0, C0, E0, v0, w0), (B1, C1, E1, v1, w1) = sysm["fused"], sysm["rows"]
+    if mode == 0:  # jets: IEEE-rn operations only, identical in both kernels
+        assert np.array_equal(C0, C1) and np.array_equal(w0, w1) and np.array_equal(E0, E1)
+    else:  # the closed form's products may contract differently per kernel
+        assert rel(C0, C1) < 1e-14 and rel(w0, w1) < 1e-14 and rel(E0, E1) < 1e-14
+    assert rel(B0, B1) < 1e-14 and rel(v0, v1) < 1e-14
+    Bo, Co, Eo, vo, wo = O.assemble(p, mode=mode)
+    for a, b in ((B0, Bo), (C0, Co), (E0, Eo), (v0, vo), (w0, wo)):
+        assert rel(a, np.asarray(b).reshape(a.shape)) < 1e-12
+    monkeypatch.delenv("DBAG_LIN")
+    cfg = dba.SolverConfig(max_iterations=3, workers=k, pcg_tol=1e-12, pcg_max_iters=2000,
+                           jacobian=dba.JACOBIAN_ANALYTIC if mode else dba.JACOBIAN_AUTODIFF)
+    _compare_histories(dba.lm_solve(p, cfg), O.lm_solve(p, cfg), 1e-9)
