@@ -674,6 +674,14 @@ class Rank {
     DBAG_CUDA(cudaStreamSynchronize(st_));
     unsigned long long raw[2];
     std::memcpy(raw, hbuf_, sizeof(raw));
+    // Points no edge observes keep a zero C block (no rank holds them); the
+    // reference factors all n blocks, so its damped zero block — lambda I or
+    // lambda * 1e-6 I — fails the pivot test when it is not positive.
+    if (!orphans_.empty()) {
+      const S d = policy == 0 ? lam : lam * static_cast<S>(1e-6);
+      if (!(d > S(0)) && !(d != d))
+        raw[0] = std::min<unsigned long long>(raw[0], static_cast<unsigned long long>(orphans_.front()));
+    }
     // -index (none = -inf): the max over ranks is the lowest failing index.
     const double none = -std::numeric_limits<double>::infinity();
     double agree[2] = {raw[0] == ~0ull ? none : -double(raw[0]), raw[1] == ~0ull ? none : -double(raw[1])};

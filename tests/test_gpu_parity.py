@@ -508,6 +508,20 @@ def test_unobserved_camera_and_point(k):
     _compare_histories(g, o, 1e-9)
     assert np.array_equal(g.x_c.reshape(-1, 9)[12], cams2[12]) and np.array_equal(g.x_p.reshape(-1, 3)[80], pts2[80])
     assert np.abs(g.x_c - o.x_c).max() < 1e-6 and np.abs(g.x_p - o.x_p).max() < 1e-8
+    # lambda0 = 0: the reference factors the unobserved point's zero block
+    # too and names it (dba/block_matrix.hpp:123-134; C before B)
+    with dba.RankContext(0, 8) as c:
+        c.upload(p)
+        c.linearize()
+        for policy in (dba.DAMPING_IDENTITY, dba.DAMPING_DIAG_SCALED):
+            with pytest.raises(dba.SingularBlockError) as ei:
+                c.damp_factor(0.0, policy)
+            assert ei.value.block_index == 80 and ei.value.block_size == 3
+        c.damp_factor(1e-4, dba.DAMPING_DIAG_SCALED)  # damped: factorable
+    # inside LM the failure is a reject (dba/solver.hpp:426-430), as in the oracle
+    cfg0 = dba.SolverConfig(max_iterations=2, workers=k, lambda0=0.0)
+    g0, o0 = dba.lm_solve(p, cfg0), O.lm_solve(p, cfg0)
+    assert [r.accepted for r in g0.history] == [r.accepted for r in o0.history] == [False, False]
     empty = dba.BAProblem.from_arrays(cams[:2], pts[:3], np.zeros(0, np.int32), np.zeros(0, np.int32), np.zeros((0, 2)))
     with pytest.raises(dba.InvalidArgumentError):
         dba.lm_solve(empty, dba.SolverConfig(max_iterations=3))
