@@ -1,10 +1,13 @@
 // comm.cu — Group (in-process ranks) and NCCL backends of comm.hpp.
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <memory>
 #include <string>
 
 #include "comm.hpp"
+#include "peer.cuh"
 
 namespace dbag {
 namespace {
@@ -58,6 +61,7 @@ Group::Group(int k, std::vector<int> devices, std::chrono::milliseconds timeout)
   scratch_bytes_.assign(static_cast<std::size_t>(k), 0);
   peer_mem_.resize(static_cast<std::size_t>(k));
   peer_dep_.resize(static_cast<std::size_t>(k));
+  peer_ok_.assign(static_cast<std::size_t>(k), 0);
   int prev = 0;
   DBAG_CUDA(cudaGetDevice(&prev));
   for (int r = 0; r < k; ++r) {
@@ -124,12 +128,17 @@ bool Group::make_peer_site(int rank, std::int64_t max_len, DType t, PeerSite* ou
   PeerSite s;
   s.k = k_;
   s.rank = rank;
-  PeerSite::plan(max_len, s.k, &s.slice, &s.nslice);
+  std::vector<int> devs(devices_);
+  std::sort(devs.begin(), devs.end());
+  const bool shared = std::adjacent_find(devs.begin(), devs.end()) != devs.end();
+  PeerSite::plan(max_len, s.k, shared, &s.slice, &s.nslice);
+  s.len = std::max<std::int64_t>(max_len, 1);
   int prev = 0;
   DBAG_CUDA(cudaGetDevice(&prev));
   DBAG_CUDA(cudaSetDevice(device_of(rank)));
   const PeerAlloc a = peer_alloc(max_len, t, s.nslice);
   DBAG_CUDA(cudaSetDevice(prev));
+  auto check = std::make_unique<PeerCheck>(s, device_of(rank));
   {
     std::lock_guard<std::mutex> lk(mu_);
     peer_mem_[static_cast<std::size_t>(rank)].push_back(a.base);
@@ -149,8 +158,64 @@ bool Group::make_peer_site(int rank, std::int64_t max_len, DType t, PeerSite* ou
     s.epoch = peer_dep_[static_cast<std::size_t>(rank)].epoch;
   }
   rendezvous(rank);  // every rank has read the table before the next site overwrites it
+  // the same self-check as the IPC path (k_peer_selftest), agreed over the group
+  const int ok = check->run(s);
+  check.reset();  // freed before the rendezvous: no rank frees while another's check may still wait on it
+  {
+    std::lock_guard<std::mutex> lk(mu_);
+    peer_ok_[static_cast<std::size_t>(rank)] = ok;
+  }
+  rendezvous(rank);
+  int all = 1;
+  {
+    std::lock_guard<std::mutex> lk(mu_);
+    for (int v : peer_ok_) all = std::min(all, v);
+  }
+  rendezvous(rank);  // peer_ok_ read by every rank before the next site
+  if (!all) return false;
   *out = s;
   return true;
+}
+
+// Buffers of the site self-check, allocated before any rank's check kernel
+// can be spinning: cudaMalloc / cudaFree may wait for the whole device, and
+// with several ranks on one device that wait would starve the peer the
+// spinning kernel is waiting for.
+PeerCheck::PeerCheck(const PeerSite& s, int device) : device_(device) {
+  int prev = 0;
+  DBAG_CUDA(cudaGetDevice(&prev));
+  DBAG_CUDA(cudaSetDevice(device));
+  DBAG_CUDA(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking));
+  DBAG_CUDA(cudaMalloc(&buf_, static_cast<std::size_t>(s.slice) * std::max(s.nslice, 1) * sizeof(double)));
+  DBAG_CUDA(cudaMalloc(&bad_, sizeof(int)));
+  DBAG_CUDA(cudaMemset(bad_, 0, sizeof(int)));
+  DBAG_CUDA(cudaDeviceSynchronize());
+  DBAG_CUDA(cudaSetDevice(prev));
+}
+PeerCheck::~PeerCheck() {
+  cudaSetDevice(device_);
+  cudaFree(buf_);
+  cudaFree(bad_);
+  cudaStreamDestroy(st_);
+}
+// 1 if two all-reduces through the site give the closed-form sums on this
+// rank (2 s peer timeout); DBAG_PEER_SELFTEST_FAIL=1 forces 0 (tests of the
+// fallback). Collective: every rank of the site runs it; no allocation or
+// device-wide synchronization between the launch and the stream sync.
+int PeerCheck::run(const PeerSite& s) {
+  int prev = 0;
+  DBAG_CUDA(cudaGetDevice(&prev));
+  DBAG_CUDA(cudaSetDevice(device_));
+  dev::k_peer_selftest<double><<<s.nslice, dev::kPeerThreads, 0, st_>>>(s, buf_, 2, bad_);
+  DBAG_LAUNCH_CHECK();
+  int h = 1;
+  DBAG_CUDA(cudaMemcpyAsync(&h, bad_, sizeof(int), cudaMemcpyDeviceToHost, st_));
+  DBAG_CUDA(cudaStreamSynchronize(st_));
+  DBAG_CUDA(cudaSetDevice(prev));
+  const char* f = std::getenv("DBAG_PEER_SELFTEST_FAIL");
+  if (f && std::string(f) == "1") return 0;
+  if (h) std::fprintf(stderr, "[dbag] peer all-reduce self-check failed on rank %d of %d\n", s.rank, s.k);
+  return h ? 0 : 1;
 }
 
 void Group::abort(const std::string& why) {
@@ -299,20 +364,24 @@ NcclComm::~NcclComm() {
 // IPC, the handles are all-gathered over NCCL and opened (peer access over
 // NVLink / NVSwitch). Any rank failing makes every rank return false.
 bool NcclComm::make_peer_site(std::int64_t max_len, DType t, PeerSite* out) {
-  // Opt-in (DBAG_PEER_IPC=1): the cross-process mapping has not run on a
-  // multi-GPU node yet (one GPU cannot host two NCCL ranks), so one-process-
-  // per-GPU runs keep the host-driven NCCL loop by default. Every rank reads
-  // the same environment (torchrun), so the answer agrees.
+  // DBAG_PEER_IPC=0 keeps the host-driven NCCL loop. The mapping is
+  // verified before use (k_peer_selftest: two all-reduces per slice with a
+  // 2 s peer timeout, agreed over NCCL); any failure falls back to NCCL on
+  // every rank. Every rank reads the same environment (torchrun).
   const char* ipc = std::getenv("DBAG_PEER_IPC");
-  if (!(ipc && std::string(ipc) == "1")) return false;
+  if (ipc && std::string(ipc) == "0") return false;
   if (size_ < 2 || size_ > PeerSite::kMaxPeers) return false;
   PeerSite s;
   s.k = size_;
   s.rank = rank_;
-  PeerSite::plan(max_len, s.k, &s.slice, &s.nslice);
+  PeerSite::plan(max_len, s.k, false, &s.slice, &s.nslice);  // one process per GPU
+  s.len = std::max<std::int64_t>(max_len, 1);
   const PeerAlloc a = peer_alloc(max_len, t, s.nslice);
   own_.push_back(a.base);
   peer_fill(a, s.nslice, rank_, &s, true);
+  int dev = 0;
+  DBAG_CUDA(cudaGetDevice(&dev));
+  auto check = std::make_unique<PeerCheck>(s, dev);
   constexpr int kRec = 72;  // IPC handle (64 bytes) + status
   std::vector<unsigned char> rec(static_cast<std::size_t>(kRec) * static_cast<std::size_t>(size_), 0);
   unsigned char* mine = rec.data() + static_cast<std::size_t>(rank_) * kRec;
@@ -357,6 +426,15 @@ bool NcclComm::make_peer_site(std::int64_t max_len, DType t, PeerSite* out) {
   DBAG_NCCL(ncclAllReduce(dok, dok, 1, ncclInt, ncclMin, comm_, st));
   DBAG_CUDA(cudaStreamSynchronize(st));
   DBAG_CUDA(cudaMemcpy(&ok, dok, sizeof(int), cudaMemcpyDeviceToHost));
+  if (ok) {  // self-check of the mapped site, then agree again
+    ok = check->run(s);
+    check.reset();
+    DBAG_CUDA(cudaMemcpy(dok, &ok, sizeof(int), cudaMemcpyHostToDevice));
+    DBAG_NCCL(ncclAllReduce(dok, dok, 1, ncclInt, ncclMin, comm_, st));
+    DBAG_CUDA(cudaStreamSynchronize(st));
+    DBAG_CUDA(cudaMemcpy(&ok, dok, sizeof(int), cudaMemcpyDeviceToHost));
+    if (!ok) std::fprintf(stderr, "[dbag] CUDA-IPC peer all-reduce self-check failed: NCCL loop used\n");
+  }
   cudaFree(d);
   cudaStreamDestroy(st);
   if (!ok) {

@@ -41,16 +41,23 @@ struct PeerSite {
   static constexpr int kMaxPeers = 16;
   int k = 0, rank = 0, nslice = 0;
   std::int64_t slice = 0;               // elements per slice (one CTA each)
+  std::int64_t len = 0;                 // slot capacity in elements
   void* slot[2][kMaxPeers] = {};        // rank p's deposit buffers, by epoch parity
   unsigned* flag[kMaxPeers] = {};       // rank p's per-slice arrival epochs
   unsigned* epoch = nullptr;            // this rank's per-slice epoch (local)
-  // Slice plan, a function of (max_len, k) only, so every rank agrees:
-  // slices of whole 9-vectors (one camera each), at most max(1, min(148,
-  // 512 / k)) of them, so the spinning CTAs of k ranks sharing one device
-  // stay co-resident.
-  static void plan(std::int64_t max_len, int k, std::int64_t* slice, int* nslice) {
+  // Slice plan, a function of (max_len, k, shared) only, so every rank
+  // agrees: slices of whole 9-vectors (one camera each). One rank per device:
+  // up to 148 slices (one CTA per SM folds and exchanges its cameras). Ranks
+  // sharing a device: at most kSharedCap per rank — a rank's spinning CTAs wait for
+  // the other ranks' passes on the same SMs, so few and small is better
+  // there (and k x kSharedCap stays co-resident).
+#ifndef DBAG_PEER_SHARED_CAP
+#define DBAG_PEER_SHARED_CAP 48
+#endif
+  static constexpr int kSharedCap = DBAG_PEER_SHARED_CAP;
+  static void plan(std::int64_t max_len, int k, bool shared, std::int64_t* slice, int* nslice) {
     const std::int64_t units = std::max<std::int64_t>(1, (max_len + 8) / 9);
-    const std::int64_t cap = std::max<std::int64_t>(1, std::min<std::int64_t>(148, 512 / std::max(k, 1)));
+    const std::int64_t cap = shared ? kSharedCap : std::max<std::int64_t>(1, std::min<std::int64_t>(148, 512 / std::max(k, 1)));
     const std::int64_t per = (units + cap - 1) / cap;
     *slice = per * 9;
     *nslice = static_cast<int>((units + per - 1) / per);
@@ -143,6 +150,23 @@ class Group {
   std::vector<std::size_t> scratch_bytes_;
   std::vector<std::vector<void*>> peer_mem_;  // per rank: peer-site allocations (freed with the group)
   std::vector<PeerSite> peer_dep_;            // per rank: its own buffers, published for the others
+  std::vector<int> peer_ok_;                  // per rank: its site self-check
+};
+
+// Self-check of a peer site (peer.cuh k_peer_selftest); run() is collective.
+class PeerCheck {
+ public:
+  PeerCheck(const PeerSite& s, int device);
+  ~PeerCheck();
+  PeerCheck(const PeerCheck&) = delete;
+  PeerCheck& operator=(const PeerCheck&) = delete;
+  int run(const PeerSite& s);
+
+ private:
+  int device_;
+  cudaStream_t st_ = nullptr;
+  double* buf_ = nullptr;
+  int* bad_ = nullptr;
 };
 
 class GroupComm final : public Comm {

@@ -38,17 +38,30 @@ constexpr int kPeerThreads = 256;
 
 // The exchange of one slice [b0, b1): fill(mine) deposits this rank's values
 // into its slot, then the epoch handshake, then out[i] = ascending-rank sum.
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// timeout_ns > 0 (the setup self-check only): give up waiting after that
+// long and raise *failed; 0 waits for as long as the peers take.
 template <class T, class Fill>
 __device__ __forceinline__ void peer_slice(const PeerSite& s, int c, std::int64_t b0, std::int64_t b1, T* out,
-                                           Fill fill) {
+                                           Fill fill, unsigned long long timeout_ns = 0, int* failed = nullptr) {
   const unsigned e = s.epoch[c] + 1u;
   fill(static_cast<T*>(s.slot[e & 1u][s.rank]));
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence_system();  // the CTA's deposits (ordered by bar.sync) before the epoch
     st_release_sys(s.flag[s.rank] + c, e);
+    const unsigned long long t0 = timeout_ns ? global_ns() : 0;
     for (int p = 0; p < s.k; ++p)
       while (static_cast<int>(ld_acquire_sys(s.flag[p] + c) - e) < 0) {
+        if (timeout_ns && global_ns() - t0 > timeout_ns) {
+          *failed = 1;
+          break;
+        }
       }
     s.epoch[c] = e;
   }
@@ -78,6 +91,29 @@ __global__ void __launch_bounds__(kPeerThreads) k_peer_allreduce(PeerSite s, con
   peer_slice<T>(s, c, b0, b1, out, [&](T* mine) {
     for (std::int64_t i = b0 + threadIdx.x; i < b1; i += kPeerThreads) mine[i] = in[i];
   });
+}
+
+// Setup self-check of a site (NcclComm, CUDA-IPC peers): `rounds`
+// all-reduces of rank-dependent values (both slot parities), every slice,
+// each compared with the closed-form sum; *bad = 1 on a mismatch or a peer
+// that never arrives (2 s). Leaves every rank's epochs advanced alike.
+template <class T = double>
+__global__ void __launch_bounds__(kPeerThreads) k_peer_selftest(PeerSite s, T* buf, int rounds, int* bad) {
+  const int c = blockIdx.x;
+  const std::int64_t b0 = std::int64_t(c) * s.slice, b1 = b0 + s.slice < s.len ? b0 + s.slice : s.len;
+  for (int q = 0; q < rounds; ++q) {
+    peer_slice<T>(
+        s, c, b0, b1, buf,
+        [&](T* mine) {
+          for (std::int64_t i = b0 + threadIdx.x; i < b1; i += kPeerThreads)
+            mine[i] = T(s.rank + 1) * T(i % 1009 + q + 1);
+        },
+        2000000000ull, bad);
+    const T k = T(s.k);
+    for (std::int64_t i = b0 + threadIdx.x; i < b1; i += kPeerThreads)
+      if (buf[i] != k * (k + 1) / 2 * T(i % 1009 + q + 1)) *bad = 1;
+    __syncthreads();
+  }
 }
 
 // The camera side of a K > 1 DSE in one kernel: fold of this rank's

@@ -691,3 +691,18 @@ def test_fused_linearize_assembly_matches_rows(k, mode, monkeypatch):
     cfg = dba.SolverConfig(max_iterations=3, workers=k, pcg_tol=1e-12, pcg_max_iters=2000,
                            jacobian=dba.JACOBIAN_ANALYTIC if mode else dba.JACOBIAN_AUTODIFF)
     _compare_histories(dba.lm_solve(p, cfg), O.lm_solve(p, cfg), 1e-9)
+
+
+def test_peer_site_selftest_fallback(monkeypatch):
+    """Every peer site is verified before use (k_peer_selftest: two
+    all-reduces of closed-form values per slice, agreed over the ranks); a
+    failed check (forced here) makes every rank fall back to the
+    host-driven loop, with the same oracle trajectory."""
+    p = ring(30, 300, 6, radius=1.0, noise=0.5, seed=21, nobs=300 * 6 - 5)
+    cfg = dba.SolverConfig(max_iterations=3, workers=2, pcg_tol=1e-12, pcg_max_iters=2000)
+    ok = dba.lm_solve(p, cfg, devices=[0])
+    monkeypatch.setenv("DBAG_PEER_SELFTEST_FAIL", "1")
+    fb = dba.lm_solve(p, cfg, devices=[0])
+    o = O.lm_solve(p, cfg)
+    _compare_histories(ok, o, 1e-9)
+    _compare_histories(fb, o, 1e-9)
