@@ -220,7 +220,7 @@ class Rank {
   }
   // Batch boundaries in device points (first 0, last n_loc).
   static std::vector<std::int32_t> jb_batches(const std::vector<std::int32_t>& dpt_ptr) {
-    const std::int64_t cap = jb_batch_cap();
+    const std::int64_t cap = lin_rows() ? jb_batch_cap() : std::numeric_limits<std::int64_t>::max();
     const std::int32_t np = static_cast<std::int32_t>(dpt_ptr.size()) - 1;
     std::vector<std::int32_t> b{0};
     for (std::int32_t d = 0; d < np; ++d)
@@ -263,7 +263,7 @@ class Rank {
     if (lin_rows())
       for (std::size_t b = 0; b < nb; ++b)
         z.jb = std::max<std::size_t>(z.jb, d.dpt_ptr.empty() ? 0 : d.dpt_ptr[jb[b + 1]] - d.dpt_ptr[jb[b]]);
-    z.cam_ptr = nb * pl.cam_ptr.size();
+    z.cam_ptr = lin_rows() ? nb * pl.cam_ptr.size() : 0;  // camera-major slot lists: row assembly only
     z.carry = nb > 1 ? (pl.cam_ptr.size() - 1) * 54 : 0;
     z.cam_list = nb > 1 ? nb * (pl.cam_ptr.size() - 1) : 0;
     z.bounce = pl.ranks > 1 ? 4 * static_cast<std::size_t>(pl.ranks) : 0;  // tallies (2K) and identity probe (4K)
@@ -274,8 +274,9 @@ class Rank {
   // list both the prediction and the allocation walk.
   template <class F>
   static void shard_buffers(const ShardSizes& z, F&& f) {
-    for (auto pm : {&Rank::slot_cam_, &Rank::slot_dpt_, &Rank::slot_edge_, &Rank::cslot_dslot_})
+    for (auto pm : {&Rank::slot_cam_, &Rank::slot_dpt_, &Rank::slot_edge_})
       f(pm, pm == &Rank::slot_dpt_ || pm == &Rank::slot_edge_ ? z.slots : z.N);
+    f(&Rank::cslot_dslot_, lin_rows() ? z.N : 0);
     for (auto pm : {&Rank::slot_px_, &Rank::slot_py_, &Rank::slot_w_}) f(pm, z.N);
     f(&Rank::dpt_ptr_, z.dpt_ptr);
     f(&Rank::chunk_slot_, z.chunk_slot);
@@ -442,10 +443,12 @@ class Rank {
         cslot.swap(bslot);
       }
     }
-    cam_ptr_.copy_in(cptr32);
-    cam_list_.copy_in(cam_list_h);
+    if (lin_rows()) {
+      cam_ptr_.copy_in(cptr32);
+      cam_list_.copy_in(cam_list_h);
+      cslot_dslot_.copy_in(cslot);
+    }
     cam_glob_.copy_in(plan_.cams.to_global);
-    cslot_dslot_.copy_in(cslot);
     dpt_glob_d_.copy_in(dpt_glob_);
     halo_of_.copy_in(halo_of);
     owned_.copy_in(owned);

@@ -20,10 +20,11 @@ LANES = 18  # factored coupling records: G = sqrt(w) Jc per slot (kernels.cuh kL
 
 def _floor_bytes(p, k, rank, s, t):
     """Lower bound from the dominant per-edge arrays alone: E records
-    (18 lanes of t bytes per slot), the assembly rows (28 s per edge), the
-    slot arrays (4 int32 + 3 scalars per edge)."""
+    (18 lanes of t bytes per slot), the slot arrays (4 int32 + 3 scalars per
+    edge). (The fused linearize keeps no per-edge assembly rows; with
+    DBAG_LIN=rows they add 28 s per edge, checked below.)"""
     n_k = len(dba.partition_edges(p, k)[rank].edge_ids)
-    return n_k * (LANES * t + 28 * s + 16 + 3 * s)
+    return n_k * (LANES * t + 16 + 3 * s)
 
 
 @pytest.mark.parametrize("k", [1, 2, 4])
@@ -61,11 +62,24 @@ def test_prediction_is_deterministic_and_validates(ladybug):
 
 def test_assembly_scratch_is_bounded(ladybug, monkeypatch):
     """The Jb assembly rows (28 scalars per edge) are held for one batch of
-    whole points at a time: with DBAG_JB_BATCH slots the pool shrinks by
-    the rows of all but one batch, plus a 54-double carry per camera."""
+    whole points at a time (row assembly, DBAG_LIN=rows): with DBAG_JB_BATCH
+    slots the pool shrinks by the rows of all but one batch, plus a
+    54-double carry per camera."""
+    monkeypatch.setenv("DBAG_LIN", "rows")
     full = dba.predict_memory(ladybug)
     monkeypatch.setenv("DBAG_JB_BATCH", "4096")
     small = dba.predict_memory(ladybug)
     n = ladybug.num_observations
     saved = full - small
     assert (n - 4096 - 64) * 28 * 8 - 49 * 54 * 8 - 8 * 2**10 <= saved <= (n - 4096) * 28 * 8 + 4 * 2**10
+
+
+def test_row_assembly_scratch_in_the_prediction(ladybug, monkeypatch):
+    """DBAG_LIN=rows (the two-kernel assembly through per-edge Jacobian rows)
+    adds its 28 scalars per edge of row scratch to the pool, and the fused
+    path's 54-double camera partials are gone from it."""
+    fused = dba.predict_memory(ladybug)
+    monkeypatch.setenv("DBAG_LIN", "rows")
+    rows = dba.predict_memory(ladybug)
+    n = ladybug.num_observations
+    assert 28 * 8 * n * 0.6 < rows - fused < 33 * 8 * n  # + camera-major slot lists (4 B per edge)
