@@ -257,7 +257,7 @@ def run_reference(args):
         "impl": "reference", "metric": "edges_per_sec_per_lm_iteration", "value": value, "unit": "edges/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": workload_config(args.workload, info["full_pcg_iterations"]),
+        "config": bench_config(args.workload, info["full_pcg_iterations"], max(args.gpus, 1)),
         "cpu_baseline": {"value": value, "unit": "edges/s", "cores": k, "kind": "port", "sample": sample,
                          "host": host, "jacobian": "autodiff", "detail": info,
                          "k1": {"value": N / secs1[0], "unit": "edges/s", "cores": 1, "seconds": secs1[0],
@@ -286,6 +286,12 @@ def workload_config(name, pcg):
             "solver": "SolverConfig defaults (diag_scaled, lambda0 1e-4, pcg_tol 1e-6, pcg_max_iters 500)",
             "step": "one LM iteration from x0 (linearize+assemble, damp+factor, rhs, DPCG, backsub, trial cost)",
             "instance": "dba/synthetic.hpp ring, seed 1, count-exact, +-0.5 px noise (BASELINE.md §3)"}
+
+
+def bench_config(name, pcg, world):
+    """The `config` both arms print (identical for the same workload and N)."""
+    return dict(workload_config(name, pcg), parallelism=f"edge-partitioned x{world}",
+                l2="flushed (512 MiB write) between timed steps; the E stream exceeds L2 anyway at venice and above")
 
 
 def flush_l2(buf):
@@ -447,8 +453,7 @@ def run_ours(args):
         "metric": "edges_per_sec_per_lm_iteration", "value": value, "unit": "edges/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": dict(workload_config(args.workload, pcg), parallelism=f"edge-partitioned x{world}",
-                       l2="flushed (512 MiB write) between timed steps; the E stream (1.2 GB) exceeds L2 anyway"),
+        "config": bench_config(args.workload, pcg, world),
         "roofline": roof,
         "e2e": {"value": N / e2e_s, "unit": "edges/s", "h2d_bytes_per_step": state_bytes,
                 "d2h_bytes_per_step": state_bytes},
