@@ -385,13 +385,15 @@ def run_ours(args):
     dist = None
     ndev = max(dba.device_count(), 1)
     device = local % ndev
-    uid = None
+    uid = uid_solve = None
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("gloo")
-        uid = [dba.nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(uid, src=0)
-        uid = uid[0]
+        # one ncclUniqueId per communicator: the bench context's and the
+        # t_LM solve's (an id is spent by its communicator's bootstrap)
+        uids = [(dba.nccl_unique_id(), dba.nccl_unique_id()) if rank == 0 else None]
+        dist.broadcast_object_list(uids, src=0)
+        uid, uid_solve = uids[0]
         ctx = dba.RankContext(device, 8, nccl=(rank, world, uid))
         print(f"[bench] rank {rank}/{world}: NCCL communicator up on cuda:{device}", file=sys.stderr, flush=True)
     else:
@@ -462,7 +464,7 @@ def run_ours(args):
         "lm_roofline": lm_roofline(N, n, m, 8, pcg, world, peak, ms_step, prof, args.steps),
     }
     if not args.no_solve:
-        line["solve"] = solve_t_lm(p, world, rank, uid, device)
+        line["solve"] = solve_t_lm(p, world, rank, uid_solve if world > 1 else None, device)
     if world == 1 and rank == 0 and not args.no_secondary:
         line["secondary"] = secondary(flush, SECONDARY_WORKLOAD)
         line["secondary_fp32"] = secondary(flush, SECONDARY_WORKLOAD, np.float32)
