@@ -107,8 +107,8 @@ def _shard_worker(rank, world, port, q):
             assert rel(sums[0].numpy(), B1) < 1e-13 and rel(sums[2].numpy(), v1) < 1e-13
             assert rel(sums[1].numpy(), C1) < 1e-13 and rel(sums[3].numpy(), w1) < 1e-13
             assert abs(float(sums[4][0]) - cost1) <= 1e-13 * cost1
-            for ids, Ek in Es:  # the coupling blocks are per edge, wherever the edge lives
-                assert rel(np.asarray(Ek), np.asarray(E1)[ids]) < 1e-13
+            for ids, Ek in Es:  # the coupling blocks are per edge: identical wherever the edge lives
+                assert np.array_equal(np.asarray(Ek)[:len(ids)], np.asarray(E1)[ids])
         dist.barrier()
         dist.destroy_process_group()
         q.put((rank, "ok"))
