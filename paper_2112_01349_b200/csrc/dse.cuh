@@ -134,7 +134,8 @@ template <class S, class Y, class T>
 __device__ __forceinline__ void fold_cameras(const DseArgs<S, T>& A, int nu, const std::uint8_t* ubeg,
                                              const std::uint8_t* uslot, const std::int32_t* upart, const Y& y) {
   const int tid = threadIdx.x;
-  const int G = nu <= 32 ? (1 << (31 - __clz(32 / max(nu, 1)))) : 1;
+  // the largest power of two G with nu * G <= 32: 32 >> ceil(log2 nu)
+  const int G = nu <= 32 ? 32 >> (32 - __clz(max(nu, 1) - 1)) : 1;
   const int nact = nu * G;
   if ((tid & ~31) >= nact) return;  // the warp has no camera
   const int u = tid / G, j = tid & (G - 1);
@@ -190,6 +191,7 @@ struct GatherX {
     S v;
   };
   __device__ __forceinline__ Raw raw(std::int32_t cam, int i) const { return {__ldg(x + std::size_t(cam) * 9 + i)}; }
+  __device__ __forceinline__ Raw raw_at(int k) const { return {__ldg(x + k)}; }
   __device__ __forceinline__ S combine(const Raw& r) const { return r.v; }
 };
 // One 128-slot chunk whose record is at R (global or shared memory);
@@ -217,23 +219,37 @@ __device__ __forceinline__ void dse_chunk_at(const DseArgs<S, T>& A, DseWork<S>&
   S L9[9], wv[3];
   if (tid < np) load_point<S, MODE>(A, p0 + tid, L9, wv);
   const bool staged = nu <= kXsCams;
-  S rraw[3];
-  if (kFact && staged) {
+  // the chunk's camera rows: element t = tid + 128 j of the staged (camera,
+  // row) list is row r of distinct camera u (t = 9 u + r; 128 = 9 * 14 + 2),
+  // at offset ucam[u] * 9 + r of the camera-space vectors (shared by the R
+  // and the x gathers)
+  int goff[3];
+  bool gon[3];
+  {
+    int u = tid / 9, r = tid - 9 * (tid / 9);
 #pragma unroll
     for (int j = 0; j < 3; ++j) {
-      const int t = tid + kTile * j;
-      if (t < nu * 9) rraw[j] = __ldg(A.Rm + std::size_t(M.ucam[t / 9]) * 9 + (t - (t / 9) * 9));
+      gon[j] = staged && u < nu;
+      goff[j] = gon[j] ? M.ucam[u] * 9 + r : 0;
+      u += 14;
+      r += 2;
+      if (r >= 9) {
+        r -= 9;
+        ++u;
+      }
     }
   }
+  S rraw[3];
+  if (kFact)
+#pragma unroll
+    for (int j = 0; j < 3; ++j)
+      if (gon[j]) rraw[j] = __ldg(A.Rm + goff[j]);
   if (!gx.ready()) return;
   typename G::Raw graw[3];  // the chunk's camera vectors, once per (camera, row)
-  if (MODE != 2 && staged) {
+  if (MODE != 2)
 #pragma unroll
-    for (int j = 0; j < 3; ++j) {
-      const int t = tid + kTile * j;
-      if (t < nu * 9) graw[j] = gx.raw(M.ucam[t / 9], t - (t / 9) * 9);
-    }
-  }
+    for (int j = 0; j < 3; ++j)
+      if (gon[j]) graw[j] = gx.raw_at(goff[j]);
 #if DBAG_RELOAD_E
   // E lanes are read where they are used (a-phase, y-phase) instead of being
   // held in registers across the point solve: the second read hits L1 / L2
@@ -250,7 +266,7 @@ __device__ __forceinline__ void dse_chunk_at(const DseArgs<S, T>& A, DseWork<S>&
   if (staged && (kFact || MODE != 2)) {
 #pragma unroll
     for (int j = 0; j < 3; ++j)
-      if (tid + kTile * j < nu * 9) {
+      if (gon[j]) {
         if (MODE != 2) sm.xs()[tid + kTile * j] = gx.combine(graw[j]);
         if (kFact) sm.rs[tid + kTile * j] = rraw[j];
       }
@@ -263,8 +279,13 @@ __device__ __forceinline__ void dse_chunk_at(const DseArgs<S, T>& A, DseWork<S>&
     S a[3] = {S(0), S(0), S(0)};
     if (tid < hdr.z) {
       S xv[9];
+      if (staged) {
 #pragma unroll
-      for (int i = 0; i < 9; ++i) xv[i] = staged ? sm.xs()[su * 9 + i] : gx(cam, i);
+        for (int i = 0; i < 9; ++i) xv[i] = sm.xs()[su * 9 + i];
+      } else {
+#pragma unroll
+        for (int i = 0; i < 9; ++i) xv[i] = gx(cam, i);
+      }
 #if DBAG_RELOAD_E
       S e[L];
       lanes(e);

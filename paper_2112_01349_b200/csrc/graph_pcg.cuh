@@ -135,8 +135,8 @@ struct GatherGraph {
   struct Raw {
     S v, pp;
   };
-  __device__ __forceinline__ Raw raw(std::int32_t cam, int i) const {
-    const std::size_t k = std::size_t(cam) * 9 + i;
+  __device__ __forceinline__ Raw raw(std::int32_t cam, int i) const { return raw_at(int(cam) * 9 + i); }
+  __device__ __forceinline__ Raw raw_at(int k) const {
     return {__ldg(v + k), (!pcg || first) ? S(0) : __ldg(pprev + k)};
   }
   __device__ __forceinline__ S combine(const Raw& r) const { return (!pcg || first) ? r.v : r.v + beta * r.pp; }
