@@ -225,19 +225,12 @@ __device__ __forceinline__ void dse_chunk_at(const DseArgs<S, T>& A, DseWork<S>&
   // and the x gathers)
   int goff[3];
   bool gon[3];
-  {
-    int u = tid / 9, r = tid - 9 * (tid / 9);
 #pragma unroll
-    for (int j = 0; j < 3; ++j) {
-      gon[j] = staged && u < nu;
-      goff[j] = gon[j] ? M.ucam[u] * 9 + r : 0;
-      u += 14;
-      r += 2;
-      if (r >= 9) {
-        r -= 9;
-        ++u;
-      }
-    }
+  for (int j = 0; j < 3; ++j) {
+    const int t = tid + kTile * j;
+    const int u = (t * 7282) >> 16;  // t / 9 for t < 384 (9 * 7282 = 65538)
+    gon[j] = staged && u < nu;
+    goff[j] = gon[j] ? M.ucam[u] * 9 + (t - 9 * u) : 0;
   }
   S rraw[3];
   if (kFact)
@@ -274,23 +267,26 @@ __device__ __forceinline__ void dse_chunk_at(const DseArgs<S, T>& A, DseWork<S>&
   }
   // this slot's camera R: staged, or straight from global for > kXsCams cameras
   const std::int32_t cam = staged ? 0 : M.cam[tid];
-  const S* Rc = kFact ? (staged ? sm.rs + su * 9 : A.Rm + std::size_t(cam) * 9) : nullptr;
+  // the slot's camera R: staged in shared memory (the compiler sees the
+  // address space: LDS, not generic loads) or from global beyond kXsCams
+  const S* Rg = kFact ? A.Rm + std::size_t(cam) * 9 : nullptr;
   if (MODE != 2) {
     S a[3] = {S(0), S(0), S(0)};
     if (tid < hdr.z) {
       S xv[9];
-      if (staged) {
-#pragma unroll
-        for (int i = 0; i < 9; ++i) xv[i] = sm.xs()[su * 9 + i];
-      } else {
-#pragma unroll
-        for (int i = 0; i < 9; ++i) xv[i] = gx(cam, i);
-      }
 #if DBAG_RELOAD_E
       S e[L];
       lanes(e);
 #endif
-      coupling_t<S, L>(e, Rc, xv, a);
+      if (staged) {
+#pragma unroll
+        for (int i = 0; i < 9; ++i) xv[i] = sm.xs()[su * 9 + i];
+        coupling_t<S, L>(e, kFact ? sm.rs + su * 9 : nullptr, xv, a);
+      } else {
+#pragma unroll
+        for (int i = 0; i < 9; ++i) xv[i] = gx(cam, i);
+        coupling_t<S, L>(e, Rg, xv, a);
+      }
     }
 #pragma unroll
     for (int j = 0; j < 3; ++j) sm.a()[tid][j] = a[j];
@@ -317,7 +313,8 @@ __device__ __forceinline__ void dse_chunk_at(const DseArgs<S, T>& A, DseWork<S>&
     S e[L];
     lanes(e);
 #endif
-    coupling_b<S, L>(e, Rc, b0, b1, b2, y);
+    if (staged) coupling_b<S, L>(e, kFact ? sm.rs + su * 9 : nullptr, b0, b1, b2, y);
+    else coupling_b<S, L>(e, Rg, b0, b1, b2, y);
 #pragma unroll
     for (int i = 0; i < 9; ++i) sm.y()[tid][i] = y[i];
     __syncthreads();
