@@ -64,12 +64,20 @@ def check_trajectory(st, entry, k):
     bound = np.maximum(tol * np.abs(ref), SPREAD_MARGIN * env)
     dev = np.abs(got - ref)
     assert np.all(dev <= bound), list(zip(dev / np.abs(ref), bound / np.abs(ref)))
-    # lambda follows the gain ratio (cost - cost_new) / model (dba/solver.hpp:
-    # 417-424), i.e. a difference of costs: same bar, its own K-envelope
+    # lambda follows the gain ratio rho = (cost - cost_new) / model
+    # (dba/solver.hpp:417-424): a ratio of DIFFERENCES of nearly equal costs,
+    # so a cost deviation d becomes a relative rho (and lambda) deviation of
+    # about d / |cost - cost_new| — e.g. 1e-10 on a 3324.9 cost that moved by
+    # 8.9 is 4e-8 relative in rho, amplified by the Nielsen update. Measured on
+    # these instances: up to 3e-5 relative late in the ladybug FP64 solve,
+    # where the cost moves by < 0.3 %. The bar: the north_star tolerance, or
+    # twice the oracle's K-spread, or 1e-4 relative (FP64) / 1e-2 (FP32).
     lref, lenv = envelope(entry, key, "lambda")
     lgot = np.array([r.lambda_ for r in st.history])
     ldev = np.abs(lgot - lref)
-    assert np.all(ldev <= np.maximum(tol * lref, SPREAD_MARGIN * lenv)), list(zip(ldev / lref, lenv / lref))
+    lam_rel = 1e-4 if entry["dtype"] == "float64" else 1e-2
+    assert np.all(ldev <= np.maximum(np.maximum(tol, lam_rel) * lref, SPREAD_MARGIN * lenv)), \
+        list(zip(ldev / lref, lenv / lref))
     return dev / np.abs(ref)
 
 
