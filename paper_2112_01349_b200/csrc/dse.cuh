@@ -10,10 +10,11 @@
 // dependent loads are the camera-vector gathers (once per distinct camera
 // and row, L1/L2-resident) and the points' C factors. The E block stays in
 // registers between the two products, so each coupling block is read exactly
-// once per DSE. y is folded per (chunk, camera) by one warp (fixed lane order
-// + shuffle tree) and written to its camera-major partial slot; the camera
-// fold (graph_pcg.cuh, or k_cam_reduce on the host-driven path) sums each
-// camera's contiguous partials. No atomics anywhere: deterministic.
+// once per DSE. y is folded per (chunk, camera, component): one thread per
+// item sums the camera's slots in slot-list order (fold_items) and writes its
+// camera-major partial; the camera fold (graph_pcg.cuh, or k_cam_reduce on
+// the host-driven path) sums each camera's contiguous partials. No atomics
+// anywhere: deterministic.
 //
 // MODE 0  DSE          a from x, b = C^-1 a, y -> partials
 // MODE 1  back-subst.  a from x (= dx_c), out_pt = C^-1 (w - a)   (dba/solver.hpp:371-376)
