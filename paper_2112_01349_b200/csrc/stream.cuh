@@ -208,7 +208,7 @@ __device__ __forceinline__ void stream_chunk(const DseArgs<S, T>& A, S* work, T*
 #pragma unroll
   for (int i = 0; i < 9; ++i) yb[tid][i] = y[i];
   cbar();
-  fold_cameras4(A, nu, M.ubeg, M.uslot, M.upart, yb);
+  fold_items(A, nu, M.ubeg, M.uslot, M.upart, YRows<S>{yb});
 }
 
 // A long tile (one point, several chunk records), from global memory.
