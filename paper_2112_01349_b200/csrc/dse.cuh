@@ -365,8 +365,10 @@ __device__ __forceinline__ void dse_chunk(const DseArgs<S, T>& A, DseWork<S>& sm
   dse_chunk_at<S, MODE, L>(A, sm, A.rec + std::size_t(chunk) * Rec<T, L>::kLen, gx);
 }
 
-// Resident CTAs per SM the chunk pass is compiled for (register budget):
-// measured best 5 with FP64 E lanes in registers, 7 with FP32 lanes.
+// Resident CTAs per SM the chunk pass is compiled for (register budget),
+// measured: 5 with FP64 E lanes in registers, 7 for FP32 lanes under FP64
+// arithmetic (coupling_fp32), 8 for the all-FP32 solve (64 registers, no
+// spill; 0.117 -> 0.110 ms per venice pass).
 #ifndef DBAG_RELOAD_E
 #define DBAG_RELOAD_E 0
 #endif
@@ -376,13 +378,16 @@ __device__ __forceinline__ void dse_chunk(const DseArgs<S, T>& A, DseWork<S>& sm
 #ifndef DBAG_PASS_MINB_F64E
 #define DBAG_PASS_MINB_F64E 5
 #endif
-template <class T>
+#ifndef DBAG_PASS_MINB_F32
+#define DBAG_PASS_MINB_F32 8
+#endif
+template <class T, class S = double>
 constexpr int pass_min_blocks() {
-  return sizeof(T) == 4 ? DBAG_PASS_MINB_F32E : DBAG_PASS_MINB_F64E;
+  return sizeof(T) == 4 ? (sizeof(S) == 4 ? DBAG_PASS_MINB_F32 : DBAG_PASS_MINB_F32E) : DBAG_PASS_MINB_F64E;
 }
 
 template <class S, int MODE, class T = S, int L = kLanesFact>
-__global__ void __launch_bounds__(kTile, pass_min_blocks<T>()) k_dse_chunk(DseArgs<S, T> A) {
+__global__ void __launch_bounds__(kTile, pass_min_blocks<T, S>()) k_dse_chunk(DseArgs<S, T> A) {
   __shared__ DseWork<S> sm;
   dse_chunk<S, MODE, L>(A, sm, blockIdx.x, GatherX<S>{A.x});
 }

@@ -264,7 +264,7 @@ __device__ __forceinline__ void camera_fold(const GBufs<S>& B, std::int32_t cam,
 // The body's DSE pass: CTAs [0, n_long) take the long tiles, the rest one
 // chunk each (GatherGraph).
 template <class S, class T = S, int L = kLanesFact>
-__global__ void __launch_bounds__(kTile, pass_min_blocks<T>()) k_g_pass(DseArgs<S, T> A, GBufs<S> B, const GScal<S>* sc) {
+__global__ void __launch_bounds__(kTile, pass_min_blocks<T, S>()) k_g_pass(DseArgs<S, T> A, GBufs<S> B, const GScal<S>* sc) {
   __shared__ DseWork<S> sm;
   pdl_allow_dependents();
   const std::int32_t blk = blockIdx.x;
