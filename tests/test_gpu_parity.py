@@ -706,3 +706,34 @@ def test_peer_site_selftest_fallback(monkeypatch):
     o = O.lm_solve(p, cfg)
     _compare_histories(ok, o, 1e-9)
     _compare_histories(fb, o, 1e-9)
+
+
+@pytest.mark.parametrize("k", [1, 2])
+def test_chunks_with_many_cameras(k):
+    """Chunks whose points are seen by more than 32 distinct cameras (the
+    unstaged gather path of the pass, camera vectors read per slot) and by
+    more than 14 (the fold runs more than one round of (camera, component)
+    items per thread): 100 cameras, points of 40-70 observations each, DSE
+    vs the oracle at 1e-12 and the LM trajectory at the same K."""
+    rng = np.random.default_rng(17)
+    base = ring(100, 2, 2, seed=3, radius=1.0, noise=0.5)
+    cams = base.arrays()[0]
+    pts = rng.uniform(-0.3, 0.3, (60, 3))
+    cid, pid = [], []
+    for q in range(60):
+        obs = rng.choice(100, size=int(rng.integers(40, 71)), replace=False)
+        cid += sorted(obs.tolist())
+        pid += [q] * len(obs)
+    cid, pid = np.array(cid, np.int32), np.array(pid, np.int32)
+    P = np.zeros((len(cid), 2))
+    p0 = dba.BAProblem.from_arrays(cams, pts, cid, pid, P)
+    # pixels = the projection plus noise (a well-posed problem)
+    r, _ = O.linearize(p0)  # r = projection - pixel, pixel = 0
+    P = np.asarray(r).T + rng.uniform(-0.5, 0.5, P.shape)
+    p = dba.BAProblem.from_arrays(cams, pts, cid, pid, P)
+    x = rng.uniform(-1, 1, 9 * p.num_cameras)
+    out, _, ident = dba.group_operator(p, k, x, mode=0, lam=1e-3, policy=0)
+    orc, _ = O.dse(p, k, 1e-3, 0, x)
+    assert ident and rel(out, orc) < 1e-12
+    cfg = dba.SolverConfig(max_iterations=3, workers=k, pcg_tol=1e-12, pcg_max_iters=2000)
+    _compare_histories(dba.lm_solve(p, cfg), O.lm_solve(p, cfg), 1e-9)
