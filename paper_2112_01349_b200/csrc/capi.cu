@@ -812,6 +812,8 @@ int dbag_lm_solve_ctx(dbag_ctx* ctx, const dbag_config* c, dbag_result* out) {
       using S = typename R::Scalar;
       if (c->workers != ctx->comm->size())
         throw Error(DBAG_INVALID_ARGUMENT, "config.workers must equal the context's rank count");
+      if (ctx->num_obs <= 0) throw Error(DBAG_INVALID_ARGUMENT, "lm_solve_ctx needs an uploaded problem");
+      if (c->max_iterations < 0 || !out) throw Error(DBAG_INVALID_ARGUMENT, "bad config or result");
       const Outcome o = lm_solve_rank(rk, *c, ctx->num_obs);
       rk.gather_state(static_cast<S*>(out->x_c), static_cast<S*>(out->x_p));
       fill_result(o, ctx->comm->size(), out);
@@ -874,6 +876,7 @@ int dbag_block_factor(int device, int precision, int bs, int64_t nblocks, const 
   return guarded([&] {
     check_precision(precision);
     check_bs(bs);
+    if (nblocks < 0 || (nblocks > 0 && (!blocks || !factor))) throw Error(DBAG_INVALID_ARGUMENT, "bad block arrays");
     DBAG_CUDA(cudaSetDevice(device));
     std::int64_t bad = -1;
     if (precision == 8) {
@@ -894,6 +897,7 @@ int dbag_block_solve(int device, int precision, int bs, int64_t nblocks, const v
   return guarded([&] {
     check_precision(precision);
     check_bs(bs);
+    if (nblocks < 0 || (nblocks > 0 && (!factor || !x))) throw Error(DBAG_INVALID_ARGUMENT, "bad block arrays");
     DBAG_CUDA(cudaSetDevice(device));
     if (precision == 8) {
       if (bs == 3) block_solve<double, 3>(nblocks, factor, x);
