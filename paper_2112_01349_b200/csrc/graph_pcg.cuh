@@ -42,12 +42,13 @@ namespace dbag {
 namespace dev {
 
 #if DBAG_GTIMING  // per-iteration timeline of the graph body (development builds)
-__device__ unsigned long long g_tl[8 * 1024];
+constexpr int kTlStride = 16;  // marks of one iteration: a 128-byte line of their own
+__device__ unsigned long long g_tl[kTlStride * 1024];
 __device__ __forceinline__ void tl_mark(int n, int k) {
   if (n < 1024) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    g_tl[n * 8 + k] = t;
+    g_tl[n * kTlStride + k] = t;
   }
 }
 #define DBAG_TL(n, k, cond) \
@@ -271,8 +272,11 @@ __global__ void __launch_bounds__(kTile, pass_min_blocks<T, S>()) k_g_pass(DseAr
   const GatherGraph<S> gx{sc, B.z, B.x, B.p0, B.p1, nullptr, nullptr, S(0), false, true};
 #if DBAG_GTIMING
   if (blk == 0 && threadIdx.x == 0) {
+    unsigned long long t_s;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_s));
     pdl_wait();
     tl_mark(sc->n, 0);
+    if (sc->n < 1024) g_tl[sc->n * kTlStride + 7] = t_s;
   }
 #endif
   if (blk < A.n_long)
@@ -447,7 +451,7 @@ __global__ void __maxnreg__(128) k_g_fs(GBufs<S> B, RedWs ws, GScal<S>* sc,  // 
   const double rho_cur = sc->rho;
   if (done) return;
 #if DBAG_GTIMING
-  if (blockIdx.x == 0 && threadIdx.x == 0 && n < 1024) g_tl[n * 8 + 1] = t_w;
+  if (blockIdx.x == 0 && threadIdx.x == 0 && n < 1024) g_tl[n * kTlStride + 1] = t_w;
 #endif
   DBAG_TL(n, 2, blockIdx.x == 0 && threadIdx.x == 0);
   const bool pcg = phase == 0;

@@ -1072,7 +1072,7 @@ class Rank {
     collect_profile();
 #if DBAG_GTIMING
     {
-      static unsigned long long t[8 * 1024];
+      static unsigned long long t[dev::kTlStride * 1024];
       DBAG_CUDA(cudaMemcpyFromSymbol(t, dev::g_tl, sizeof(t)));
       const int nn = std::min(gsc_h_->n, 1023);
       double acc[8] = {0};
@@ -1080,12 +1080,44 @@ class Rank {
       for (int k = 1; k + 1 < nn; ++k) {
         if ((k + 1) % 50 == 0 || k % 50 == 0) continue;
         bool ok = true;
-        for (int q = 0; q < 7; ++q) ok = ok && t[k * 8 + q] != 0;
+        for (int q = 0; q < 7; ++q) ok = ok && t[k * dev::kTlStride + q] != 0;
         if (!ok) continue;
-        for (int q = 0; q < 6; ++q) acc[q] += double(t[k * 8 + q + 1]) - double(t[k * 8 + q]);
-        acc[6] += double(t[(k + 1) * 8]) - double(t[k * 8 + 6]);
+        for (int q = 0; q < 6; ++q) acc[q] += double(t[k * dev::kTlStride + q + 1]) - double(t[k * dev::kTlStride + q]);
+        acc[6] += double(t[(k + 1) * dev::kTlStride]) - double(t[k * dev::kTlStride + 6]);
         ++cnt;
       }
+      double lr[64] = {0};
+      int lc[64] = {0};
+      const int u = std::max(1, std::min(g_unroll_, 64));
+      for (int k = 1; k + 1 < nn; ++k) {
+        if ((k + 1) % 50 == 0 || k % 50 == 0 || !t[k * dev::kTlStride + 6] || !t[(k + 1) * dev::kTlStride]) continue;
+        lr[k % u] += double(t[(k + 1) * dev::kTlStride]) - double(t[k * dev::kTlStride + 6]);
+        ++lc[k % u];
+      }
+      for (int par = 0; par < 2; ++par) {
+        double a[8] = {0};
+        int c2 = 0;
+        for (int k = 1; k + 1 < nn; ++k) {
+          if ((k + 1) % 50 == 0 || k % 50 == 0 || (k & 1) != par) continue;
+          bool ok = t[(k + 1) * dev::kTlStride] != 0;
+          for (int q = 0; q < 7; ++q) ok = ok && t[k * dev::kTlStride + q] != 0;
+          if (!ok) continue;
+          for (int q = 0; q < 6; ++q) a[q] += double(t[k * dev::kTlStride + q + 1]) - double(t[k * dev::kTlStride + q]);
+          a[6] += double(t[(k + 1) * dev::kTlStride]) - double(t[k * dev::kTlStride + 6]);
+          ++c2;
+        }
+        double st = 0.0;
+        for (int k = 1; k + 1 < nn; ++k) {
+          if ((k + 1) % 50 == 0 || k % 50 == 0 || (k & 1) != par || !t[(k + 1) * dev::kTlStride + 7] || !t[k * dev::kTlStride + 6]) continue;
+          st += double(t[(k + 1) * dev::kTlStride + 7]) - double(t[k * dev::kTlStride + 6]);
+        }
+        std::fprintf(stderr, "GTIMING n%%2=%d: next-pass CTA0 start - decision %.2f; segs", par, c2 ? st / c2 / 1e3 : 0.0);
+        for (int q = 0; q < 7; ++q) std::fprintf(stderr, " %.2f", c2 ? a[q] / c2 / 1e3 : 0.0);
+        std::fprintf(stderr, "\n");
+      }
+      std::fprintf(stderr, "GTIMING loop by n mod %d (us):", u);
+      for (int q = 0; q < u; ++q) std::fprintf(stderr, " %.2f", lc[q] ? lr[q] / lc[q] / 1e3 : 0.0);
+      std::fprintf(stderr, "\n");
       if (cnt)
         std::fprintf(stderr, "GTIMING n=%d marks(us): pass->fs %.2f sc %.2f fold %.2f barrier %.2f pqsum %.2f step %.2f loop %.2f\n",
                      nn, acc[0] / cnt / 1e3, acc[1] / cnt / 1e3, acc[2] / cnt / 1e3, acc[3] / cnt / 1e3, acc[4] / cnt / 1e3,

@@ -285,6 +285,15 @@ __global__ void __launch_bounds__(kStreamThreads, 3) k_g_stream(DseArgs<S, T> A,
   unsigned char* stages = smem + Lay::kHead + Lay::kWorkBytes;
   const int tid = threadIdx.x;
   pdl_allow_dependents();
+#if DBAG_GTIMING
+  if (blockIdx.x == 0 && tid == 0) {
+    unsigned long long t_s;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_s));
+    pdl_wait();
+    tl_mark(sc->n, 0);
+    if (sc->n < 1024) g_tl[sc->n * kTlStride + 7] = t_s;
+  }
+#endif
   if (tid == 0) {
     for (int s = 0; s < NST; ++s) {
       mbar_init(&full[s], 1);
