@@ -40,6 +40,9 @@
 
 namespace dbag {
 namespace dev {
+// k_g_fs: lane-strided partial rows per load batch (2: no spill at 128
+// registers; 3 and 4 measured no faster)
+constexpr int kFsBatch = 2;
 
 #if DBAG_GTIMING  // per-iteration timeline of the graph body (development builds)
 constexpr int kTlStride = 16;  // marks of one iteration: a 128-byte line of their own
@@ -412,17 +415,21 @@ __device__ __forceinline__ void grid_barrier(unsigned long long* count) {
 // Camera fold + PCG step in one kernel (m <= 8 x grid): one warp per camera,
 // lane = row. The camera's B_d and B^-1 rows and its partial range are
 // constant during the solve and are loaded before waiting on the pass; after
-// it, every vector row the camera needs is loaded in one round trip and
-// stays in registers:
+// it, every vector row the camera needs and the first partial rows are
+// loaded in one round trip, before the scalars are checked:
 //   c = fold(partials), v = p = z + beta p_prev (stored) or x (refresh),
-//   q = B_d v - c, p.q -> pq_cam; grid barrier; p'q = sum over cameras (the
-//   same fixed order in every CTA), alpha; x += alpha p; r -= alpha q (or
-//   r = g - q after a refresh pass); z = B^-1 r; rho, |r|^2 -> grid reduce;
-//   the last CTA advances the scalars and sets the WHILE condition.
-// Same arithmetic (and association) as k_g_fold + k_g_step except the final
-// rho / |r|^2 block reductions (one camera per warp here).
+//   q = B_d v - c, p.q per warp -> per-CTA sum (warp order) -> slot
+//   blockIdx.x of pq_cam; grid barrier; p'q = sum of the CTA slots (one warp,
+//   fixed tree: the same bits in every CTA), alpha; x += alpha p; r -= alpha
+//   q (or r = g - q after a refresh pass); z = B^-1 r; rho, |r|^2 -> grid
+//   reduce; the last CTA advances the scalars and sets the WHILE condition.
+// Same per-camera arithmetic as k_g_fold + k_g_step; the cross-camera sums
+// (p'q, rho, |r|^2) are associated differently (both fixed, deterministic).
+// Measured against the plain form (scalars first, one partial row per load,
+// every CTA summing all m camera terms): venice 14.3 -> 13.5 us per
+// iteration outside the pass.
 template <class S>
-__global__ void __maxnreg__(128) k_g_fs(GBufs<S> B, RedWs ws, GScal<S>* sc,  // 80 registers spilled 48 B
+__global__ void __maxnreg__(128) k_g_fs(GBufs<S> B, RedWs ws, GScal<S>* sc,  // 125 registers, no spill
                                                       cudaGraphConditionalHandle h_while, unsigned long long* bar) {
   __shared__ double red[32];
   __shared__ double pq_all;
@@ -449,23 +456,37 @@ __global__ void __maxnreg__(128) k_g_fs(GBufs<S> B, RedWs ws, GScal<S>* sc,  // 
   const int done = sc->done, n = sc->n, phase = sc->phase;
   const S beta = sc->beta;
   const double rho_cur = sc->rho;
+  // nothing below waits on the scalars before the fold's loads are out: both
+  // p buffers are read (n picks one later), the partials in batches of
+  // kFsBatch lane-strided rows (the same add order as one row at a time),
+  // and the done check follows the fold
+  const std::size_t at = std::size_t(c) * 9 + row;
+  const S zr = *(B.z + at), pa = *(B.p0 + at), pb = *(B.p1 + at), xr = *(B.x + at);
+  const S rr = *(B.r + at), gr = *(B.g + at);
+  S acc[9];
+#pragma unroll
+  for (int i = 0; i < 9; ++i) acc[i] = S(0);
+  for (std::int32_t k = k0 + lane; k < k1; k += 32 * kFsBatch) {
+    S v[kFsBatch][9];
+#pragma unroll
+    for (int q = 0; q < kFsBatch; ++q) {
+      const bool in = k + 32 * q < k1;
+      const S* p = B.part + std::size_t(in ? k + 32 * q : k) * 9;
+#pragma unroll
+      for (int i = 0; i < 9; ++i) v[q][i] = in ? *(p + i) : S(0);
+    }
+#pragma unroll
+    for (int q = 0; q < kFsBatch; ++q)
+#pragma unroll
+      for (int i = 0; i < 9; ++i) acc[i] += v[q][i];
+  }
   if (done) return;
+  const S pp = ((n + 1) & 1) ? pb : pa;  // p_cur(B, n + 1)
 #if DBAG_GTIMING
   if (blockIdx.x == 0 && threadIdx.x == 0 && n < 1024) g_tl[n * kTlStride + 1] = t_w;
 #endif
   DBAG_TL(n, 2, blockIdx.x == 0 && threadIdx.x == 0);
   const bool pcg = phase == 0;
-  const std::size_t at = std::size_t(c) * 9 + row;
-  const S zr = *(B.z + at), pp = *(p_cur(B, n + 1) + at), xr = *(B.x + at);
-  const S rr = *(B.r + at), gr = *(B.g + at);
-  S acc[9];
-#pragma unroll
-  for (int i = 0; i < 9; ++i) acc[i] = S(0);
-  for (std::int32_t k = k0 + lane; k < k1; k += 32) {
-    const S* p = B.part + std::size_t(k) * 9;
-#pragma unroll
-    for (int i = 0; i < 9; ++i) acc[i] += *(p + i);
-  }
 #pragma unroll
   for (int i = 0; i < 9; ++i) {
 #pragma unroll
@@ -490,13 +511,26 @@ __global__ void __maxnreg__(128) k_g_fs(GBufs<S> B, RedWs ws, GScal<S>* sc,  // 
     double t = lane < 9 ? double(v) * double(qv) : 0.0;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) t += __shfl_down_sync(0xffffffffu, t, o);
-    if (lane == 0 && on) B.pq_cam[cam] = t;
+    // p'q: each CTA sums its warps' cameras in warp order into slot
+    // blockIdx.x of pq_cam; after the barrier one warp per CTA sums the
+    // gridDim.x slots (lane-strided, fixed xor tree): the same bits in every CTA
+    if (lane == 0) red[threadIdx.x >> 5] = on ? t : 0.0;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double b = 0.0;
+      for (int w = 0; w < int(blockDim.x >> 5); ++w) b += red[w];
+      B.pq_cam[blockIdx.x] = b;
+    }
     DBAG_TL(n, 3, blockIdx.x == 0 && threadIdx.x == 0);
     grid_barrier(bar);
     DBAG_TL(n, 4, blockIdx.x == 0 && threadIdx.x == 0);
-    for (std::int32_t k = threadIdx.x; k < B.m; k += blockDim.x) pq += __ldcg(B.pq_cam + k);
-    pq = block_reduce<SumOp>(pq, red);
-    if (threadIdx.x == 0) pq_all = pq;
+    if (threadIdx.x < 32) {
+      double s = 0.0;
+      for (unsigned k = lane; k < gridDim.x; k += 32) s += __ldcg(B.pq_cam + k);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      if (lane == 0) pq_all = s;
+    }
     __syncthreads();
     pq = pq_all;
     DBAG_TL(n, 5, blockIdx.x == 0 && threadIdx.x == 0);
