@@ -62,11 +62,19 @@ struct DseArgs {
 #ifndef DBAG_Y_OVERLAY
 #define DBAG_Y_OVERLAY 0
 #endif
+// y rows padded to 10 scalars (DBAG_FOLD_PAIRS): the y-phase writes each row
+// with 16-byte (FP64) stores and the fold reads two components per load
+// (fold_pairs).
+#ifndef DBAG_FOLD_PAIRS
+#define DBAG_FOLD_PAIRS 1
+#endif
+static_assert(!(DBAG_FOLD_PAIRS && DBAG_Y_OVERLAY), "padded y rows do not fit the overlay");
+constexpr int kYW = DBAG_FOLD_PAIRS ? 10 : 9;
 template <class S>
-struct DseWork {
+struct alignas(16) DseWork {
   S buf[kTile * 9];
 #if !DBAG_Y_OVERLAY
-  S ybuf[kTile * 9];
+  S ybuf[kTile * kYW];
 #endif
   S rs[kXsCams * 9];  // R of the chunk's distinct cameras (factored records)
   std::int32_t upart[kTile];
@@ -78,7 +86,7 @@ struct DseWork {
 #if DBAG_Y_OVERLAY
   __device__ __forceinline__ S (*y())[9] { return reinterpret_cast<S(*)[9]>(buf); }
 #else
-  __device__ __forceinline__ S (*y())[9] { return reinterpret_cast<S(*)[9]>(ybuf); }
+  __device__ __forceinline__ S (*y())[kYW] { return reinterpret_cast<S(*)[kYW]>(ybuf); }
 #endif
 };
 static_assert(6 * kTile + kXsCams * 9 <= 9 * kTile, "a, b and xs must fit under y");
@@ -184,11 +192,61 @@ __device__ __forceinline__ void fold_items(const DseArgs<S, T>& A, int nu, const
   }
 }
 
-template <class S>
-struct YRows {  // y[slot][9] rows (DseWork)
-  const S (*y)[9];
+template <class S, int W = 9>
+struct YRows {  // y[slot][W] rows (DseWork: W = kYW)
+  const S (*y)[W];
   __device__ __forceinline__ S operator()(int o, int i) const { return y[o][i]; }
 };
+
+// y row of slot tid into the work area (padded rows: component pairs).
+template <class S>
+__device__ __forceinline__ void store_y(DseWork<S>& sm, int tid, const S* y) {
+#if DBAG_FOLD_PAIRS
+  using V = typename Pair<S>::type;
+  V* row = reinterpret_cast<V*>(sm.y()[tid]);
+#pragma unroll
+  for (int h = 0; h < 4; ++h) row[h] = V{y[2 * h], y[2 * h + 1]};
+  row[4] = V{y[8], S(0)};
+#else
+#pragma unroll
+  for (int i = 0; i < 9; ++i) sm.y()[tid][i] = y[i];
+#endif
+}
+
+// Fold by (camera, component pair) items: thread t sums components 2h and
+// 2h + 1 of camera u (t = 5 u + h) over the camera's slots in slot-list
+// order with one paired load per slot — the same per-component order as
+// fold_items, with about half its instructions.
+template <class S, class T>
+__device__ __forceinline__ void fold_pairs(const DseArgs<S, T>& A, int nu, const std::uint8_t* ubeg,
+                                           const std::uint8_t* uslot, const std::int32_t* upart,
+                                           const S (*y)[kYW]) {
+  using V = typename Pair<S>::type;
+  const int n = nu * 5;
+  for (int t = threadIdx.x; t < n; t += kTile) {
+    const int u = (t * 13108) >> 16, h = t - 5 * u;  // t / 5 for t < 640
+    S a0 = S(0), a1 = S(0);
+    for (int k = ubeg[u]; k < ubeg[u + 1]; ++k) {
+      const V v = reinterpret_cast<const V*>(y[uslot[k]])[h];
+      a0 += v.x;
+      a1 += v.y;
+    }
+    S* out = A.part + std::size_t(upart[u]) * 9 + 2 * h;
+    out[0] = a0;
+    if (h < 4) out[1] = a1;
+  }
+}
+
+template <class S, class T>
+__device__ __forceinline__ void fold_y(const DseArgs<S, T>& A, int nu, const DseWork<S>& sm) {
+#if DBAG_FOLD_PAIRS
+  fold_pairs(A, nu, sm.ubeg, sm.uslot, sm.upart, const_cast<DseWork<S>&>(sm).y());
+#elif DBAG_FOLD_ITEMS
+  fold_items(A, nu, sm.ubeg, sm.uslot, sm.upart, YRows<S, kYW>{const_cast<DseWork<S>&>(sm).y()});
+#else
+  fold_cameras(A, nu, sm.ubeg, sm.uslot, sm.upart, YRows<S, kYW>{const_cast<DseWork<S>&>(sm).y()});
+#endif
+}
 
 template <class S>
 __device__ __forceinline__ void stage_meta(const RecMeta& M, DseWork<S>& sm) {
@@ -354,14 +412,9 @@ __device__ __forceinline__ void dse_chunk_at(const DseArgs<S, T>& A, DseWork<S>&
 #endif
     if (staged) coupling_b<S, L>(e, rcs, b0, b1, b2, y);
     else coupling_b<S, L>(e, Rg, b0, b1, b2, y);
-#pragma unroll
-    for (int i = 0; i < 9; ++i) sm.y()[tid][i] = y[i];
+    store_y(sm, tid, y);
     __syncthreads();
-#if DBAG_FOLD_ITEMS
-    fold_items(A, nu, sm.ubeg, sm.uslot, sm.upart, YRows<S>{sm.y()});
-#else
-    fold_cameras(A, nu, sm.ubeg, sm.uslot, sm.upart, YRows<S>{sm.y()});
-#endif
+    fold_y(A, nu, sm);
     // one chunk per CTA (k_g_pass, k_dse_chunk): no trailing barrier
   }
 }
@@ -462,14 +515,9 @@ __device__ __forceinline__ void dse_long(const DseArgs<S, T>& A, DseWork<S>& sm,
 #pragma unroll
       for (int k = 0; k < L; ++k) e[k] = S(R[k * kTile + tid]);
       coupling_b<S, L>(e, kFact ? A.Rm + std::size_t(M.cam[tid]) * 9 : nullptr, b0, b1, b2, y);
-#pragma unroll
-      for (int i = 0; i < 9; ++i) sm.y()[tid][i] = y[i];
+      store_y(sm, tid, y);
       __syncthreads();
-#if DBAG_FOLD_ITEMS
-      fold_items(A, M.nu, sm.ubeg, sm.uslot, sm.upart, YRows<S>{sm.y()});
-#else
-      fold_cameras(A, M.nu, sm.ubeg, sm.uslot, sm.upart, YRows<S>{sm.y()});
-#endif
+      fold_y(A, M.nu, sm);
     }
   }
   __syncthreads();

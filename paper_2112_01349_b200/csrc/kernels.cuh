@@ -77,6 +77,18 @@ static_assert(rec_hot_bytes<double>() % 16 == 0 && rec_hot_bytes<float>() % 16 =
 static_assert(rec_hot_bytes<double, kLanesDense>() % 16 == 0 && rec_hot_bytes<float, kLanesDense>() % 16 == 0,
               "bulk prefetch size");
 
+// double2 / float2: paired shared-memory rows (dse.cuh fold_pairs)
+template <class T>
+struct Pair;
+template <>
+struct Pair<double> {
+  using type = double2;
+};
+template <>
+struct Pair<float> {
+  using type = float2;
+};
+
 // E chunk record: L lanes x kTile slots (lane-major) then RecMeta; one
 // record per 128-slot chunk of the device slot order.
 template <class S, int L = kLanesFact>
