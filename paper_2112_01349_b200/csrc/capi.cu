@@ -167,6 +167,7 @@ void lm_nccl(const dbag_problem* p, const dbag_config* c, int rank, int nranks, 
   DBAG_CUDA(cudaSetDevice(device));
   if (c->workers != nranks) throw Error(DBAG_INVALID_ARGUMENT, "config.workers must equal nranks");
   NcclComm comm(rank, nranks, id);
+  comm.set_timeout(timeout_of(*c));
   Rank<S, T> rk(device, &comm);
   rk.upload(*p, c->jacobian);
   const Outcome o = lm_solve_rank(rk, *c, p->num_observations);

@@ -45,6 +45,12 @@ struct PeerSite {
   void* slot[2][kMaxPeers] = {};        // rank p's deposit buffers, by epoch parity
   unsigned* flag[kMaxPeers] = {};       // rank p's per-slice arrival epochs
   unsigned* epoch = nullptr;            // this rank's per-slice epoch (local)
+  // Production waits (the DPCG graph): give up on a peer after timeout_ns
+  // (SolverConfig::collective_timeout) and OR bit p of an absent rank p into
+  // *failed; once *failed is set, later waits return at once so the graph
+  // drains and the host raises CollectiveError. 0 / null: wait indefinitely.
+  unsigned long long timeout_ns = 0;
+  int* failed = nullptr;
   // Slice plan, a function of (max_len, k, shared) only, so every rank
   // agrees: slices of whole 9-vectors (one camera each). One rank per device:
   // up to 148 slices (one CTA per SM folds and exchanges its cameras). Ranks
@@ -77,6 +83,9 @@ class Comm {
   // max_len elements (false where the backend has none; every rank gets the
   // same answer).
   virtual bool make_peer_site(std::int64_t /*max_len*/, DType /*t*/, PeerSite* /*out*/) { return false; }
+  // SolverConfig::collective_timeout (dba/solver.hpp:54): also bounds the
+  // device-side peer waits of the DPCG graph (PeerSite::timeout_ns).
+  virtual std::chrono::milliseconds timeout() const { return std::chrono::milliseconds(60000); }
 };
 
 class SelfComm final : public Comm {
@@ -110,6 +119,7 @@ class Group {
   Group(int k, std::vector<int> devices, std::chrono::milliseconds timeout = std::chrono::milliseconds(60000));
   ~Group();
   int size() const { return k_; }
+  std::chrono::milliseconds timeout() const { return timeout_; }
   int device_of(int rank) const { return devices_[static_cast<std::size_t>(rank)]; }
 
   void allreduce(int rank, void* data, std::int64_t count, DType t, bool is_max, cudaStream_t s);
@@ -179,6 +189,7 @@ class GroupComm final : public Comm {
   bool make_peer_site(std::int64_t max_len, DType t, PeerSite* out) override {
     return g_->make_peer_site(rank_, max_len, t, out);
   }
+  std::chrono::milliseconds timeout() const override { return g_->timeout(); }
 
  private:
   Group* g_;
@@ -194,8 +205,11 @@ class NcclComm final : public Comm {
   void allreduce_sum(void* d, std::int64_t n, DType t, cudaStream_t s) override;
   void allreduce_max(void* d, std::int64_t n, DType t, cudaStream_t s) override;
   bool make_peer_site(std::int64_t max_len, DType t, PeerSite* out) override;
+  std::chrono::milliseconds timeout() const override { return timeout_; }
+  void set_timeout(std::chrono::milliseconds t) { timeout_ = t; }
 
  private:
+  std::chrono::milliseconds timeout_{60000};
   ncclComm_t comm_ = nullptr;
   int rank_, size_;
   std::vector<void*> own_;    // local peer-site allocations

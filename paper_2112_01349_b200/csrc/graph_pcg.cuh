@@ -67,6 +67,7 @@ struct GScal {
   int n, max_iters, status, dse_count;
   int phase;  // 0: PCG pass, 1: residual-refresh pass (DSE on x)
   int done;   // loop finished: the remaining kernels of an unrolled body return at once
+  int peer_fail;  // K > 1: bit p = rank p missed a peer all-reduce (PeerSite::failed)
 };
 
 template <class S>

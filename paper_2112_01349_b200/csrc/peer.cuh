@@ -44,8 +44,12 @@ __device__ __forceinline__ unsigned long long global_ns() {
   return t;
 }
 
-// timeout_ns > 0 (the setup self-check only): give up waiting after that
-// long and raise *failed; 0 waits for as long as the peers take.
+// Waiting for the peers: timeout_ns / failed given (the setup self-check,
+// 2 s) or the site's own (SolverConfig::collective_timeout in the DPCG
+// graph); past the timeout bit p of the absent rank p is ORed into *failed
+// and the wait ends. A set *failed ends every later wait at once (the graph
+// drains; the host raises CollectiveError naming the ranks). No timeout and
+// no flag: wait for as long as the peers take.
 template <class T, class Fill>
 __device__ __forceinline__ void peer_slice(const PeerSite& s, int c, std::int64_t b0, std::int64_t b1, T* out,
                                            Fill fill, unsigned long long timeout_ns = 0, int* failed = nullptr) {
@@ -55,14 +59,21 @@ __device__ __forceinline__ void peer_slice(const PeerSite& s, int c, std::int64_
   if (threadIdx.x == 0) {
     __threadfence_system();  // the CTA's deposits (ordered by bar.sync) before the epoch
     st_release_sys(s.flag[s.rank] + c, e);
-    const unsigned long long t0 = timeout_ns ? global_ns() : 0;
-    for (int p = 0; p < s.k; ++p)
+    const unsigned long long tmo = timeout_ns ? timeout_ns : s.timeout_ns;
+    int* fl = timeout_ns ? failed : s.failed;
+    const volatile int* vfl = fl;
+    const unsigned long long t0 = tmo ? global_ns() : 0;
+    for (int p = 0; p < s.k; ++p) {
+      unsigned spins = 0;
       while (static_cast<int>(ld_acquire_sys(s.flag[p] + c) - e) < 0) {
-        if (timeout_ns && global_ns() - t0 > timeout_ns) {
-          *failed = 1;
+        if ((++spins & 255u) != 0u) continue;
+        if (vfl && *vfl) break;  // a peer is already known absent
+        if (tmo && global_ns() - t0 > tmo) {
+          atomicOr(fl, 1 << p);
           break;
         }
       }
+    }
     s.epoch[c] = e;
   }
   __syncthreads();

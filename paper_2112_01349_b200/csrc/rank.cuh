@@ -1153,6 +1153,13 @@ class Rank {
     dev::GBufs<S> B = gbufs();
     dev::RedWs ws = red();
     dev::GScal<S>* sc = gsc_.get();
+    // peer waits bounded by the collective timeout; absent ranks -> sc->peer_fail
+    const unsigned long long tmo_ns =
+        static_cast<unsigned long long>(std::max<std::int64_t>(comm_->timeout().count(), 1)) * 1000000ull;
+    for (PeerSite* ps : {&ps_cam_, &ps_halo_}) {
+      ps->timeout_ns = tmo_ns;
+      ps->failed = &sc->peer_fail;
+    }
     const dev::GScal<S>* csc = sc;
     dev::DseArgs<S, T> A = dse_args(nullptr);
     const int lane_blocks = static_cast<int>((static_cast<std::int64_t>(m_) * 32 / 3 + 255) / 256 + 1);
@@ -1236,6 +1243,14 @@ class Rank {
     DBAG_CUDA(cudaStreamSynchronize(st_));
     collect_profile();
     const dev::GScal<S> o = *gsc_h_;
+    if (o.peer_fail) {
+      std::string who;
+      for (int p = 0; p < comm_->size(); ++p)
+        if (o.peer_fail & (1 << p)) who += (who.empty() ? "" : ", ") + std::to_string(p);
+      throw Error(DBAG_COLLECTIVE, "collective timeout after " + std::to_string(comm_->timeout().count()) +
+                                       " ms in the device all-reduce of the DPCG graph: rank(s) " + who +
+                                       " did not arrive");
+    }
     const std::int64_t passes = std::max(o.dse_count - 1, 0);
     const int per_body = 2 + (H_ > 0 ? 1 : 0) + (g_fused_ || g_cluster_ > 0 ? 1 : 2);
     launches_ += 1 + per_body * ((passes + gk_unroll_ - 1) / gk_unroll_) * gk_unroll_;

@@ -558,14 +558,20 @@ class RankContext:
     """One rank's device context (include/dbag.h "rank context"): the operator
     level of lm_solve_rank. K = 1 unless created with ``nccl=(rank, nranks, uid)``."""
 
-    def __init__(self, device: int = 0, precision: int = 8, nccl=None, coupling_fp32: bool = False, shard=None):
+    def __init__(self, device: int = 0, precision: int = 8, nccl=None, coupling_fp32: bool = False, shard=None,
+                 group=None):
         """shard=(rank, nranks): partition `rank` of `nranks` with local
         collectives (EdgeEvaluator / assemble_local semantics: costs and the
-        assembled system are this partition's own contribution)."""
+        assembled system are this partition's own contribution).
+        group=(WorkerGroup, rank): rank `rank` of an in-process group (the
+        reference's run_on_workers model; the device is the group's)."""
         self.precision = precision
         self.dtype = np.float64 if precision == 8 else np.float32
         h = C.c_void_p()
-        if shard is not None:
+        if group is not None:
+            g, rank = group
+            _check(N.lib().dbag_create_group_rank(g.h, int(rank), precision, int(coupling_fp32), C.byref(h)))
+        elif shard is not None:
             _check(N.lib().dbag_create_shard(device, precision, int(coupling_fp32), int(shard[0]), int(shard[1]),
                                              C.byref(h)))
         elif nccl is None:

@@ -693,6 +693,37 @@ def test_fused_linearize_assembly_matches_rows(k, mode, monkeypatch):
     _compare_histories(dba.lm_solve(p, cfg), O.lm_solve(p, cfg), 1e-9)
 
 
+def test_peer_graph_timeout_names_absent_rank():
+    """The device-side peer waits of the K > 1 DPCG graph are bounded by the
+    collective timeout (SolverConfig::collective_timeout, dba/solver.hpp:54):
+    a rank whose peer never enters the solve gets CollectiveError naming the
+    absent rank (dba/comms.hpp:136-193 semantics) instead of spinning
+    forever; the graph drains once the first wait gives up."""
+    import time
+    p = ring(30, 300, 6, radius=1.0, noise=0.5, seed=21, nobs=300 * 6 - 5)
+    g = dba.WorkerGroup(2, timeout_ms=300)
+    ctx = [dba.RankContext(0, 8, group=(g, r)) for r in range(2)]
+    out = {}
+
+    def body(r):
+        c = ctx[r]
+        c.upload(p)
+        c.linearize()
+        c.damp_factor(1e-4)
+        c.rhs()
+        out[r] = c.pcg(1e-12, 200)
+
+    dba.run_on_workers(g, body)  # both ranks: peer sites and graphs built
+    assert out[0] == out[1] and out[0][0] > 0
+    t0 = time.monotonic()
+    with pytest.raises(dba.CollectiveError, match=r"rank\(s\) 1 did not arrive"):
+        ctx[0].pcg(1e-12, 200)  # rank 1 never joins
+    assert time.monotonic() - t0 < 30.0
+    for c in ctx:
+        c.close()
+    g.close()
+
+
 def test_peer_site_selftest_fallback(monkeypatch):
     """Every peer site is verified before use (k_peer_selftest: two
     all-reduces of closed-form values per slice, agreed over the ranks); a
