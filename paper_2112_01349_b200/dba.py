@@ -581,6 +581,7 @@ class RankContext:
             _check(N.lib().dbag_create_nccl_ex(device, rank, nranks, C.create_string_buffer(bytes(uid), 128),
                                                precision, int(coupling_fp32), C.byref(h)))
         self.h = h
+        self._group = group[0] if group is not None else None  # the group outlives its rank contexts
         self.m = self.n = self.nobs = 0
 
     def close(self):
