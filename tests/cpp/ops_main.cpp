@@ -4,7 +4,8 @@
 // rank-identical bitwise), tests/test_linear.cpp:270-298 (singular block
 // index, damping) and tests/test_comms.cpp:20-60 (all-reduce), plus the
 // evaluator / assembly / lm_solve_rank path. Needs a GPU (every operator runs
-// on the device); `compile` only checks that the header instantiates.
+// on the device); `compile` only checks that the header instantiates and
+// runs the host-only port (check_convergence, tests/test_solver.cpp:457-486).
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -470,9 +471,41 @@ void evaluator_assembly_and_lm_rank() {
   CHECK(ref.previous_cost >= ref.cost || !ref.last_accepted);
 }
 
+// tests/test_solver.cpp:457-486 (host logic, runs in `compile` mode too).
+void check_convergence_decisions() {
+  SolverConfig config;
+  config.max_iterations = 50;
+  SolverState<double> state;
+  state.iteration = 3;
+  state.lambda = 1e-4;
+  state.cost = 10.0;
+  state.previous_cost = 10.0;
+
+  state.last_accepted = true;
+  state.last_cost_change = 0.0;
+  state.last_step_inf = 1.0;
+  CHECK(check_convergence(state, config) == ConvergenceDecision::converged);
+
+  state.last_cost_change = 5.0;
+  CHECK(check_convergence(state, config) == ConvergenceDecision::keep_going);
+
+  state.last_step_inf = 1e-9;
+  CHECK(check_convergence(state, config) == ConvergenceDecision::converged);
+
+  state.last_accepted = false;
+  state.last_step_inf = 1.0;
+  state.iteration = 50;
+  CHECK(check_convergence(state, config) == ConvergenceDecision::max_iterations);
+
+  state.iteration = 3;
+  state.lambda = 2e32;
+  CHECK(check_convergence(state, config) == ConvergenceDecision::stalled);
+}
+
 }  // namespace
 
 int main(int argc, char** argv) {
+  check_convergence_decisions();
   if (argc > 1 && std::strcmp(argv[1], "compile") == 0) {
     std::printf("ops compiled\n");
     return 0;
