@@ -111,3 +111,30 @@ def test_k8_integer_exact_at_baseline_shapes(shape, split):
     expect = sorted({int(a) for a, b in zip(last[:-1], first[1:]) if a == b})
     shared = dba.shared_points(p, k)
     assert list(shared) == expect and len(shared) <= k - 1
+
+
+def test_single_partition_identity_maps():  # tests/test_partition.cpp:26-37
+    p = ProblemFactory(5).random_problem(3, 4, 8)
+    parts = dba.partition_edges(p, 1)
+    assert len(parts) == 1 and len(parts[0].edge_ids) == 8
+    assert parts[0].camera_map.size() == 3 and parts[0].point_map.size() == 4
+    assert all(parts[0].camera_map.local(c) == c for c in range(3))
+    assert all(parts[0].point_map.local(q) == q for q in range(4))
+
+
+def test_map_composed_with_inverse_is_identity():  # tests/test_partition.cpp:73-89
+    p = ProblemFactory(17).random_problem(6, 9, 30)
+    cid = p.arrays()[2]
+    for k in (1, 2, 3, 4, 7):
+        for part in dba.partition_edges(p, k):
+            touched = set(int(c) for c in cid[part.edge_ids])
+            cm = part.camera_map
+            assert cm.size() == len(touched)
+            assert all(cm.global_(cm.local(g)) == g for g in touched)
+            assert all(cm.local(cm.global_(l)) == l for l in range(cm.size()))
+
+
+def test_touched_camera_counts_bound_the_global_count():  # tests/test_partition.cpp:113-123
+    p = ProblemFactory(31).random_problem(6, 8, 24)
+    for k in (1, 2, 3):
+        assert sum(part.camera_map.size() for part in dba.partition_edges(p, k)) >= p.num_cameras
