@@ -418,6 +418,30 @@ class SolverState:
     cost: float
     termination: str
     history: List[IterationRecord]
+    # the most recent trial, feeding the convergence decision (dba/solver.hpp:80-84)
+    last_accepted: bool = False
+    last_cost_change: float = float("inf")
+    last_step_inf: float = float("inf")
+    previous_cost: float = float("inf")
+
+
+CONVERGENCE = {0: "keep_going", 1: "converged", 2: "max_iterations", 3: "stalled"}
+
+
+def check_convergence(state: SolverState, config: SolverConfig) -> str:
+    """dba::check_convergence (dba/solver.hpp:91-104): "converged" when an
+    accepted step changed the cost by less than rel_tol (relatively) or moved
+    the state by less than step_tol; "stalled" when lambda exceeds
+    lambda_max; "max_iterations" at the cap; else "keep_going"."""
+    if state.last_accepted:
+        denom = max(state.previous_cost, 1e-300)
+        if abs(state.last_cost_change) / denom < config.rel_tol or state.last_step_inf < config.step_tol:
+            return "converged"
+    if state.lambda_ > config.lambda_max:
+        return "stalled"
+    if state.iteration >= config.max_iterations:
+        return "max_iterations"
+    return "keep_going"
 
 
 class _ResultBuf:
@@ -458,7 +482,8 @@ class _ResultBuf:
                                 [int(v) for v in self.wb[i * k:(i + 1) * k]])
                 for i in range(min(r.iterations, self.cap))]
         return SolverState(self.xc.copy(), self.xp[:3 * n].copy(), r.lam, r.nu, r.iterations, r.cost,
-                           TERMINATION[r.termination], hist)
+                           TERMINATION[r.termination], hist, bool(r.last_accepted), float(r.last_cost_change),
+                           float(r.last_step_inf), float(r.previous_cost))
 
 
 def lm_solve(problem: BAProblem, config: Optional[SolverConfig] = None, devices: Sequence[int] = (0,)) -> SolverState:

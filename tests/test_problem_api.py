@@ -36,3 +36,32 @@ def test_validate_flags_unreferenced_nodes():  # test_problem.cpp:220-232
     p.add_edge(Observation())
     w = p.validate()
     assert len(w) == 1 and "camera 1" in w[0]
+
+
+def test_check_convergence_decisions():  # tests/test_solver.cpp:457-486
+    cfg = dba.SolverConfig(max_iterations=50)
+    st = dba.SolverState(x_c=None, x_p=None, lambda_=1e-4, nu=2.0, iteration=3, cost=10.0, termination="",
+                         history=[], previous_cost=10.0)
+    st.last_accepted, st.last_cost_change, st.last_step_inf = True, 0.0, 1.0
+    assert dba.check_convergence(st, cfg) == "converged"
+    st.last_cost_change = 5.0
+    assert dba.check_convergence(st, cfg) == "keep_going"
+    st.last_step_inf = 1e-9
+    assert dba.check_convergence(st, cfg) == "converged"
+    st.last_accepted, st.last_step_inf, st.iteration = False, 1.0, 50
+    assert dba.check_convergence(st, cfg) == "max_iterations"
+    st.iteration, st.lambda_ = 3, 2e32
+    assert dba.check_convergence(st, cfg) == "stalled"
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("cfg", [dict(max_iterations=3), dict(max_iterations=50, pcg_tol=1e-10)])
+def test_returned_state_decides_its_termination(cfg):
+    """The state lm_solve returns carries the last trial (dba/solver.hpp:80-84):
+    check_convergence on it gives the solve's own termination reason."""
+    p = dba.generate_synthetic(dba.SyntheticOptions(cameras=24, points=200, obs_per_point=6, seed=2024,
+                                                    circle_radius=1.0, pixel_noise=0.5))
+    c = dba.SolverConfig(**cfg)
+    st = dba.lm_solve(p, c)
+    assert st.last_accepted == st.history[-1].accepted
+    assert dba.check_convergence(st, c) == st.termination
