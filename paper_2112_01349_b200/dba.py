@@ -97,6 +97,28 @@ def _check(rc: int) -> None:
 MSE_PER_OBSERVATION, MSE_HALF_PER_OBSERVATION = 0, 1
 
 
+def pack_cameras(problem: "BAProblem"):
+    """dba/problem.hpp:294-306: x_c (9m)."""
+    return problem.pack_cameras()
+
+
+def pack_points(problem: "BAProblem"):
+    """dba/problem.hpp:308-318: x_p (3n)."""
+    return problem.pack_points()
+
+
+def unpack_states(x_c, x_p, problem: "BAProblem") -> None:
+    """dba/problem.hpp:341-353: writes packed parameter vectors back into the
+    problem's camera and point states (in place)."""
+    cams, pts, cid, pid, px, py, w = problem.arrays()
+    x_c = np.asarray(x_c, dtype=problem.dtype).reshape(-1)
+    x_p = np.asarray(x_p, dtype=problem.dtype).reshape(-1)
+    if x_c.size != cams.size or x_p.size != pts.size:
+        raise ShapeError(f"unpack_states: expected {cams.size} + {pts.size} parameters, got {x_c.size} + {x_p.size}")
+    problem._frozen = (np.ascontiguousarray(x_c.reshape(-1, 9)), np.ascontiguousarray(x_p.reshape(-1, 3)),
+                       cid, pid, px, py, w)
+
+
 def mse_from_cost(cost: float, num_observations: int, convention: int = MSE_HALF_PER_OBSERVATION) -> float:
     """dba/problem.hpp:22-29."""
     if num_observations <= 0:
@@ -231,6 +253,28 @@ class BAProblem:
     @property
     def num_observations(self) -> int:
         return len(self.arrays()[2])
+
+    # node / edge accessors (dba/problem.hpp:219-227), as value objects
+    def camera(self, i: int) -> CameraState:
+        c = self.arrays()[0][i]
+        return CameraState(tuple(float(v) for v in c[:3]), tuple(float(v) for v in c[3:6]), float(c[6]),
+                           float(c[7]), float(c[8]))
+
+    def point(self, i: int) -> PointState:
+        return PointState(tuple(float(v) for v in self.arrays()[1][i]))
+
+    def observation(self, e: int) -> Observation:
+        _, _, cid, pid, px, py, w = self.arrays()
+        return Observation(int(cid[e]), int(pid[e]), (float(px[e]), float(py[e])), float(w[e]))
+
+    def cameras(self) -> List[CameraState]:
+        return [self.camera(i) for i in range(self.num_cameras)]
+
+    def points(self) -> List[PointState]:
+        return [self.point(i) for i in range(self.num_points)]
+
+    def observations(self) -> List[Observation]:
+        return [self.observation(e) for e in range(self.num_observations)]
 
     def pack_cameras(self):
         return self.arrays()[0].reshape(-1).copy()

@@ -65,3 +65,18 @@ def test_returned_state_decides_its_termination(cfg):
     st = dba.lm_solve(p, c)
     assert st.last_accepted == st.history[-1].accepted
     assert dba.check_convergence(st, c) == st.termination
+
+
+def test_accessors_and_pack_unpack_round_trip():  # dba/problem.hpp:219-227, 294-353
+    from tests.factory import ProblemFactory
+    p = ProblemFactory(7).random_problem(3, 5, 9)
+    cams, pts, cid, pid, px, py, w = p.arrays()
+    assert p.camera(1).params() == list(cams[1]) and list(p.point(4).position) == list(pts[4])
+    o = p.observation(8)
+    assert (o.camera_id, o.point_id, o.pixel, o.weight) == (cid[8], pid[8], (px[8], py[8]), w[8])
+    assert len(p.cameras()) == 3 and len(p.points()) == 5 and len(p.observations()) == 9
+    xc, xp = dba.pack_cameras(p), dba.pack_points(p)
+    dba.unpack_states(xc + 1.0, xp - 2.0, p)
+    assert (dba.pack_cameras(p) == xc + 1.0).all() and (dba.pack_points(p) == xp - 2.0).all()
+    with pytest.raises(dba.dba.ShapeError):
+        dba.unpack_states(xc[:-1], xp, p)
